@@ -1,0 +1,492 @@
+"""Pins for the fp64 CPU oracle (CPU only, no GPU).
+
+The oracle is checked against what the paper and mathematics fix — worked examples printed in
+the sources (tests/golden/spec_examples.json, each cited), closed forms, invariants, special
+cases that reduce to a textbook or library routine, and brute force on tiny inputs — never
+against itself.  Pin ids P1..P21 follow DESIGN.md §5.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import kaze_inputs
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+@pytest.fixture(scope="module")
+def O(oracle_lib):
+    return oracle_lib
+
+
+# ----------------------------------------------------------------------------- P17 schedule
+def test_schedule_spec_examples(O):
+    for ex in GOLD["schedule"]:
+        if "o" in ex:
+            sg, t, st = O.schedule(ex["o"] + 1, ex["S"], ex["sigma0"])
+            assert sg[ex["o"] * ex["S"] + ex["s"]] == pytest.approx(ex["sigma"], rel=1e-15)
+        else:
+            sg, t, _ = O.schedule(1, 1, ex["sigma"])
+            assert t[0] == pytest.approx(ex["t"], rel=1e-15)
+
+
+def test_schedule_invariants(O):
+    sg, t, st = O.schedule(4, 4, 1.6)
+    assert np.all(np.diff(sg) > 0)
+    np.testing.assert_allclose(t, sg ** 2 / 2, rtol=0, atol=0)  # Eq. 7 exactly
+    # an octave doubles sigma (Eq. 6 read as 2^{o + s/S}); S sublevels per octave
+    np.testing.assert_allclose(sg[4:] / sg[:-4], 2.0, rtol=1e-15)
+    # s_i = nearest integer to sigma_i, never below 1
+    assert np.all(np.abs(st - sg) <= 0.5) and st.min() >= 1
+
+
+# ----------------------------------------------------------------------------- P1/P2 Gaussian
+def test_gaussian_taps_shape(O):
+    g = O.gaussian_taps(1.0)
+    assert len(g) == 7 and g.sum() == pytest.approx(1.0, abs=1e-15)
+    np.testing.assert_array_equal(g, g[::-1])
+    assert len(O.gaussian_taps(1.6)) == 11  # r = ceil(3*1.6) = 5
+    g01 = O.gaussian_taps(0.1)  # S:L54 delta limit
+    assert g01[len(g01) // 2] > 1 - 1e-12
+
+
+def test_gaussian_blur_impulse_and_corner(O):
+    sigma = 1.6
+    r = 5
+    x = np.arange(-r, r + 1)
+    g = np.exp(-x ** 2 / (2 * sigma ** 2))
+    g /= g.sum()  # closed form of the sampled normalised Gaussian
+    img = np.zeros((31, 29))
+    img[15, 11] = 1.0
+    out = O.gaussian_blur(img, sigma)
+    np.testing.assert_allclose(out[15 - r:15 + r + 1, 11 - r:11 + r + 1], np.outer(g, g), atol=1e-15)
+    assert np.abs(out).sum() == pytest.approx(1.0, abs=1e-13)
+    # corner impulse with replicate border: out(0,0) = (sum of taps with offset <= 0)^2
+    img = np.zeros((20, 20))
+    img[0, 0] = 1.0
+    out = O.gaussian_blur(img, sigma)
+    assert out[0, 0] == pytest.approx(g[: r + 1].sum() ** 2, rel=1e-13)
+    # (0, 1): dx in {-r..-1} clamps x+dx to 0 only for dx <= -1
+    assert out[0, 1] == pytest.approx(g[: r + 1].sum() * g[:r].sum(), rel=1e-13)
+
+
+def test_gaussian_blur_invariants(O):
+    rng = np.random.default_rng(0)
+    c = np.full((16, 16), 0.37)
+    np.testing.assert_allclose(O.gaussian_blur(c, 1.6), 0.37, atol=1e-15)
+    # linearity and ramp preservation in the interior (symmetric kernel)
+    yy, xx = np.mgrid[0:40, 0:40].astype(float)
+    ramp = 0.3 * xx - 0.2 * yy + 1.0
+    out = O.gaussian_blur(ramp, 1.0)
+    np.testing.assert_allclose(out[3:-3, 3:-3], ramp[3:-3, 3:-3], atol=1e-13)
+    a, b = rng.random((16, 16)), rng.random((16, 16))
+    np.testing.assert_allclose(O.gaussian_blur(2 * a - 3 * b, 1.3),
+                               2 * O.gaussian_blur(a, 1.3) - 3 * O.gaussian_blur(b, 1.3), atol=1e-13)
+
+
+def test_gaussian_semigroup(O):
+    """blur(blur(I, a), b) ~ blur(I, sqrt(a^2 + b^2)) on smooth images (1e-3 RMS)."""
+    yy, xx = np.mgrid[0:64, 0:64].astype(float)
+    img = np.sin(xx / 5.0) * np.cos(yy / 7.0) + 0.5
+    two = O.gaussian_blur(O.gaussian_blur(img, 1.0), 1.6)
+    one = O.gaussian_blur(img, math.sqrt(1.0 + 1.6 ** 2))
+    assert np.sqrt(np.mean((two - one)[10:-10, 10:-10] ** 2)) < 1e-3
+
+
+# ----------------------------------------------------------------------------- P3 Scharr / Hessian
+@pytest.mark.parametrize("s", [1, 2, 3, 5, 8])
+def test_scharr_ramp_and_quadratics(O, s):
+    yy, xx = np.mgrid[0:64, 0:64].astype(float)
+    inner = (slice(2 * s + 1, -2 * s - 1), slice(2 * s + 1, -2 * s - 1))
+    np.testing.assert_allclose(O.scharr(xx, s, 0)[inner], 1.0, atol=1e-13)
+    np.testing.assert_allclose(O.scharr(xx, s, 1)[inner], 0.0, atol=1e-13)
+    np.testing.assert_allclose(O.scharr(yy, s, 1)[inner], 1.0, atol=1e-13)
+    np.testing.assert_allclose(O.scharr(np.full((20, 20), 3.0), s, 0), 0.0, atol=0)
+    # Hessian closed forms: Ldet = s^4 * det(Hessian) for quadratics
+    for ex in GOLD["hessian"]:
+        img = (xx ** 2 + yy ** 2) if ex["image"] == "x2+y2" else xx * yy
+        img = img / 64.0  # keep values O(1)
+        Lx, Ly, Ld = O.hessian(img, s)
+        want = ex["factor"] * s ** 4 / 64.0 ** 2 * (1.0 if ex["image"] == "x2+y2" else 1.0)
+        np.testing.assert_allclose(Ld[inner], want, rtol=1e-9)
+    # first derivatives are s-normalised: Lx = s * d/dx
+    Lx, Ly, _ = O.hessian(0.5 * xx + 0.25 * yy, s)
+    np.testing.assert_allclose(Lx[inner], 0.5 * s, rtol=1e-12)
+    np.testing.assert_allclose(Ly[inner], 0.25 * s, rtol=1e-12)
+
+
+def test_hessian_mixed_order_is_y_of_x(O):
+    """A10: Lxy = Sy[Lx] on the materialised (clamped) Lx — differs from Sx[Ly] only in the 2s band."""
+    rng = np.random.default_rng(3)
+    img = O.gaussian_blur(rng.random((48, 48)), 2.0)
+    s = 3
+    lx = O.scharr(img, s, 0)
+    ly = O.scharr(img, s, 1)
+    dxx, dyy, dxy = O.scharr(lx, s, 0), O.scharr(ly, s, 1), O.scharr(lx, s, 1)
+    _, _, Ld = O.hessian(img, s)
+    np.testing.assert_allclose(Ld, s ** 4 * (dxx * dyy - dxy ** 2), rtol=1e-12, atol=1e-16)
+    dyx = O.scharr(ly, s, 0)
+    band = 2 * s
+    np.testing.assert_allclose(dxy[band:-band, band:-band], dyx[band:-band, band:-band], atol=1e-14)
+
+
+# ----------------------------------------------------------------------------- P4 blob scale
+def _blob_closed_form(s, v, A):
+    """Ldet at the centre of A*exp(-rho^2/2v) for the dilated-Scharr Hessian (derived in DESIGN §5)."""
+    e1, e2 = math.exp(-s * s / (2 * v)), math.exp(-2 * s * s / v)
+    sm = (118 + 120 * e1 + 18 * e2) / 256.0
+    lxx = A * (e2 - 1.0) / (2 * s * s) * sm
+    return s ** 4 * lxx * lxx
+
+
+def test_hessian_blob_closed_form_and_peak_scale(O):
+    """BASELINE north_star: 'the Hessian of a synthetic Gaussian blob peaks at its known scale'.
+    A blob of std r seen at scale sigma is (r^2/v) exp(-rho^2/2v), v = r^2 + sigma^2 (linear scale
+    space); the oracle's Ldet at its centre must equal the closed form, and its argmax over the
+    KAZE schedule must be the closed form's argmax (the discrete 'known scale')."""
+    sg, _, st = O.schedule(4, 4, 1.6)
+    n = 257
+    yy, xx = np.mgrid[0:n, 0:n].astype(float) - n // 2
+    for r in (4.0, 6.0, 9.0):
+        got, want = [], []
+        for i in range(16):
+            v = r * r + sg[i] ** 2
+            A = r * r / v
+            img = A * np.exp(-(xx ** 2 + yy ** 2) / (2 * v))
+            _, _, Ld = O.hessian(img, int(st[i]))
+            got.append(Ld[n // 2, n // 2])
+            want.append(_blob_closed_form(int(st[i]), v, A))
+        np.testing.assert_allclose(got, want, rtol=1e-10)
+        assert int(np.argmax(got)) == int(np.argmax(want))
+        # the discrete known scale: levels 3, 6, 9 (closed-form argmax); within 0.6 octave of r —
+        # the continuous analogue sigma^4 r^4 / (r^2 + sigma^2)^4 peaks exactly at sigma = r
+        assert int(np.argmax(got)) == {4.0: 3, 6.0: 6, 9.0: 9}[r]
+        assert abs(math.log2(sg[int(np.argmax(got))] / r)) <= 0.6
+
+
+# ----------------------------------------------------------------------------- P5 conductivity
+def test_conductivity_examples(O):
+    yy, xx = np.mgrid[0:40, 0:40].astype(float)
+    k = 0.05
+    for ex in GOLD["conductivity"]:
+        m = ex["grad_over_k"] * k
+        img = m * xx  # a ramp stays a ramp of slope m under the symmetric G(1); Scharr gives m
+        for g in (1, 2):
+            c = O.conductivity(img, k, g)
+            np.testing.assert_allclose(c[5:-5, 5:-5], ex[f"g{g}"], rtol=1e-12)
+    rng = np.random.default_rng(1)
+    L = rng.random((24, 24))
+    c1 = O.conductivity(L, 0.04, 2)
+    c2 = O.conductivity(3.0 * L, 0.12, 2)  # joint (L, k) scaling invariance
+    np.testing.assert_allclose(c1, c2, rtol=1e-12)
+    assert c1.min() > 0 and c1.max() <= 1.0
+
+
+# ----------------------------------------------------------------------------- P6 contrast k
+def test_contrast_k_brute_force(O):
+    """k from the histogram equals the brute-force order statistic: with the n nonzero interior
+    magnitudes sorted, g_(thr) (1-indexed) falls in bin b = min(floor(300 g/hmax), 299), k = hmax(b+1)/300."""
+    for seed, (w, h) in [(5, (96, 64)), (6, (64, 64)), (7, (50, 77))]:
+        img = kaze_inputs.synth_image(w, h, seed).astype(np.float64)
+        L0 = O.gaussian_blur(img, 1.6)
+        k, hist, fb = O.contrast_k(L0)
+        Ls = O.gaussian_blur(L0, 1.0)
+        gx, gy = O.scharr(Ls, 1, 0), O.scharr(Ls, 1, 1)
+        g = np.sqrt(gx ** 2 + gy ** 2)[1:-1, 1:-1].ravel()
+        hmax = g.max()
+        nz = np.sort(g[g > 0])
+        thr = int(math.floor(0.7 * len(nz)))
+        b = min(int(math.floor(300 * nz[thr - 1] / hmax)), 299)
+        assert not fb
+        assert k == pytest.approx(hmax * (b + 1) / 300, rel=1e-15)
+        assert hist.sum() == len(nz)
+        # lambda = 2 scales every magnitude exactly, hence k exactly
+        k2, _, _ = O.contrast_k(2.0 * L0)
+        assert k2 == 2.0 * k
+
+
+def test_contrast_k_degenerate(O):
+    ex = GOLD["contrast_k"][0]
+    k, hist, fb = O.contrast_k(np.full((32, 32), 0.25))
+    assert k == ex["constant_image_k"] and fb == ex["fallback"] and hist.sum() == 0
+
+
+# ----------------------------------------------------------------------------- P10 Thomas / AOS matrix
+def test_thomas_vs_dense(O):
+    rng = np.random.default_rng(2)
+    for n in range(1, 17):
+        a, c = -rng.random(n), -rng.random(n)
+        b = 1.0 + rng.random(n) + np.abs(a) + np.abs(c)
+        d = rng.standard_normal(n)
+        M = np.diag(b) + np.diag(a[1:], -1) + np.diag(c[:-1], 1)
+        np.testing.assert_allclose(O.thomas(a, b, c, d), np.linalg.solve(M, d), rtol=1e-12, atol=1e-14)
+
+
+def _aos_matrix(cline, tau):
+    """I - 2 tau A with A_{j,j+-1} = (c_j + c_{j+-1})/2 and zero row sums (reading A2)."""
+    n = len(cline)
+    A = np.zeros((n, n))
+    for j in range(n - 1):
+        w = 0.5 * (cline[j] + cline[j + 1])
+        A[j, j + 1] += w
+        A[j + 1, j] += w
+        A[j, j] -= w
+        A[j + 1, j + 1] -= w
+    return np.eye(n) - 2 * tau * A
+
+
+def test_aos_lines_vs_dense(O):
+    rng = np.random.default_rng(4)
+    for (h, w, tau) in [(5, 7, 0.53), (9, 4, 67.86), (16, 13, 5.99)]:
+        L = rng.random((h, w))
+        c = rng.uniform(0.05, 1.0, (h, w))
+        out, U, V = O.aos_step(L, c, tau)
+        for x in range(w):
+            np.testing.assert_allclose(U[:, x], np.linalg.solve(_aos_matrix(c[:, x], tau), L[:, x]), rtol=1e-11)
+        for y in range(h):
+            np.testing.assert_allclose(V[y], np.linalg.solve(_aos_matrix(c[y], tau), L[y]), rtol=1e-11)
+        np.testing.assert_allclose(out, 0.5 * (U + V), rtol=0, atol=0)
+
+
+# ----------------------------------------------------------------------------- P7-P9, P11, P12 AOS
+def test_aos_identity_mean_maxprinciple(O):
+    rng = np.random.default_rng(5)
+    c = rng.uniform(0.01, 1.0, (37, 53))
+    out, _, _ = O.aos_step(np.full((37, 53), 0.42), c, 12.0)
+    np.testing.assert_allclose(out, 0.42, rtol=1e-14)  # P7
+    for tau in (0.53, 5.99, 67.86):
+        L = rng.random((37, 53))
+        out, U, V = O.aos_step(L, c, tau)
+        assert out.mean() == pytest.approx(L.mean(), rel=1e-13)  # P8
+        np.testing.assert_allclose(U.sum(axis=0), L.sum(axis=0), rtol=1e-12)
+        np.testing.assert_allclose(V.sum(axis=1), L.sum(axis=1), rtol=1e-12)
+        assert out.min() >= L.min() - 1e-14 and out.max() <= L.max() + 1e-14  # P9
+
+
+def test_aos_dct_closed_form(O):
+    """P11: with c = 1 every DCT-II mode is an eigenvector of both line operators."""
+    H, W = 24, 40
+    yy, xx = np.mgrid[0:H, 0:W].astype(float)
+    c = np.ones((H, W))
+    for (k, l, tau) in [(3, 2, 1.5), (7, 0, 20.0), (0, 5, 0.53), (13, 11, 67.86)]:
+        mode = np.cos(np.pi * k * (xx + 0.5) / W) * np.cos(np.pi * l * (yy + 0.5) / H)
+        lw = 2 - 2 * np.cos(np.pi * k / W)
+        lh = 2 - 2 * np.cos(np.pi * l / H)
+        out, _, _ = O.aos_step(mode, c, tau)
+        np.testing.assert_allclose(out, 0.5 * (1 / (1 + 2 * tau * lw) + 1 / (1 + 2 * tau * lh)) * mode, atol=1e-13)
+
+
+def test_aos_symmetries(O):
+    rng = np.random.default_rng(6)
+    L = rng.random((21, 34))
+    c = rng.uniform(0.1, 1.0, (21, 34))
+    out, _, _ = O.aos_step(L, c, 8.48)
+    outT, _, _ = O.aos_step(L.T, c.T, 8.48)
+    np.testing.assert_allclose(outT, out.T, rtol=1e-13)
+    outR, _, _ = O.aos_step(L[:, ::-1], c[:, ::-1], 8.48)
+    np.testing.assert_allclose(outR, out[:, ::-1], rtol=1e-13)
+
+
+def test_aos_small_steps_approach_gaussian(O):
+    """P12 (S:L197 analogue): c = 1, M steps of tau = t/M approach G(sqrt(2t)); error shrinks with M."""
+    yy, xx = np.mgrid[0:64, 0:64].astype(float)
+    img = np.exp(-((xx - 32) ** 2 + (yy - 32) ** 2) / (2 * 4.0 ** 2))
+    t = 4.0
+    ref = O.gaussian_blur(img, math.sqrt(2 * t))
+    errs = []
+    for M in (4, 32):
+        L = img.copy()
+        for _ in range(M):
+            L, _, _ = O.aos_step(L, np.ones_like(L), t / M)
+        errs.append(np.sqrt(np.mean((L - ref) ** 2)))
+    assert errs[1] < errs[0] and errs[1] < 1e-2
+
+
+# ----------------------------------------------------------------------------- P19 edge / sub-pixel
+def test_refine_spec_examples(O):
+    e = GOLD["edge_test"]
+    # isotropic peak: D = -(x^2 + y^2) gives Dxx = Dyy = -2, Dxy = 0
+    patch = -np.array([[2, 1, 2], [1, 0, 1], [2, 1, 2]], float) + 5.0
+    keep, dx, dy = O.refine(patch, e[0]["r"])
+    assert keep is e[0]["keep"] and dx == 0.0 and dy == 0.0
+    # ridge: Dxx = -10, Dyy = -0.01 -> Tr^2/Det ~ 1002 > 12.1 -> reject
+    patch = np.array([[-5.005, -0.005, -5.005], [-5.0, 0.0, -5.0], [-5.005, -0.005, -5.005]]) + 5.0
+    keep, _, _ = O.refine(patch, e[1]["r"])
+    assert keep is e[1]["keep"]
+    assert (-10.01) ** 2 / (10 * 0.01) == pytest.approx(e[1]["ratio_approx"], rel=1e-3)
+    # the minimum possible Tr^2/Det is 4 (alpha = beta), i.e. (r+1)^2/r at r = 1
+    assert (e[2]["r"] + 1) ** 2 / e[2]["r"] == e[2]["min_ratio"]
+
+
+@pytest.mark.parametrize("ex", GOLD["subpixel"])
+def test_refine_quadratic_recovery(O, ex):
+    px, py = ex["peak"]
+    yy, xx = np.mgrid[-1:2, -1:2].astype(float)
+    patch = 1.0 - (xx - px) ** 2 - (yy - py) ** 2
+    keep, dx, dy = O.refine(patch, 10.0)
+    assert keep is ex["keep"]
+    if keep:
+        assert abs(dx - px) < ex["tol"] and abs(dy - py) < ex["tol"]
+
+
+def test_refine_anisotropic_quadratic(O):
+    """Exact recovery for a rotated elliptic quadratic with a cross term (not only the isotropic case)."""
+    yy, xx = np.mgrid[-1:2, -1:2].astype(float)
+    px, py = -0.35, 0.41
+    q = 1.3 * (xx - px) ** 2 + 0.8 * (yy - py) ** 2 + 0.5 * (xx - px) * (yy - py)
+    keep, dx, dy = O.refine(2.0 - q, 10.0)
+    assert keep and abs(dx - px) < 1e-12 and abs(dy - py) < 1e-12
+
+
+# ----------------------------------------------------------------------------- P18 extrema
+def test_extrema_constant_and_single_blob(O):
+    sg, _, st = O.schedule(4, 4, 1.6)
+    res = O.run(np.full((64, 64), 0.5, np.float32))
+    assert res["count"] == 0 and res["fallback"]
+    yy, xx = np.mgrid[0:96, 0:96].astype(float)
+    blob = 0.2 + 0.6 * np.exp(-((xx - 47.3) ** 2 + (yy - 48.6) ** 2) / (2 * 2.0 ** 2))
+    res = O.run(blob.astype(np.float32), octaves=2, sublevels=2)
+    kp = res["kps"]
+    assert res["count"] == 1
+    assert abs(kp["x"][0] - 47.3) <= 1.0 and abs(kp["y"][0] - 48.6) <= 1.0
+
+
+def test_extrema_vs_vectorised_scan(O):
+    """A second, vectorised statement of the 3x3x3 rule (numpy shifts) gives the same set."""
+    sg, _, st = O.schedule(2, 2, 1.6)
+    for seed in range(3):
+        img = kaze_inputs.synth_image(64, 64, 100 + seed)
+        res = O.run(img, octaves=2, sublevels=2, want_levels=True, edge_ratio=0.0)
+        D = res["Ldet"]
+        N, H, W = D.shape
+        found = set()
+        for i in range(1, N - 1):
+            c = D[i, 1:-1, 1:-1]
+            ok = c > 1e-3
+            for l in (-1, 0, 1):
+                for dy in (-1, 0, 1):
+                    for dx in (-1, 0, 1):
+                        if l == dy == dx == 0:
+                            continue
+                        ok &= c > D[i + l, 1 + dy:H - 1 + dy, 1 + dx:W - 1 + dx]
+            for y, x in zip(*np.nonzero(ok)):
+                keep, _, _ = O.refine(D[i, y:y + 3, x:x + 3], 0.0)
+                if keep:
+                    found.add((i, float(D[i, y + 1, x + 1])))
+        got = {(int(k["level"]), float(k["response"])) for k in res["kps"]}
+        assert res["count"] == len(found) > 0
+        assert got == found
+
+
+# ----------------------------------------------------------------------------- P14 / P15 / P13 invariances
+def test_translation_invariance(O):
+    base = kaze_inputs.synth_image(48, 48, 77)
+    canvas_a = np.full((200, 200), 0.5, np.float32)
+    canvas_b = canvas_a.copy()
+    canvas_a[76:124, 76:124] = base
+    canvas_b[83:131, 69:117] = base
+    ra = O.run(canvas_a, octaves=2, sublevels=2)
+    rb = O.run(canvas_b, octaves=2, sublevels=2)
+    assert ra["k"] == pytest.approx(rb["k"], rel=1e-12)
+    assert ra["count"] == rb["count"] > 0
+    ka, kb = np.sort(ra["kps"], order=["level", "y", "x"]), np.sort(rb["kps"], order=["level", "y", "x"])
+    np.testing.assert_allclose(kb["x"] - ka["x"], -7.0, atol=1e-9)
+    np.testing.assert_allclose(kb["y"] - ka["y"], 7.0, atol=1e-9)
+    np.testing.assert_allclose(kb["angle"], ka["angle"], atol=1e-9)
+
+
+def test_offset_invariance(O):
+    img = np.round(kaze_inputs.synth_image(80, 64, 9) * 512) / 1024  # values exact in fp32
+    ra = O.run(img.astype(np.float32), octaves=2, sublevels=2)
+    rb = O.run((img + 0.25).astype(np.float32), octaves=2, sublevels=2)
+    assert ra["count"] == rb["count"] > 0
+    np.testing.assert_allclose(ra["kps"]["x"], rb["kps"]["x"], atol=1e-9)
+    np.testing.assert_allclose(ra["desc"], rb["desc"], atol=1e-9)
+
+
+def test_rot90_scale_space_equivariance(O):
+    img = kaze_inputs.synth_image(72, 56, 11)
+    la, ka, _ = O.scale_space(img, octaves=2, sublevels=3)
+    lb, kb, _ = O.scale_space(np.ascontiguousarray(np.rot90(img)), octaves=2, sublevels=3)
+    assert ka == pytest.approx(kb, rel=1e-12)
+    for i in range(la.shape[0]):
+        np.testing.assert_allclose(lb[i], np.rot90(la[i]), atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- P20 orientation
+@pytest.mark.parametrize("theta", [0.0, 0.3, math.pi / 6, 2.0, 4.4, 6.0])
+def test_orientation_uniform_gradient(O, theta):
+    Lx = np.full((64, 64), math.cos(theta))
+    Ly = np.full((64, 64), math.sin(theta))
+    ang, deg = O.orientation(Lx, Ly, 31.4, 30.2, 2.3)
+    assert not deg
+    assert abs(((ang - theta + math.pi) % (2 * math.pi)) - math.pi) < 1e-12
+
+
+def test_orientation_degenerate_and_windows(O):
+    z = np.zeros((32, 32))
+    ang, deg = O.orientation(z, z, 16.0, 16.0, 2.0)
+    assert ang == 0.0 and deg
+    # two populations: a strong direction wins against a weaker one more than pi/3 away
+    yy, xx = np.mgrid[0:64, 0:64].astype(float)
+    Lx = np.where(xx < 32, 1.0, 0.0) + np.where(xx >= 32, 0.0, 0.0)
+    Ly = np.where(xx >= 32, 0.3, 0.0)
+    ang, _ = O.orientation(Lx, Ly, 32.0, 32.0, 1.0)
+    assert abs(ang) < 1e-12 or abs(ang - 2 * math.pi) < 1e-12
+
+
+# ----------------------------------------------------------------------------- P21 descriptor
+def test_descriptor_uniform_field_closed_form(O):
+    """Uniform (Lx, Ly) = (1, 0) at angle 0 (and (0, 1) at angle pi/2): du = 1, dv = 0 everywhere,
+    so desc[4(4b+a)] = w2(a,b) * S and desc[4(4b+a)+2] = w2(a,b) * S with S = (sum_i exp(-(i-4)^2/12.5))^2."""
+    i = np.arange(9)
+    S = np.exp(-((i - 4.0) ** 2) / 12.5).sum() ** 2
+    want = np.zeros(64)
+    for b in range(4):
+        for a in range(4):
+            w2 = math.exp(-((a - 1.5) ** 2 + (b - 1.5) ** 2) / 4.5)
+            want[4 * (4 * b + a)] = w2 * S
+            want[4 * (4 * b + a) + 2] = w2 * S
+    want /= np.linalg.norm(want)
+    one, zero = np.ones((80, 80)), np.zeros((80, 80))
+    d = O.descriptor(one, zero, 40.2, 39.7, 1.7, 0.0)
+    np.testing.assert_allclose(d, want, atol=1e-14)
+    d = O.descriptor(zero, one, 40.2, 39.7, 1.7, math.pi / 2)
+    np.testing.assert_allclose(d, want, atol=1e-14)
+    assert np.all(O.descriptor(zero, zero, 40.0, 40.0, 2.0, 1.0) == 0)  # degenerate -> zero vector
+
+
+def test_descriptor_subregion_indexing(O):
+    """A field that is nonzero only for v > 0 (rows below the keypoint at angle 0) puts its energy
+    in the subregions with b >= 2, and a field nonzero only for u > 0 in a >= 2 (index 4(4b+a)+j)."""
+    yy, xx = np.mgrid[0:100, 0:100].astype(float)
+    cy = cx = 50.0
+    sigma = 1.0
+    Lx = np.where(yy > cy + 4, 1.0, 0.0)
+    d = O.descriptor(Lx, np.zeros_like(Lx), cx, cy, sigma, 0.0).reshape(4, 4, 4)  # [b, a, j]
+    assert np.abs(d[:2]).sum() == 0 and np.abs(d[2:]).sum() > 0
+    Lx = np.where(xx > cx + 4, 1.0, 0.0)
+    d = O.descriptor(Lx, np.zeros_like(Lx), cx, cy, sigma, 0.0).reshape(4, 4, 4)
+    assert np.abs(d[:, :2]).sum() == 0 and np.abs(d[:, 2:]).sum() > 0
+
+
+def test_descriptor_unit_norm_and_affine_invariance(O):
+    img = kaze_inputs.synth_image(96, 80, 21).astype(np.float64)
+    ra = O.run(img.astype(np.float32), octaves=2, sublevels=2, want_levels=True)
+    assert ra["count"] > 0
+    norms = np.linalg.norm(ra["desc"], axis=1)
+    np.testing.assert_allclose(norms[norms > 0], 1.0, atol=1e-12)
+    # pinned keypoints + angles, derivatives of a*I + b are a times those of I
+    k2, d2 = O.describe(3.0 * ra["Lx"], 3.0 * ra["Ly"], ra["kps"], keep_angle=True)
+    np.testing.assert_allclose(d2, ra["desc"], atol=1e-12)
+
+
+def test_bilinear_exact_on_planes(O):
+    yy, xx = np.mgrid[0:10, 0:12].astype(float)
+    img = 0.7 * xx - 1.3 * yy + 2.0
+    for (x, y) in [(3.25, 4.75), (0.0, 0.0), (10.9, 8.1)]:
+        assert O.bilinear(img, x, y) == pytest.approx(0.7 * x - 1.3 * y + 2.0, abs=1e-13)
+    assert O.bilinear(img, -5.0, 4.0) == pytest.approx(img[4, 0])  # clamped
