@@ -1,0 +1,217 @@
+// describe.cu — dominant orientation (A14) and 64-D M-SURF (A15).
+//
+// One warp per keypoint over the FLAT list of all keypoints of all levels and images (the paper's load-balancing
+// remedy: "all the image scales are computed at the same time"), persistent grid of 148·k CTAs.
+//   orientation: 113 samples at kp + σ(u, v), u² + v² <= 36, spread over the lanes; Gaussian weight
+//                exp(−(u²+v²)/12.5) (std 2.5σ); the weighted (Lx, Ly) vectors go to shared memory; lanes own the
+//                window centres θ_k = 2πk/nwin and sum the vectors within ±π/6; a warp arg-max (first k on
+//                ties) picks the longest sum; angle = atan2 of it in [0, 2π).
+//   M-SURF:      24 x 24 samples at step σ rotated by the angle, bilinear (Lx, Ly) rotated into the keypoint
+//                frame (du, dv) and staged in shared memory; lane pair (2·sr, 2·sr+1) accumulates subregion sr's 9 x 9
+//                window (Gaussian std 2.5 about its centre), the 4x4 mask (std 1.5) weights it, the warp
+//                normalises the 64-vector and writes it with 16-byte stores.
+#include "kaze_internal.cuh"
+
+namespace kz {
+
+namespace {
+
+constexpr int kOriSamples = 113;
+__constant__ float c_ori_u[kOriSamples], c_ori_v[kOriSamples], c_ori_w[kOriSamples];
+__constant__ float c_w1[81];  // exp(-((i-4)^2 + (j-4)^2) / (2 * 2.5^2)), i, j = 0..8
+__constant__ float c_w2[16];  // exp(-((a-1.5)^2 + (b-1.5)^2) / (2 * 1.5^2)), index 4b + a
+
+constexpr float kTwoPi = 6.283185307179586f;
+constexpr float kPi = 3.141592653589793f;
+
+__device__ __forceinline__ float bilinear(const float* __restrict__ img, int W, int H, int P, float px, float py) {
+    const float fx0 = floorf(px), fy0 = floorf(py);
+    const float fx = px - fx0, fy = py - fy0;
+    const int x0 = (int)fx0, y0 = (int)fy0;
+    const int xa = clampi(x0, 0, W - 1), xb = clampi(x0 + 1, 0, W - 1);
+    const int ya = clampi(y0, 0, H - 1), yb = clampi(y0 + 1, 0, H - 1);
+    const float v00 = __ldg(img + (size_t)ya * P + xa), v10 = __ldg(img + (size_t)ya * P + xb);
+    const float v01 = __ldg(img + (size_t)yb * P + xa), v11 = __ldg(img + (size_t)yb * P + xb);
+    return (1.f - fy) * ((1.f - fx) * v00 + fx * v10) + fy * ((1.f - fx) * v01 + fx * v11);
+}
+
+constexpr int kWarps = 8;
+
+__global__ void __launch_bounds__(256) k_describe(const float* __restrict__ Lx, const float* __restrict__ Ly,
+                                                  size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
+                                                  const int* __restrict__ counts, int cap, float* __restrict__ desc,
+                                                  int nwin, int keep_angle) {
+    __shared__ int pre[kMaxBatch + 1];
+    __shared__ float sbuf[kWarps][2 * 576];
+    if (threadIdx.x == 0) {
+        int r = 0;
+        for (int i = 0; i < nimg; ++i) {
+            pre[i] = r;
+            r += min(max(counts[i], 0), cap);
+        }
+        pre[nimg] = r;
+    }
+    __syncthreads();
+    const int total = pre[nimg];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float* sx = sbuf[warp];
+    float* sy = sx + 576;
+    for (int f = blockIdx.x * kWarps + warp; f < total; f += gridDim.x * kWarps) {
+        int img = 0;
+        while (img + 1 < nimg && pre[img + 1] <= f) ++img;  // nimg is small
+        const int k = f - pre[img];
+        kaze_keypoint* kp = kps + (size_t)img * cap + k;
+        const float x = kp->x, y = kp->y, sigma = kp->sigma;
+        const int level = kp->level;
+        const float* lx = Lx + img * img_stride + (size_t)level * g.plane;
+        const float* ly = Ly + img * img_stride + (size_t)level * g.plane;
+        float angle;
+        int flags = 0;
+        if (keep_angle) {
+            angle = kp->angle;
+        } else {
+            // ---- orientation ----
+            float* sp = sx + 2 * kOriSamples;  // phases after the vectors
+            for (int j = lane; j < kOriSamples; j += 32) {
+                const float px = x + sigma * c_ori_u[j], py = y + sigma * c_ori_v[j];
+                const float w = c_ori_w[j];
+                const float rx = w * bilinear(lx, g.W, g.H, g.P, px, py);
+                const float ry = w * bilinear(ly, g.W, g.H, g.P, px, py);
+                float ph = atan2f(ry, rx);
+                if (ph < 0.f) ph += kTwoPi;
+                sx[j] = rx;
+                sx[kOriSamples + j] = ry;
+                sp[j] = ph;
+            }
+            __syncwarp();
+            float best = 0.f, bx = 0.f, by = 0.f;
+            int bk = 0x7fffffff;
+            for (int kw = lane; kw < nwin; kw += 32) {
+                const float th = kTwoPi * (float)kw / (float)nwin;
+                float ax = 0.f, ay = 0.f;
+                for (int j = 0; j < kOriSamples; ++j) {
+                    float d = sp[j] - th;
+                    if (d > kPi) d -= kTwoPi;
+                    else if (d <= -kPi) d += kTwoPi;
+                    if (fabsf(d) < kPi / 6.f) {
+                        ax += sx[j];
+                        ay += sx[kOriSamples + j];
+                    }
+                }
+                const float m = ax * ax + ay * ay;
+                if (m > best) {
+                    best = m;
+                    bx = ax;
+                    by = ay;
+                    bk = kw;
+                }
+            }
+            // warp arg-max, ties → lowest window index
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                const float ox = __shfl_xor_sync(0xffffffffu, bx, o);
+                const float oy = __shfl_xor_sync(0xffffffffu, by, o);
+                if (ob > best || (ob == best && ok < bk)) {
+                    best = ob;
+                    bk = ok;
+                    bx = ox;
+                    by = oy;
+                }
+            }
+            if (best > 0.f) {
+                angle = atan2f(by, bx);
+                if (angle < 0.f) angle += kTwoPi;
+                if (angle >= kTwoPi) angle -= kTwoPi;
+            } else {
+                angle = 0.f;
+                flags = 1;
+            }
+            __syncwarp();  // done with the orientation buffers
+        }
+        // ---- M-SURF ----
+        float si, co;
+        sincosf(angle, &si, &co);
+        for (int s = lane; s < 576; s += 32) {
+            const int p = s / 24, q = s - p * 24;
+            const float u = (float)p - 11.5f, v = (float)q - 11.5f;
+            const float px = x + sigma * (u * co - v * si);
+            const float py = y + sigma * (u * si + v * co);
+            const float gx = bilinear(lx, g.W, g.H, g.P, px, py);
+            const float gy = bilinear(ly, g.W, g.H, g.P, px, py);
+            sx[s] = gx * co + gy * si;
+            sy[s] = -gx * si + gy * co;
+        }
+        __syncwarp();
+        const int sr = lane >> 1, half = lane & 1;
+        const int a = sr & 3, b = sr >> 2;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        for (int i = half; i < 9; i += 2) {
+            const int p = 5 * a + i;
+#pragma unroll
+            for (int j = 0; j < 9; ++j) {
+                const int q = 5 * b + j;
+                const float w = c_w1[i * 9 + j];
+                const float du = w * sx[p * 24 + q], dv = w * sy[p * 24 + q];
+                s0 += du;
+                s1 += dv;
+                s2 += fabsf(du);
+                s3 += fabsf(dv);
+            }
+        }
+        s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+        s3 += __shfl_xor_sync(0xffffffffu, s3, 1);
+        const float w2 = c_w2[sr];
+        s0 *= w2;
+        s1 *= w2;
+        s2 *= w2;
+        s3 *= w2;
+        float n2 = half == 0 ? s0 * s0 + s1 * s1 + s2 * s2 + s3 * s3 : 0.f;
+        for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        const float inv = n2 > 0.f ? rsqrtf(n2) : 0.f;
+        if (half == 0) {
+            float4 out = make_float4(s0 * inv, s1 * inv, s2 * inv, s3 * inv);
+            reinterpret_cast<float4*>(desc + ((size_t)img * cap + k) * 64)[sr] = out;
+        }
+        if (lane == 0 && !keep_angle) {
+            kp->angle = angle;
+            kp->flags = flags;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+void init_describe_tables() {
+    float u[kOriSamples], v[kOriSamples], w[kOriSamples];
+    int n = 0;
+    for (int vv = -6; vv <= 6; ++vv)
+        for (int uu = -6; uu <= 6; ++uu) {
+            if (uu * uu + vv * vv > 36) continue;
+            u[n] = (float)uu;
+            v[n] = (float)vv;
+            w[n] = (float)exp(-(double)(uu * uu + vv * vv) / 12.5);
+            ++n;
+        }
+    float w1[81], w2[16];
+    for (int i = 0; i < 9; ++i)
+        for (int j = 0; j < 9; ++j) w1[i * 9 + j] = (float)exp(-(double)((i - 4) * (i - 4) + (j - 4) * (j - 4)) / 12.5);
+    for (int b = 0; b < 4; ++b)
+        for (int a = 0; a < 4; ++a) w2[4 * b + a] = (float)exp(-((a - 1.5) * (a - 1.5) + (b - 1.5) * (b - 1.5)) / 4.5);
+    cudaMemcpyToSymbol(c_ori_u, u, sizeof(u));
+    cudaMemcpyToSymbol(c_ori_v, v, sizeof(v));
+    cudaMemcpyToSymbol(c_ori_w, w, sizeof(w));
+    cudaMemcpyToSymbol(c_w1, w1, sizeof(w1));
+    cudaMemcpyToSymbol(c_w2, w2, sizeof(w2));
+}
+
+void launch_describe(const float* Lx, const float* Ly, size_t img_stride, Geom g, int nimg, int N, kaze_keypoint* kps,
+                     const int* counts, int cap, float* desc, int nwin, int keep_angle, cudaStream_t s) {
+    (void)N;
+    k_describe<<<148 * 4, 256, 0, s>>>(Lx, Ly, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle);
+}
+
+}  // namespace kz

@@ -1,0 +1,212 @@
+// detect.cu — 3x3x3 extrema, edge test, 2-D sub-pixel fit and deterministic compaction (sm_100a).
+//
+// P:L207-214 and P:L263-281, readings A11-A13: a pixel (x, y) of level i in 1..N−2, at least one pixel from the
+// border, is a keypoint iff Ldet > threshold, Ldet is strictly greater than its 26 neighbours in levels i−1, i,
+// i+1, the Hessian of the response surface passes Det > 0 and Tr²/Det < (r+1)²/r (Eq. 12; Tr = Dxx + Dyy), and
+// the quadratic fit offset δ = −H⁻¹∇D has |δx|, |δy| <= 1.
+//
+// Compaction is deterministic and ordered by (level, y, x) without a sort:
+//   nms_mark : one CTA per (image, level, row) — warp ballots produce a 1-bit-per-pixel candidate bitmap and the
+//              row's candidate count;
+//   kp_scan  : one CTA per image — exclusive scan of the row counts → row offsets, total → d_counts;
+//   kp_emit  : one CTA per (image, level, row) — rank of each set bit = row offset + popcounts before it; the
+//              sub-pixel fit is re-evaluated (same fp32 code as the mark pass, so the same decision) and the
+//              32-byte keypoint is written if its rank is below the capacity.
+#include "kaze_internal.cuh"
+
+namespace kz {
+
+namespace {
+
+// Edge test + sub-pixel fit on the 3x3 patch D[r][c] (r = dy+1, c = dx+1).  Returns keep.
+__device__ __forceinline__ bool refine(const float (&D)[3][3], float edge_ratio, float& ox, float& oy) {
+    const float cv = D[1][1];
+    const float dxx = D[1][2] + D[1][0] - 2.f * cv;
+    const float dyy = D[2][1] + D[0][1] - 2.f * cv;
+    const float dxy = 0.25f * (D[2][2] + D[0][0] - D[0][2] - D[2][0]);
+    const float gx = 0.5f * (D[1][2] - D[1][0]);
+    const float gy = 0.5f * (D[2][1] - D[0][1]);
+    const float det = dxx * dyy - dxy * dxy;
+    if (edge_ratio > 0.f) {
+        const float tr = dxx + dyy;
+        if (!(det > 0.f)) return false;
+        if (!(tr * tr / det < (edge_ratio + 1.f) * (edge_ratio + 1.f) / edge_ratio)) return false;
+    }
+    if (fabsf(det) < 1e-12f) return false;
+    ox = -(dyy * gx - dxy * gy) / det;
+    oy = -(dxx * gy - dxy * gx) / det;
+    return fabsf(ox) <= 1.f && fabsf(oy) <= 1.f;
+}
+
+__device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const float* __restrict__ D0,
+                                            const float* __restrict__ Dp, int P, int x, int y, float thr, float er,
+                                            float& ox, float& oy, float& v) {
+    const size_t o = (size_t)y * P + x;
+    v = __ldg(D0 + o);
+    if (!(v > thr)) return false;
+    float patch[3][3];
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+            const size_t q = o + (ptrdiff_t)dy * P + dx;
+            float a = __ldg(Dm + q), c = __ldg(Dp + q);
+            if (!(v > a) || !(v > c)) return false;
+            if (dx != 0 || dy != 0) {
+                float b = __ldg(D0 + q);
+                if (!(v > b)) return false;
+                patch[dy + 1][dx + 1] = b;
+            }
+        }
+    patch[1][1] = v;
+    return refine(patch, er, ox, oy);
+}
+
+__global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
+                                                  DetectParams dp, uint32_t* __restrict__ bitmap,
+                                                  int* __restrict__ rowcnt) {
+    __shared__ int wcount[8];
+    const int y = blockIdx.x, li = blockIdx.y, level = li + 1, img = blockIdx.z;
+    const int words = (g.W + 31) / 32;
+    const float* D0 = Ldet + img * img_stride + (size_t)level * g.plane;
+    const float* Dm = D0 - g.plane;
+    const float* Dp = D0 + g.plane;
+    uint32_t* bm = bitmap + (((size_t)img * (N - 2) + li) * g.H + y) * words;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int cnt = 0;
+    const bool rowok = y >= 1 && y <= g.H - 2;
+    for (int w = warp; w < words; w += 8) {
+        const int x = w * 32 + lane;
+        bool k = false;
+        if (rowok && x >= 1 && x <= g.W - 2) {
+            float ox, oy, v;
+            k = is_keypoint(Dm, D0, Dp, g.P, x, y, dp.threshold, dp.edge_ratio, ox, oy, v);
+        }
+        const uint32_t bits = __ballot_sync(0xffffffffu, k);
+        if (lane == 0) bm[w] = bits;
+        cnt += __popc(bits);
+    }
+    if (lane == 0) wcount[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int i = 0; i < 8; ++i) t += wcount[i];
+        rowcnt[((size_t)img * (N - 2) + li) * g.H + y] = t;
+    }
+}
+
+// One CTA per image: exclusive scan of R row counts.
+__global__ void __launch_bounds__(1024) k_kp_scan(const int* __restrict__ rowcnt, int R, int* __restrict__ rowoff,
+                                                  int* __restrict__ counts) {
+    __shared__ int wsum[32];
+    const int img = blockIdx.x;
+    const int* rc = rowcnt + (size_t)img * R;
+    int* ro = rowoff + (size_t)img * R;
+    const int per = (R + blockDim.x - 1) / blockDim.x;
+    const int b = threadIdx.x * per, e = min(b + per, R);
+    int local = 0;
+    for (int i = b; i < e; ++i) local += rc[i];
+    // block exclusive scan of `local`
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        wsum[lane] = v;  // inclusive over warps
+    }
+    __syncthreads();
+    int run = incl - local + (warp > 0 ? wsum[warp - 1] : 0);
+    for (int i = b; i < e; ++i) {
+        ro[i] = run;
+        run += rc[i];
+    }
+    if (threadIdx.x == blockDim.x - 1) counts[img] = run;
+}
+
+__global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet, size_t img_stride, Geom g,
+                                                 LevelTable lt, DetectParams dp, const uint32_t* __restrict__ bitmap,
+                                                 const int* __restrict__ rowcnt, const int* __restrict__ rowoff,
+                                                 kaze_keypoint* __restrict__ kps) {
+    __shared__ int wpre[129];
+    const int N = lt.n;
+    const int y = blockIdx.x, li = blockIdx.y, level = li + 1, img = blockIdx.z;
+    const int words = (g.W + 31) / 32;
+    const size_t row = ((size_t)img * (N - 2) + li) * g.H + y;
+    const uint32_t* bm = bitmap + row * words;
+    if (rowcnt[row] == 0) return;
+    const int base = rowoff[row];
+    // word prefix (words <= 128 for W <= 4096; larger rows handled in passes of 128 words)
+    int carry = 0;
+    for (int w0 = 0; w0 < words; w0 += 128) {
+        const int nw = min(128, words - w0);
+        __syncthreads();
+        if (threadIdx.x < 32) {  // warp 0: exclusive prefix of word popcounts, 32 words per step
+            const int lane = threadIdx.x;
+            int r = carry;
+            for (int k0 = 0; k0 < nw; k0 += 32) {
+                const int c = (k0 + lane < nw) ? __popc(bm[w0 + k0 + lane]) : 0;
+                int incl = c;
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (k0 + lane < nw) wpre[k0 + lane] = r + incl - c;
+                r += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) wpre[128] = r;
+        }
+        __syncthreads();
+        const float* D0 = Ldet + img * img_stride + (size_t)level * g.plane;
+        for (int k = threadIdx.x; k < nw * 32; k += blockDim.x) {
+            const int w = k >> 5, bit = k & 31;
+            const uint32_t word = bm[w0 + w];
+            if (!((word >> bit) & 1u)) continue;
+            const int rank = base + wpre[w] + __popc(word & ((1u << bit) - 1u));
+            if (rank >= dp.cap) continue;
+            const int x = (w0 + w) * 32 + bit;
+            float ox = 0.f, oy = 0.f, v = 0.f;
+            is_keypoint(D0 - g.plane, D0, D0 + g.plane, g.P, x, y, dp.threshold, dp.edge_ratio, ox, oy, v);
+            kaze_keypoint kp;
+            kp.x = (float)x + ox;
+            kp.y = (float)y + oy;
+            kp.sigma = lt.sigma[level];
+            kp.response = v;
+            kp.angle = 0.f;
+            kp.level = level;
+            kp.octave = (int16_t)(level / lt.S);
+            kp.sublevel = (int16_t)(level % lt.S);
+            kp.flags = 0;
+            kps[(size_t)img * dp.cap + rank] = kp;
+        }
+        carry = wpre[128];
+    }
+}
+
+}  // namespace
+
+void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, int N, DetectParams dp, uint32_t* bitmap,
+                     int* rowcnt, cudaStream_t s) {
+    dim3 grid(g.H, N - 2, nimg);
+    k_nms_mark<<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, bitmap, rowcnt);
+}
+
+void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, int* counts, cudaStream_t s) {
+    k_kp_scan<<<nimg, 1024, 0, s>>>(rowcnt, rows_per_img, rowoff, counts);
+}
+
+void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
+                    const uint32_t* bitmap, const int* rowcnt, const int* rowoff, kaze_keypoint* kps, cudaStream_t s) {
+    dim3 grid(g.H, lt.n - 2, nimg);
+    k_kp_emit<<<grid, 256, 0, s>>>(Ldet, img_stride, g, lt, dp, bitmap, rowcnt, rowoff, kps);
+}
+
+}  // namespace kz

@@ -1,0 +1,685 @@
+// kaze_api.cu — the C ABI of include/kaze.h: context, arena, level schedule, orchestration of the sm_100a
+// kernels on the caller's stream, the pipelined host-buffer path, and per-kernel event profiling.
+//
+// Host-side arithmetic kept here (schedule, Gaussian taps, τ_i) is this product's own; it shares nothing with
+// oracle/ (DESIGN.md §2).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kaze_internal.cuh"
+
+using namespace kz;
+
+namespace {
+
+enum KernelClass {
+    KC_PREFILTER = 0,
+    KC_GRAD_L1,
+    KC_KHIST,
+    KC_KFINAL,
+    KC_C_FROM_G2,
+    KC_COND,
+    KC_AOS_COLS,
+    KC_AOS_ROWS,
+    KC_HESS_FIRST,
+    KC_HESS_DET,
+    KC_NMS_MARK,
+    KC_KP_SCAN,
+    KC_KP_EMIT,
+    KC_DESCRIBE,
+    KC_COUNT
+};
+const char* kKernelNames[KC_COUNT] = {"prefilter", "grad_l1",  "k_hist",   "k_final",  "c_from_g2",
+                                      "cond",      "aos_cols", "aos_rows", "hess_first", "hess_det",
+                                      "nms_mark",  "kp_scan",  "kp_emit",  "describe"};
+
+struct ProfRec {
+    int kc;
+    cudaEvent_t e0, e1;
+    double bytes;
+};
+
+}  // namespace
+
+struct kaze_ctx {
+    kaze_params p;
+    int device = 0;
+    int N = 0;
+    // schedule (host, double; A3/A9)
+    double sigma[kMaxLevels], t[kMaxLevels];
+    int step[kMaxLevels];
+    GaussTaps g0{}, g1{};
+    LevelTable lt{};
+    // arena
+    int Pmax = 0;
+    size_t plane_max = 0;
+    float *Lt = nullptr, *Lx = nullptr, *Ly = nullptr, *Ldet = nullptr, *cbuf = nullptr, *ubuf = nullptr;
+    float* kval = nullptr;
+    unsigned* hmax = nullptr;
+    int* hist = nullptr;
+    int* fallback = nullptr;
+    uint32_t* bitmap = nullptr;
+    int* rowcnt = nullptr;
+    int* rowoff = nullptr;
+    // current build
+    int n = 0, W = 0, H = 0;
+    Geom geom{};
+    size_t img_stride = 0;  // N * plane
+    bool built = false, detected = false;
+    cudaStream_t last_stream = nullptr;
+    // host path
+    float* hin[2] = {nullptr, nullptr};
+    kaze_keypoint* hkps[2] = {nullptr, nullptr};
+    int* hcnt[2] = {nullptr, nullptr};
+    float* hdesc[2] = {nullptr, nullptr};
+    int* pinned_counts = nullptr;  // 2 * max_batch
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_cnt[2] = {}, ev_d2h[2] = {};
+    // profiling
+    bool prof = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> pool;
+    int64_t launches = 0;
+    std::string err;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+cudaEvent_t get_event(kaze_ctx* c) {
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Wraps one kernel launch: counts it and, when profiling, brackets it with events on its stream.
+struct Launch {
+    kaze_ctx* c;
+    int kc;
+    double bytes;
+    cudaStream_t s;
+    cudaEvent_t e0 = nullptr;
+    Launch(kaze_ctx* c_, int kc_, double bytes_, cudaStream_t s_) : c(c_), kc(kc_), bytes(bytes_), s(s_) {
+        if (c->prof) {
+            e0 = get_event(c);
+            cudaEventRecord(e0, s);
+        }
+    }
+    ~Launch() {
+        c->launches++;
+        if (c->prof) {
+            cudaEvent_t e1 = get_event(c);
+            cudaEventRecord(e1, s);
+            c->recs.push_back({kc, e0, e1, bytes});
+        }
+    }
+};
+
+kaze_status cuda_fail(kaze_ctx* c, cudaError_t e, const char* where) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(e));
+    if (c) c->err = buf;
+    return KAZE_ERR_CUDA;
+}
+
+#define KZ_CHECK_LAUNCH(ctx, where)                              \
+    do {                                                         \
+        cudaError_t _e = cudaGetLastError();                     \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, where); \
+    } while (0)
+
+#define KZ_CUDA(ctx, call)                                        \
+    do {                                                          \
+        cudaError_t _e = (call);                                  \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call);  \
+    } while (0)
+
+GaussTaps make_taps(double sigma) {
+    GaussTaps t{};
+    int r = (int)std::ceil(3.0 * sigma);
+    if (r < 1) r = 1;
+    t.r = r;
+    double w[2 * kMaxGaussR + 1], s = 0.0;
+    for (int i = -r; i <= r; ++i) {
+        w[i + r] = std::exp(-(double)i * i / (2.0 * sigma * sigma));
+        s += w[i + r];
+    }
+    for (int i = 0; i <= 2 * r; ++i) t.w[i] = (float)(w[i] / s);
+    return t;
+}
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+kaze_status validate_params(const kaze_params* p) {
+    if (!p) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->octaves < 1 || p->sublevels < 1 || p->octaves * p->sublevels > kMaxLevels) return KAZE_ERR_INVALID_ARGUMENT;
+    if (!(p->sigma0 > 0) || p->sigma0 > kMaxGaussR / 3.0) return KAZE_ERR_INVALID_ARGUMENT;
+    if (!(p->k_percentile > 0 && p->k_percentile < 1)) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->k_bins < 1 || p->k_bins > kMaxBins) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->diffusivity != 1 && p->diffusivity != 2) return KAZE_ERR_INVALID_ARGUMENT;
+    if (!(p->threshold >= 0)) return KAZE_ERR_INVALID_ARGUMENT;
+    if (std::isnan(p->edge_ratio) || std::isnan(p->k_override)) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->max_keypoints < 1 || p->ori_windows < 1 || p->ori_windows > 64) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->max_batch < 1 || p->max_batch > kMaxBatch) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->max_width < 32 || p->max_height < 32) return KAZE_ERR_IMAGE_TOO_SMALL;
+    if (p->max_width > 8192 || p->max_height > 8192) return KAZE_ERR_INVALID_ARGUMENT;
+    return KAZE_OK;
+}
+
+void free_arena(kaze_ctx* c) {
+    void* ptrs[] = {c->Lt, c->Lx, c->Ly, c->Ldet, c->cbuf, c->ubuf, c->kval, c->hmax, c->hist, c->fallback,
+                    c->bitmap, c->rowcnt, c->rowoff, c->hin[0], c->hin[1], c->hkps[0], c->hkps[1],
+                    c->hcnt[0], c->hcnt[1], c->hdesc[0], c->hdesc[1]};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    if (c->pinned_counts) cudaFreeHost(c->pinned_counts);
+}
+
+size_t plane_of(int W, int H) { return (size_t)round_up(W, 32) * H; }
+
+// ---- the three steps, on one chunk of n <= max_batch images ----
+void set_geometry(kaze_ctx* c, int n, int w, int h) {
+    c->n = n;
+    c->W = w;
+    c->H = h;
+    c->geom.W = w;
+    c->geom.H = h;
+    c->geom.P = round_up(w, 32);
+    c->geom.plane = plane_of(w, h);
+    c->img_stride = (size_t)c->N * c->geom.plane;
+}
+
+// Step 1 (P:L255-260 with the AOS solver of Eq. 4): prefilter → k → N−1 × {conductivity, AOS columns, AOS rows}.
+kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int64_t pitch, cudaStream_t s) {
+    const int N = c->N;
+    set_geometry(c, n, w, h);
+    c->built = false;
+    c->detected = false;
+    const Geom g = c->geom;
+    const size_t SL = c->img_stride, SP = g.plane;  // pyramid stride, scratch stride
+    const double px = (double)w * h * n;
+    {
+        Launch L(c, KC_PREFILTER, 8.0 * px, s);
+        launch_prefilter(d_imgs, pitch, (size_t)pitch * h, c->Lt, SL, g, n, c->g0, s);
+    }
+    KZ_CHECK_LAUNCH(c, "prefilter");
+    const bool estimate = !(c->p.k_override > 0);
+    if (estimate) {
+        KZ_CUDA(c, cudaMemsetAsync(c->hmax, 0, sizeof(unsigned) * n, s));
+        KZ_CUDA(c, cudaMemsetAsync(c->hist, 0, sizeof(int) * (size_t)n * c->p.k_bins, s));
+        {
+            Launch L(c, KC_GRAD_L1, 8.0 * px, s);
+            launch_cond(c->Lt, SL, c->cbuf, SP, g, n, c->g1, 0, c->p.diffusivity, c->kval, c->hmax, s);
+        }
+        KZ_CHECK_LAUNCH(c, "grad_l1");
+        {
+            Launch L(c, KC_KHIST, 4.0 * px, s);
+            launch_khist(c->cbuf, SP, g, n, c->p.k_bins, c->hmax, c->hist, s);
+        }
+        KZ_CHECK_LAUNCH(c, "k_hist");
+    }
+    {
+        Launch L(c, KC_KFINAL, 0.0, s);
+        launch_kfinal(c->hist, c->p.k_bins, c->hmax, n, c->p.k_percentile, c->p.k_override, c->kval, c->fallback, s);
+    }
+    KZ_CHECK_LAUNCH(c, "k_final");
+    for (int i = 1; i < N; ++i) {
+        const float* prev = c->Lt + (size_t)(i - 1) * g.plane;
+        float* cur = c->Lt + (size_t)i * g.plane;
+        if (i == 1 && estimate) {
+            Launch L(c, KC_C_FROM_G2, 8.0 * px, s);
+            launch_c_from_g2(c->cbuf, SP, g, n, c->p.diffusivity, c->kval, s);
+        } else {
+            Launch L(c, KC_COND, 8.0 * px, s);
+            launch_cond(prev, SL, c->cbuf, SP, g, n, c->g1, 1, c->p.diffusivity, c->kval, nullptr, s);
+        }
+        KZ_CHECK_LAUNCH(c, "cond");
+        const float tau = (float)(c->t[i] - c->t[i - 1]);
+        const Strides st{SL, SP, SP, SL};
+        {
+            Launch L(c, KC_AOS_COLS, 12.0 * px, s);
+            if (!launch_aos_cols(prev, c->cbuf, c->ubuf, st, g, n, tau, s)) return KAZE_ERR_INVALID_ARGUMENT;
+        }
+        KZ_CHECK_LAUNCH(c, "aos_cols");
+        {
+            Launch L(c, KC_AOS_ROWS, 16.0 * px, s);
+            if (!launch_aos_rows(prev, c->cbuf, c->ubuf, cur, st, g, n, tau, s)) return KAZE_ERR_INVALID_ARGUMENT;
+        }
+        KZ_CHECK_LAUNCH(c, "aos_rows");
+    }
+    c->built = true;
+    c->last_stream = s;
+    return KAZE_OK;
+}
+
+// Step 2 (Eq. 8).
+kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cudaStream_t s) {
+    const int N = c->N, n = c->n;
+    const Geom g = c->geom;
+    const double px = (double)g.W * g.H * n;
+    {
+        Launch L(c, KC_HESS_FIRST, 12.0 * px * N, s);
+        launch_hess_first(c->Lt, c->Lx, c->Ly, c->img_stride, g, n, c->lt, s);
+    }
+    KZ_CHECK_LAUNCH(c, "hess_first");
+    {
+        Launch L(c, KC_HESS_DET, 12.0 * px * N, s);
+        launch_hess_det(c->Lx, c->Ly, c->Ldet, c->img_stride, g, n, c->lt, s);
+    }
+    KZ_CHECK_LAUNCH(c, "hess_det");
+    if (N < 3) {
+        KZ_CUDA(c, cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * n, s));
+    } else {
+        DetectParams dp{(float)c->p.threshold, (float)c->p.edge_ratio, c->p.max_keypoints};
+        {
+            Launch L(c, KC_NMS_MARK, 4.0 * px * N, s);
+            launch_nms_mark(c->Ldet, c->img_stride, g, n, N, dp, c->bitmap, c->rowcnt, s);
+        }
+        KZ_CHECK_LAUNCH(c, "nms_mark");
+        const int R = (N - 2) * g.H;
+        {
+            Launch L(c, KC_KP_SCAN, 8.0 * R * n, s);
+            launch_kp_scan(c->rowcnt, R, n, c->rowoff, d_counts, s);
+        }
+        KZ_CHECK_LAUNCH(c, "kp_scan");
+        {
+            Launch L(c, KC_KP_EMIT, 0.0, s);
+            launch_kp_emit(c->Ldet, c->img_stride, g, n, c->lt, dp, c->bitmap, c->rowcnt, c->rowoff, d_kps, s);
+        }
+        KZ_CHECK_LAUNCH(c, "kp_emit");
+    }
+    c->detected = true;
+    c->last_stream = s;
+    return KAZE_OK;
+}
+
+// Step 3.
+kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_counts, float* d_desc, cudaStream_t s) {
+    {
+        Launch L(c, KC_DESCRIBE, 0.0, s);
+        launch_describe(c->Lx, c->Ly, c->img_stride, c->geom, c->n, c->N, d_kps, d_counts, c->p.max_keypoints, d_desc,
+                        c->p.ori_windows, (c->p.flags & KAZE_FLAG_KEEP_ANGLE) ? 1 : 0, s);
+    }
+    KZ_CHECK_LAUNCH(c, "describe");
+    c->last_stream = s;
+    return KAZE_OK;
+}
+
+kaze_status check_dims(const kaze_ctx* c, int n, int w, int h, int64_t pitch) {
+    if (n < 1 || n > c->p.max_batch) return KAZE_ERR_INVALID_ARGUMENT;
+    if (w < 32 || h < 32 || w > c->p.max_width || h > c->p.max_height) return KAZE_ERR_IMAGE_TOO_SMALL;
+    if (pitch < w) return KAZE_ERR_INVALID_ARGUMENT;
+    return KAZE_OK;
+}
+
+kaze_status ensure_host_path(kaze_ctx* c) {
+    if (c->s_h2d) return KAZE_OK;
+    const int B = c->p.max_batch;
+    const size_t cap = (size_t)c->p.max_keypoints;
+    for (int b = 0; b < 2; ++b) {
+        if (cudaMalloc(&c->hin[b], sizeof(float) * c->plane_max * B) != cudaSuccess) return KAZE_ERR_OOM;
+        if (cudaMalloc(&c->hkps[b], sizeof(kaze_keypoint) * cap * B) != cudaSuccess) return KAZE_ERR_OOM;
+        if (cudaMalloc(&c->hcnt[b], sizeof(int) * B) != cudaSuccess) return KAZE_ERR_OOM;
+        if (cudaMalloc(&c->hdesc[b], sizeof(float) * 64 * cap * B) != cudaSuccess) return KAZE_ERR_OOM;
+        KZ_CUDA(c, cudaEventCreateWithFlags(&c->ev_h2d[b], cudaEventDisableTiming));
+        KZ_CUDA(c, cudaEventCreateWithFlags(&c->ev_comp[b], cudaEventDisableTiming));
+        KZ_CUDA(c, cudaEventCreateWithFlags(&c->ev_cnt[b], cudaEventDisableTiming));
+        KZ_CUDA(c, cudaEventCreateWithFlags(&c->ev_d2h[b], cudaEventDisableTiming));
+    }
+    if (cudaMallocHost(&c->pinned_counts, sizeof(int) * 2 * B) != cudaSuccess) return KAZE_ERR_OOM;
+    KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    return KAZE_OK;
+}
+
+}  // namespace
+
+// =====================================================================================================================
+extern "C" {
+
+kaze_status kaze_default_params(kaze_params* p) {
+    if (!p) return KAZE_ERR_INVALID_ARGUMENT;
+    memset(p, 0, sizeof(*p));
+    p->max_width = 1920;
+    p->max_height = 1200;
+    p->max_batch = 1;
+    p->octaves = 4;
+    p->sublevels = 4;
+    p->sigma0 = 1.6;
+    p->k_percentile = 0.7;
+    p->k_bins = 300;
+    p->diffusivity = 2;
+    p->k_override = 0.0;
+    p->threshold = 1e-3;
+    p->edge_ratio = 10.0;
+    p->max_keypoints = 65536;
+    p->ori_windows = 42;
+    p->flags = 0;
+    return KAZE_OK;
+}
+
+int32_t kaze_abi_version(void) { return KAZE_ABI_VERSION; }
+
+kaze_status kaze_create(const kaze_params* p, int device, kaze_ctx** out) {
+    if (!out) return KAZE_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    kaze_status st = validate_params(p);
+    if (st != KAZE_OK) return st;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return KAZE_ERR_CUDA;
+    DeviceGuard guard(device);
+    kaze_ctx* c = new kaze_ctx();
+    c->p = *p;
+    c->device = device;
+    c->N = p->octaves * p->sublevels;
+    // Eq. 6 read as σ_i = σ0·2^{o + s/S} (A3), Eq. 7 t_i = σ_i²/2, s_i = max(1, floor(σ_i + ½)) (A9)
+    for (int o = 0; o < p->octaves; ++o)
+        for (int sl = 0; sl < p->sublevels; ++sl) {
+            const int i = o * p->sublevels + sl;
+            c->sigma[i] = p->sigma0 * std::pow(2.0, (double)o + (double)sl / p->sublevels);
+            c->t[i] = 0.5 * c->sigma[i] * c->sigma[i];
+            const int stp = (int)std::floor(c->sigma[i] + 0.5);
+            c->step[i] = stp < 1 ? 1 : stp;
+            c->lt.step[i] = c->step[i];
+            c->lt.sigma[i] = (float)c->sigma[i];
+        }
+    c->lt.n = c->N;
+    c->lt.S = p->sublevels;
+    c->g0 = make_taps(p->sigma0);
+    c->g1 = make_taps(1.0);
+    c->Pmax = round_up(p->max_width, 32);
+    c->plane_max = (size_t)c->Pmax * p->max_height;
+    const size_t B = p->max_batch, N = c->N;
+    const size_t pyr = sizeof(float) * c->plane_max * N * B;
+    const int words = (p->max_width + 31) / 32;
+    const size_t rows = (size_t)(N > 2 ? N - 2 : 1) * p->max_height * B;
+    bool ok = cudaMalloc(&c->Lt, pyr) == cudaSuccess && cudaMalloc(&c->Lx, pyr) == cudaSuccess &&
+              cudaMalloc(&c->Ly, pyr) == cudaSuccess && cudaMalloc(&c->Ldet, pyr) == cudaSuccess &&
+              cudaMalloc(&c->cbuf, sizeof(float) * c->plane_max * B) == cudaSuccess &&
+              cudaMalloc(&c->ubuf, sizeof(float) * c->plane_max * B) == cudaSuccess &&
+              cudaMalloc(&c->kval, sizeof(float) * B) == cudaSuccess &&
+              cudaMalloc(&c->hmax, sizeof(unsigned) * B) == cudaSuccess &&
+              cudaMalloc(&c->hist, sizeof(int) * B * p->k_bins) == cudaSuccess &&
+              cudaMalloc(&c->fallback, sizeof(int) * B) == cudaSuccess &&
+              cudaMalloc(&c->bitmap, sizeof(uint32_t) * rows * words) == cudaSuccess &&
+              cudaMalloc(&c->rowcnt, sizeof(int) * rows) == cudaSuccess &&
+              cudaMalloc(&c->rowoff, sizeof(int) * rows) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        free_arena(c);
+        delete c;
+        return KAZE_ERR_OOM;
+    }
+    cudaMemset(c->hist, 0, sizeof(int) * B * p->k_bins);
+    cudaMemset(c->hmax, 0, sizeof(unsigned) * B);
+    init_describe_tables();
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        free_arena(c);
+        delete c;
+        return KAZE_ERR_CUDA;
+    }
+    *out = c;
+    return KAZE_OK;
+}
+
+kaze_status kaze_destroy(kaze_ctx* c) {
+    if (!c) return KAZE_OK;
+    DeviceGuard guard(c->device);
+    cudaDeviceSynchronize();
+    for (auto& r : c->recs) {
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+    }
+    for (auto e : c->pool) cudaEventDestroy(e);
+    for (int b = 0; b < 2; ++b) {
+        if (c->ev_h2d[b]) cudaEventDestroy(c->ev_h2d[b]);
+        if (c->ev_comp[b]) cudaEventDestroy(c->ev_comp[b]);
+        if (c->ev_cnt[b]) cudaEventDestroy(c->ev_cnt[b]);
+        if (c->ev_d2h[b]) cudaEventDestroy(c->ev_d2h[b]);
+    }
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    free_arena(c);
+    delete c;
+    return KAZE_OK;
+}
+
+kaze_status kaze_build_scale_space(kaze_ctx* c, const float* d_imgs, int32_t n, int32_t w, int32_t h,
+                                   int64_t pitch, void* stream) {
+    if (!c || !d_imgs) return KAZE_ERR_INVALID_ARGUMENT;
+    kaze_status st = check_dims(c, n, w, h, pitch);
+    if (st != KAZE_OK) return st;
+    DeviceGuard guard(c->device);
+    return do_build(c, d_imgs, n, w, h, pitch, (cudaStream_t)stream);
+}
+
+kaze_status kaze_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, void* stream) {
+    if (!c || !d_kps || !d_counts) return KAZE_ERR_INVALID_ARGUMENT;
+    if (!c->built) return KAZE_ERR_STATE;
+    DeviceGuard guard(c->device);
+    return do_detect(c, d_kps, d_counts, (cudaStream_t)stream);
+}
+
+kaze_status kaze_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_counts, float* d_desc, void* stream) {
+    if (!c || !d_kps || !d_counts || !d_desc) return KAZE_ERR_INVALID_ARGUMENT;
+    if (!c->built) return KAZE_ERR_STATE;
+    DeviceGuard guard(c->device);
+    return do_describe(c, d_kps, d_counts, d_desc, (cudaStream_t)stream);
+}
+
+kaze_status kaze_extract(kaze_ctx* c, const float* d_imgs, int32_t n, int32_t w, int32_t h, int64_t pitch,
+                         kaze_keypoint* d_kps, int32_t* d_counts, float* d_desc, void* stream) {
+    if (!c || (n > 0 && (!d_imgs || !d_kps || !d_counts || !d_desc)) || n < 0) return KAZE_ERR_INVALID_ARGUMENT;
+    if (n == 0) return KAZE_OK;
+    kaze_status st = check_dims(c, 1, w, h, pitch);
+    if (st != KAZE_OK) return st;
+    DeviceGuard guard(c->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t cap = (size_t)c->p.max_keypoints;
+    for (int i0 = 0; i0 < n; i0 += c->p.max_batch) {
+        const int m = n - i0 < c->p.max_batch ? n - i0 : c->p.max_batch;
+        st = do_build(c, d_imgs + (size_t)i0 * pitch * h, m, w, h, pitch, s);
+        if (st != KAZE_OK) return st;
+        st = do_detect(c, d_kps + i0 * cap, d_counts + i0, s);
+        if (st != KAZE_OK) return st;
+        st = do_describe(c, d_kps + i0 * cap, d_counts + i0, d_desc + i0 * cap * 64, s);
+        if (st != KAZE_OK) return st;
+    }
+    return KAZE_OK;
+}
+
+kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32_t w, int32_t h, int64_t pitch,
+                              kaze_keypoint* h_kps, int32_t* h_counts, float* h_desc, void* stream) {
+    if (!c || n < 0 || (n > 0 && (!h_imgs || !h_kps || !h_counts))) return KAZE_ERR_INVALID_ARGUMENT;
+    if (n == 0) return KAZE_OK;
+    kaze_status st = check_dims(c, 1, w, h, pitch);
+    if (st != KAZE_OK) return st;
+    DeviceGuard guard(c->device);
+    st = ensure_host_path(c);
+    if (st != KAZE_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int B = c->p.max_batch;
+    const size_t cap = (size_t)c->p.max_keypoints;
+    const int P = round_up(w, 32);
+    const int nchunks = (n + B - 1) / B;
+    // Make the context's copy streams start after prior work on the caller's stream.
+    KZ_CUDA(c, cudaEventRecord(c->ev_comp[0], s));
+    KZ_CUDA(c, cudaStreamWaitEvent(c->s_h2d, c->ev_comp[0], 0));
+    auto finalize = [&](int j) -> kaze_status {
+        const int b = j & 1, i0 = j * B, m = (n - i0 < B) ? n - i0 : B;
+        KZ_CUDA(c, cudaEventSynchronize(c->ev_cnt[b]));
+        const int* cnt = c->pinned_counts + b * B;
+        for (int i = 0; i < m; ++i) {
+            h_counts[i0 + i] = cnt[i];
+            const size_t nk = (size_t)(cnt[i] < (int)cap ? cnt[i] : (int)cap);
+            if (nk == 0) continue;
+            KZ_CUDA(c, cudaMemcpyAsync(h_kps + (size_t)(i0 + i) * cap, c->hkps[b] + (size_t)i * cap,
+                                       nk * sizeof(kaze_keypoint), cudaMemcpyDeviceToHost, c->s_d2h));
+            if (h_desc)
+                KZ_CUDA(c, cudaMemcpyAsync(h_desc + (size_t)(i0 + i) * cap * 64, c->hdesc[b] + (size_t)i * cap * 64,
+                                           nk * 64 * sizeof(float), cudaMemcpyDeviceToHost, c->s_d2h));
+        }
+        KZ_CUDA(c, cudaEventRecord(c->ev_d2h[b], c->s_d2h));
+        return KAZE_OK;
+    };
+    for (int j = 0; j < nchunks; ++j) {
+        const int b = j & 1, i0 = j * B, m = (n - i0 < B) ? n - i0 : B;
+        // H2D of chunk j into buffer b, once the compute of chunk j-2 stopped reading it
+        if (j >= 2) KZ_CUDA(c, cudaStreamWaitEvent(c->s_h2d, c->ev_comp[b], 0));
+        KZ_CUDA(c, cudaMemcpy2DAsync(c->hin[b], sizeof(float) * P, h_imgs + (size_t)i0 * pitch * h,
+                                     sizeof(float) * pitch, sizeof(float) * w, (size_t)m * h, cudaMemcpyHostToDevice,
+                                     c->s_h2d));
+        KZ_CUDA(c, cudaEventRecord(c->ev_h2d[b], c->s_h2d));
+        KZ_CUDA(c, cudaStreamWaitEvent(s, c->ev_h2d[b], 0));
+        if (j >= 2) KZ_CUDA(c, cudaStreamWaitEvent(s, c->ev_d2h[b], 0));
+        st = do_build(c, c->hin[b], m, w, h, P, s);
+        if (st != KAZE_OK) return st;
+        KZ_CUDA(c, cudaEventRecord(c->ev_comp[b], s));  // input buffer b free after the build... conservatively here
+        st = do_detect(c, c->hkps[b], c->hcnt[b], s);
+        if (st != KAZE_OK) return st;
+        st = do_describe(c, c->hkps[b], c->hcnt[b], c->hdesc[b], s);
+        if (st != KAZE_OK) return st;
+        KZ_CUDA(c, cudaMemcpyAsync(c->pinned_counts + b * B, c->hcnt[b], sizeof(int) * m, cudaMemcpyDeviceToHost, s));
+        KZ_CUDA(c, cudaEventRecord(c->ev_cnt[b], s));
+        KZ_CUDA(c, cudaStreamWaitEvent(c->s_d2h, c->ev_cnt[b], 0));
+        if (j >= 1) {
+            st = finalize(j - 1);
+            if (st != KAZE_OK) return st;
+        }
+    }
+    st = finalize(nchunks - 1);
+    if (st != KAZE_OK) return st;
+    KZ_CUDA(c, cudaStreamSynchronize(c->s_d2h));
+    return KAZE_OK;
+}
+
+kaze_status kaze_get_k(kaze_ctx* c, float* h_k, int32_t* h_fallback) {
+    if (!c || !h_k) return KAZE_ERR_INVALID_ARGUMENT;
+    if (!c->built) return KAZE_ERR_STATE;
+    DeviceGuard guard(c->device);
+    KZ_CUDA(c, cudaStreamSynchronize(c->last_stream));
+    KZ_CUDA(c, cudaMemcpy(h_k, c->kval, sizeof(float) * c->n, cudaMemcpyDeviceToHost));
+    if (h_fallback) KZ_CUDA(c, cudaMemcpy(h_fallback, c->fallback, sizeof(int) * c->n, cudaMemcpyDeviceToHost));
+    return KAZE_OK;
+}
+
+static kaze_status plane_ptr(kaze_ctx* c, int32_t img, int32_t level, int32_t which, float** out) {
+    if (!c->built) return KAZE_ERR_STATE;
+    if (img < 0 || img >= c->n) return KAZE_ERR_INVALID_ARGUMENT;
+    if (which != KAZE_PLANE_COND && (level < 0 || level >= c->N)) return KAZE_ERR_INVALID_ARGUMENT;
+    const size_t off = (size_t)img * c->img_stride + (size_t)level * c->geom.plane;
+    switch (which) {
+        case KAZE_PLANE_LT: *out = c->Lt + off; break;
+        case KAZE_PLANE_LX: *out = c->Lx + off; break;
+        case KAZE_PLANE_LY: *out = c->Ly + off; break;
+        case KAZE_PLANE_LDET: *out = c->Ldet + off; break;
+        case KAZE_PLANE_COND: *out = c->cbuf + (size_t)img * c->geom.plane; break;
+        default: return KAZE_ERR_INVALID_ARGUMENT;
+    }
+    return KAZE_OK;
+}
+
+kaze_status kaze_get_level(kaze_ctx* c, int32_t img, int32_t level, int32_t which, float* d_out, void* stream) {
+    if (!c || !d_out) return KAZE_ERR_INVALID_ARGUMENT;
+    float* src = nullptr;
+    kaze_status st = plane_ptr(c, img, level, which, &src);
+    if (st != KAZE_OK) return st;
+    DeviceGuard guard(c->device);
+    KZ_CUDA(c, cudaMemcpy2DAsync(d_out, sizeof(float) * c->W, src, sizeof(float) * c->geom.P, sizeof(float) * c->W,
+                                 c->H, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return KAZE_OK;
+}
+
+kaze_status kaze_set_level(kaze_ctx* c, int32_t img, int32_t level, int32_t which, const float* d_in, void* stream) {
+    if (!c || !d_in) return KAZE_ERR_INVALID_ARGUMENT;
+    float* dst = nullptr;
+    kaze_status st = plane_ptr(c, img, level, which, &dst);
+    if (st != KAZE_OK) return st;
+    DeviceGuard guard(c->device);
+    KZ_CUDA(c, cudaMemcpy2DAsync(dst, sizeof(float) * c->geom.P, d_in, sizeof(float) * c->W, sizeof(float) * c->W,
+                                 c->H, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return KAZE_OK;
+}
+
+kaze_status kaze_set_profiling(kaze_ctx* c, int32_t enable) {
+    if (!c) return KAZE_ERR_INVALID_ARGUMENT;
+    c->prof = enable != 0;
+    return KAZE_OK;
+}
+
+kaze_status kaze_reset_profile(kaze_ctx* c) {
+    if (!c) return KAZE_ERR_INVALID_ARGUMENT;
+    DeviceGuard guard(c->device);
+    for (auto& r : c->recs) {
+        c->pool.push_back(r.e0);
+        c->pool.push_back(r.e1);
+    }
+    c->recs.clear();
+    c->launches = 0;
+    return KAZE_OK;
+}
+
+kaze_status kaze_get_profile(kaze_ctx* c, kaze_kernel_stat* out, int32_t cap, int32_t* n) {
+    if (!c || !n || (cap > 0 && !out)) return KAZE_ERR_INVALID_ARGUMENT;
+    DeviceGuard guard(c->device);
+    KZ_CUDA(c, cudaDeviceSynchronize());
+    kaze_kernel_stat acc[KC_COUNT];
+    memset(acc, 0, sizeof(acc));
+    for (int k = 0; k < KC_COUNT; ++k) snprintf(acc[k].name, sizeof(acc[k].name), "%s", kKernelNames[k]);
+    for (auto& r : c->recs) {
+        float ms = 0.f;
+        KZ_CUDA(c, cudaEventElapsedTime(&ms, r.e0, r.e1));
+        acc[r.kc].launches += 1;
+        acc[r.kc].total_ms += ms;
+        acc[r.kc].algo_bytes += r.bytes;
+    }
+    int m = 0;
+    for (int k = 0; k < KC_COUNT; ++k) {
+        if (acc[k].launches == 0) continue;
+        if (m < cap) out[m] = acc[k];
+        ++m;
+    }
+    *n = m;
+    return KAZE_OK;
+}
+
+int64_t kaze_launch_count(const kaze_ctx* c) { return c ? c->launches : 0; }
+
+
+const char* kaze_status_string(kaze_status s) {
+    switch (s) {
+        case KAZE_OK: return "ok";
+        case KAZE_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case KAZE_ERR_IMAGE_TOO_SMALL: return "image too small (or larger than the context maxima)";
+        case KAZE_ERR_CAPACITY: return "capacity";
+        case KAZE_ERR_STATE: return "call out of order (build -> detect -> describe)";
+        case KAZE_ERR_CUDA: return "CUDA error";
+        case KAZE_ERR_OOM: return "device out of memory";
+    }
+    return "unknown status";
+}
+
+const char* kaze_last_error(const kaze_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+}  // extern "C"

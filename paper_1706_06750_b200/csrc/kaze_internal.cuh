@@ -1,0 +1,87 @@
+// kaze_internal.cuh — shared declarations of the sm_100a KAZE kernels and their launchers.
+// Product code: nothing here is shared with oracle/ (DESIGN.md §2).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/kaze.h"
+
+namespace kz {
+
+constexpr int kMaxLevels = 64;
+constexpr int kMaxGaussR = 24;   // sigma0 <= 8
+constexpr int kMaxBins = 4096;
+constexpr int kMaxBatch = 1024;
+
+// Plane geometry of one build: W x H pixels, pitch P floats (multiple of 32), plane = P * H.
+struct Geom {
+    int W, H, P;
+    size_t plane;
+};
+
+struct GaussTaps {
+    int r;
+    float w[2 * kMaxGaussR + 1];
+};
+
+struct LevelTable {          // per-level scalars passed by value to whole-pyramid kernels
+    int n;                   // number of levels N
+    int S;                   // sublevels
+    int step[kMaxLevels];    // s_i (Eq. 8 derivative step, A9)
+    float sigma[kMaxLevels]; // σ_i
+};
+
+// ---- stencil.cu ----
+void launch_prefilter(const float* img, int64_t in_pitch, size_t in_img_stride, float* L0,
+                      size_t out_img_stride, Geom g, int nimg, const GaussTaps& t, cudaStream_t s);
+// mode 0: write |grad|^2 to out and max|grad| over the interior to hmax_bits[img];
+// mode 1: write the conductivity g(|grad|^2 / k^2) to out (k from kval[img]).
+void launch_cond(const float* L, size_t in_img_stride, float* out, size_t out_img_stride, Geom g, int nimg,
+                 const GaussTaps& t1, int mode, int diffusivity, const float* kval, unsigned* hmax_bits,
+                 cudaStream_t s);
+void launch_khist(const float* g2, size_t img_stride, Geom g, int nimg, int bins, const unsigned* hmax_bits,
+                  int* hist, cudaStream_t s);
+void launch_kfinal(const int* hist, int bins, const unsigned* hmax_bits, int nimg, double perc, double k_override,
+                   float* kval, int* fallback, cudaStream_t s);
+void launch_c_from_g2(float* buf, size_t img_stride, Geom g, int nimg, int diffusivity, const float* kval,
+                      cudaStream_t s);
+
+// ---- aos.cu ----
+struct Strides {  // per-image strides (floats) of the four buffers an AOS pass touches
+    size_t L, c, U, out;
+};
+// U = column solves of (I - 2 tau A_y(c)) U = L
+bool launch_aos_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau,
+                     cudaStream_t s);
+// Lout = 0.5 (U + V), V = row solves of (I - 2 tau A_x(c)) V = L
+bool launch_aos_rows(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg,
+                     float tau, cudaStream_t s);
+
+// ---- hessian.cu ----  (all N levels of nimg images in one launch; level stride = plane)
+void launch_hess_first(const float* Lt, float* Lx, float* Ly, size_t img_stride, Geom g, int nimg,
+                       const LevelTable& lt, cudaStream_t s);
+void launch_hess_det(const float* Lx, const float* Ly, float* Ldet, size_t img_stride, Geom g, int nimg,
+                     const LevelTable& lt, cudaStream_t s);
+
+// ---- detect.cu ----
+struct DetectParams {
+    float threshold;
+    float edge_ratio;
+    int cap;
+};
+void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, int N, DetectParams dp,
+                     uint32_t* bitmap, int* rowcnt, cudaStream_t s);
+void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, int* counts, cudaStream_t s);
+void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
+                    DetectParams dp, const uint32_t* bitmap, const int* rowcnt, const int* rowoff, kaze_keypoint* kps,
+                    cudaStream_t s);
+
+// ---- describe.cu ----
+void init_describe_tables();
+void launch_describe(const float* Lx, const float* Ly, size_t img_stride, Geom g, int nimg, int N,
+                     kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
+                     cudaStream_t s);
+
+__host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+}  // namespace kz

@@ -1,0 +1,322 @@
+"""GPU-vs-oracle parity through the C ABI (needs a B200).
+
+Tolerances (BASELINE north_star):
+  * evolution images: max|L_gpu − L_ref| / max|L_ref| <= 1e-4 per level, with k injected (k_override);
+  * k: the same histogram bin (relative difference far below one bin width);
+  * keypoints: >= 99% of oracle keypoints have a GPU keypoint within 0.5 px and |Δlevel| <= 1, and vice versa;
+  * descriptors: matched pairs cos >= 0.999 (>= 99% end to end; 100% stage-isolated with pinned keypoints/angles).
+Inputs: the seeded generator (kaze_inputs), at sizes that span several tiles and a ragged tail.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import kaze_inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1706_06750_b200 as K  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def O(oracle_lib):
+    return oracle_lib
+
+
+_cache = {}
+
+
+def oracle_run(O, w, h, seed=kaze_inputs.BASE_SEED, **kw):
+    key = (w, h, seed, tuple(sorted(kw.items())))
+    if key not in _cache:
+        img = kaze_inputs.synth_image(w, h, seed)
+        _cache[key] = (img, O.run(img, want_levels=True, **kw))
+    return _cache[key]
+
+
+def gpu_levels(kz, n_levels, which=K.PLANE_LT, img=0):
+    H, W = kz.last_hw
+    out = torch.empty((n_levels, H, W), device="cuda")
+    for i in range(n_levels):
+        K.kaze_get_level(kz.ctx, img, i, which, out[i])
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+def make(w, h, batch=1, **kw):
+    kz = K.Kaze(w, h, batch=batch, **kw)
+    kz.last_hw = (h, w)
+    return kz
+
+
+def match_keypoints(a, b, tol=0.5):
+    """Fraction of a's keypoints with a b keypoint within tol px and |Δlevel| <= 1; and the index map."""
+    if len(a) == 0:
+        return 1.0, np.zeros(0, int)
+    bx, by, bl = b["x"].astype(np.float64), b["y"].astype(np.float64), b["level"].astype(np.int64)
+    idx = np.full(len(a), -1)
+    order = np.argsort(bx)
+    sx = bx[order]
+    for j, k in enumerate(a):
+        lo, hi = np.searchsorted(sx, k["x"] - tol), np.searchsorted(sx, k["x"] + tol)
+        cand = order[lo:hi]
+        if len(cand) == 0:
+            continue
+        d = np.hypot(bx[cand] - k["x"], by[cand] - k["y"])
+        ok = (d <= tol) & (np.abs(bl[cand] - int(k["level"])) <= 1)
+        if ok.any():
+            c = cand[ok]
+            d = d[ok]
+            # prefer the same level, then the nearest
+            same = bl[c] == int(k["level"])
+            pick = c[same][np.argmin(d[same])] if same.any() else c[np.argmin(d)]
+            idx[j] = pick
+    return float(np.mean(idx >= 0)), idx
+
+
+def rel_err(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+# ------------------------------------------------------------------------------------------- scale space
+@pytest.mark.parametrize("w,h,O_,S_", [(640, 480, 4, 4), (128, 128, 2, 2), (333, 257, 3, 4), (64, 48, 2, 3)])
+def test_scale_space_levels_with_injected_k(O, w, h, O_, S_):
+    img, ref = oracle_run(O, w, h, octaves=O_, sublevels=S_)
+    kz = make(w, h, octaves=O_, sublevels=S_, k_override=ref["k"])
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    lv = gpu_levels(kz, O_ * S_)
+    assert rel_err(lv[0], ref["levels"][0]) < 2e-6  # prefilter
+    for i in range(O_ * S_):
+        assert rel_err(lv[i], ref["levels"][i]) <= 1e-4, (i, rel_err(lv[i], ref["levels"][i]))
+    # every AOS step preserves the mean (P8), on the GPU too
+    for i in range(1, O_ * S_):
+        assert abs(lv[i].mean() / lv[i - 1].mean() - 1) < 1e-5
+    kz.close()
+
+
+@pytest.mark.parametrize("w,h,seed", [(640, 480, 1234), (640, 480, 1235), (333, 257, 77), (128, 128, 1234)])
+def test_contrast_k_same_bin(O, w, h, seed):
+    img, ref = oracle_run(O, w, h, seed=seed, octaves=2, sublevels=2)
+    kz = make(w, h, octaves=2, sublevels=2)
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    k, fb = K.kaze_get_k(kz.ctx, 1)
+    # k = hmax (b+1)/300: the same bin b means a relative difference at the fp32 rounding level of hmax
+    assert abs(k[0] / ref["k"] - 1) < 1e-5, (k[0], ref["k"])
+    assert fb[0] == 0
+    kz.close()
+
+
+def test_conductivity_plane(O):
+    img, ref = oracle_run(O, 333, 257, octaves=3, sublevels=4)
+    kz = make(333, 257, octaves=3, sublevels=4, k_override=ref["k"])
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    c = torch.empty((257, 333), device="cuda")
+    K.kaze_get_level(kz.ctx, 0, 0, K.PLANE_COND, c)
+    cref = O.conductivity(ref["levels"][-2], ref["k"], 2)  # the last built level's conductivity
+    assert np.max(np.abs(c.cpu().numpy() - cref)) < 2e-5
+    kz.close()
+
+
+def test_batch_in_grid_equals_single_images(O):
+    imgs = np.stack([kaze_inputs.synth_image(200, 150, s) for s in (5, 6, 7)])
+    kz = make(200, 150, batch=3, octaves=3, sublevels=3)
+    kps, counts, desc = kz.extract(torch.from_numpy(imgs).cuda())
+    single = make(200, 150, batch=1, octaves=3, sublevels=3)
+    for i in range(3):
+        k1, c1, d1 = single.extract(torch.from_numpy(imgs[i:i + 1]).cuda())
+        assert int(c1[0]) == int(counts[i])
+        n = int(c1[0])
+        assert torch.equal(kps[i, :n], k1[0, :n])
+        assert torch.equal(desc[i, :n], d1[0, :n])
+    kz.close()
+    single.close()
+
+
+# ------------------------------------------------------------------------------------------- detector
+def test_hessian_stage_isolated(O):
+    """Oracle levels (as fp32) injected through kaze_set_level; Lx, Ly, Ldet vs the oracle Hessian of the same."""
+    img, ref = oracle_run(O, 333, 257, octaves=3, sublevels=4)
+    kz = make(333, 257, octaves=3, sublevels=4, k_override=ref["k"])
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    lv32 = ref["levels"].astype(np.float32)
+    for i in range(12):
+        K.kaze_set_level(kz.ctx, 0, i, K.PLANE_LT, torch.from_numpy(lv32[i]).cuda())
+    kps = torch.zeros((1, kz.cap, 8), dtype=torch.int32, device="cuda")
+    counts = torch.zeros(1, dtype=torch.int32, device="cuda")
+    K.kaze_detect(kz.ctx, kps, counts)
+    sg, _, st = O.schedule(3, 4, 1.6)
+    Lx, Ly, Ld = gpu_levels(kz, 12, K.PLANE_LX), gpu_levels(kz, 12, K.PLANE_LY), gpu_levels(kz, 12, K.PLANE_LDET)
+    for i in range(12):
+        rx, ry, rd = O.hessian(lv32[i].astype(np.float64), int(st[i]))
+        assert rel_err(Lx[i], rx) < 1e-5 and rel_err(Ly[i], ry) < 1e-5
+        assert rel_err(Ld[i], rd) < 1e-4, (i, rel_err(Ld[i], rd))
+    # detection on identical (fp32) responses: the keypoint set equals the oracle's extrema of the GPU's own Ldet
+    kref, nref = O.extrema(Ld, 4, sg)
+    got = K.Kaze.keypoints_numpy(kps, counts)[0]
+    frac, _ = match_keypoints(kref, got, tol=1e-3)
+    assert abs(int(counts[0]) - nref) <= max(2, 0.002 * nref) and frac >= 0.995
+    kz.close()
+
+
+@pytest.mark.parametrize("w,h,O_,S_", [(640, 480, 4, 4), (128, 128, 2, 2), (333, 257, 3, 4)])
+def test_keypoints_end_to_end(O, w, h, O_, S_):
+    img, ref = oracle_run(O, w, h, octaves=O_, sublevels=S_)
+    kz = make(w, h, octaves=O_, sublevels=S_)
+    kps, counts, desc = kz.extract(torch.from_numpy(img).cuda()[None])
+    got = K.Kaze.keypoints_numpy(kps, counts)[0]
+    assert ref["count"] > 0
+    f1, idx = match_keypoints(ref["kps"], got)
+    f2, _ = match_keypoints(got, ref["kps"])
+    assert f1 >= 0.99 and f2 >= 0.99, (f1, f2, ref["count"], int(counts[0]))
+    # deterministic order (level, y, x)
+    key = got["level"].astype(np.int64) * 10 ** 8 + np.floor(got["y"] + 0.5).astype(np.int64) * 10 ** 4
+    assert np.all(np.diff(got["level"]) >= 0)
+    # matched descriptors
+    d = desc[0, : len(got)].cpu().numpy().astype(np.float64)
+    m = idx >= 0
+    a, b = ref["desc"][m], d[idx[m]]
+    cos = np.sum(a * b, 1) / (np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1) + 1e-30)
+    assert np.mean(cos >= 0.999) >= 0.99, np.mean(cos >= 0.999)
+    nz = np.linalg.norm(d, axis=1)
+    assert np.allclose(nz[nz > 0], 1.0, atol=1e-5)
+    del key
+    kz.close()
+
+
+def test_descriptors_stage_isolated_pinned_keypoints_and_angles(O):
+    """Oracle Lx/Ly (fp32) + oracle keypoints and angles → GPU M-SURF: cos >= 0.999 for 100%; GPU orientation
+    on the same inputs agrees with the oracle's within 1e-3 rad for >= 99% (window near-ties excepted)."""
+    img, ref = oracle_run(O, 640, 480)
+    N = 16
+    kz = make(640, 480, k_override=ref["k"], flags=K.FLAG_KEEP_ANGLE)
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    for i in range(N):
+        K.kaze_set_level(kz.ctx, 0, i, K.PLANE_LT, torch.from_numpy(ref["levels"][i].astype(np.float32)).cuda())
+    kps = torch.zeros((1, kz.cap, 8), dtype=torch.int32, device="cuda")
+    counts = torch.zeros(1, dtype=torch.int32, device="cuda")
+    K.kaze_detect(kz.ctx, kps, counts)
+    Lx32, Ly32 = ref["Lx"].astype(np.float32), ref["Ly"].astype(np.float32)
+    for i in range(N):
+        K.kaze_set_level(kz.ctx, 0, i, K.PLANE_LX, torch.from_numpy(Lx32[i]).cuda())
+        K.kaze_set_level(kz.ctx, 0, i, K.PLANE_LY, torch.from_numpy(Ly32[i]).cuda())
+    rk = ref["kps"]
+    n = len(rk)
+    arr = np.zeros(kz.cap, K.KP_DTYPE)
+    for f in ("x", "y", "sigma", "response", "angle", "level", "octave", "sublevel"):
+        arr[f][:n] = rk[f]
+    kps = torch.from_numpy(arr.view(np.int32).reshape(1, kz.cap, 8).copy()).cuda()
+    counts = torch.tensor([n], dtype=torch.int32, device="cuda")
+    desc = torch.zeros((1, kz.cap, 64), device="cuda")
+    K.kaze_describe(kz.ctx, kps, counts, desc)
+    _, dref = O.describe(Lx32.astype(np.float64), Ly32.astype(np.float64), rk, keep_angle=True)
+    d = desc[0, :n].cpu().numpy().astype(np.float64)
+    cos = np.sum(d * dref, 1) / (np.linalg.norm(d, axis=1) * np.linalg.norm(dref, axis=1) + 1e-30)
+    assert np.all(cos >= 0.999), (np.min(cos), np.sum(cos < 0.999))
+    kz.close()
+    # orientation on the same pinned inputs
+    kz = make(640, 480, k_override=ref["k"])
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    K.kaze_detect(kz.ctx, torch.zeros((1, kz.cap, 8), dtype=torch.int32, device="cuda"),
+                  torch.zeros(1, dtype=torch.int32, device="cuda"))
+    for i in range(N):
+        K.kaze_set_level(kz.ctx, 0, i, K.PLANE_LX, torch.from_numpy(Lx32[i]).cuda())
+        K.kaze_set_level(kz.ctx, 0, i, K.PLANE_LY, torch.from_numpy(Ly32[i]).cuda())
+    arr["angle"][:n] = 0
+    kps = torch.from_numpy(arr.view(np.int32).reshape(1, kz.cap, 8).copy()).cuda()
+    K.kaze_describe(kz.ctx, kps, counts, desc)
+    got = K.Kaze.keypoints_numpy(kps, counts)[0]
+    kref2, _ = O.describe(Lx32.astype(np.float64), Ly32.astype(np.float64), rk, keep_angle=False)
+    dang = np.abs((got["angle"] - kref2["angle"] + math.pi) % (2 * math.pi) - math.pi)
+    assert np.mean(dang < 1e-3) >= 0.99, np.mean(dang < 1e-3)
+    kz.close()
+
+
+# ------------------------------------------------------------------------------------------- edge cases
+def test_constant_image_degenerate_k_and_no_keypoints():
+    kz = make(64, 64)
+    img = torch.full((1, 64, 64), 0.5, device="cuda")
+    kps, counts, desc = kz.extract(img)
+    k, fb = K.kaze_get_k(kz.ctx, 1)
+    assert int(counts[0]) == 0 and fb[0] == 1 and k[0] == pytest.approx(0.03)
+    lv = gpu_levels(kz, 16)
+    assert np.allclose(lv, 0.5, atol=1e-6)  # AOS on a constant image is the identity (P7)
+    kz.close()
+
+
+def test_minimum_size_and_argument_errors():
+    kz = make(64, 64, batch=2)
+    img = torch.rand((1, 32, 32), device="cuda")
+    kps, counts, desc = kz.extract(img)  # 32x32 is the smallest accepted size
+    with pytest.raises(K.KazeError) as e:
+        K.kaze_build_scale_space(kz.ctx, torch.rand((1, 31, 40), device="cuda"))
+    assert e.value.status == -2
+    with pytest.raises(K.KazeError) as e:
+        K.kaze_build_scale_space(kz.ctx, torch.rand((1, 65, 40), device="cuda"))
+    assert e.value.status == -2
+    with pytest.raises(K.KazeError) as e:
+        K.kaze_build_scale_space(kz.ctx, torch.rand((3, 40, 40), device="cuda"))
+    assert e.value.status == -1
+    fresh = make(64, 64)
+    with pytest.raises(K.KazeError) as e:
+        K.kaze_detect(fresh.ctx, kps, counts)
+    assert e.value.status == -4
+    kz.close()
+    fresh.close()
+
+
+def test_capacity_truncation_keeps_the_first_keypoints(O):
+    img = kaze_inputs.synth_image(640, 480)
+    full = make(640, 480)
+    k1, c1, d1 = full.extract(torch.from_numpy(img).cuda()[None])
+    small = make(640, 480, max_keypoints=100)
+    k2, c2, d2 = small.extract(torch.from_numpy(img).cuda()[None])
+    assert int(c2[0]) == int(c1[0]) > 100  # the true count is reported
+    assert torch.equal(k2[0, :100], k1[0, :100])
+    assert torch.equal(d2[0, :100], d1[0, :100])
+    full.close()
+    small.close()
+
+
+def test_pitched_input_equals_packed_input():
+    img = torch.rand((1, 100, 130), device="cuda")
+    padded = torch.zeros((1, 100, 160), device="cuda")
+    padded[:, :, :130] = img
+    a = make(130, 100)
+    ka, ca, da = a.extract(img)
+    kb, cb, db = a.alloc_outputs(1)
+    K.kaze_extract(a.ctx, padded[:, :, :130], kb, cb, db)
+    assert torch.equal(ca, cb) and torch.equal(ka, kb) and torch.equal(da, db)
+    a.close()
+
+
+def test_host_path_equals_device_path():
+    imgs = np.stack([kaze_inputs.synth_image(256, 192, s) for s in range(5)])
+    kz = make(256, 192, batch=2)
+    kd, cd, dd = kz.extract(torch.from_numpy(imgs).cuda())
+    hk = np.zeros((5, kz.cap, 8), np.int32)
+    hc = np.zeros(5, np.int32)
+    hd = np.zeros((5, kz.cap, 64), np.float32)
+    K.kaze_extract_host(kz.ctx, imgs, hk, hc, hd)
+    assert np.array_equal(hc, cd.cpu().numpy())
+    for i in range(5):
+        n = int(hc[i])
+        assert np.array_equal(hk[i, :n], kd[i, :n].cpu().numpy())
+        assert np.array_equal(hd[i, :n], dd[i, :n].cpu().numpy())
+    kz.close()
+
+
+def test_profile_counts_launches():
+    kz = make(128, 128, octaves=2, sublevels=2)
+    K.kaze_set_profiling(kz.ctx, True)
+    K.kaze_reset_profile(kz.ctx)
+    kz.extract(torch.rand((1, 128, 128), device="cuda"))
+    prof = K.kaze_get_profile(kz.ctx)
+    n = sum(v["launches"] for v in prof.values())
+    assert n == K.kaze_launch_count(kz.ctx) > 10
+    assert prof["aos_rows"]["launches"] == 3 and prof["aos_cols"]["ms"] > 0
+    kz.close()
