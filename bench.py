@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native KAZE hot path (BASELINE.json metric / configs[4]).
+
+Workload: a batch of 256 synthetic 1920x1200 images, KAZE defaults (4 octaves x 4 sublevels, σ0 = 1.6, g2, k at
+the 70th percentile), full path: nonlinear scale space (AOS) → Hessian detector → orientation + 64-D M-SURF.
+The batch is sharded over the N ranks (strong scaling: 256 / N images per rank); a step is one pass of the whole
+path over the rank's shard, plus the C1 all-gather of keypoint counts (NCCL) when N > 1.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kaze|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every key).  --impl reference times the fp64 CPU oracle
+(oracle/, plain C) on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KAZE ms/image @1920x1200; images/s at 1/2/4/8 B200; AOS % of HBM peak"
+W_IMG, H_IMG, N_IMAGES = 1920, 1200, 256
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kaze", choices=["kaze", "reference"])
+    ap.add_argument("--images", type=int, default=N_IMAGES)
+    ap.add_argument("--batch", type=int, default=4, help="images per launch (max_batch of the context)")
+    ap.add_argument("--max-keypoints", type=int, default=32768)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--distinct", type=int, default=8, help="distinct generated images (the rest are shifts/flips)")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for i, nm in enumerate(names):
+                if r[4 + i].lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_inputs(n_local: int, first: int, distinct: int):
+    import kaze_inputs
+
+    return kaze_inputs.synth_batch(n_local, W_IMG, H_IMG, first=first, distinct=min(distinct, n_local))
+
+
+def run_reference(args):
+    """The oracle (plain fp64 C, OpenMP over images only) on the host cores, bounded sample per step."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import kaze_inputs
+    import oracle
+
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    threads = max(1, min(cores, 8))
+    imgs = np.stack([kaze_inputs.synth_image(W_IMG, H_IMG, kaze_inputs.BASE_SEED + i) for i in range(threads)])
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        counts = oracle.run_batch(imgs, cap=1 << 17, nthreads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    sec = statistics.mean(times)
+    value = threads / sec
+    cpu = next((l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")), "?")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "configs[4]: 1920x1200 synthetic images, full KAZE path (bounded sample)",
+                   "width": W_IMG, "height": H_IMG, "octaves": 4, "sublevels": 4},
+        "ms_per_image": sec * 1e3 / threads,
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{threads} images (seeds 1234..{1233 + threads}) per step, one per thread, "
+                                   f"of the 1920x1200 full path; host '{cpu}', {cores} cores visible",
+                         "keypoints": [int(c) for c in counts]},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline_sample():
+    """Oracle timed on one image of the workload (1 thread) — ~10-20 s of CPU work."""
+    import kaze_inputs
+    import oracle
+
+    oracle.build()
+    img = kaze_inputs.synth_image(W_IMG, H_IMG, kaze_inputs.BASE_SEED)
+    t0 = time.perf_counter()
+    r = oracle.run(img, cap=1 << 17)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": "images/s", "cores": 1, "kind": "oracle",
+            "sample": f"1 image (seed 1234) of 1920x1200, full path, single thread: {dt:.2f} s, "
+                      f"{r['count']} keypoints"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1706_06750_b200 as K
+    from paper_1706_06750_b200 import dist as D
+
+    rank, local_rank, ws = D.world()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    first, n_local = D.shard(args.images, rank, ws)
+    assert args.warmup >= 3 or os.environ.get("KAZE_BENCH_ALLOW_SHORT"), "timing rules: W >= 3"
+
+    host = make_inputs(n_local, first, args.distinct)  # untimed staging
+    imgs = torch.from_numpy(host).to(dev)
+    B = min(args.batch, max(1, n_local))
+    kz = K.Kaze(W_IMG, H_IMG, batch=B, device=local_rank, max_keypoints=args.max_keypoints)
+    kps, counts, desc = kz.alloc_outputs(n_local)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        K.kaze_extract(kz.ctx, imgs, kps, counts, desc)
+        if ws > 1:
+            D.gather_counts(counts)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    launches0 = K.kaze_launch_count(kz.ctx)
+    K.kaze_set_profiling(kz.ctx, True)
+    K.kaze_reset_profile(kz.ctx)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    prof = K.kaze_get_profile(kz.ctx)
+    launches = K.kaze_launch_count(kz.ctx)
+    K.kaze_set_profiling(kz.ctx, False)
+    del launches0
+    ms = D.max_over_ranks(ms_local, device=dev)
+    total_counts = D.gather_counts(counts) if ws > 1 else counts
+    kp_total = int(torch.clamp(total_counts, max=args.max_keypoints).sum())
+
+    # ---- roofline of the dominant kernel (largest device time in the step) ----
+    peak, peak_kind = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    dname, d = dom
+    achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9 if d["ms"] > 0 else 0.0
+    aos_bytes = prof.get("aos_cols", {}).get("bytes", 0) + prof.get("aos_rows", {}).get("bytes", 0)
+    aos_ms = prof.get("aos_cols", {}).get("ms", 0) + prof.get("aos_rows", {}).get("ms", 0)
+    aos_gbs = aos_bytes / (aos_ms * 1e-3) / 1e9 if aos_ms > 0 else 0.0
+    traffic = None
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = summ.get("kernels", {}).get(dname, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roof = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "algo_bytes_per_launch": d["bytes"] / max(1, d["launches"]),
+            "avg_launch_ms": d["ms"] / max(1, d["launches"]), "peak_source": peak_kind,
+            "aos_achieved_gbs": aos_gbs, "aos_frac": aos_gbs / peak}
+    step_kernel_ms = sum(v["ms"] for v in prof.values()) / args.steps
+
+    # ---- end to end through the host-buffer C ABI (pinned host memory, copies inside the timed region) ----
+    e2e = None
+    if not args.no_e2e:
+        h_imgs = torch.from_numpy(host).pin_memory()
+        h_kps = torch.zeros((n_local, args.max_keypoints, 8), dtype=torch.int32).pin_memory()
+        h_cnt = torch.zeros(n_local, dtype=torch.int32).pin_memory()
+        h_desc = torch.zeros((n_local, args.max_keypoints, 64), dtype=torch.float32).pin_memory()
+        K.kaze_extract_host(kz.ctx, h_imgs, h_kps, h_cnt, h_desc)  # warm-up
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            K.kaze_extract_host(kz.ctx, h_imgs, h_kps, h_cnt, h_desc)
+        torch.cuda.synchronize(dev)
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        e2e_ms = D.max_over_ranks(e2e_ms, device=dev)
+        nk = int(torch.clamp(h_cnt, max=args.max_keypoints).sum())
+        e2e = {"value": args.images / (e2e_ms * 1e-3), "unit": "images/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(n_local * H_IMG * W_IMG * 4),
+               "d2h_bytes_per_step": int(n_local * 4 + nk * (32 + 256)),
+               "api": "kaze_extract_host (pinned host buffers, chunked H2D/compute/D2H overlap)"}
+
+    if rank == 0:
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_sample()
+        out = {
+            "metric": METRIC,
+            "value": args.images / (ms * 1e-3),
+            "unit": "images/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "ms_per_image": ms / args.images * ws,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "configs[4]: batch of 256 synthetic 1920x1200 images sharded over the GPUs, "
+                                   "full path (AOS scale space, Hessian detector, orientation, 64-D M-SURF)",
+                       "images": args.images, "width": W_IMG, "height": H_IMG, "octaves": 4, "sublevels": 4,
+                       "max_batch": B, "max_keypoints": args.max_keypoints, "parallelism": f"dp{ws}",
+                       "l2": "inputs (%.2f GB) larger than L2; no flush" % (args.images * H_IMG * W_IMG * 4 / 1e9),
+                       "keypoints_per_image": kp_total / args.images},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * ws,
+            "kernel_ms_per_step": step_kernel_ms,
+            "kernels": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                            "gbs": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] > 0 else None}
+                        for k, v in prof.items()},
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    kz.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
