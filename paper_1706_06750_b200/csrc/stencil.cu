@@ -13,129 +13,140 @@ namespace kz {
 namespace {
 
 constexpr int TW = 32;  // tile width  (one warp per tile row → coalesced 128 B rows)
-constexpr int TH = 16;  // tile height
+constexpr int TH = 32;  // tile height (block 32 x 8, four output rows per thread)
+
+__device__ __forceinline__ float frcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 // -------------------------------------------------------------------------------------------------
 // Separable Gaussian over a TW x TH output tile.  The input tile stores I(clamp(u)) for the virtual
 // coordinates u of the tile + radius halo, so the separable passes equal the 2-D clamped convolution.
+template <int R>
 __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ in, int64_t in_pitch,
                                                    size_t in_img_stride, float* __restrict__ out,
                                                    size_t out_img_stride, Geom g, GaussTaps t) {
-    extern __shared__ float sm[];
-    const int R = t.r;
-    const int LW = TW + 2 * R, LH = TH + 2 * R;
-    float* tin = sm;               // LH x LW
-    float* tmid = sm + LH * LW;    // LH x TW
+    constexpr int LW = TW + 2 * R, LH = TH + 2 * R;
+    __shared__ float tin[LH][LW];
+    __shared__ float tmid[LH][TW];
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
     const float* src = in + blockIdx.z * in_img_stride;
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
-    for (int i = tid; i < LH * LW; i += nt) {
-        int ly = i / LW, lx = i - ly * LW;
-        int gx = clampi(x0 - R + lx, 0, g.W - 1), gy = clampi(y0 - R + ly, 0, g.H - 1);
-        tin[i] = __ldg(src + (int64_t)gy * in_pitch + gx);
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int ly = ty; ly < LH; ly += 8) {
+        const float* row = src + (int64_t)clampi(y0 - R + ly, 0, g.H - 1) * in_pitch;
+        for (int lx = tx; lx < LW; lx += 32) tin[ly][lx] = __ldg(row + clampi(x0 - R + lx, 0, g.W - 1));
     }
+    float w[2 * R + 1];
+#pragma unroll
+    for (int d = 0; d <= 2 * R; ++d) w[d] = t.w[d];
     __syncthreads();
-    for (int i = tid; i < LH * TW; i += nt) {
-        int ly = i / TW, lx = i - ly * TW;
-        const float* row = tin + ly * LW + lx;
+    for (int ly = ty; ly < LH; ly += 8) {
         float acc = 0.f;
-        for (int d = 0; d <= 2 * R; ++d) acc = fmaf(t.w[d], row[d], acc);
-        tmid[i] = acc;
+#pragma unroll
+        for (int d = 0; d <= 2 * R; ++d) acc = fmaf(w[d], tin[ly][tx + d], acc);
+        tmid[ly][tx] = acc;
     }
     __syncthreads();
     float* dst = out + blockIdx.z * out_img_stride;
-    for (int i = tid; i < TH * TW; i += nt) {
-        int ly = i / TW, lx = i - ly * TW;
-        int x = x0 + lx, y = y0 + ly;
-        if (x >= g.W || y >= g.H) continue;
+    const int x = x0 + tx;
+#pragma unroll
+    for (int k = 0; k < TH / 8; ++k) {
+        const int ly = ty + 8 * k, y = y0 + ly;
         float acc = 0.f;
-        for (int d = 0; d <= 2 * R; ++d) acc = fmaf(t.w[d], tmid[(ly + d) * TW + lx], acc);
-        dst[(size_t)y * g.P + x] = acc;
+#pragma unroll
+        for (int d = 0; d <= 2 * R; ++d) acc = fmaf(w[d], tmid[ly + d][tx], acc);
+        if (x < g.W && y < g.H) dst[(size_t)y * g.P + x] = acc;
     }
 }
 
 // -------------------------------------------------------------------------------------------------
-// |∇(G1 * L)|² → c (mode 1) or |∇|² + max|∇| (mode 0).  R1 = radius of G(1) (3).
+// |∇(G1 * L)|² → c (mode 1) or |∇|² + max|∇| (mode 0).  G(σ=1) has radius 3 (A6).
+constexpr int R1 = 3;
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cond(const float* __restrict__ L, size_t in_img_stride,
                                               float* __restrict__ out, size_t out_img_stride, Geom g,
                                               GaussTaps t, int diffusivity, const float* __restrict__ kval,
                                               unsigned* __restrict__ hmax_bits) {
-    extern __shared__ float sm[];
-    const int R = t.r;
-    const int H0 = R + 1;                       // halo of the L tile
-    const int LW = TW + 2 * H0, LH = TH + 2 * H0;
-    const int SW = TW + 2, SH = TH + 2;         // Ls tile: virtual coords [x0-1, x0+TW]
-    float* tL = sm;                             // LH x LW : L(clamp(u))
-    float* tH = tL + LH * LW;                   // LH x SW : horizontal pass at clamped Ls columns
-    float* tS = tH + LH * SW;                   // SH x SW : Ls(clamp(v))
+    constexpr int H0 = R1 + 1;                  // halo of the L tile
+    constexpr int LW = TW + 2 * H0, LH = TH + 2 * H0;
+    constexpr int SW = TW + 2, SH = TH + 2;     // Ls tile: virtual coords [x0-1, x0+TW]
+    __shared__ float tL[LH][LW];                // L(clamp(u))
+    __shared__ float tH[LH][SW + 1];            // horizontal pass at clamped Ls columns
+    __shared__ float tS[SH][SW + 1];            // Ls(clamp(v))
     __shared__ float red[8];
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, img = blockIdx.z;
     const float* src = L + img * in_img_stride;
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
-    for (int i = tid; i < LH * LW; i += nt) {
-        int ly = i / LW, lx = i - ly * LW;
-        int gx = clampi(x0 - H0 + lx, 0, g.W - 1), gy = clampi(y0 - H0 + ly, 0, g.H - 1);
-        tL[i] = __ldg(src + (size_t)gy * g.P + gx);
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+    for (int ly = ty; ly < LH; ly += 8) {
+        const float* row = src + (size_t)clampi(y0 - H0 + ly, 0, g.H - 1) * g.P;
+        for (int lx = tx; lx < LW; lx += 32) tL[ly][lx] = __ldg(row + clampi(x0 - H0 + lx, 0, g.W - 1));
+    }
+    float w[2 * R1 + 1];
+#pragma unroll
+    for (int d = 0; d <= 2 * R1; ++d) w[d] = t.w[d];
+    __syncthreads();
+    // horizontal pass for every L-tile row at the clamped Ls columns cv = clamp(x0 - 1 + sx)
+    for (int ly = ty; ly < LH; ly += 8) {
+        for (int sx = tx; sx < SW; sx += 32) {
+            const int base = clampi(x0 - 1 + sx, 0, g.W - 1) - (x0 - H0) - R1;
+            float acc = 0.f;
+#pragma unroll
+            for (int d = 0; d <= 2 * R1; ++d) acc = fmaf(w[d], tL[ly][base + d], acc);
+            tH[ly][sx] = acc;
+        }
     }
     __syncthreads();
-    // horizontal pass for every L-tile row, at Ls columns v = x0-1+sx, evaluated at clamp(v)
-    for (int i = tid; i < LH * SW; i += nt) {
-        int ly = i / SW, sx = i - ly * SW;
-        int cv = clampi(x0 - 1 + sx, 0, g.W - 1);      // clamped Ls column (image coords)
-        int base = cv - (x0 - H0) - R;                 // tile column of cv - R
-        const float* row = tL + ly * LW + base;
-        float acc = 0.f;
-        for (int d = 0; d <= 2 * R; ++d) acc = fmaf(t.w[d], row[d], acc);
-        tH[i] = acc;
+    for (int sy = ty; sy < SH; sy += 8) {
+        const int base = clampi(y0 - 1 + sy, 0, g.H - 1) - (y0 - H0) - R1;
+        for (int sx = tx; sx < SW; sx += 32) {
+            float acc = 0.f;
+#pragma unroll
+            for (int d = 0; d <= 2 * R1; ++d) acc = fmaf(w[d], tH[base + d][sx], acc);
+            tS[sy][sx] = acc;
+        }
     }
     __syncthreads();
-    for (int i = tid; i < SH * SW; i += nt) {
-        int sy = i / SW, sx = i - sy * SW;
-        int cv = clampi(y0 - 1 + sy, 0, g.H - 1);
-        int base = cv - (y0 - H0) - R;
-        float acc = 0.f;
-        for (int d = 0; d <= 2 * R; ++d) acc = fmaf(t.w[d], tH[(base + d) * SW + sx], acc);
-        tS[i] = acc;
-    }
-    __syncthreads();
-    float k2 = 1.f;
+    float ik2 = 1.f;
     if (MODE == 1) {
-        float k = kval[img];
-        k2 = k * k;
+        const float k = kval[img];
+        ik2 = frcp(k * k);
     }
     float lmax = 0.f;
     float* dst = out + img * out_img_stride;
-    for (int i = tid; i < TH * TW; i += nt) {
-        int ly = i / TW, lx = i - ly * TW;
-        int x = x0 + lx, y = y0 + ly;
-        if (x >= g.W || y >= g.H) continue;
-        // Ls tile index of virtual coordinate v: v - (x0 - 1); Scharr reads Ls(clamp(x±1), clamp(y+k))
-        int xm = clampi(x - 1, 0, g.W - 1) - (x0 - 1), xp = clampi(x + 1, 0, g.W - 1) - (x0 - 1);
-        int ym = clampi(y - 1, 0, g.H - 1) - (y0 - 1), yp = clampi(y + 1, 0, g.H - 1) - (y0 - 1);
-        int xc = x - (x0 - 1), yc = y - (y0 - 1);
-        float gx = 0.1875f * (tS[ym * SW + xp] - tS[ym * SW + xm]) + 0.625f * (tS[yc * SW + xp] - tS[yc * SW + xm]) +
-                   0.1875f * (tS[yp * SW + xp] - tS[yp * SW + xm]);
-        float gy = 0.1875f * (tS[yp * SW + xm] - tS[ym * SW + xm]) + 0.625f * (tS[yp * SW + xc] - tS[ym * SW + xc]) +
-                   0.1875f * (tS[yp * SW + xp] - tS[ym * SW + xp]);
+    const int x = x0 + tx;
+    // Ls tile index of virtual coordinate v is v - (x0 - 1); the Scharr reads Ls(clamp(x±1), clamp(y±1))
+    const int xm = clampi(x - 1, 0, g.W - 1) - (x0 - 1), xp = clampi(x + 1, 0, g.W - 1) - (x0 - 1), xc = tx + 1;
+#pragma unroll
+    for (int k = 0; k < TH / 8; ++k) {
+        const int y = y0 + ty + 8 * k;
+        const int ym = clampi(y - 1, 0, g.H - 1) - (y0 - 1), yp = clampi(y + 1, 0, g.H - 1) - (y0 - 1);
+        const int yc = y - (y0 - 1);
+        float gx = 0.1875f * (tS[ym][xp] - tS[ym][xm]) + 0.625f * (tS[yc][xp] - tS[yc][xm]) +
+                   0.1875f * (tS[yp][xp] - tS[yp][xm]);
+        float gy = 0.1875f * (tS[yp][xm] - tS[ym][xm]) + 0.625f * (tS[yp][xc] - tS[ym][xc]) +
+                   0.1875f * (tS[yp][xp] - tS[ym][xp]);
         gx *= 0.5f;
         gy *= 0.5f;
-        float g2 = gx * gx + gy * gy;
-        if (MODE == 0) {
-            dst[(size_t)y * g.P + x] = g2;
-            if (x >= 1 && x <= g.W - 2 && y >= 1 && y <= g.H - 2) lmax = fmaxf(lmax, sqrtf(g2));
-        } else {
-            float q = g2 / k2;
-            dst[(size_t)y * g.P + x] = diffusivity == 2 ? 1.f / (1.f + q) : expf(-q);
+        const float g2 = gx * gx + gy * gy;
+        if (x < g.W && y < g.H) {
+            if (MODE == 0) {
+                dst[(size_t)y * g.P + x] = g2;
+                if (x >= 1 && x <= g.W - 2 && y >= 1 && y <= g.H - 2) lmax = fmaxf(lmax, sqrtf(g2));
+            } else {
+                const float q = g2 * ik2;
+                dst[(size_t)y * g.P + x] = diffusivity == 2 ? frcp(1.f + q) : __expf(-q);
+            }
         }
     }
     if (MODE == 0) {
         for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-        if ((tid & 31) == 0) red[tid >> 5] = lmax;
+        if (tx == 0) red[ty] = lmax;
         __syncthreads();
         if (tid == 0) {
             float m = 0.f;
-            for (int w = 0; w < nt / 32; ++w) m = fmaxf(m, red[w]);
+            for (int wv = 0; wv < 8; ++wv) m = fmaxf(m, red[wv]);
             atomicMax(hmax_bits + img, __float_as_uint(m));  // non-negative floats order as uints
         }
     }
@@ -209,8 +220,8 @@ __global__ void __launch_bounds__(256) k_c_from_g2(float* __restrict__ buf, size
     if (x >= g.W) return;
     float k = kval[img];
     float* p = buf + img * img_stride + (size_t)y * g.P + x;
-    float q = *p / (k * k);
-    *p = diffusivity == 2 ? 1.f / (1.f + q) : expf(-q);
+    const float q = *p * frcp(k * k);
+    *p = diffusivity == 2 ? frcp(1.f + q) : __expf(-q);
 }
 
 }  // namespace
@@ -218,22 +229,28 @@ __global__ void __launch_bounds__(256) k_c_from_g2(float* __restrict__ buf, size
 void launch_prefilter(const float* img, int64_t in_pitch, size_t in_img_stride, float* L0, size_t out_img_stride,
                       Geom g, int nimg, const GaussTaps& t, cudaStream_t s) {
     dim3 grid((g.W + TW - 1) / TW, (g.H + TH - 1) / TH, nimg);
-    size_t smem = sizeof(float) * ((TH + 2 * t.r) * (TW + 2 * t.r) + (TH + 2 * t.r) * TW);
-    k_prefilter<<<grid, dim3(32, 8), smem, s>>>(img, in_pitch, in_img_stride, L0, out_img_stride, g, t);
+    dim3 block(32, 8);
+    switch (t.r) {
+#define KZ_PF(R) \
+    case R: k_prefilter<R><<<grid, block, 0, s>>>(img, in_pitch, in_img_stride, L0, out_img_stride, g, t); break;
+        KZ_PF(1) KZ_PF(2) KZ_PF(3) KZ_PF(4) KZ_PF(5) KZ_PF(6) KZ_PF(7) KZ_PF(8) KZ_PF(9) KZ_PF(10) KZ_PF(11)
+        KZ_PF(12) KZ_PF(13) KZ_PF(14) KZ_PF(15) KZ_PF(16) KZ_PF(17) KZ_PF(18) KZ_PF(19) KZ_PF(20) KZ_PF(21)
+        KZ_PF(22) KZ_PF(23) KZ_PF(24)
+#undef KZ_PF
+        default: break;
+    }
 }
 
 void launch_cond(const float* L, size_t in_img_stride, float* out, size_t out_img_stride, Geom g, int nimg,
                  const GaussTaps& t1, int mode, int diffusivity, const float* kval, unsigned* hmax_bits,
                  cudaStream_t s) {
     dim3 grid((g.W + TW - 1) / TW, (g.H + TH - 1) / TH, nimg);
-    const int H0 = t1.r + 1;
-    size_t smem = sizeof(float) * ((TH + 2 * H0) * (TW + 2 * H0) + (TH + 2 * H0) * (TW + 2) + (TH + 2) * (TW + 2));
     if (mode == 0)
-        k_cond<0><<<grid, dim3(32, 8), smem, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval,
-                                                  hmax_bits);
+        k_cond<0><<<grid, dim3(32, 8), 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval,
+                                               hmax_bits);
     else
-        k_cond<1><<<grid, dim3(32, 8), smem, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval,
-                                                  hmax_bits);
+        k_cond<1><<<grid, dim3(32, 8), 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval,
+                                               hmax_bits);
 }
 
 void launch_khist(const float* g2, size_t img_stride, Geom g, int nimg, int bins, const unsigned* hmax_bits, int* hist,
