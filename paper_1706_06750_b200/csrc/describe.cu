@@ -24,25 +24,26 @@ __constant__ float c_w2[16];  // exp(-((a-1.5)^2 + (b-1.5)^2) / (2 * 1.5^2)), in
 constexpr float kTwoPi = 6.283185307179586f;
 constexpr float kPi = 3.141592653589793f;
 
-__device__ __forceinline__ float bilinear(const float* __restrict__ img, int W, int H, int P, float px, float py) {
+// Bilinear (Lx, Ly) at (px, py) with clamped taps (A14, A16): four 8-byte loads of the interleaved plane.
+__device__ __forceinline__ float2 bilinear2(const float2* __restrict__ img, int W, int H, int P, float px, float py) {
     const float fx0 = floorf(px), fy0 = floorf(py);
     const float fx = px - fx0, fy = py - fy0;
     const int x0 = (int)fx0, y0 = (int)fy0;
     const int xa = clampi(x0, 0, W - 1), xb = clampi(x0 + 1, 0, W - 1);
     const int ya = clampi(y0, 0, H - 1), yb = clampi(y0 + 1, 0, H - 1);
-    const float v00 = __ldg(img + (size_t)ya * P + xa), v10 = __ldg(img + (size_t)ya * P + xb);
-    const float v01 = __ldg(img + (size_t)yb * P + xa), v11 = __ldg(img + (size_t)yb * P + xb);
-    return (1.f - fy) * ((1.f - fx) * v00 + fx * v10) + fy * ((1.f - fx) * v01 + fx * v11);
+    const float2 v00 = __ldg(img + (size_t)ya * P + xa), v10 = __ldg(img + (size_t)ya * P + xb);
+    const float2 v01 = __ldg(img + (size_t)yb * P + xa), v11 = __ldg(img + (size_t)yb * P + xb);
+    return make_float2((1.f - fy) * ((1.f - fx) * v00.x + fx * v10.x) + fy * ((1.f - fx) * v01.x + fx * v11.x),
+                       (1.f - fy) * ((1.f - fx) * v00.y + fx * v10.y) + fy * ((1.f - fx) * v01.y + fx * v11.y));
 }
 
 constexpr int kWarps = 8;
 
-__global__ void __launch_bounds__(256) k_describe(const float* __restrict__ Lx, const float* __restrict__ Ly,
-                                                  size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
+__global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy, size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
                                                   const int* __restrict__ counts, int cap, float* __restrict__ desc,
                                                   int nwin, int keep_angle) {
     __shared__ int pre[kMaxBatch + 1];
-    __shared__ float sbuf[kWarps][2 * 576];
+    __shared__ __align__(16) float sbuf[kWarps][2 * 576];
     if (threadIdx.x == 0) {
         int r = 0;
         for (int i = 0; i < nimg; ++i) {
@@ -63,25 +64,23 @@ __global__ void __launch_bounds__(256) k_describe(const float* __restrict__ Lx, 
         kaze_keypoint* kp = kps + (size_t)img * cap + k;
         const float x = kp->x, y = kp->y, sigma = kp->sigma;
         const int level = kp->level;
-        const float* lx = Lx + img * img_stride + (size_t)level * g.plane;
-        const float* ly = Ly + img * img_stride + (size_t)level * g.plane;
+        const float2* lxy = Lxy + img * img_stride + (size_t)level * g.plane;
         float angle;
         int flags = 0;
         if (keep_angle) {
             angle = kp->angle;
         } else {
             // ---- orientation ----
-            float* sp = sx + 2 * kOriSamples;  // phases after the vectors
+            float4* so = reinterpret_cast<float4*>(sx);  // (phase, w·Lx, w·Ly, -) per sample
+#pragma unroll
             for (int j = lane; j < kOriSamples; j += 32) {
                 const float px = x + sigma * c_ori_u[j], py = y + sigma * c_ori_v[j];
                 const float w = c_ori_w[j];
-                const float rx = w * bilinear(lx, g.W, g.H, g.P, px, py);
-                const float ry = w * bilinear(ly, g.W, g.H, g.P, px, py);
+                const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);
+                const float rx = w * gv.x, ry = w * gv.y;
                 float ph = atan2f(ry, rx);
                 if (ph < 0.f) ph += kTwoPi;
-                sx[j] = rx;
-                sx[kOriSamples + j] = ry;
-                sp[j] = ph;
+                so[j] = make_float4(ph, rx, ry, 0.f);
             }
             __syncwarp();
             float best = 0.f, bx = 0.f, by = 0.f;
@@ -89,14 +88,15 @@ __global__ void __launch_bounds__(256) k_describe(const float* __restrict__ Lx, 
             for (int kw = lane; kw < nwin; kw += 32) {
                 const float th = kTwoPi * (float)kw / (float)nwin;
                 float ax = 0.f, ay = 0.f;
+#pragma unroll 4
                 for (int j = 0; j < kOriSamples; ++j) {
-                    float d = sp[j] - th;
+                    const float4 e = so[j];  // broadcast read
+                    float d = e.x - th;
                     if (d > kPi) d -= kTwoPi;
                     else if (d <= -kPi) d += kTwoPi;
-                    if (fabsf(d) < kPi / 6.f) {
-                        ax += sx[j];
-                        ay += sx[kOriSamples + j];
-                    }
+                    const bool in = fabsf(d) < kPi / 6.f;
+                    ax += in ? e.y : 0.f;
+                    ay += in ? e.z : 0.f;
                 }
                 const float m = ax * ax + ay * ay;
                 if (m > best) {
@@ -132,13 +132,14 @@ __global__ void __launch_bounds__(256) k_describe(const float* __restrict__ Lx, 
         // ---- M-SURF ----
         float si, co;
         sincosf(angle, &si, &co);
+#pragma unroll 6
         for (int s = lane; s < 576; s += 32) {
             const int p = s / 24, q = s - p * 24;
             const float u = (float)p - 11.5f, v = (float)q - 11.5f;
             const float px = x + sigma * (u * co - v * si);
             const float py = y + sigma * (u * si + v * co);
-            const float gx = bilinear(lx, g.W, g.H, g.P, px, py);
-            const float gy = bilinear(ly, g.W, g.H, g.P, px, py);
+            const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);
+            const float gx = gv.x, gy = gv.y;
             sx[s] = gx * co + gy * si;
             sy[s] = -gx * si + gy * co;
         }
@@ -208,10 +209,10 @@ void init_describe_tables() {
     cudaMemcpyToSymbol(c_w2, w2, sizeof(w2));
 }
 
-void launch_describe(const float* Lx, const float* Ly, size_t img_stride, Geom g, int nimg, int N, kaze_keypoint* kps,
+void launch_describe(const float2* Lxy, size_t img_stride, Geom g, int nimg, int N, kaze_keypoint* kps,
                      const int* counts, int cap, float* desc, int nwin, int keep_angle, cudaStream_t s) {
     (void)N;
-    k_describe<<<148 * 4, 256, 0, s>>>(Lx, Ly, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle);
+    k_describe<<<148 * 5, 256, 0, s>>>(Lxy, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle);
 }
 
 }  // namespace kz

@@ -62,37 +62,73 @@ __device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const 
     return refine(patch, er, ox, oy);
 }
 
+// nms_mark tile: 256 columns x 4 rows of one level of one image; the three levels' (4+2) x (256+2) neighbourhoods
+// are staged in shared memory with coalesced loads, then every pixel is tested from shared memory.
+constexpr int NX = 256, NY = 4;
+
+__device__ __forceinline__ bool is_keypoint_smem(const float (*T)[NY + 2][NX + 2], int r, int c, float thr, float er) {
+    const float v = T[1][r][c];
+    if (!(v > thr)) return false;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            if (!(v > T[1][r + dy][c + dx])) return false;
+        }
+#pragma unroll
+    for (int l = 0; l <= 2; l += 2)
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+            for (int dx = -1; dx <= 1; ++dx)
+                if (!(v > T[l][r + dy][c + dx])) return false;
+    float patch[3][3];
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) patch[dy + 1][dx + 1] = T[1][r + dy][c + dx];
+    float ox, oy;
+    return refine(patch, er, ox, oy);
+}
+
 __global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
                                                   DetectParams dp, uint32_t* __restrict__ bitmap,
                                                   int* __restrict__ rowcnt) {
-    __shared__ int wcount[8];
-    const int y = blockIdx.x, li = blockIdx.y, level = li + 1, img = blockIdx.z;
-    const int words = (g.W + 31) / 32;
+    __shared__ float T[3][NY + 2][NX + 2];
+    __shared__ int rc[NY];
+    const int x0 = blockIdx.x * NX, y0 = blockIdx.y * NY;
+    const int li = blockIdx.z % (N - 2), img = blockIdx.z / (N - 2), level = li + 1;
     const float* D0 = Ldet + img * img_stride + (size_t)level * g.plane;
-    const float* Dm = D0 - g.plane;
-    const float* Dp = D0 + g.plane;
-    uint32_t* bm = bitmap + (((size_t)img * (N - 2) + li) * g.H + y) * words;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int cnt = 0;
-    const bool rowok = y >= 1 && y <= g.H - 2;
-    for (int w = warp; w < words; w += 8) {
-        const int x = w * 32 + lane;
-        bool k = false;
-        if (rowok && x >= 1 && x <= g.W - 2) {
-            float ox, oy, v;
-            k = is_keypoint(Dm, D0, Dp, g.P, x, y, dp.threshold, dp.edge_ratio, ox, oy, v);
+    const int tid = threadIdx.x;
+    if (tid < NY) rc[tid] = 0;
+    // stage rows y0-1 .. y0+NY, columns x0-1 .. x0+NX (clamped; border pixels are never candidates)
+    for (int l = 0; l < 3; ++l) {
+        const float* Dl = D0 + (ptrdiff_t)(l - 1) * (ptrdiff_t)g.plane;
+        for (int r = 0; r < NY + 2; ++r) {
+            const float* row = Dl + (size_t)clampi(y0 - 1 + r, 0, g.H - 1) * g.P;
+            for (int cidx = tid; cidx < NX + 2; cidx += 256) T[l][r][cidx] = __ldg(row + clampi(x0 - 1 + cidx, 0, g.W - 1));
         }
-        const uint32_t bits = __ballot_sync(0xffffffffu, k);
-        if (lane == 0) bm[w] = bits;
-        cnt += __popc(bits);
     }
-    if (lane == 0) wcount[warp] = cnt;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int t = 0;
-        for (int i = 0; i < 8; ++i) t += wcount[i];
-        rowcnt[((size_t)img * (N - 2) + li) * g.H + y] = t;
+    const int words = (g.W + 31) / 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int x = x0 + tid;
+    for (int r = 0; r < NY; ++r) {
+        const int y = y0 + r;
+        const bool k = (y >= 1 && y <= g.H - 2 && x >= 1 && x <= g.W - 2) &&
+                       is_keypoint_smem(T, r + 1, tid + 1, dp.threshold, dp.edge_ratio);
+        const uint32_t bits = __ballot_sync(0xffffffffu, k);
+        if (y < g.H && x0 + warp * 32 < g.W) {
+            const size_t row = ((size_t)img * (N - 2) + li) * g.H + y;
+            if (lane == 0) {
+                bitmap[row * words + (x0 >> 5) + warp] = bits;
+                if (bits) atomicAdd(&rc[r], __popc(bits));
+            }
+        }
     }
+    __syncthreads();
+    if (tid < NY && y0 + tid < g.H && rc[tid]) atomicAdd(&rowcnt[((size_t)img * (N - 2) + li) * g.H + y0 + tid], rc[tid]);
 }
 
 // One CTA per image: exclusive scan of R row counts.
@@ -195,7 +231,8 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
 
 void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, int N, DetectParams dp, uint32_t* bitmap,
                      int* rowcnt, cudaStream_t s) {
-    dim3 grid(g.H, N - 2, nimg);
+    cudaMemsetAsync(rowcnt, 0, sizeof(int) * (size_t)nimg * (N - 2) * g.H, s);
+    dim3 grid((g.W + NX - 1) / NX, (g.H + NY - 1) / NY, nimg * (N - 2));
     k_nms_mark<<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, bitmap, rowcnt);
 }
 

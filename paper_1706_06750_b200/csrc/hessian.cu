@@ -15,9 +15,8 @@ namespace {
 
 constexpr float kW0 = 0.1875f, kW1 = 0.625f;  // (3, 10, 3) / 16
 
-__global__ void __launch_bounds__(256) k_hess_first(const float* __restrict__ Lt, float* __restrict__ Lx,
-                                                    float* __restrict__ Ly, size_t img_stride, Geom g, LevelTable lt,
-                                                    int tiles_y) {
+__global__ void __launch_bounds__(256) k_hess_first(const float* __restrict__ Lt, float2* __restrict__ Lxy,
+                                                    size_t img_stride, Geom g, LevelTable lt, int tiles_y) {
     const int level = blockIdx.y / tiles_y, ty = blockIdx.y - level * tiles_y;
     const int x = blockIdx.x * 32 + threadIdx.x, y = ty * 8 + threadIdx.y;
     if (x >= g.W || y >= g.H) return;
@@ -34,49 +33,57 @@ __global__ void __launch_bounds__(256) k_hess_first(const float* __restrict__ Lt
     float h = __ldg(rp + xm), i = __ldg(rp + x), j = __ldg(rp + xp);
     float dx = 0.5f * (kW0 * (c - a) + kW1 * (f - d) + kW0 * (j - h));
     float dy = 0.5f * (kW0 * (h - a) + kW1 * (i - b) + kW0 * (j - c));
-    Lx[base + (size_t)y * g.P + x] = dx;
-    Ly[base + (size_t)y * g.P + x] = dy;
+    Lxy[base + (size_t)y * g.P + x] = make_float2(dx, dy);
 }
 
-__global__ void __launch_bounds__(256) k_hess_det(const float* __restrict__ Lx, const float* __restrict__ Ly,
-                                                  float* __restrict__ Ldet, size_t img_stride, Geom g, LevelTable lt,
-                                                  int tiles_y) {
+__global__ void __launch_bounds__(256) k_hess_det(const float2* __restrict__ Lxy, float* __restrict__ Ldet,
+                                                  size_t img_stride, Geom g, LevelTable lt, int tiles_y) {
     const int level = blockIdx.y / tiles_y, ty = blockIdx.y - level * tiles_y;
     const int x = blockIdx.x * 32 + threadIdx.x, y = ty * 8 + threadIdx.y;
     if (x >= g.W || y >= g.H) return;
     const int s = lt.step[level];
     const size_t base = blockIdx.z * img_stride + (size_t)level * g.plane;
-    const float* X = Lx + base;
-    const float* Y = Ly + base;
+    const float2* D = Lxy + base;
     const int xm = max(x - s, 0), xp = min(x + s, g.W - 1);
     const int ym = max(y - s, 0), yp = min(y + s, g.H - 1);
     const size_t om = (size_t)ym * g.P, o0 = (size_t)y * g.P, op = (size_t)yp * g.P;
-    // N_x(Lx): x-derivative, smoothing over rows ym, y, yp
-    float lxx = 0.5f * (kW0 * (__ldg(X + om + xp) - __ldg(X + om + xm)) + kW1 * (__ldg(X + o0 + xp) - __ldg(X + o0 + xm)) +
-                        kW0 * (__ldg(X + op + xp) - __ldg(X + op + xm)));
-    // N_y(Lx): y-derivative, smoothing over columns xm, x, xp
-    float lxy = 0.5f * (kW0 * (__ldg(X + op + xm) - __ldg(X + om + xm)) + kW1 * (__ldg(X + op + x) - __ldg(X + om + x)) +
-                        kW0 * (__ldg(X + op + xp) - __ldg(X + om + xp)));
-    // N_y(Ly)
-    float lyy = 0.5f * (kW0 * (__ldg(Y + op + xm) - __ldg(Y + om + xm)) + kW1 * (__ldg(Y + op + x) - __ldg(Y + om + x)) +
-                        kW0 * (__ldg(Y + op + xp) - __ldg(Y + om + xp)));
+    // the 8 ring taps at distance s (clamped), each an (Lx, Ly) pair
+    const float2 a = __ldg(D + om + xm), b = __ldg(D + om + x), c = __ldg(D + om + xp);
+    const float2 d = __ldg(D + o0 + xm), f = __ldg(D + o0 + xp);
+    const float2 h = __ldg(D + op + xm), i = __ldg(D + op + x), j = __ldg(D + op + xp);
+    const float lxx = 0.5f * (kW0 * (c.x - a.x) + kW1 * (f.x - d.x) + kW0 * (j.x - h.x));  // N_x(Lx)
+    const float lxy = 0.5f * (kW0 * (h.x - a.x) + kW1 * (i.x - b.x) + kW0 * (j.x - c.x));  // N_y(Lx)
+    const float lyy = 0.5f * (kW0 * (h.y - a.y) + kW1 * (i.y - b.y) + kW0 * (j.y - c.y));  // N_y(Ly)
     Ldet[base + o0 + x] = lxx * lyy - lxy * lxy;
+}
+
+__global__ void k_component_copy(float2* __restrict__ plane, int comp, float* __restrict__ tight, int to_tight,
+                                 Geom g) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= g.W) return;
+    float* e = reinterpret_cast<float*>(plane + (size_t)y * g.P + x) + comp;
+    if (to_tight) tight[(size_t)y * g.W + x] = *e;
+    else *e = tight[(size_t)y * g.W + x];
 }
 
 }  // namespace
 
-void launch_hess_first(const float* Lt, float* Lx, float* Ly, size_t img_stride, Geom g, int nimg,
-                       const LevelTable& lt, cudaStream_t s) {
+void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
+                       cudaStream_t s) {
     int ty = (g.H + 7) / 8;
     dim3 grid((g.W + 31) / 32, ty * lt.n, nimg);
-    k_hess_first<<<grid, dim3(32, 8), 0, s>>>(Lt, Lx, Ly, img_stride, g, lt, ty);
+    k_hess_first<<<grid, dim3(32, 8), 0, s>>>(Lt, Lxy, img_stride, g, lt, ty);
 }
 
-void launch_hess_det(const float* Lx, const float* Ly, float* Ldet, size_t img_stride, Geom g, int nimg,
-                     const LevelTable& lt, cudaStream_t s) {
+void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
+                     cudaStream_t s) {
     int ty = (g.H + 7) / 8;
     dim3 grid((g.W + 31) / 32, ty * lt.n, nimg);
-    k_hess_det<<<grid, dim3(32, 8), 0, s>>>(Lx, Ly, Ldet, img_stride, g, lt, ty);
+    k_hess_det<<<grid, dim3(32, 8), 0, s>>>(Lxy, Ldet, img_stride, g, lt, ty);
+}
+
+void launch_component_copy(float2* plane, int comp, float* tight, int to_tight, Geom g, cudaStream_t s) {
+    k_component_copy<<<dim3((g.W + 255) / 256, g.H), 256, 0, s>>>(plane, comp, tight, to_tight, g);
 }
 
 }  // namespace kz

@@ -56,7 +56,8 @@ struct kaze_ctx {
     // arena
     int Pmax = 0;
     size_t plane_max = 0;
-    float *Lt = nullptr, *Lx = nullptr, *Ly = nullptr, *Ldet = nullptr, *cbuf = nullptr, *ubuf = nullptr;
+    float *Lt = nullptr, *Ldet = nullptr, *cbuf = nullptr, *ubuf = nullptr;
+    float2* Lxy = nullptr;  // interleaved (Lx, Ly)
     float* kval = nullptr;
     unsigned* hmax = nullptr;
     int* hist = nullptr;
@@ -187,7 +188,7 @@ kaze_status validate_params(const kaze_params* p) {
 }
 
 void free_arena(kaze_ctx* c) {
-    void* ptrs[] = {c->Lt, c->Lx, c->Ly, c->Ldet, c->cbuf, c->ubuf, c->kval, c->hmax, c->hist, c->fallback,
+    void* ptrs[] = {c->Lt, c->Lxy, c->Ldet, c->cbuf, c->ubuf, c->kval, c->hmax, c->hist, c->fallback,
                     c->bitmap, c->rowcnt, c->rowoff, c->hin[0], c->hin[1], c->hkps[0], c->hkps[1],
                     c->hcnt[0], c->hcnt[1], c->hdesc[0], c->hdesc[1]};
     for (void* q : ptrs)
@@ -279,12 +280,12 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     const double px = (double)g.W * g.H * n;
     {
         Launch L(c, KC_HESS_FIRST, 12.0 * px * N, s);
-        launch_hess_first(c->Lt, c->Lx, c->Ly, c->img_stride, g, n, c->lt, s);
+        launch_hess_first(c->Lt, c->Lxy, c->img_stride, g, n, c->lt, s);
     }
     KZ_CHECK_LAUNCH(c, "hess_first");
     {
         Launch L(c, KC_HESS_DET, 12.0 * px * N, s);
-        launch_hess_det(c->Lx, c->Ly, c->Ldet, c->img_stride, g, n, c->lt, s);
+        launch_hess_det(c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s);
     }
     KZ_CHECK_LAUNCH(c, "hess_det");
     if (N < 3) {
@@ -317,7 +318,7 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
 kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_counts, float* d_desc, cudaStream_t s) {
     {
         Launch L(c, KC_DESCRIBE, 0.0, s);
-        launch_describe(c->Lx, c->Ly, c->img_stride, c->geom, c->n, c->N, d_kps, d_counts, c->p.max_keypoints, d_desc,
+        launch_describe(c->Lxy, c->img_stride, c->geom, c->n, c->N, d_kps, d_counts, c->p.max_keypoints, d_desc,
                         c->p.ori_windows, (c->p.flags & KAZE_FLAG_KEEP_ANGLE) ? 1 : 0, s);
     }
     KZ_CHECK_LAUNCH(c, "describe");
@@ -413,8 +414,8 @@ kaze_status kaze_create(const kaze_params* p, int device, kaze_ctx** out) {
     const size_t pyr = sizeof(float) * c->plane_max * N * B;
     const int words = (p->max_width + 31) / 32;
     const size_t rows = (size_t)(N > 2 ? N - 2 : 1) * p->max_height * B;
-    bool ok = cudaMalloc(&c->Lt, pyr) == cudaSuccess && cudaMalloc(&c->Lx, pyr) == cudaSuccess &&
-              cudaMalloc(&c->Ly, pyr) == cudaSuccess && cudaMalloc(&c->Ldet, pyr) == cudaSuccess &&
+    bool ok = cudaMalloc(&c->Lt, pyr) == cudaSuccess && cudaMalloc(&c->Lxy, 2 * pyr) == cudaSuccess &&
+              cudaMalloc(&c->Ldet, pyr) == cudaSuccess &&
               cudaMalloc(&c->cbuf, sizeof(float) * c->plane_max * B) == cudaSuccess &&
               cudaMalloc(&c->ubuf, sizeof(float) * c->plane_max * B) == cudaSuccess &&
               cudaMalloc(&c->kval, sizeof(float) * B) == cudaSuccess &&
@@ -591,8 +592,8 @@ static kaze_status plane_ptr(kaze_ctx* c, int32_t img, int32_t level, int32_t wh
     const size_t off = (size_t)img * c->img_stride + (size_t)level * c->geom.plane;
     switch (which) {
         case KAZE_PLANE_LT: *out = c->Lt + off; break;
-        case KAZE_PLANE_LX: *out = c->Lx + off; break;
-        case KAZE_PLANE_LY: *out = c->Ly + off; break;
+        case KAZE_PLANE_LX:
+        case KAZE_PLANE_LY: *out = reinterpret_cast<float*>(c->Lxy + off); break;
         case KAZE_PLANE_LDET: *out = c->Ldet + off; break;
         case KAZE_PLANE_COND: *out = c->cbuf + (size_t)img * c->geom.plane; break;
         default: return KAZE_ERR_INVALID_ARGUMENT;
@@ -606,6 +607,12 @@ kaze_status kaze_get_level(kaze_ctx* c, int32_t img, int32_t level, int32_t whic
     kaze_status st = plane_ptr(c, img, level, which, &src);
     if (st != KAZE_OK) return st;
     DeviceGuard guard(c->device);
+    if (which == KAZE_PLANE_LX || which == KAZE_PLANE_LY) {
+        launch_component_copy(reinterpret_cast<float2*>(src), which == KAZE_PLANE_LY, d_out, 1, c->geom,
+                              (cudaStream_t)stream);
+        KZ_CHECK_LAUNCH(c, "get_level");
+        return KAZE_OK;
+    }
     KZ_CUDA(c, cudaMemcpy2DAsync(d_out, sizeof(float) * c->W, src, sizeof(float) * c->geom.P, sizeof(float) * c->W,
                                  c->H, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     return KAZE_OK;
@@ -617,6 +624,12 @@ kaze_status kaze_set_level(kaze_ctx* c, int32_t img, int32_t level, int32_t whic
     kaze_status st = plane_ptr(c, img, level, which, &dst);
     if (st != KAZE_OK) return st;
     DeviceGuard guard(c->device);
+    if (which == KAZE_PLANE_LX || which == KAZE_PLANE_LY) {
+        launch_component_copy(reinterpret_cast<float2*>(dst), which == KAZE_PLANE_LY, const_cast<float*>(d_in), 0,
+                              c->geom, (cudaStream_t)stream);
+        KZ_CHECK_LAUNCH(c, "set_level");
+        return KAZE_OK;
+    }
     KZ_CUDA(c, cudaMemcpy2DAsync(dst, sizeof(float) * c->geom.P, d_in, sizeof(float) * c->W, sizeof(float) * c->W,
                                  c->H, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     return KAZE_OK;

@@ -58,10 +58,14 @@ bool launch_aos_rows(const float* L, const float* c, const float* U, float* Lout
                      float tau, cudaStream_t s);
 
 // ---- hessian.cu ----  (all N levels of nimg images in one launch; level stride = plane)
-void launch_hess_first(const float* Lt, float* Lx, float* Ly, size_t img_stride, Geom g, int nimg,
-                       const LevelTable& lt, cudaStream_t s);
-void launch_hess_det(const float* Lx, const float* Ly, float* Ldet, size_t img_stride, Geom g, int nimg,
-                     const LevelTable& lt, cudaStream_t s);
+// Lxy: interleaved (s·∂x L, s·∂y L) float2 planes, same element strides as the float pyramids.
+void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
+                       cudaStream_t s);
+void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
+                     cudaStream_t s);
+// Diagnostic copy of one component of an interleaved plane to/from a tightly packed w x h buffer
+// (to_tight = 1: plane → tight).
+void launch_component_copy(float2* plane, int comp, float* tight, int to_tight, Geom g, cudaStream_t s);
 
 // ---- detect.cu ----
 struct DetectParams {
@@ -78,7 +82,7 @@ void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, cons
 
 // ---- describe.cu ----
 void init_describe_tables();
-void launch_describe(const float* Lx, const float* Ly, size_t img_stride, Geom g, int nimg, int N,
+void launch_describe(const float2* Lxy, size_t img_stride, Geom g, int nimg, int N,
                      kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
                      cudaStream_t s);
 

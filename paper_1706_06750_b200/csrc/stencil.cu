@@ -63,48 +63,67 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ in,
 
 // -------------------------------------------------------------------------------------------------
 // |∇(G1 * L)|² → c (mode 1) or |∇|² + max|∇| (mode 0).  G(σ=1) has radius 3 (A6).
+// Shared-memory traffic is kept to ~12 accesses per pixel with register sliding windows:
+//   L tile  tL[u]  = L(clamp(u)) for u in [x0-4, x0+35]²   (odd pitch 41: per-row sweeps are conflict free)
+//   tH[r][v]       = Σ_d g_d tL[r][v+d]      horizontal G1, one thread per tile row (two halves)
+//   tS[v][v']      = Σ_d g_d tH[v+d][v']     vertical G1, one thread per column (four row groups)
+// tS holds Ls at the virtual coordinates [x0-1, x0+32]²; it equals Ls(clamp(v)) wherever v is inside the
+// image, and the Scharr reads Ls at clamped coordinates only (A16), so border tiles need no special path.
 constexpr int R1 = 3;
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cond(const float* __restrict__ L, size_t in_img_stride,
                                               float* __restrict__ out, size_t out_img_stride, Geom g,
                                               GaussTaps t, int diffusivity, const float* __restrict__ kval,
                                               unsigned* __restrict__ hmax_bits) {
-    constexpr int H0 = R1 + 1;                  // halo of the L tile
-    constexpr int LW = TW + 2 * H0, LH = TH + 2 * H0;
-    constexpr int SW = TW + 2, SH = TH + 2;     // Ls tile: virtual coords [x0-1, x0+TW]
-    __shared__ float tL[LH][LW];                // L(clamp(u))
-    __shared__ float tH[LH][SW + 1];            // horizontal pass at clamped Ls columns
-    __shared__ float tS[SH][SW + 1];            // Ls(clamp(v))
+    constexpr int H0 = R1 + 1;              // halo of the L tile
+    constexpr int LN = TW + 2 * H0;         // 40 (square tile, TW == TH)
+    constexpr int SN = TW + 2;              // 34
+    __shared__ float tL[LN][LN + 1];
+    __shared__ float tH[LN][SN + 1];
+    __shared__ float tS[SN][SN + 1];
     __shared__ float red[8];
+    static_assert(TW == TH, "square tiles");
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, img = blockIdx.z;
     const float* src = L + img * in_img_stride;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-    for (int ly = ty; ly < LH; ly += 8) {
+    for (int ly = ty; ly < LN; ly += 8) {
         const float* row = src + (size_t)clampi(y0 - H0 + ly, 0, g.H - 1) * g.P;
-        for (int lx = tx; lx < LW; lx += 32) tL[ly][lx] = __ldg(row + clampi(x0 - H0 + lx, 0, g.W - 1));
+        for (int lx = tx; lx < LN; lx += 32) tL[ly][lx] = __ldg(row + clampi(x0 - H0 + lx, 0, g.W - 1));
     }
     float w[2 * R1 + 1];
 #pragma unroll
     for (int d = 0; d <= 2 * R1; ++d) w[d] = t.w[d];
     __syncthreads();
-    // horizontal pass for every L-tile row at the clamped Ls columns cv = clamp(x0 - 1 + sx)
-    for (int ly = ty; ly < LH; ly += 8) {
-        for (int sx = tx; sx < SW; sx += 32) {
-            const int base = clampi(x0 - 1 + sx, 0, g.W - 1) - (x0 - H0) - R1;
+    if (tid < 2 * LN) {  // horizontal: row r, output columns [17h, 17h+17)
+        constexpr int NO = SN / 2;  // 17
+        const int r = tid % LN, h = tid / LN;
+        float win[NO + 2 * R1];
+#pragma unroll
+        for (int i = 0; i < NO + 2 * R1; ++i) win[i] = tL[r][NO * h + i];
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
             float acc = 0.f;
 #pragma unroll
-            for (int d = 0; d <= 2 * R1; ++d) acc = fmaf(w[d], tL[ly][base + d], acc);
-            tH[ly][sx] = acc;
+            for (int d = 0; d <= 2 * R1; ++d) acc = fmaf(w[d], win[o + d], acc);
+            tH[r][NO * h + o] = acc;
         }
     }
     __syncthreads();
-    for (int sy = ty; sy < SH; sy += 8) {
-        const int base = clampi(y0 - 1 + sy, 0, g.H - 1) - (y0 - H0) - R1;
-        for (int sx = tx; sx < SW; sx += 32) {
-            float acc = 0.f;
+    if (tid < 4 * SN) {  // vertical: column v, output rows [9q, min(9q+9, 34))
+        constexpr int NO = 9;
+        const int v = tid % SN, q = tid / SN;
+        const int r0 = NO * q;
+        float win[NO + 2 * R1];
 #pragma unroll
-            for (int d = 0; d <= 2 * R1; ++d) acc = fmaf(w[d], tH[base + d][sx], acc);
-            tS[sy][sx] = acc;
+        for (int i = 0; i < NO + 2 * R1; ++i) win[i] = (r0 + i < LN) ? tH[r0 + i][v] : 0.f;
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
+            if (r0 + o < SN) {
+                float acc = 0.f;
+#pragma unroll
+                for (int d = 0; d <= 2 * R1; ++d) acc = fmaf(w[d], win[o + d], acc);
+                tS[r0 + o][v] = acc;
+            }
         }
     }
     __syncthreads();
@@ -116,17 +135,26 @@ __global__ void __launch_bounds__(256) k_cond(const float* __restrict__ L, size_
     float lmax = 0.f;
     float* dst = out + img * out_img_stride;
     const int x = x0 + tx;
-    // Ls tile index of virtual coordinate v is v - (x0 - 1); the Scharr reads Ls(clamp(x±1), clamp(y±1))
+    // tS index of virtual coordinate v is v - (x0 - 1); the Scharr reads Ls(clamp(x±1), clamp(y±1))
     const int xm = clampi(x - 1, 0, g.W - 1) - (x0 - 1), xp = clampi(x + 1, 0, g.W - 1) - (x0 - 1), xc = tx + 1;
+    const int yb = y0 + 4 * ty;  // four output rows per thread
+    float cm[6], cc[6], cp[6];
 #pragma unroll
-    for (int k = 0; k < TH / 8; ++k) {
-        const int y = y0 + ty + 8 * k;
-        const int ym = clampi(y - 1, 0, g.H - 1) - (y0 - 1), yp = clampi(y + 1, 0, g.H - 1) - (y0 - 1);
-        const int yc = y - (y0 - 1);
-        float gx = 0.1875f * (tS[ym][xp] - tS[ym][xm]) + 0.625f * (tS[yc][xp] - tS[yc][xm]) +
-                   0.1875f * (tS[yp][xp] - tS[yp][xm]);
-        float gy = 0.1875f * (tS[yp][xm] - tS[ym][xm]) + 0.625f * (tS[yp][xc] - tS[ym][xc]) +
-                   0.1875f * (tS[yp][xp] - tS[ym][xp]);
+    for (int i = 0; i < 6; ++i) {
+        const int yy = clampi(yb - 1 + i, 0, g.H - 1) - (y0 - 1);
+        cm[i] = tS[yy][xm];
+        cc[i] = tS[yy][xc];
+        cp[i] = tS[yy][xp];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int y = yb + k;
+        // window rows k, k+1, k+2 hold clamp(y-1), y, clamp(y+1) unless y is the first/last image row
+        const bool top = (y == 0), bot = (y == g.H - 1);
+        const float mm = top ? cm[k + 1] : cm[k], mc = top ? cc[k + 1] : cc[k], mp = top ? cp[k + 1] : cp[k];
+        const float pm = bot ? cm[k + 1] : cm[k + 2], pc = bot ? cc[k + 1] : cc[k + 2], pp = bot ? cp[k + 1] : cp[k + 2];
+        float gx = 0.1875f * (mp - mm) + 0.625f * (cp[k + 1] - cm[k + 1]) + 0.1875f * (pp - pm);
+        float gy = 0.1875f * (pm - mm) + 0.625f * (pc - mc) + 0.1875f * (pp - mp);
         gx *= 0.5f;
         gy *= 0.5f;
         const float g2 = gx * gx + gy * gy;
