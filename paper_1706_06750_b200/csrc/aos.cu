@@ -18,16 +18,11 @@
 // memory with coalesced 16-byte loads; the chunk length M is odd so the per-thread sweeps (stride M) are
 // bank-conflict free.
 #include "kaze_internal.cuh"
+#include "ptx.cuh"
 
 namespace kz {
 
 namespace {
-
-__device__ __forceinline__ float frcp(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
 
 // Parallel cyclic reduction of a tridiagonal system with one equation per thread (p = 0..TP-1 within its
 // system, idx = p*stride + off in the shared arrays).  Threads p >= T carry identity rows.  Returns x_p.
@@ -217,94 +212,120 @@ __global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, co
 }
 
 // -------------------------------------------------------------------------------------------------------------
-// Row systems: one row per CTA, staged contiguously in shared memory (M odd → stride-M sweeps are conflict free).
+// Row systems: a persistent CTA walks rows q = blockIdx.x, +gridDim.x, ... of all images.  Each row's L, c and U
+// are fetched by the TMA engine (1-D bulk copies, one mbarrier per stage) into a double-buffered shared stage, so
+// the next row streams in while the current one is solved.  The row is solved from shared memory (contiguous
+// layout; M odd → stride-M sweeps are conflict free), x overwrites L in place, and L_i = ½(U + x) is written with
+// coalesced 16-byte stores.
 template <int M>
 __global__ void __launch_bounds__(256) k_aos_rows(const float* __restrict__ L, const float* __restrict__ c,
                                                   const float* __restrict__ U, float* __restrict__ Lout, Strides st,
-                                                  Geom g, float tau, int T, int TP) {
+                                                  Geom g, float tau, int T, int TP, int total_rows) {
     static_assert(M % 2 == 1, "row chunks must have odd length");
     constexpr int MC = M + 1;
-    extern __shared__ float4 sm4[];
+    extern __shared__ __align__(128) float smf[];
     const int n = g.W;
-    const int nv = (n + 3) >> 2;
-    float* sL = reinterpret_cast<float*>(sm4);  // 4*nv
-    float* sC = sL + 4 * nv;                     // 4*nv
-    float* sa = sC + 4 * nv;                     // TP each
+    const int Wp = (n + 3) & ~3;              // row floats fetched (16-byte multiple; stays inside the pitch)
+    float* stage = smf;                        // [2][3][Wp]: L, c, U
+    float* sa = stage + 6 * Wp;                // PCR + last-equation exchange, TP each
     float* sb = sa + TP;
     float* sc = sb + TP;
     float* sd = sc + TP;
     float* sla = sd + TP;
     float* slg = sla + TP;
     float* sld = slg + TP;
-    const size_t ry = (size_t)blockIdx.x * g.P;
-    const float* Lr = L + blockIdx.z * st.L + ry;
-    const float* cr = c + blockIdx.z * st.c + ry;
-    const float* Ur = U + blockIdx.z * st.U + ry;
-    float* Or = Lout + blockIdx.z * st.out + ry;
-    // rows start 128-byte aligned (pitch multiple of 32 floats); reading up to 4*nv <= P floats stays in the row
-    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-        reinterpret_cast<float4*>(sL)[v] = __ldg(reinterpret_cast<const float4*>(Lr) + v);
-        reinterpret_cast<float4*>(sC)[v] = __ldg(reinterpret_cast<const float4*>(cr) + v);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sld + TP + ((TP & 1) ? 1 : 0));
+    const int tid = threadIdx.x;
+    const uint32_t bytes = (uint32_t)Wp * 4u;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
     }
     __syncthreads();
-    const int p = threadIdx.x;
+    auto issue = [&](int q, int sidx) {
+        const int img = q / g.H, y = q - img * g.H;
+        const size_t ry = (size_t)y * g.P;
+        float* dst = stage + sidx * 3 * Wp;
+        mbar_arrive_expect_tx(&bar[sidx], 3u * bytes);
+        bulk_g2s(dst, L + img * st.L + ry, bytes, &bar[sidx]);
+        bulk_g2s(dst + Wp, c + img * st.c + ry, bytes, &bar[sidx]);
+        bulk_g2s(dst + 2 * Wp, U + img * st.U + ry, bytes, &bar[sidx]);
+    };
+    int q = blockIdx.x;
+    if (tid == 0 && q < total_rows) issue(q, 0);
+    const int p = tid;
     const bool active = p < T;
     const int j0 = p * M;
     const int j1 = (p == T - 1) ? n : j0 + M;
     const int m = active ? j1 - j0 : 0;
-    Chunk<MC> ch;
-    if (active) {
-        float dv[MC], cv[MC];
+    for (int it = 0; q < total_rows; ++it, q += gridDim.x) {
+        const int sidx = it & 1;
+        if (tid == 0 && q + (int)gridDim.x < total_rows) issue(q + gridDim.x, sidx ^ 1);
+        mbar_wait(&bar[sidx], (uint32_t)(it >> 1) & 1u);
+        float* sL = stage + sidx * 3 * Wp;
+        const float* sC = sL + Wp;
+        const float* sU = sL + 2 * Wp;
+        Chunk<MC> ch;
+        if (active) {
+            float dv[MC], cv[MC];
 #pragma unroll
-        for (int i = 0; i < MC; ++i) {
-            dv[i] = i < m ? sL[j0 + i] : 0.f;
-            cv[i] = i < m ? sC[j0 + i] : 0.f;
+            for (int i = 0; i < MC; ++i) {
+                dv[i] = i < m ? sL[j0 + i] : 0.f;
+                cv[i] = i < m ? sC[j0 + i] : 0.f;
+            }
+            const float cprev = p > 0 ? sC[j0 - 1] : 0.f;
+            const float cnext = j1 < n ? sC[j1] : 0.f;
+            eliminate<MC>(ch, dv, cv, cprev, cnext, m, p == 0, p == T - 1, tau);
+        } else {
+            ch.A = ch.C = ch.D = 0.f;
+            ch.lA = ch.lG = ch.lD = 0.f;
         }
-        const float cprev = p > 0 ? sC[j0 - 1] : 0.f;
-        const float cnext = j1 < n ? sC[j1] : 0.f;
-        eliminate<MC>(ch, dv, cv, cprev, cnext, m, p == 0, p == T - 1, tau);
-    } else {
-        ch.A = ch.C = ch.D = 0.f;
-        ch.lA = ch.lG = ch.lD = 0.f;
-    }
-    sla[p] = ch.lA;
-    slg[p] = ch.lG;
-    sld[p] = ch.lD;
-    __syncthreads();
-    float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
-    if (active) {
-        float pA = 0.f, pG = 0.f, pD = 0.f;
-        if (p > 0) {
-            pA = sla[p - 1];
-            pG = slg[p - 1];
-            pD = sld[p - 1];
+        sla[p] = ch.lA;
+        slg[p] = ch.lG;
+        sld[p] = ch.lD;
+        __syncthreads();
+        float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
+        if (active) {
+            float pA = 0.f, pG = 0.f, pD = 0.f;
+            if (p > 0) {
+                pA = sla[p - 1];
+                pG = slg[p - 1];
+                pD = sld[p - 1];
+            }
+            af = -ch.A * pA;
+            bf = 1.f - ch.A * pG - ch.C * ch.lA;
+            cf = -ch.C * ch.lG;
+            df = ch.D - ch.A * pD - ch.C * ch.lD;
         }
-        af = -ch.A * pA;
-        bf = 1.f - ch.A * pG - ch.C * ch.lA;
-        cf = -ch.C * ch.lG;
-        df = ch.D - ch.A * pD - ch.C * ch.lD;
-    }
-    const float xf = pcr_solve(af, bf, cf, df, p, TP, 1, p, sa, sb, sc, sd);
-    sa[p] = xf;
-    __syncthreads();
-    if (active) {
-        const float xnext = (p + 1 < T) ? sa[p + 1] : 0.f;
-        const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
-        sL[j0] = xf;
+        const float xf = pcr_solve(af, bf, cf, df, p, TP, 1, p, sa, sb, sc, sd);
+        sa[p] = xf;
+        __syncthreads();
+        if (active) {
+            const float xnext = (p + 1 < T) ? sa[p + 1] : 0.f;
+            const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
+            sL[j0] = xf;
 #pragma unroll
-        for (int i = 1; i < MC; ++i)
-            if (i < m - 1) sL[j0 + i] = ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl;
-        sL[j1 - 1] = xl;
+            for (int i = 1; i < MC; ++i)
+                if (i < m - 1) sL[j0 + i] = ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl;
+            sL[j1 - 1] = xl;
+        }
+        __syncthreads();
+        {
+            const int img = q / g.H, y = q - img * g.H;
+            float* Or = Lout + img * st.out + (size_t)y * g.P;
+            const int nfull = n >> 2;
+            for (int v = tid; v < nfull; v += blockDim.x) {
+                const float4 u = reinterpret_cast<const float4*>(sU)[v];
+                const float4 x = reinterpret_cast<const float4*>(sL)[v];
+                reinterpret_cast<float4*>(Or)[v] =
+                    make_float4(0.5f * (u.x + x.x), 0.5f * (u.y + x.y), 0.5f * (u.z + x.z), 0.5f * (u.w + x.w));
+            }
+            for (int j = 4 * nfull + tid; j < n; j += blockDim.x) Or[j] = 0.5f * (sU[j] + sL[j]);
+        }
+        fence_proxy_async();  // generic-proxy writes of this stage before the TMA refills it
+        __syncthreads();
     }
-    __syncthreads();
-    const int nfull = n >> 2;
-    for (int v = threadIdx.x; v < nfull; v += blockDim.x) {
-        const float4 u = __ldg(reinterpret_cast<const float4*>(Ur) + v);
-        const float4 x = reinterpret_cast<const float4*>(sL)[v];
-        reinterpret_cast<float4*>(Or)[v] = make_float4(0.5f * (u.x + x.x), 0.5f * (u.y + x.y), 0.5f * (u.z + x.z),
-                                                       0.5f * (u.w + x.w));
-    }
-    for (int j = 4 * nfull + threadIdx.x; j < n; j += blockDim.x) Or[j] = 0.5f * (__ldg(Ur + j) + sL[j]);
 }
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -318,19 +339,34 @@ void run_cols(const float* L, const float* c, float* U, Strides st, Geom g, int 
     k_aos_cols<CW, M, NT><<<grid, CW * TP, smem, s>>>(L, c, U, st, g, tau, T, TP);
 }
 
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
 template <int M>
 void run_rows(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg, float tau,
               cudaStream_t s) {
     const int T = n_chunks(g.W, M);
     const int TP = round_up(T, 32);
-    const size_t smem = sizeof(float) * (8 * ((g.W + 3) / 4) + 7 * TP);
+    const int Wp = (g.W + 3) & ~3;
+    const size_t smem = sizeof(float) * (6 * Wp + 7 * TP + 2) + 2 * sizeof(uint64_t);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_aos_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_aos_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    dim3 grid(g.H, 1, nimg);
-    k_aos_rows<M><<<grid, TP, smem, s>>>(L, c, U, Lout, st, g, tau, T, TP);
+    const int total = g.H * nimg;
+    int per_sm = (int)((220 * 1024) / (smem + 1024));
+    per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+    const int grid = total < num_sms() * per_sm ? total : num_sms() * per_sm;
+    k_aos_rows<M><<<grid, TP, smem, s>>>(L, c, U, Lout, st, g, tau, T, TP, total);
 }
 
 }  // namespace

@@ -66,23 +66,17 @@ __device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const 
 // are staged in shared memory with coalesced loads, then every pixel is tested from shared memory.
 constexpr int NX = 256, NY = 4;
 
+// Branch-free 26-neighbour maximum from the staged tile, then the (rare) edge test and sub-pixel fit.
 __device__ __forceinline__ bool is_keypoint_smem(const float (*T)[NY + 2][NX + 2], int r, int c, float thr, float er) {
     const float v = T[1][r][c];
-    if (!(v > thr)) return false;
+    float m = fmaxf(T[1][r][c - 1], T[1][r][c + 1]);
 #pragma unroll
-    for (int dy = -1; dy <= 1; ++dy)
+    for (int dx = -1; dx <= 1; ++dx) {
+        m = fmaxf(m, fmaxf(T[1][r - 1][c + dx], T[1][r + 1][c + dx]));
 #pragma unroll
-        for (int dx = -1; dx <= 1; ++dx) {
-            if (dx == 0 && dy == 0) continue;
-            if (!(v > T[1][r + dy][c + dx])) return false;
-        }
-#pragma unroll
-    for (int l = 0; l <= 2; l += 2)
-#pragma unroll
-        for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-            for (int dx = -1; dx <= 1; ++dx)
-                if (!(v > T[l][r + dy][c + dx])) return false;
+        for (int dy = -1; dy <= 1; ++dy) m = fmaxf(m, fmaxf(T[0][r + dy][c + dx], T[2][r + dy][c + dx]));
+    }
+    if (!(v > thr) || !(v > m)) return false;
     float patch[3][3];
 #pragma unroll
     for (int dy = -1; dy <= 1; ++dy)
@@ -103,12 +97,11 @@ __global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet
     const int tid = threadIdx.x;
     if (tid < NY) rc[tid] = 0;
     // stage rows y0-1 .. y0+NY, columns x0-1 .. x0+NX (clamped; border pixels are never candidates)
-    for (int l = 0; l < 3; ++l) {
-        const float* Dl = D0 + (ptrdiff_t)(l - 1) * (ptrdiff_t)g.plane;
-        for (int r = 0; r < NY + 2; ++r) {
-            const float* row = Dl + (size_t)clampi(y0 - 1 + r, 0, g.H - 1) * g.P;
-            for (int cidx = tid; cidx < NX + 2; cidx += 256) T[l][r][cidx] = __ldg(row + clampi(x0 - 1 + cidx, 0, g.W - 1));
-        }
+    for (int i = tid; i < 3 * (NY + 2) * (NX + 2); i += 256) {
+        const int l = i / ((NY + 2) * (NX + 2)), rem = i - l * (NY + 2) * (NX + 2);
+        const int r = rem / (NX + 2), cidx = rem - r * (NX + 2);
+        const float* row = D0 + (ptrdiff_t)(l - 1) * (ptrdiff_t)g.plane + (size_t)clampi(y0 - 1 + r, 0, g.H - 1) * g.P;
+        T[l][r][cidx] = __ldg(row + clampi(x0 - 1 + cidx, 0, g.W - 1));
     }
     __syncthreads();
     const int words = (g.W + 31) / 32;
