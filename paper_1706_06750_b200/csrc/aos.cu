@@ -34,26 +34,17 @@ __device__ __forceinline__ float pcr_solve(float af, float bf, float cf, float d
         sc[idx] = cf;
         sd[idx] = df;
         __syncthreads();
-        float na = 0.f, nc = 0.f, nb = bf, nd = df;
-        if (p >= st) {
-            const int j = idx - st * stride;
-            const float k1 = af * frcp(sb[j]);
-            na = -sa[j] * k1;
-            nb -= sc[j] * k1;
-            nd -= sd[j] * k1;
-        }
-        if (p + st < TP) {
-            const int j = idx + st * stride;
-            const float k2 = cf * frcp(sb[j]);
-            nc = -sc[j] * k2;
-            nb -= sa[j] * k2;
-            nd -= sd[j] * k2;
-        }
+        const bool hm = p >= st, hp = p + st < TP;
+        const int jm = hm ? idx - st * stride : idx, jp = hp ? idx + st * stride : idx;
+        const float am = sa[jm], bm = sb[jm], cm = sc[jm], dm = sd[jm];
+        const float ap = sa[jp], bp = sb[jp], cp = sc[jp], dp = sd[jp];
+        const float k1 = hm ? af * frcp(bm) : 0.f;
+        const float k2 = hp ? cf * frcp(bp) : 0.f;
         __syncthreads();
-        af = na;
-        bf = nb;
-        cf = nc;
-        df = nd;
+        af = -am * k1;
+        cf = -cp * k2;
+        bf = bf - cm * k1 - ap * k2;
+        df = df - dm * k1 - dp * k2;
     }
     return df * frcp(bf);
 }
@@ -125,6 +116,57 @@ __device__ __forceinline__ void eliminate(Chunk<MC>& ch, const float (&dv)[MC], 
     ch.D = (dv[0] - c0 * nd) * rB;
 }
 
+// Fast path for a full chunk of exactly M samples (every chunk but possibly the last): no per-sample predicates.
+// tq[i] = τ(c_{i-1} + c_i) for i = 0..M (tq[0] uses c at j0-1, tq[M] c at j0+M; zeroed at the line ends), so
+// a_i = -tq[i], cc_i = -tq[i+1], b_i = 1 + tq[i] + tq[i+1].
+template <int M>
+__device__ __forceinline__ void eliminate_full(Chunk<M + 1>& ch, const float (&dv)[M + 1], const float (&cv)[M + 1],
+                                               float cprev, float cnext, bool first_chunk, bool last_chunk, float tau) {
+    float tq[M + 1], bb[M];
+    tq[0] = first_chunk ? 0.f : tau * (cprev + cv[0]);
+#pragma unroll
+    for (int i = 1; i < M; ++i) tq[i] = tau * (cv[i - 1] + cv[i]);
+    tq[M] = last_chunk ? 0.f : tau * (cv[M - 1] + cnext);
+#pragma unroll
+    for (int i = 0; i < M; ++i) bb[i] = 1.f + tq[i] + tq[i + 1];
+    float pa = -1.f, pg = 0.f, pd = 0.f;
+#pragma unroll
+    for (int i = 1; i < M; ++i) {
+        const float r = frcp(fmaf(tq[i], pg, bb[i]));  // b_i - a_i γ_{i-1}
+        const float na = tq[i] * pa * r;
+        const float ng = -tq[i + 1] * r;
+        const float nd = fmaf(tq[i], pd, dv[i]) * r;
+        ch.al[i] = na;
+        ch.ga[i] = ng;
+        ch.de[i] = nd;
+        pa = na;
+        pg = ng;
+        pd = nd;
+    }
+    ch.lA = pa;
+    ch.lG = pg;
+    ch.lD = pd;
+    float na = 0.f, ng = -1.f, nd = 0.f;
+#pragma unroll
+    for (int i = M - 2; i >= 1; --i) {
+        const float gi = ch.ga[i];
+        const float a2 = ch.al[i] - gi * na;
+        const float g2 = -gi * ng;
+        const float d2 = ch.de[i] - gi * nd;
+        ch.al[i] = a2;
+        ch.ga[i] = g2;
+        ch.de[i] = d2;
+        na = a2;
+        ng = g2;
+        nd = d2;
+    }
+    // row 0: a0 = -tq[0], cc0 = -tq[1], b0 = bb[0]
+    const float rB = frcp(fmaf(tq[1], na, bb[0]));
+    ch.A = -tq[0] * rB;
+    ch.C = tq[1] * ng * rB;
+    ch.D = fmaf(tq[1], nd, dv[0]) * rB;
+}
+
 // Chunking of a line of n samples into chunks of M: T chunks, chunk p = [p*M, p*M + size), the last one takes the
 // remainder; a remainder of 1 is merged into the previous chunk (so 2 <= size <= M+1).
 __host__ __device__ inline int n_chunks(int n, int M) {
@@ -173,7 +215,8 @@ __global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, co
         }
         const float cprev = j0 > 0 ? __ldg(cc - g.P) : 0.f;
         const float cnext = j1 < n ? __ldg(cc + (size_t)m * g.P) : 0.f;
-        eliminate<MC>(ch, dv, cv, cprev, cnext, m, j0 == 0, j1 == n, tau);
+        if (m == M) eliminate_full<M>(ch, dv, cv, cprev, cnext, j0 == 0, j1 == n, tau);
+        else eliminate<MC>(ch, dv, cv, cprev, cnext, m, j0 == 0, j1 == n, tau);
     } else {
         ch.A = ch.C = ch.D = 0.f;
         ch.lA = ch.lG = ch.lD = 0.f;
@@ -276,7 +319,8 @@ __global__ void __launch_bounds__(256) k_aos_rows(const float* __restrict__ L, c
             }
             const float cprev = p > 0 ? sC[j0 - 1] : 0.f;
             const float cnext = j1 < n ? sC[j1] : 0.f;
-            eliminate<MC>(ch, dv, cv, cprev, cnext, m, p == 0, p == T - 1, tau);
+            if (m == M) eliminate_full<M>(ch, dv, cv, cprev, cnext, p == 0, p == T - 1, tau);
+            else eliminate<MC>(ch, dv, cv, cprev, cnext, m, p == 0, p == T - 1, tau);
         } else {
             ch.A = ch.C = ch.D = 0.f;
             ch.lA = ch.lG = ch.lD = 0.f;

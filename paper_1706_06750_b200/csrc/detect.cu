@@ -62,62 +62,75 @@ __device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const 
     return refine(patch, er, ox, oy);
 }
 
-// nms_mark tile: 256 columns x 4 rows of one level of one image; the three levels' (4+2) x (256+2) neighbourhoods
-// are staged in shared memory with coalesced loads, then every pixel is tested from shared memory.
-constexpr int NX = 256, NY = 4;
-
-// Branch-free 26-neighbour maximum from the staged tile, then the (rare) edge test and sub-pixel fit.
-__device__ __forceinline__ bool is_keypoint_smem(const float (*T)[NY + 2][NX + 2], int r, int c, float thr, float er) {
-    const float v = T[1][r][c];
-    float m = fmaxf(T[1][r][c - 1], T[1][r][c + 1]);
-#pragma unroll
-    for (int dx = -1; dx <= 1; ++dx) {
-        m = fmaxf(m, fmaxf(T[1][r - 1][c + dx], T[1][r + 1][c + dx]));
-#pragma unroll
-        for (int dy = -1; dy <= 1; ++dy) m = fmaxf(m, fmaxf(T[0][r + dy][c + dx], T[2][r + dy][c + dx]));
-    }
-    if (!(v > thr) || !(v > m)) return false;
-    float patch[3][3];
-#pragma unroll
-    for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-        for (int dx = -1; dx <= 1; ++dx) patch[dy + 1][dx + 1] = T[1][r + dy][c + dx];
-    float ox, oy;
-    return refine(patch, er, ox, oy);
-}
+// nms_mark tile: 256 columns x NY rows of one level of one image, one thread per column.  Each thread loads its
+// column of the three levels (NY+2 rows each) into registers with coalesced row loads, forms the vertical 3-maxima
+// in registers and publishes them in shared memory; the 26-neighbour maximum of a pixel is then
+//   max( V_{i-1}[c-1..c+1][r], V_{i+1}[c-1..c+1][r], V_i[c±1][r], D_i[c][r±1] )
+// (V = vertical 3-max), a handful of operations per pixel.  Only candidates run the edge test / sub-pixel fit.
+constexpr int NX = 256, NY = 8;
 
 __global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
                                                   DetectParams dp, uint32_t* __restrict__ bitmap,
                                                   int* __restrict__ rowcnt) {
-    __shared__ float T[3][NY + 2][NX + 2];
+    __shared__ float V[3][NY][NX + 2];   // vertical 3-max per level, row r (output rows), column c (tile coords)
+    __shared__ float C1[NY + 2][NX + 2]; // level-i values (for the 3x3 patch of candidates)
     __shared__ int rc[NY];
     const int x0 = blockIdx.x * NX, y0 = blockIdx.y * NY;
     const int li = blockIdx.z % (N - 2), img = blockIdx.z / (N - 2), level = li + 1;
     const float* D0 = Ldet + img * img_stride + (size_t)level * g.plane;
     const int tid = threadIdx.x;
     if (tid < NY) rc[tid] = 0;
-    // stage rows y0-1 .. y0+NY, columns x0-1 .. x0+NX (clamped; border pixels are never candidates)
-    for (int i = tid; i < 3 * (NY + 2) * (NX + 2); i += 256) {
-        const int l = i / ((NY + 2) * (NX + 2)), rem = i - l * (NY + 2) * (NX + 2);
-        const int r = rem / (NX + 2), cidx = rem - r * (NX + 2);
-        const float* row = D0 + (ptrdiff_t)(l - 1) * (ptrdiff_t)g.plane + (size_t)clampi(y0 - 1 + r, 0, g.H - 1) * g.P;
-        T[l][r][cidx] = __ldg(row + clampi(x0 - 1 + cidx, 0, g.W - 1));
+    // columns handled by this thread: its own (tile column tid+1) and, for threads 0 / 1, the halo columns 0 / NX+1
+    for (int pass = 0; pass < 2; ++pass) {
+        int col;
+        if (pass == 0) col = tid + 1;
+        else if (tid == 0) col = 0;
+        else if (tid == 1) col = NX + 1;
+        else break;
+        const int gx = clampi(x0 - 1 + col, 0, g.W - 1);
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            const float* Dl = D0 + (ptrdiff_t)(l - 1) * (ptrdiff_t)g.plane + gx;
+            float v[NY + 2];
+#pragma unroll
+            for (int r = 0; r < NY + 2; ++r) v[r] = __ldg(Dl + (size_t)clampi(y0 - 1 + r, 0, g.H - 1) * g.P);
+#pragma unroll
+            for (int r = 0; r < NY; ++r) V[l][r][col] = fmaxf(v[r], fmaxf(v[r + 1], v[r + 2]));
+            if (l == 1) {
+#pragma unroll
+                for (int r = 0; r < NY + 2; ++r) C1[r][col] = v[r];
+            }
+        }
     }
     __syncthreads();
     const int words = (g.W + 31) / 32;
     const int lane = tid & 31, warp = tid >> 5;
-    const int x = x0 + tid;
+    const int x = x0 + tid, c = tid + 1;
+#pragma unroll 1
     for (int r = 0; r < NY; ++r) {
         const int y = y0 + r;
-        const bool k = (y >= 1 && y <= g.H - 2 && x >= 1 && x <= g.W - 2) &&
-                       is_keypoint_smem(T, r + 1, tid + 1, dp.threshold, dp.edge_ratio);
-        const uint32_t bits = __ballot_sync(0xffffffffu, k);
-        if (y < g.H && x0 + warp * 32 < g.W) {
-            const size_t row = ((size_t)img * (N - 2) + li) * g.H + y;
-            if (lane == 0) {
-                bitmap[row * words + (x0 >> 5) + warp] = bits;
-                if (bits) atomicAdd(&rc[r], __popc(bits));
+        bool k = false;
+        if (y >= 1 && y <= g.H - 2 && x >= 1 && x <= g.W - 2) {
+            const float v = C1[r + 1][c];
+            float m = fmaxf(fmaxf(V[0][r][c - 1], V[0][r][c]), V[0][r][c + 1]);
+            m = fmaxf(m, fmaxf(fmaxf(V[2][r][c - 1], V[2][r][c]), V[2][r][c + 1]));
+            m = fmaxf(m, fmaxf(V[1][r][c - 1], V[1][r][c + 1]));
+            m = fmaxf(m, fmaxf(C1[r][c], C1[r + 2][c]));
+            if (v > dp.threshold && v > m) {
+                float patch[3][3];
+#pragma unroll
+                for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < 3; ++dx) patch[dy][dx] = C1[r + dy][c - 1 + dx];
+                float ox, oy;
+                k = refine(patch, dp.edge_ratio, ox, oy);
             }
+        }
+        const uint32_t bits = __ballot_sync(0xffffffffu, k);
+        if (lane == 0 && y < g.H && x0 + warp * 32 < g.W) {
+            const size_t row = ((size_t)img * (N - 2) + li) * g.H + y;
+            bitmap[row * words + (x0 >> 5) + warp] = bits;
+            if (bits) atomicAdd(&rc[r], __popc(bits));
         }
     }
     __syncthreads();
