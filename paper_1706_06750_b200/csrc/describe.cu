@@ -132,9 +132,12 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
         // ---- M-SURF ----
         float si, co;
         sincosf(angle, &si, &co);
+        // lanes walk the rotated axis that runs closest to image x, so a warp's gathers share cache lines
+        const bool u_fast = fabsf(co) >= fabsf(si);
 #pragma unroll 6
         for (int s = lane; s < 576; s += 32) {
-            const int p = s / 24, q = s - p * 24;
+            const int hi = s / 24, lo = s - hi * 24;
+            const int p = u_fast ? lo : hi, q = u_fast ? hi : lo;
             const float u = (float)p - 11.5f, v = (float)q - 11.5f;
             const float px = x + sigma * (u * co - v * si);
             const float py = y + sigma * (u * si + v * co);

@@ -24,8 +24,7 @@ enum KernelClass {
     KC_COND,
     KC_AOS_COLS,
     KC_AOS_ROWS,
-    KC_HESS_FIRST,
-    KC_HESS_DET,
+    KC_HESSIAN,
     KC_NMS_MARK,
     KC_KP_SCAN,
     KC_KP_EMIT,
@@ -33,7 +32,7 @@ enum KernelClass {
     KC_COUNT
 };
 const char* kKernelNames[KC_COUNT] = {"prefilter", "grad_l1",  "k_hist",   "k_final",  "c_from_g2",
-                                      "cond",      "aos_cols", "aos_rows", "hess_first", "hess_det",
+                                      "cond",      "aos_cols", "aos_rows", "hessian",
                                       "nms_mark",  "kp_scan",  "kp_emit",  "describe"};
 
 struct ProfRec {
@@ -278,16 +277,15 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     const int N = c->N, n = c->n;
     const Geom g = c->geom;
     const double px = (double)g.W * g.H * n;
-    {
-        Launch L(c, KC_HESS_FIRST, 12.0 * px * N, s);
-        launch_hess_first(c->Lt, c->Lxy, c->img_stride, g, n, c->lt, s);
+    for (int level = 0; level < N; ++level) {
+        LevelTable one = c->lt;  // launch_hessian walks the levels of the table; one level per launch
+        Launch L(c, KC_HESSIAN, 16.0 * px, s);
+        one.n = 1;
+        one.step[0] = c->lt.step[level];
+        launch_hessian(c->Lt + (size_t)level * g.plane, c->Lxy + (size_t)level * g.plane,
+                       c->Ldet + (size_t)level * g.plane, c->img_stride, g, n, one, s);
     }
-    KZ_CHECK_LAUNCH(c, "hess_first");
-    {
-        Launch L(c, KC_HESS_DET, 12.0 * px * N, s);
-        launch_hess_det(c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s);
-    }
-    KZ_CHECK_LAUNCH(c, "hess_det");
+    KZ_CHECK_LAUNCH(c, "hessian");
     if (N < 3) {
         KZ_CUDA(c, cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * n, s));
     } else {

@@ -34,9 +34,26 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ in,
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
     const float* src = in + blockIdx.z * in_img_stride;
     const int tx = threadIdx.x, ty = threadIdx.y;
-    for (int ly = ty; ly < LH; ly += 8) {
-        const float* row = src + (int64_t)clampi(y0 - R + ly, 0, g.H - 1) * in_pitch;
-        for (int lx = tx; lx < LW; lx += 32) tin[ly][lx] = __ldg(row + clampi(x0 - R + lx, 0, g.W - 1));
+    {   // all tile loads issued before any shared store
+        constexpr int KR = (LH + 7) / 8, KC = (LW + 31) / 32;
+        float v[KR][KC];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int ly = ty + 8 * k;
+            const float* row = src + (int64_t)clampi(y0 - R + ly, 0, g.H - 1) * in_pitch;
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                const int lx = tx + 32 * j;
+                v[k][j] = (ly < LH && lx < LW) ? __ldg(row + clampi(x0 - R + lx, 0, g.W - 1)) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k)
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                const int ly = ty + 8 * k, lx = tx + 32 * j;
+                if (ly < LH && lx < LW) tin[ly][lx] = v[k][j];
+            }
     }
     float w[2 * R + 1];
 #pragma unroll
@@ -86,9 +103,21 @@ __global__ void __launch_bounds__(256) k_cond(const float* __restrict__ L, size_
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, img = blockIdx.z;
     const float* src = L + img * in_img_stride;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-    for (int ly = ty; ly < LN; ly += 8) {
-        const float* row = src + (size_t)clampi(y0 - H0 + ly, 0, g.H - 1) * g.P;
-        for (int lx = tx; lx < LN; lx += 32) tL[ly][lx] = __ldg(row + clampi(x0 - H0 + lx, 0, g.W - 1));
+    {   // all tile loads issued before any shared store (LN = 40 rows: 5 per warp; 40 columns: 32 + 8 lanes)
+        constexpr int KR = LN / 8;
+        const int gx0 = clampi(x0 - H0 + tx, 0, g.W - 1), gx1 = clampi(x0 - H0 + 32 + tx, 0, g.W - 1);
+        float v0[KR], v1[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const float* row = src + (size_t)clampi(y0 - H0 + ty + 8 * k, 0, g.H - 1) * g.P;
+            v0[k] = __ldg(row + gx0);
+            v1[k] = tx < LN - 32 ? __ldg(row + gx1) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            tL[ty + 8 * k][tx] = v0[k];
+            if (tx < LN - 32) tL[ty + 8 * k][32 + tx] = v1[k];
+        }
     }
     float w[2 * R1 + 1];
 #pragma unroll
