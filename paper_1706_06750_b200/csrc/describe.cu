@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
             const float py = y + sigma * (u * si + v * co);
             const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);
             const float gx = gv.x, gy = gv.y;
-            sx[s] = gx * co + gy * si;
-            sy[s] = -gx * si + gy * co;
+            sx[p * 24 + q] = gx * co + gy * si;
+            sy[p * 24 + q] = -gx * si + gy * co;
         }
         __syncwarp();
         const int sr = lane >> 1, half = lane & 1;

@@ -278,12 +278,20 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     const Geom g = c->geom;
     const double px = (double)g.W * g.H * n;
     for (int level = 0; level < N; ++level) {
-        LevelTable one = c->lt;  // launch_hessian walks the levels of the table; one level per launch
-        Launch L(c, KC_HESSIAN, 16.0 * px, s);
-        one.n = 1;
-        one.step[0] = c->lt.step[level];
-        launch_hessian(c->Lt + (size_t)level * g.plane, c->Lxy + (size_t)level * g.plane,
-                       c->Ldet + (size_t)level * g.plane, c->img_stride, g, n, one, s);
+        const size_t lo = (size_t)level * g.plane;
+        bool ok;
+        {
+            Launch L(c, KC_HESSIAN, 16.0 * px, s);
+            ok = launch_hessian(c->Lt + lo, c->Lxy + lo, c->Ldet + lo, c->img_stride, g, n, c->lt.step[level], s);
+        }
+        if (!ok) {  // steps above 24 (σ0·2^O beyond the compiled range): two-pass fallback for this level
+            LevelTable one = c->lt;
+            one.n = 1;
+            one.step[0] = c->lt.step[level];
+            Launch L(c, KC_HESSIAN, 24.0 * px, s);
+            launch_hess_first(c->Lt + lo, c->Lxy + lo, c->img_stride, g, n, one, s);
+            launch_hess_det(c->Lxy + lo, c->Ldet + lo, c->img_stride, g, n, one, s);
+        }
     }
     KZ_CHECK_LAUNCH(c, "hessian");
     if (N < 3) {
