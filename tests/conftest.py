@@ -10,7 +10,7 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device")
-    config.addinivalue_line("markers", "slow: long-running CPU oracle case")
+    config.addinivalue_line("markers", "slow: long-running oracle case (full-size inputs)")
 
 
 @pytest.fixture(scope="session")

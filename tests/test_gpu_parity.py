@@ -320,3 +320,55 @@ def test_profile_counts_launches():
     assert n == K.kaze_launch_count(kz.ctx) > 10
     assert prof["aos_rows"]["launches"] == 3 and prof["aos_cols"]["ms"] > 0
     kz.close()
+
+
+# ------------------------------------------------------------------------------------------- full sizes
+@pytest.mark.slow
+def test_full_size_1920x1200_in_bench_launch_configuration(O):
+    """BASELINE configs[2]/[4] size, in the launch configuration bench.py times (batch of 4 per launch,
+    32768-keypoint capacity): image 0 of the batch against the full oracle."""
+    imgs = kaze_inputs.synth_batch(4, 1920, 1200, distinct=2)
+    ref = O.run(imgs[0], cap=1 << 17)
+    kz = make(1920, 1200, batch=4, max_keypoints=32768)
+    kps, counts, desc = kz.extract(torch.from_numpy(imgs).cuda())
+    k, _ = K.kaze_get_k(kz.ctx, 4)  # the last chunk is the whole batch here
+    assert abs(k[0] / ref["k"] - 1) < 1e-5
+    got = K.Kaze.keypoints_numpy(kps, counts)[0]
+    f1, idx = match_keypoints(ref["kps"], got)
+    f2, _ = match_keypoints(got, ref["kps"])
+    assert f1 >= 0.99 and f2 >= 0.99, (f1, f2, ref["count"], int(counts[0]))
+    d = desc[0, : len(got)].cpu().numpy().astype(np.float64)
+    m = idx >= 0
+    a, b = ref["desc"][m], d[idx[m]]
+    cos = np.sum(a * b, 1) / (np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1) + 1e-30)
+    assert np.mean(cos >= 0.999) >= 0.99, np.mean(cos >= 0.999)
+    # images 2 and 3 are shifted/flipped copies of 0 and 1: same keypoint counts up to border effects
+    assert abs(int(counts[2]) - int(counts[0])) < 0.05 * int(counts[0])
+    kz.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("level", [1, 15])
+def test_aos_step_4096_stage_isolated(O, level):
+    """configs[3] (4096x4096, long AOS lines): one AOS step from the GPU's own L_{i-1}, against the oracle's
+    conductivity + Thomas line solves on the same input (k injected)."""
+    img = kaze_inputs.synth_image(4096, 4096, 4242)
+    k = 0.033
+    kz = make(4096, 4096, k_override=k)
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    prev = torch.empty((4096, 4096), device="cuda")
+    cur = torch.empty((4096, 4096), device="cuda")
+    K.kaze_get_level(kz.ctx, 0, level - 1, K.PLANE_LT, prev)
+    K.kaze_get_level(kz.ctx, 0, level, K.PLANE_LT, cur)
+    torch.cuda.synchronize()
+    Lp = prev.cpu().numpy().astype(np.float64)
+    _, t, _ = O.schedule(4, 4, 1.6)
+    c = O.conductivity(Lp, k, 2)
+    Lnew, _, _ = O.aos_step(Lp, c, t[level] - t[level - 1])
+    assert rel_err(cur.cpu().numpy().astype(np.float64), Lnew) <= 1e-4
+    assert abs(cur.cpu().numpy().mean() / Lp.mean() - 1) < 1e-5
+    if level == 15:
+        cg = torch.empty((4096, 4096), device="cuda")
+        K.kaze_get_level(kz.ctx, 0, 0, K.PLANE_COND, cg)
+        assert np.max(np.abs(cg.cpu().numpy() - c)) < 2e-5
+    kz.close()
