@@ -49,6 +49,100 @@ __device__ __forceinline__ float pcr_solve(float af, float bf, float cf, float d
     return df * frcp(bf);
 }
 
+// Warp-level SPIKE solve of NS independent tridiagonal systems of TP equations (TP % 32 == 0, TP/32 <= 8) that
+// the CTA holds one equation per thread.  Threads are re-mapped so each warp owns 32 consecutive equations of one
+// system: the warp solves its 32x32 block for the right-hand side and the two coupling columns by PCR over
+// shuffles (5 steps, no barriers); one thread per system then solves the 2·(TP/32) warp-boundary unknowns by a
+// serial block recursion, and every equation reads x = y − v·x_{prev warp last} − z·x_{next warp first}.
+// Four block barriers in total (against 2·⌈log2 TP⌉ for a shared-memory PCR).  Returns the calling thread's x.
+// Scratch: e* [NS][TP+1], bnd [NS][8][6], sol [NS][8][2].
+__device__ __forceinline__ float spike_solve(float af, float bf, float cf, float df, int s, int p, int NS, int TP,
+                                             float* ea, float* eb, float* ec, float* ed, float* bnd, float* sol) {
+    const int SP = TP + 1;
+    ea[s * SP + p] = af;
+    eb[s * SP + p] = bf;
+    ec[s * SP + p] = cf;
+    ed[s * SP + p] = df;
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int s2 = t / TP, p2 = t - s2 * TP;
+    const int lane = t & 31, w = p2 >> 5, nw = TP >> 5;
+    const bool live = s2 < NS;
+    float a = 0.f, b = 1.f, c = 0.f, r0 = 0.f, r1 = 0.f, r2 = 0.f;
+    if (live) {
+        const int i2 = s2 * SP + p2;
+        a = ea[i2];
+        b = eb[i2];
+        c = ec[i2];
+        r0 = ed[i2];
+        if (lane == 0) {
+            r1 = a;  // coupling to the previous warp's last unknown → right-hand side v
+            a = 0.f;
+        }
+        if (lane == 31) {
+            r2 = c;  // coupling to the next warp's first unknown → right-hand side z
+            c = 0.f;
+        }
+    }
+#pragma unroll
+    for (int st = 1; st < 32; st <<= 1) {
+        const bool hm = lane >= st, hp = lane + st < 32;
+        float am = __shfl_up_sync(0xffffffffu, a, st), bm = __shfl_up_sync(0xffffffffu, b, st);
+        float cm = __shfl_up_sync(0xffffffffu, c, st), q0m = __shfl_up_sync(0xffffffffu, r0, st);
+        float q1m = __shfl_up_sync(0xffffffffu, r1, st), q2m = __shfl_up_sync(0xffffffffu, r2, st);
+        float ap = __shfl_down_sync(0xffffffffu, a, st), bp = __shfl_down_sync(0xffffffffu, b, st);
+        float cp = __shfl_down_sync(0xffffffffu, c, st), q0p = __shfl_down_sync(0xffffffffu, r0, st);
+        float q1p = __shfl_down_sync(0xffffffffu, r1, st), q2p = __shfl_down_sync(0xffffffffu, r2, st);
+        const float k1 = hm ? a * frcp(bm) : 0.f;
+        const float k2 = hp ? c * frcp(bp) : 0.f;
+        a = hm ? -am * k1 : 0.f;
+        c = hp ? -cp * k2 : 0.f;
+        b = b - (hm ? cm * k1 : 0.f) - (hp ? ap * k2 : 0.f);
+        r0 = r0 - (hm ? q0m * k1 : 0.f) - (hp ? q0p * k2 : 0.f);
+        r1 = r1 - (hm ? q1m * k1 : 0.f) - (hp ? q1p * k2 : 0.f);
+        r2 = r2 - (hm ? q2m * k1 : 0.f) - (hp ? q2p * k2 : 0.f);
+    }
+    const float rb = frcp(b);
+    const float y = r0 * rb, v = r1 * rb, z = r2 * rb;
+    if (live && (lane == 0 || lane == 31)) {
+        float* o = bnd + ((s2 * 8 + w) * 6 + (lane == 0 ? 0 : 3));
+        o[0] = y;
+        o[1] = v;
+        o[2] = z;
+    }
+    __syncthreads();
+    if (live && p2 == 0) {  // F_w = y0 - v0 G_{w-1} - z0 F_{w+1},  G_w = y31 - v31 G_{w-1} - z31 F_{w+1}
+        float* o = bnd + s2 * 48;  // per warp: y0 v0 z0 y31 v31 z31, overwritten by phi psi gam mu
+        float gp = 0.f, mp = 0.f;  // G_{w-1} = gp - mp F_w
+        for (int k = 0; k < nw; ++k, o += 6) {
+            const float rden = 1.f / (1.f - o[1] * mp);
+            const float phi = (o[0] - o[1] * gp) * rden, psi = o[2] * rden;
+            const float gam = o[3] - o[4] * gp + o[4] * mp * phi, mu = o[4] * mp * psi + o[5];
+            o[0] = phi;
+            o[1] = psi;
+            o[2] = gam;
+            o[3] = mu;
+            gp = gam;
+            mp = mu;
+        }
+        float Fn = 0.f;
+        for (int k = nw - 1; k >= 0; --k) {
+            const float* q = bnd + (s2 * 8 + k) * 6;
+            sol[(s2 * 8 + k) * 2 + 1] = q[2] - q[3] * Fn;
+            Fn = q[0] - q[1] * Fn;
+            sol[(s2 * 8 + k) * 2 + 0] = Fn;
+        }
+    }
+    __syncthreads();
+    if (live) {
+        const float Gprev = w > 0 ? sol[(s2 * 8 + w - 1) * 2 + 1] : 0.f;
+        const float Fnext = w + 1 < nw ? sol[(s2 * 8 + w + 1) * 2 + 0] : 0.f;
+        ed[s2 * SP + p2] = y - v * Gprev - z * Fnext;
+    }
+    __syncthreads();
+    return ed[s * SP + p];
+}
+
 template <int MC>
 struct Chunk {
     float al[MC], ga[MC], de[MC];  // α', γ', δ' of rows 1..m-2
@@ -270,14 +364,16 @@ __global__ void __launch_bounds__(256) k_aos_rows(const float* __restrict__ L, c
     const int n = g.W;
     const int Wp = (n + 3) & ~3;              // row floats fetched (16-byte multiple; stays inside the pitch)
     float* stage = smf;                        // [2][3][Wp]: L, c, U
-    float* sa = stage + 6 * Wp;                // PCR + last-equation exchange, TP each
-    float* sb = sa + TP;
-    float* sc = sb + TP;
-    float* sd = sc + TP;
-    float* sla = sd + TP;
+    float* sa = stage + 6 * Wp;                // SPIKE arrays [TP+1] each, boundary data, last-equation exchange
+    float* sb = sa + (TP + 1);
+    float* sc = sb + (TP + 1);
+    float* sd = sc + (TP + 1);
+    float* bnd = sd + (TP + 1);
+    float* sol = bnd + 48;
+    float* sla = sol + 16;
     float* slg = sla + TP;
     float* sld = slg + TP;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sld + TP + ((TP & 1) ? 1 : 0));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(sld + TP + 1) & ~uintptr_t(7));
     const int tid = threadIdx.x;
     const uint32_t bytes = (uint32_t)Wp * 4u;
     if (tid == 0) {
@@ -342,11 +438,9 @@ __global__ void __launch_bounds__(256) k_aos_rows(const float* __restrict__ L, c
             cf = -ch.C * ch.lG;
             df = ch.D - ch.A * pD - ch.C * ch.lD;
         }
-        const float xf = pcr_solve(af, bf, cf, df, p, TP, 1, p, sa, sb, sc, sd);
-        sa[p] = xf;
-        __syncthreads();
+        const float xf = spike_solve(af, bf, cf, df, 0, p, 1, TP, sa, sb, sc, sd, bnd, sol);
         if (active) {
-            const float xnext = (p + 1 < T) ? sa[p + 1] : 0.f;
+            const float xnext = (p + 1 < T) ? sd[p + 1] : 0.f;
             const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
             sL[j0] = xf;
 #pragma unroll
@@ -400,7 +494,7 @@ void run_rows(const float* L, const float* c, const float* U, float* Lout, Strid
     const int T = n_chunks(g.W, M);
     const int TP = round_up(T, 32);
     const int Wp = (g.W + 3) & ~3;
-    const size_t smem = sizeof(float) * (6 * Wp + 7 * TP + 2) + 2 * sizeof(uint64_t);
+    const size_t smem = sizeof(float) * (6 * Wp + 4 * (TP + 1) + 64 + 3 * TP + 4) + 2 * sizeof(uint64_t);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_aos_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
