@@ -112,25 +112,31 @@ __device__ __forceinline__ float spike_solve(float af, float bf, float cf, float
     }
     __syncthreads();
     if (live && p2 == 0) {  // F_w = y0 - v0 G_{w-1} - z0 F_{w+1},  G_w = y31 - v31 G_{w-1} - z31 F_{w+1}
-        float* o = bnd + s2 * 48;  // per warp: y0 v0 z0 y31 v31 z31, overwritten by phi psi gam mu
+        float o[8][6];          // all boundary data loaded up front (one shared-memory latency, not eight)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int e = 0; e < 6; ++e) o[k][e] = k < nw ? bnd[(s2 * 8 + k) * 6 + e] : 0.f;
+        float phi[8], psi[8], gam[8], mu[8];
         float gp = 0.f, mp = 0.f;  // G_{w-1} = gp - mp F_w
-        for (int k = 0; k < nw; ++k, o += 6) {
-            const float rden = 1.f / (1.f - o[1] * mp);
-            const float phi = (o[0] - o[1] * gp) * rden, psi = o[2] * rden;
-            const float gam = o[3] - o[4] * gp + o[4] * mp * phi, mu = o[4] * mp * psi + o[5];
-            o[0] = phi;
-            o[1] = psi;
-            o[2] = gam;
-            o[3] = mu;
-            gp = gam;
-            mp = mu;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float rden = frcp(1.f - o[k][1] * mp);
+            phi[k] = (o[k][0] - o[k][1] * gp) * rden;
+            psi[k] = o[k][2] * rden;
+            gam[k] = o[k][3] - o[k][4] * gp + o[k][4] * mp * phi[k];
+            mu[k] = o[k][4] * mp * psi[k] + o[k][5];
+            gp = gam[k];
+            mp = mu[k];
         }
         float Fn = 0.f;
-        for (int k = nw - 1; k >= 0; --k) {
-            const float* q = bnd + (s2 * 8 + k) * 6;
-            sol[(s2 * 8 + k) * 2 + 1] = q[2] - q[3] * Fn;
-            Fn = q[0] - q[1] * Fn;
-            sol[(s2 * 8 + k) * 2 + 0] = Fn;
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+            if (k < nw) {
+                sol[(s2 * 8 + k) * 2 + 1] = gam[k] - mu[k] * Fn;
+                Fn = phi[k] - psi[k] * Fn;
+                sol[(s2 * 8 + k) * 2 + 0] = Fn;
+            }
         }
     }
     __syncthreads();
@@ -273,7 +279,8 @@ __host__ __device__ inline int n_chunks(int n, int M) {
 // Column systems.  Thread (cx, p): column x0 + cx, chunk p of T.  blockDim.x = CW * TP; shared index p*CW + cx.
 template <int CW, int M, int NT>
 __global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, const float* __restrict__ c,
-                                                 float* __restrict__ U, Strides st, Geom g, float tau, int T, int TP) {
+                                                 const float* __restrict__ U, float* __restrict__ Lout, Strides st,
+                                                 Geom g, float tau, int T, int TP) {
     constexpr int MC = M + 1;
     extern __shared__ float sm[];
     const int NTOT = CW * TP;
@@ -339,13 +346,15 @@ __global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, co
     if (!active) return;
     const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
     const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
-    float* Uc = U + blockIdx.z * st.U + (size_t)j0 * g.P + x;
-    Uc[0] = xf;
+    // L_i = ½(U + V): the row pass already wrote V (passed in as U's buffer); the average is formed here.
+    const float* Vc = U + blockIdx.z * st.U + (size_t)j0 * g.P + x;
+    float* Oc = Lout + blockIdx.z * st.out + (size_t)j0 * g.P + x;
+    Oc[0] = 0.5f * (xf + __ldg(Vc));
 #pragma unroll
     for (int i = 1; i < MC; ++i) {
-        if (i < m - 1) Uc[(size_t)i * g.P] = ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl;
+        if (i < m - 1) Oc[(size_t)i * g.P] = 0.5f * (ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl + __ldg(Vc + (size_t)i * g.P));
     }
-    Uc[(size_t)(m - 1) * g.P] = xl;
+    Oc[(size_t)(m - 1) * g.P] = 0.5f * (xl + __ldg(Vc + (size_t)(m - 1) * g.P));
 }
 
 // -------------------------------------------------------------------------------------------------------------
@@ -466,15 +475,142 @@ __global__ void __launch_bounds__(256) k_aos_rows(const float* __restrict__ L, c
     }
 }
 
+// -------------------------------------------------------------------------------------------------------------
+// Row systems, one WARP per row (the row pass runs first and writes V; the column pass then forms ½(U + V)).
+// The row (L and c) is staged in shared memory; lane l owns the chunk [l·M, l·M + m) with M odd, so the lanes'
+// strided sweeps hit 32 distinct banks.  The sweeps keep their coefficients in shared memory, in place:
+// δ overwrites L, γ overwrites c (each c is read before its slot is reused), α goes to a third array.  The
+// reduced system of one unknown per lane is solved by PCR over shuffles — no block barriers at all.
+// Shared memory per warp: 3 row buffers.
+constexpr int kRowWarps = 4;
+
+__global__ void __launch_bounds__(32 * kRowWarps) k_aos_rows_warp(const float* __restrict__ L,
+                                                                  const float* __restrict__ c, float* __restrict__ V,
+                                                                  Strides st, Geom g, float tau, int M, int T,
+                                                                  int total_rows) {
+    extern __shared__ __align__(16) float rsm[];
+    const int n = g.W;
+    const int Wp = (n + 3) & ~3;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float* sL = rsm + warp * 3 * Wp;
+    float* sC = sL + Wp;
+    float* sA = sC + Wp;
+    const int j0 = lane * M;
+    const int m = lane < T ? ((lane == T - 1) ? n - j0 : M) : 0;
+    const bool first = lane == 0, last = lane == T - 1;
+    for (int q = blockIdx.x * kRowWarps + warp; q < total_rows; q += gridDim.x * kRowWarps) {
+        const int img = q / g.H, y = q - img * g.H;
+        const size_t ry = (size_t)y * g.P;
+        const float4* Lr = reinterpret_cast<const float4*>(L + img * st.L + ry);
+        const float4* cr = reinterpret_cast<const float4*>(c + img * st.c + ry);
+        for (int v = lane; v < (Wp >> 2); v += 32) {
+            reinterpret_cast<float4*>(sL)[v] = __ldg(Lr + v);
+            reinterpret_cast<float4*>(sC)[v] = __ldg(cr + v);
+        }
+        __syncwarp();
+        float A = 0.f, C = 0.f, D = 0.f, lA = 0.f, lG = 0.f, lD = 0.f;
+        if (m > 0) {
+            const float cprev = first ? 0.f : sC[j0 - 1];
+            const float cnext = last ? 0.f : sC[j0 + m];
+            const float c0 = sC[j0], c1 = sC[j0 + 1], d0 = sL[j0];
+            __syncwarp(0xffffffffu >> (32 - T));  // neighbour boundary values read before any slot is reused
+            // downward sweep, rows 1..m-1 (virtual row 0: α = -1, γ = 0, δ = 0); q_i = τ(c_{i-1} + c_i)
+            float pa = -1.f, pg = 0.f, pd = 0.f;
+            float cm = c0, cc = c1;
+            float tqi = tau * (c0 + c1);  // τ(c_0 + c_1) = a_1 magnitude
+            for (int i = 1; i < m; ++i) {
+                const float cn = (i + 1 < m) ? sC[j0 + i + 1] : cnext;
+                const float tqn = (i == m - 1 && last) ? 0.f : tau * (cc + cn);
+                const float r = frcp(1.f + tqi + tqn + tqi * pg);
+                const float na = tqi * pa * r;
+                const float ng = -tqn * r;
+                const float nd = fmaf(tqi, pd, sL[j0 + i]) * r;
+                sA[j0 + i] = na;
+                sC[j0 + i] = ng;  // c_i was consumed into cc / tqi
+                sL[j0 + i] = nd;
+                pa = na;
+                pg = ng;
+                pd = nd;
+                cm = cc;
+                cc = cn;
+                tqi = tqn;
+            }
+            (void)cm;
+            lA = pa;
+            lG = pg;
+            lD = pd;
+            // upward sweep, rows m-2..1 (virtual row m-1: α' = 0, γ' = -1, δ' = 0)
+            float na = 0.f, ng = -1.f, nd = 0.f;
+            for (int i = m - 2; i >= 1; --i) {
+                const float gi = sC[j0 + i];
+                const float a2 = sA[j0 + i] - gi * na;
+                const float g2 = -gi * ng;
+                const float d2 = sL[j0 + i] - gi * nd;
+                sA[j0 + i] = a2;
+                sC[j0 + i] = g2;
+                sL[j0 + i] = d2;
+                na = a2;
+                ng = g2;
+                nd = d2;
+            }
+            // row 0: a0 = -τ(c_{-1} + c_0) (0 on the first chunk), cc0 = -τ(c_0 + c_1)
+            const float tq0 = first ? 0.f : tau * (cprev + c0);
+            const float tq1 = tau * (c0 + c1);
+            const float rB = frcp(fmaf(tq1, na, 1.f + tq0 + tq1));
+            A = -tq0 * rB;
+            C = tq1 * ng * rB;
+            D = fmaf(tq1, nd, d0) * rB;
+        }
+        // reduced system in the lanes' first unknowns f_l (identity rows for idle lanes)
+        const float pAl = __shfl_up_sync(0xffffffffu, lA, 1), pGl = __shfl_up_sync(0xffffffffu, lG, 1);
+        const float pDl = __shfl_up_sync(0xffffffffu, lD, 1);
+        float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
+        if (m > 0) {
+            const float qa = first ? 0.f : pAl, qg = first ? 0.f : pGl, qd = first ? 0.f : pDl;
+            af = -A * qa;
+            bf = 1.f - A * qg - C * lA;
+            cf = -C * lG;
+            df = D - A * qd - C * lD;
+        }
+#pragma unroll
+        for (int s2 = 1; s2 < 32; s2 <<= 1) {
+            const bool hm = lane >= s2, hp = lane + s2 < 32;
+            const float am = __shfl_up_sync(0xffffffffu, af, s2), bm = __shfl_up_sync(0xffffffffu, bf, s2);
+            const float cmm = __shfl_up_sync(0xffffffffu, cf, s2), dm = __shfl_up_sync(0xffffffffu, df, s2);
+            const float ap = __shfl_down_sync(0xffffffffu, af, s2), bp = __shfl_down_sync(0xffffffffu, bf, s2);
+            const float cp = __shfl_down_sync(0xffffffffu, cf, s2), dp = __shfl_down_sync(0xffffffffu, df, s2);
+            const float k1 = hm ? af * frcp(bm) : 0.f;
+            const float k2 = hp ? cf * frcp(bp) : 0.f;
+            af = hm ? -am * k1 : 0.f;
+            cf = hp ? -cp * k2 : 0.f;
+            bf = bf - (hm ? cmm * k1 : 0.f) - (hp ? ap * k2 : 0.f);
+            df = df - (hm ? dm * k1 : 0.f) - (hp ? dp * k2 : 0.f);
+        }
+        const float xf = df * frcp(bf);
+        const float xnext = __shfl_down_sync(0xffffffffu, xf, 1);
+        if (m > 0) {
+            const float xl = lD - lA * xf - lG * (last ? 0.f : xnext);
+            for (int i = 1; i < m - 1; ++i) sL[j0 + i] = sL[j0 + i] - sA[j0 + i] * xf - sC[j0 + i] * xl;
+            sL[j0] = xf;
+            sL[j0 + m - 1] = xl;
+        }
+        __syncwarp();
+        float4* Vr = reinterpret_cast<float4*>(V + img * st.out + ry);
+        for (int v = lane; v < (Wp >> 2); v += 32) Vr[v] = reinterpret_cast<const float4*>(sL)[v];
+        __syncwarp();
+    }
+}
+
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 template <int CW, int M, int NT>
-void run_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau, cudaStream_t s) {
+void run_cols(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg, float tau,
+              cudaStream_t s) {
     const int T = n_chunks(g.H, M);
     const int TP = round_up(T, 32 / CW);
     const size_t smem = sizeof(float) * 7 * CW * TP;
     dim3 grid((g.W + CW - 1) / CW, 1, nimg);
-    k_aos_cols<CW, M, NT><<<grid, CW * TP, smem, s>>>(L, c, U, st, g, tau, T, TP);
+    k_aos_cols<CW, M, NT><<<grid, CW * TP, smem, s>>>(L, c, U, Lout, st, g, tau, T, TP);
 }
 
 int num_sms() {
@@ -510,32 +646,41 @@ void run_rows(const float* L, const float* c, const float* U, float* Lout, Strid
 }  // namespace
 
 // Column chunk length: T = n_chunks(H, M) must fit the CTA (CW*TP <= NT).
-bool launch_aos_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau,
-                     cudaStream_t s) {
+bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
+                     float tau, cudaStream_t s) {
     const int H = g.H;
-    if (H <= 128 * 4) run_cols<8, 4, 1024>(L, c, U, st, g, nimg, tau, s);
-    else if (H <= 128 * 6) run_cols<8, 6, 1024>(L, c, U, st, g, nimg, tau, s);
-    else if (H <= 128 * 8) run_cols<8, 8, 1024>(L, c, U, st, g, nimg, tau, s);
-    else if (H <= 128 * 10) run_cols<8, 10, 1024>(L, c, U, st, g, nimg, tau, s);
-    else if (H <= 128 * 12) run_cols<8, 12, 1024>(L, c, U, st, g, nimg, tau, s);
-    else if (H <= 256 * 16) run_cols<2, 16, 512>(L, c, U, st, g, nimg, tau, s);
-    else if (H <= 256 * 32) run_cols<2, 32, 512>(L, c, U, st, g, nimg, tau, s);
+    if (H <= 128 * 4) run_cols<8, 4, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 6) run_cols<8, 6, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 8) run_cols<8, 8, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 10) run_cols<8, 10, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 12) run_cols<8, 12, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 256 * 16) run_cols<2, 16, 512>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 256 * 32) run_cols<2, 32, 512>(L, c, V, Lout, st, g, nimg, tau, s);
     else return false;
     return true;
 }
 
-// Row chunk length: the smallest odd M >= 5 with T <= 256.
-bool launch_aos_rows(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg,
-                     float tau, cudaStream_t s) {
+// Row systems, warp per row: chunk M = ceil(W/32) rounded up to odd (conflict-free lane stride).
+bool launch_aos_rows(const float* L, const float* c, float* V, Strides st, Geom g, int nimg, float tau,
+                     cudaStream_t s) {
     const int W = g.W;
-    if (W <= 256 * 5) run_rows<5>(L, c, U, Lout, st, g, nimg, tau, s);
-    else if (W <= 256 * 7) run_rows<7>(L, c, U, Lout, st, g, nimg, tau, s);
-    else if (W <= 256 * 9) run_rows<9>(L, c, U, Lout, st, g, nimg, tau, s);
-    else if (W <= 256 * 11) run_rows<11>(L, c, U, Lout, st, g, nimg, tau, s);
-    else if (W <= 256 * 13) run_rows<13>(L, c, U, Lout, st, g, nimg, tau, s);
-    else if (W <= 256 * 17) run_rows<17>(L, c, U, Lout, st, g, nimg, tau, s);
-    else if (W <= 256 * 33) run_rows<33>(L, c, U, Lout, st, g, nimg, tau, s);
-    else return false;
+    int M = ((W + 31) / 32) | 1;
+    int T = (W + M - 1) / M;
+    if (T > 1 && W - (T - 1) * M == 1) --T;  // merge a 1-sample tail into the previous chunk
+    const int Wp = (W + 3) & ~3;
+    const size_t smem = sizeof(float) * 3 * Wp * kRowWarps;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_aos_rows_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr = true;
+    }
+    if (smem > 220 * 1024) return false;
+    const int total = g.H * nimg;
+    int per_sm = (int)((225 * 1024) / (smem + 1024));
+    per_sm = per_sm < 1 ? 1 : (per_sm > 16 ? 16 : per_sm);
+    int grid = (total + kRowWarps - 1) / kRowWarps;
+    if (grid > num_sms() * per_sm) grid = num_sms() * per_sm;
+    k_aos_rows_warp<<<grid, 32 * kRowWarps, smem, s>>>(L, c, V, st, g, tau, M, T, total);
     return true;
 }
 
