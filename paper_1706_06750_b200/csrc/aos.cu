@@ -489,25 +489,33 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_aos_rows_warp(const float* _
                                                                   Strides st, Geom g, float tau, int M, int T,
                                                                   int total_rows) {
     extern __shared__ __align__(16) float rsm[];
+    __shared__ __align__(8) uint64_t wbar[kRowWarps];
     const int n = g.W;
     const int Wp = (n + 3) & ~3;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sL = rsm + warp * 3 * Wp;
     float* sC = sL + Wp;
     float* sA = sC + Wp;
+    if (lane == 0) {
+        mbar_init(&wbar[warp], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;
     const int j0 = lane * M;
     const int m = lane < T ? ((lane == T - 1) ? n - j0 : M) : 0;
     const bool first = lane == 0, last = lane == T - 1;
     for (int q = blockIdx.x * kRowWarps + warp; q < total_rows; q += gridDim.x * kRowWarps) {
         const int img = q / g.H, y = q - img * g.H;
         const size_t ry = (size_t)y * g.P;
-        const float4* Lr = reinterpret_cast<const float4*>(L + img * st.L + ry);
-        const float4* cr = reinterpret_cast<const float4*>(c + img * st.c + ry);
-        for (int v = lane; v < (Wp >> 2); v += 32) {
-            reinterpret_cast<float4*>(sL)[v] = __ldg(Lr + v);
-            reinterpret_cast<float4*>(sC)[v] = __ldg(cr + v);
+        if (lane == 0) {  // the TMA engine streams the row's L and c into this warp's buffers
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&wbar[warp], 8u * (uint32_t)Wp);
+            bulk_g2s(sL, L + img * st.L + ry, 4u * (uint32_t)Wp, &wbar[warp]);
+            bulk_g2s(sC, c + img * st.c + ry, 4u * (uint32_t)Wp, &wbar[warp]);
         }
-        __syncwarp();
+        mbar_wait(&wbar[warp], phase);
+        phase ^= 1u;
         float A = 0.f, C = 0.f, D = 0.f, lA = 0.f, lG = 0.f, lD = 0.f;
         if (m > 0) {
             const float cprev = first ? 0.f : sC[j0 - 1];
@@ -518,6 +526,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_aos_rows_warp(const float* _
             float pa = -1.f, pg = 0.f, pd = 0.f;
             float cm = c0, cc = c1;
             float tqi = tau * (c0 + c1);  // τ(c_0 + c_1) = a_1 magnitude
+#pragma unroll 4
             for (int i = 1; i < m; ++i) {
                 const float cn = (i + 1 < m) ? sC[j0 + i + 1] : cnext;
                 const float tqn = (i == m - 1 && last) ? 0.f : tau * (cc + cn);
@@ -541,6 +550,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_aos_rows_warp(const float* _
             lD = pd;
             // upward sweep, rows m-2..1 (virtual row m-1: α' = 0, γ' = -1, δ' = 0)
             float na = 0.f, ng = -1.f, nd = 0.f;
+#pragma unroll 4
             for (int i = m - 2; i >= 1; --i) {
                 const float gi = sC[j0 + i];
                 const float a2 = sA[j0 + i] - gi * na;
@@ -590,6 +600,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_aos_rows_warp(const float* _
         const float xnext = __shfl_down_sync(0xffffffffu, xf, 1);
         if (m > 0) {
             const float xl = lD - lA * xf - lG * (last ? 0.f : xnext);
+#pragma unroll 4
             for (int i = 1; i < m - 1; ++i) sL[j0 + i] = sL[j0 + i] - sA[j0 + i] * xf - sC[j0 + i] * xl;
             sL[j0] = xf;
             sL[j0 + m - 1] = xl;
@@ -597,6 +608,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_aos_rows_warp(const float* _
         __syncwarp();
         float4* Vr = reinterpret_cast<float4*>(V + img * st.out + ry);
         for (int v = lane; v < (Wp >> 2); v += 32) Vr[v] = reinterpret_cast<const float4*>(sL)[v];
+        fence_proxy_async();  // generic reads/writes of the buffers before the next TMA refill
         __syncwarp();
     }
 }
