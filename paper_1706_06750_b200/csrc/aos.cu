@@ -613,6 +613,157 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_aos_rows_warp(const float* _
     }
 }
 
+// -------------------------------------------------------------------------------------------------------------
+// Row systems, one CTA of NW warps per row (the row pass runs first and writes V).  The TMA engine streams the
+// row's L and c into shared memory; thread p owns the chunk [p·M, p·M + m) (M odd: conflict-free strided reads)
+// and eliminates it in registers; the reduced system (one unknown per thread) is solved by a warp-level SPIKE:
+// shuffle PCR inside each warp on three right-hand sides, a serial 2·NW-unknown boundary solve by one thread,
+// then x = y − v·x_{prev warp} − z·x_{next warp}.  x goes back to shared memory and V leaves with 16-byte stores.
+template <int M, int NW>
+__global__ void __launch_bounds__(32 * NW) k_aos_rows_cta(const float* __restrict__ L, const float* __restrict__ c,
+                                                          float* __restrict__ V, Strides st, Geom g, float tau, int T) {
+    constexpr int MC = M + 1, TP = 32 * NW;
+    extern __shared__ __align__(16) float rs[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ float lastA[TP], lastG[TP], lastD[TP], bnd[NW * 6], sol[NW * 2], fx[TP];
+    const int n = g.W;
+    const int Wp = (n + 3) & ~3;
+    float* sL = rs;
+    float* sC = rs + Wp;
+    const int p = threadIdx.x, lane = p & 31, w = p >> 5;
+    const int img = blockIdx.x / g.H, y = blockIdx.x - img * g.H;
+    const size_t ry = (size_t)y * g.P;
+    if (p == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&bar, 8u * (uint32_t)Wp);
+        bulk_g2s(sL, L + img * st.L + ry, 4u * (uint32_t)Wp, &bar);
+        bulk_g2s(sC, c + img * st.c + ry, 4u * (uint32_t)Wp, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    const bool active = p < T;
+    const int j0 = p * M;
+    const int j1 = (p == T - 1) ? n : j0 + M;
+    const int m = active ? j1 - j0 : 0;
+    Chunk<MC> ch;
+    if (active) {
+        float dv[MC], cv[MC];
+#pragma unroll
+        for (int i = 0; i < MC; ++i) {
+            dv[i] = i < m ? sL[j0 + i] : 0.f;
+            cv[i] = i < m ? sC[j0 + i] : 0.f;
+        }
+        const float cprev = p > 0 ? sC[j0 - 1] : 0.f;
+        const float cnext = j1 < n ? sC[j1] : 0.f;
+        if (m == M) eliminate_full<M>(ch, dv, cv, cprev, cnext, p == 0, p == T - 1, tau);
+        else eliminate<MC>(ch, dv, cv, cprev, cnext, m, p == 0, p == T - 1, tau);
+    } else {
+        ch.A = ch.C = ch.D = 0.f;
+        ch.lA = ch.lG = ch.lD = 0.f;
+    }
+    lastA[p] = ch.lA;
+    lastG[p] = ch.lG;
+    lastD[p] = ch.lD;
+    __syncthreads();
+    float a = 0.f, b = 1.f, cc = 0.f, r0 = 0.f;
+    if (active) {
+        const float pA = p > 0 ? lastA[p - 1] : 0.f, pG = p > 0 ? lastG[p - 1] : 0.f, pD = p > 0 ? lastD[p - 1] : 0.f;
+        a = -ch.A * pA;
+        b = 1.f - ch.A * pG - ch.C * ch.lA;
+        cc = -ch.C * ch.lG;
+        r0 = ch.D - ch.A * pD - ch.C * ch.lD;
+    }
+    // --- warp SPIKE: local block solve with couplings to the neighbouring warps moved to two extra RHS ---
+    float r1 = 0.f, r2 = 0.f;
+    if (lane == 0) {
+        r1 = a;
+        a = 0.f;
+    }
+    if (lane == 31) {
+        r2 = cc;
+        cc = 0.f;
+    }
+#pragma unroll
+    for (int s2 = 1; s2 < 32; s2 <<= 1) {
+        const bool hm = lane >= s2, hp = lane + s2 < 32;
+        const float am = __shfl_up_sync(0xffffffffu, a, s2), bm = __shfl_up_sync(0xffffffffu, b, s2);
+        const float cm = __shfl_up_sync(0xffffffffu, cc, s2), q0m = __shfl_up_sync(0xffffffffu, r0, s2);
+        const float q1m = __shfl_up_sync(0xffffffffu, r1, s2), q2m = __shfl_up_sync(0xffffffffu, r2, s2);
+        const float ap = __shfl_down_sync(0xffffffffu, a, s2), bp = __shfl_down_sync(0xffffffffu, b, s2);
+        const float cp = __shfl_down_sync(0xffffffffu, cc, s2), q0p = __shfl_down_sync(0xffffffffu, r0, s2);
+        const float q1p = __shfl_down_sync(0xffffffffu, r1, s2), q2p = __shfl_down_sync(0xffffffffu, r2, s2);
+        const float k1 = hm ? a * frcp(bm) : 0.f;
+        const float k2 = hp ? cc * frcp(bp) : 0.f;
+        a = hm ? -am * k1 : 0.f;
+        cc = hp ? -cp * k2 : 0.f;
+        b = b - (hm ? cm * k1 : 0.f) - (hp ? ap * k2 : 0.f);
+        r0 = r0 - (hm ? q0m * k1 : 0.f) - (hp ? q0p * k2 : 0.f);
+        r1 = r1 - (hm ? q1m * k1 : 0.f) - (hp ? q1p * k2 : 0.f);
+        r2 = r2 - (hm ? q2m * k1 : 0.f) - (hp ? q2p * k2 : 0.f);
+    }
+    const float rb = frcp(b);
+    const float yv = r0 * rb, vv = r1 * rb, zv = r2 * rb;
+    if (lane == 0 || lane == 31) {
+        float* o = bnd + w * 6 + (lane == 0 ? 0 : 3);
+        o[0] = yv;
+        o[1] = vv;
+        o[2] = zv;
+    }
+    __syncthreads();
+    if (p == 0) {  // F_w = y0 - v0 G_{w-1} - z0 F_{w+1},  G_w = y31 - v31 G_{w-1} - z31 F_{w+1}
+        float phi[NW], psi[NW], gam[NW], mu[NW];
+        float gp = 0.f, mp = 0.f;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const float* o = bnd + k * 6;
+            const float rden = frcp(1.f - o[1] * mp);
+            phi[k] = (o[0] - o[1] * gp) * rden;
+            psi[k] = o[2] * rden;
+            gam[k] = o[3] - o[4] * gp + o[4] * mp * phi[k];
+            mu[k] = o[4] * mp * psi[k] + o[5];
+            gp = gam[k];
+            mp = mu[k];
+        }
+        float Fn = 0.f;
+#pragma unroll
+        for (int k = NW - 1; k >= 0; --k) {
+            sol[2 * k + 1] = gam[k] - mu[k] * Fn;
+            Fn = phi[k] - psi[k] * Fn;
+            sol[2 * k] = Fn;
+        }
+    }
+    __syncthreads();
+    const float xf = yv - vv * (w > 0 ? sol[2 * w - 1] : 0.f) - zv * (w + 1 < NW ? sol[2 * w + 2] : 0.f);
+    fx[p] = xf;
+    __syncthreads();
+    if (active) {
+        const float xnext = (p + 1 < T) ? fx[p + 1] : 0.f;
+        const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
+        sL[j0] = xf;
+#pragma unroll
+        for (int i = 1; i < MC; ++i)
+            if (i < m - 1) sL[j0 + i] = ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl;
+        sL[j1 - 1] = xl;
+    }
+    __syncthreads();
+    float4* Vr = reinterpret_cast<float4*>(V + img * st.out + ry);
+    for (int v = p; v < (Wp >> 2); v += TP) Vr[v] = reinterpret_cast<const float4*>(sL)[v];
+}
+
+template <int M, int NW>
+void run_rows_cta(const float* L, const float* c, float* V, Strides st, Geom g, int nimg, float tau, cudaStream_t s) {
+    int T = (g.W + M - 1) / M;
+    if (T > 1 && g.W - (T - 1) * M == 1) --T;
+    const size_t smem = sizeof(float) * 2 * ((g.W + 3) & ~3);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_aos_rows_cta<M, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    k_aos_rows_cta<M, NW><<<g.H * nimg, 32 * NW, smem, s>>>(L, c, V, st, g, tau, T);
+}
+
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 template <int CW, int M, int NT>
@@ -672,27 +823,20 @@ bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout
     return true;
 }
 
-// Row systems, warp per row: chunk M = ceil(W/32) rounded up to odd (conflict-free lane stride).
+// Row systems, one CTA per row: the smallest odd chunk M >= 5 with T = ceil(W/M) <= 32·NW threads.
 bool launch_aos_rows(const float* L, const float* c, float* V, Strides st, Geom g, int nimg, float tau,
                      cudaStream_t s) {
     const int W = g.W;
-    int M = ((W + 31) / 32) | 1;
-    int T = (W + M - 1) / M;
-    if (T > 1 && W - (T - 1) * M == 1) --T;  // merge a 1-sample tail into the previous chunk
-    const int Wp = (W + 3) & ~3;
-    const size_t smem = sizeof(float) * 3 * Wp * kRowWarps;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_aos_rows_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr = true;
-    }
-    if (smem > 220 * 1024) return false;
-    const int total = g.H * nimg;
-    int per_sm = (int)((225 * 1024) / (smem + 1024));
-    per_sm = per_sm < 1 ? 1 : (per_sm > 16 ? 16 : per_sm);
-    int grid = (total + kRowWarps - 1) / kRowWarps;
-    if (grid > num_sms() * per_sm) grid = num_sms() * per_sm;
-    k_aos_rows_warp<<<grid, 32 * kRowWarps, smem, s>>>(L, c, V, st, g, tau, M, T, total);
+    if (W <= 128 * 5) run_rows_cta<5, 4>(L, c, V, st, g, nimg, tau, s);
+    else if (W <= 128 * 7) run_rows_cta<7, 4>(L, c, V, st, g, nimg, tau, s);
+    else if (W <= 128 * 9) run_rows_cta<9, 4>(L, c, V, st, g, nimg, tau, s);
+    else if (W <= 128 * 11) run_rows_cta<11, 4>(L, c, V, st, g, nimg, tau, s);
+    else if (W <= 128 * 13) run_rows_cta<13, 4>(L, c, V, st, g, nimg, tau, s);
+    else if (W <= 128 * 15) run_rows_cta<15, 4>(L, c, V, st, g, nimg, tau, s);
+    else if (W <= 256 * 11) run_rows_cta<11, 8>(L, c, V, st, g, nimg, tau, s);
+    else if (W <= 256 * 17) run_rows_cta<17, 8>(L, c, V, st, g, nimg, tau, s);
+    else if (W <= 256 * 33) run_rows_cta<33, 8>(L, c, V, st, g, nimg, tau, s);
+    else return false;
     return true;
 }
 
