@@ -298,8 +298,10 @@ __global__ void __launch_bounds__(1024) k_aos_cols_tma(const __grid_constant__ C
                                                        float* __restrict__ Lout, size_t out_img_stride, Geom g,
                                                        float tau, int T, int TP, ColTmaArgs ta) {
     constexpr int CW = 8, MC = M + 1;
-    extern __shared__ __align__(128) float csm[];
+    extern __shared__ __align__(128) float csm_raw[];
     __shared__ __align__(8) uint64_t barLC, barV;
+    // TMA tile destinations must be 128-byte aligned: align the base, and bh is a multiple of 4 rows (128 B)
+    float* csm = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(csm_raw) + 127) & ~uintptr_t(127));
     const int SR = ta.nb * ta.bh;      // staged rows
     float* stL = csm;                  // [SR][8]
     float* stC = stL + SR * CW;        // [SR][8]
@@ -646,7 +648,8 @@ bool run_cols_tma(const float* L, const float* c, const float* V, float* Lout, S
     const int T = n_chunks(g.H, M);
     const int TP = round_up(T, 4);
     if (8 * TP > 1024) return false;
-    const int nb = (g.H + 255) / 256, bh = (g.H + nb - 1) / nb;
+    const int nb = (g.H + 255) / 256;
+    const int bh = (((g.H + nb - 1) / nb) + 3) & ~3;  // tile rows: multiple of 4 (128-byte aligned tiles), <= 256
     ColTmaArgs ta;
     ta.rowL0 = 0;
     ta.rowsPerImgL = (int)(st.L / g.P);
@@ -661,7 +664,7 @@ bool run_cols_tma(const float* L, const float* c, const float* V, float* Lout, S
     const CUtensorMap* mC = cached_tmap(c, g.W, g.P, rowsC, bh);
     const CUtensorMap* mV = cached_tmap(V, g.W, g.P, rowsC, bh);
     if (!mL || !mC || !mV) return false;
-    const size_t smem = sizeof(float) * (3 * (size_t)nb * bh * 8 + 7 * 8 * TP);
+    const size_t smem = sizeof(float) * (3 * (size_t)nb * bh * 8 + 7 * 8 * TP) + 128;
     if (smem > 220 * 1024) return false;
     static bool attr = false;
     if (!attr) {
