@@ -17,9 +17,6 @@
 //   columns: a CTA owns CW adjacent columns; a warp covers CW columns × 32/CW chunks, so every global request is
 //            whole 32-byte sectors; the reduced systems are solved by PCR in shared memory; V is prefetched with
 //            cp.async behind the solve and L_i = ½(U + V) is written directly.
-#include <cuda.h>
-#include <stdlib.h>
-
 #include "kaze_internal.cuh"
 #include "ptx.cuh"
 
@@ -269,175 +266,6 @@ __global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, co
 }
 
 // -------------------------------------------------------------------------------------------------------------
-// Column systems, TMA-pipelined persistent form.  A CTA walks strips of CW = 8 adjacent columns (of all images).
-// The strip's L and c columns arrive as 2-D TMA tiles (8 columns x BH rows per tile) in one shared stage; as soon as
-// every thread has copied its chunk into registers the stage is refilled with the NEXT strip's L and c, so those
-// loads overlap the elimination, the PCR solve and the output of the current strip.  V arrives the same way into
-// its own stage.  L_i = ½(U + V) is written straight from registers (a warp = 8 columns x 4 chunk rows, i.e. whole
-// 32-byte sectors).
-struct ColTmaArgs {
-    int rowL0;       // tensor row of image 0's L_{i-1} plane row 0 (level offset)
-    int rowsPerImgL; // tensor rows per image in the L map (N·H)
-    int nb, bh;      // tiles per column strip and rows per tile
-    int nstrips;     // strips per image
-    int total;       // strips of all images
-};
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
-}
-
-template <int M>
-__global__ void __launch_bounds__(1024) k_aos_cols_tma(const __grid_constant__ CUtensorMap mapL,
-                                                       const __grid_constant__ CUtensorMap mapC,
-                                                       const __grid_constant__ CUtensorMap mapV,
-                                                       float* __restrict__ Lout, size_t out_img_stride, Geom g,
-                                                       float tau, int T, int TP, ColTmaArgs ta) {
-    constexpr int CW = 8, MC = M + 1;
-    extern __shared__ __align__(128) float csm_raw[];
-    __shared__ __align__(8) uint64_t barLC, barV;
-    // TMA tile destinations must be 128-byte aligned: align the base, and bh is a multiple of 4 rows (128 B)
-    float* csm = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(csm_raw) + 127) & ~uintptr_t(127));
-    const int SR = ta.nb * ta.bh;      // staged rows
-    float* stL = csm;                  // [SR][8]
-    float* stC = stL + SR * CW;        // [SR][8]
-    float* stV = stC + SR * CW;        // [SR][8]
-    const int NTOT = CW * TP;
-    float* sa = stV + SR * CW;
-    float* sb = sa + NTOT;
-    float* sc = sb + NTOT;
-    float* sd = sc + NTOT;
-    float* sla = sd + NTOT;
-    float* slg = sla + NTOT;
-    float* sld = slg + NTOT;
-    const int tid = threadIdx.x;
-    const int cx = tid % CW, p = tid / CW;
-    const uint32_t tile_bytes = (uint32_t)(ta.bh * CW * 4);
-    auto issue_lc = [&](int s) {
-        const int z = s / ta.nstrips, xs = (s - z * ta.nstrips) * CW;
-        mbar_arrive_expect_tx(&barLC, 2u * tile_bytes * (uint32_t)ta.nb);
-        for (int k = 0; k < ta.nb; ++k) {
-            tma_load_2d(stL + k * ta.bh * CW, &mapL, xs, ta.rowL0 + z * ta.rowsPerImgL + k * ta.bh, &barLC);
-            tma_load_2d(stC + k * ta.bh * CW, &mapC, xs, z * g.H + k * ta.bh, &barLC);
-        }
-    };
-    auto issue_v = [&](int s) {
-        const int z = s / ta.nstrips, xs = (s - z * ta.nstrips) * CW;
-        mbar_arrive_expect_tx(&barV, tile_bytes * (uint32_t)ta.nb);
-        for (int k = 0; k < ta.nb; ++k) tma_load_2d(stV + k * ta.bh * CW, &mapV, xs, z * g.H + k * ta.bh, &barV);
-    };
-    if (tid == 0) {
-        mbar_init(&barLC, 1);
-        mbar_init(&barV, 1);
-        fence_mbar_init();
-        if ((int)blockIdx.x < ta.total) {
-            issue_lc(blockIdx.x);
-            issue_v(blockIdx.x);
-        }
-    }
-    __syncthreads();
-    const int n = g.H;
-    const int j0 = p * M;
-    const int j1 = (p == T - 1) ? n : j0 + M;
-    int it = 0;
-    for (int s = blockIdx.x; s < ta.total; s += gridDim.x, ++it) {
-        const int z = s / ta.nstrips, x = (s - z * ta.nstrips) * CW + cx;
-        const bool active = (p < T) && (x < g.W);
-        const int m = active ? j1 - j0 : 0;
-        mbar_wait(&barLC, (uint32_t)it & 1u);
-        float dv[MC], cv[MC];
-        float cprev = 0.f, cnext = 0.f;
-        if (active) {
-#pragma unroll
-            for (int i = 0; i < MC; ++i) {
-                dv[i] = i < m ? stL[(j0 + i) * CW + cx] : 0.f;
-                cv[i] = i < m ? stC[(j0 + i) * CW + cx] : 0.f;
-            }
-            cprev = j0 > 0 ? stC[(j0 - 1) * CW + cx] : 0.f;
-            cnext = j1 < n ? stC[j1 * CW + cx] : 0.f;
-        }
-        __syncthreads();  // the L/c stage is free: stream the next strip in behind this one's solve
-        if (tid == 0 && s + (int)gridDim.x < ta.total) {
-            fence_proxy_async();
-            issue_lc(s + gridDim.x);
-        }
-        Chunk<MC> ch;
-        if (active) {
-            if (m == M) eliminate_full<M>(ch, dv, cv, cprev, cnext, j0 == 0, j1 == n, tau);
-            else eliminate<MC>(ch, dv, cv, cprev, cnext, m, j0 == 0, j1 == n, tau);
-        } else {
-            ch.A = ch.C = ch.D = 0.f;
-            ch.lA = ch.lG = ch.lD = 0.f;
-        }
-        const int idx = p * CW + cx;
-        sla[idx] = ch.lA;
-        slg[idx] = ch.lG;
-        sld[idx] = ch.lD;
-        __syncthreads();
-        float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
-        if (active) {
-            float pA = 0.f, pG = 0.f, pD = 0.f;
-            if (p > 0) {
-                pA = sla[idx - CW];
-                pG = slg[idx - CW];
-                pD = sld[idx - CW];
-            }
-            af = -ch.A * pA;
-            bf = 1.f - ch.A * pG - ch.C * ch.lA;
-            cf = -ch.C * ch.lG;
-            df = ch.D - ch.A * pD - ch.C * ch.lD;
-        }
-        const float xf = pcr_solve(af, bf, cf, df, p, TP, CW, idx, sa, sb, sc, sd);
-        sa[idx] = xf;
-        __syncthreads();
-        mbar_wait(&barV, (uint32_t)it & 1u);
-        if (active) {
-            const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
-            const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
-            const float* vv = stV + j0 * CW + cx;
-            float* Oc = Lout + z * out_img_stride + (size_t)j0 * g.P + x;
-            Oc[0] = 0.5f * (xf + vv[0]);
-#pragma unroll
-            for (int i = 1; i < MC; ++i)
-                if (i < m - 1) Oc[(size_t)i * g.P] = 0.5f * (ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl + vv[i * CW]);
-            Oc[(size_t)(m - 1) * g.P] = 0.5f * (xl + vv[(m - 1) * CW]);
-        }
-        __syncthreads();  // V stage consumed
-        if (tid == 0 && s + (int)gridDim.x < ta.total) {
-            fence_proxy_async();
-            issue_v(s + gridDim.x);
-        }
-    }
-}
-
-// 2-D fp32 tensor map over `rows` rows of `pitch` floats (row-major), box = 8 columns x bh rows.
-bool make_tmap(CUtensorMap* map, const float* base, int width, int pitch, long long rows, int bh) {
-    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static EncodeFn encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q;
-        void* fn = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !fn)
-            return false;
-        encode = (EncodeFn)fn;
-    }
-    const cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
-    const cuuint32_t box[2] = {8, (cuuint32_t)bh};
-    const cuuint32_t estr[2] = {1, 1};
-    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// -------------------------------------------------------------------------------------------------------------
 // Row systems, one CTA of NW warps per row (the row pass runs first and writes V).  The TMA engine streams the
 // row's L and c into shared memory; thread p owns the chunk [p·M, p·M + m) (M odd: conflict-free strided reads)
 // and eliminates it in registers; the reduced system (one unknown per thread) is solved by a warp-level SPIKE:
@@ -605,107 +433,12 @@ void run_cols(const float* L, const float* c, const float* U, float* Lout, Strid
     k_aos_cols<CW, M, NT><<<grid, CW * TP, smem, s>>>(L, c, U, Lout, st, g, tau, T, TP);
 }
 
-struct TmapCache {
-    const float* base;
-    int width, pitch, bh;
-    long long rows;
-    CUtensorMap map;
-};
-
-const CUtensorMap* cached_tmap(const float* base, int width, int pitch, long long rows, int bh) {
-    static TmapCache cache[64];
-    static int next = 0;
-    for (auto& e : cache)
-        if (e.base == base && e.width == width && e.pitch == pitch && e.rows == rows && e.bh == bh) return &e.map;
-    TmapCache& e = cache[next];
-    next = (next + 1) % 64;
-    if (!make_tmap(&e.map, base, width, pitch, rows, bh)) {
-        e.base = nullptr;
-        return nullptr;
-    }
-    e.base = base;
-    e.width = width;
-    e.pitch = pitch;
-    e.rows = rows;
-    e.bh = bh;
-    return &e.map;
-}
-
-int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
-
-template <int M>
-bool run_cols_tma(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
-                  float tau, cudaStream_t s) {
-    const int T = n_chunks(g.H, M);
-    const int TP = round_up(T, 4);
-    if (8 * TP > 1024) return false;
-    const int nb = (g.H + 255) / 256;
-    const int bh = (((g.H + nb - 1) / nb) + 3) & ~3;  // tile rows: multiple of 4 (128-byte aligned tiles), <= 256
-    ColTmaArgs ta;
-    ta.rowL0 = 0;
-    ta.rowsPerImgL = (int)(st.L / g.P);
-    ta.nb = nb;
-    ta.bh = bh;
-    ta.nstrips = (g.W + 7) / 8;
-    ta.total = ta.nstrips * nimg;
-    const long long rowsL = (long long)(nimg - 1) * ta.rowsPerImgL + g.H;
-    const long long rowsC = (long long)(nimg - 1) * (st.c / g.P) + g.H;
-    if ((long long)(st.c / g.P) != g.H || (long long)(st.U / g.P) != g.H) return false;
-    const CUtensorMap* mL = cached_tmap(L, g.W, g.P, rowsL, bh);
-    const CUtensorMap* mC = cached_tmap(c, g.W, g.P, rowsC, bh);
-    const CUtensorMap* mV = cached_tmap(V, g.W, g.P, rowsC, bh);
-    if (!mL || !mC || !mV) return false;
-    const size_t smem = sizeof(float) * (3 * (size_t)nb * bh * 8 + 7 * 8 * TP) + 128;
-    if (smem > 220 * 1024) return false;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_aos_cols_tma<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr = true;
-    }
-    const int grid = ta.total < num_sms() ? ta.total : num_sms();
-    k_aos_cols_tma<M><<<grid, 8 * TP, smem, s>>>(*mL, *mC, *mV, Lout, st.out, g, tau, T, TP, ta);
-    return true;
-}
-
 }  // namespace
 
 // Column chunk length: T = n_chunks(H, M) must fit the CTA (CW*TP <= NT).
 bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
                      float tau, cudaStream_t s) {
     const int H = g.H;
-    static int cw = -1, tma = -1;
-    if (cw < 0) {
-        const char* e = getenv("KAZE_COLS_CW");  // tuning knob: 8 (default) or 4 columns per CTA
-        cw = (e && atoi(e) == 4) ? 4 : 8;
-        const char* t = getenv("KAZE_COLS_TMA");  // tuning knob: 0 disables the TMA-pipelined column kernel
-        tma = (t && atoi(t) == 0) ? 0 : 1;
-    }
-    if (tma) {
-        bool done = false;
-        if (H <= 128 * 4) done = run_cols_tma<4>(L, c, V, Lout, st, g, nimg, tau, s);
-        else if (H <= 128 * 6) done = run_cols_tma<6>(L, c, V, Lout, st, g, nimg, tau, s);
-        else if (H <= 128 * 8) done = run_cols_tma<8>(L, c, V, Lout, st, g, nimg, tau, s);
-        else if (H <= 128 * 10) done = run_cols_tma<10>(L, c, V, Lout, st, g, nimg, tau, s);
-        else if (H <= 128 * 12) done = run_cols_tma<12>(L, c, V, Lout, st, g, nimg, tau, s);
-        if (done) return true;
-    }
-    if (cw == 4 && H <= 128 * 12) {
-        if (H <= 128 * 4) run_cols<4, 4, 512>(L, c, V, Lout, st, g, nimg, tau, s);
-        else if (H <= 128 * 6) run_cols<4, 6, 512>(L, c, V, Lout, st, g, nimg, tau, s);
-        else if (H <= 128 * 8) run_cols<4, 8, 512>(L, c, V, Lout, st, g, nimg, tau, s);
-        else if (H <= 128 * 10) run_cols<4, 10, 512>(L, c, V, Lout, st, g, nimg, tau, s);
-        else run_cols<4, 12, 512>(L, c, V, Lout, st, g, nimg, tau, s);
-        return true;
-    }
     if (H <= 128 * 4) run_cols<8, 4, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
     else if (H <= 128 * 6) run_cols<8, 6, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
     else if (H <= 128 * 8) run_cols<8, 8, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
