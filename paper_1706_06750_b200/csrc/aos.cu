@@ -1,7 +1,7 @@
 // aos.cu — semi-implicit AOS step of Eq. 4 (readings A1, A2) on sm_100a.
 //
 // L_i = ½[(I − 2τA_x(c))⁻¹ + (I − 2τA_y(c))⁻¹] L_{i−1}: H row systems of length W (k_aos_rows_cta → V, first) and
-// W column systems of length H (k_aos_cols → L_i = ½(U + V), second).  Every line is tridiagonal with
+// W column systems of length H (k_cols_* → L_i = ½(U + V), second).  Every line is tridiagonal with
 //   a_j = −τ(c_{j−1} + c_j),  cc_j = −τ(c_j + c_{j+1}),  b_j = 1 − a_j − cc_j   (Neumann ends: a_0 = cc_{n−1} = 0).
 //
 // Both passes use the partition ("Thomas–PCR hybrid") scheme of DESIGN.md §6: a line is cut into T chunks of M
@@ -14,40 +14,15 @@
 //            copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is solved
 //            by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve), and V
 //            leaves through shared memory with 16-byte stores.
-//   columns: a CTA owns CW adjacent columns; a warp covers CW columns × 32/CW chunks, so every global request is
-//            whole 32-byte sectors; the reduced systems are solved by PCR in shared memory; V is prefetched with
-//            cp.async behind the solve and L_i = ½(U + V) is written directly.
+//   columns: three register-light passes (k_cols_reduce / k_cols_solve / k_cols_final, see below): every warp
+//            covers 32 adjacent columns, so every access is a full 128-byte row segment; no shared memory and no
+//            barriers; L_i = ½(U + V) is written by the last pass.
 #include "kaze_internal.cuh"
 #include "ptx.cuh"
 
 namespace kz {
 
 namespace {
-
-// Parallel cyclic reduction of a tridiagonal system with one equation per thread (p = 0..TP-1 within its
-// system, idx = p*stride + off in the shared arrays).  Threads p >= T carry identity rows.  Returns x_p.
-__device__ __forceinline__ float pcr_solve(float af, float bf, float cf, float df, int p, int TP, int stride, int idx,
-                                           float* sa, float* sb, float* sc, float* sd) {
-    for (int st = 1; st < TP; st <<= 1) {
-        sa[idx] = af;
-        sb[idx] = bf;
-        sc[idx] = cf;
-        sd[idx] = df;
-        __syncthreads();
-        const bool hm = p >= st, hp = p + st < TP;
-        const int jm = hm ? idx - st * stride : idx, jp = hp ? idx + st * stride : idx;
-        const float am = sa[jm], bm = sb[jm], cm = sc[jm], dm = sd[jm];
-        const float ap = sa[jp], bp = sb[jp], cp = sc[jp], dp = sd[jp];
-        const float k1 = hm ? af * frcp(bm) : 0.f;
-        const float k2 = hp ? cf * frcp(bp) : 0.f;
-        __syncthreads();
-        af = -am * k1;
-        cf = -cp * k2;
-        bf = bf - cm * k1 - ap * k2;
-        df = df - dm * k1 - dp * k2;
-    }
-    return df * frcp(bf);
-}
 
 template <int MC>
 struct Chunk {
@@ -176,93 +151,161 @@ __host__ __device__ inline int n_chunks(int n, int M) {
 }
 
 // -------------------------------------------------------------------------------------------------------------
-// Column systems.  Thread (cx, p): column x0 + cx, chunk p of T.  blockDim.x = CW * TP; shared index p*CW + cx.
-template <int CW, int M, int NT>
-__global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, const float* __restrict__ c,
-                                                 const float* __restrict__ U, float* __restrict__ Lout, Strides st,
-                                                 Geom g, float tau, int T, int TP) {
+// Column systems in three register-light passes (no shared memory, no barriers, every warp = 32 adjacent columns,
+// so every access is a full 128-byte row segment):
+//   cols_reduce : per (column, chunk of M rows): a downward sweep keeping x_first gives the chunk's LAST equation
+//                 α x_first + x_last + γ x_next = δ, a mirrored upward sweep keeping x_last gives its FIRST equation
+//                 x_first + α~ x_prev + γ~ x_last = δ~ (O(1) state each, the chunk's L and c held in registers).
+//   cols_solve  : per column, the 2T reduced unknowns (x_first, x_last of every chunk) form a tridiagonal system,
+//                 solved by Thomas (diagonally dominant: Schur complement of an M-matrix).
+//   cols_final  : per chunk, the interior with known end values is a plain Thomas solve; L_i = ½(U + V) is written.
+// DRAM traffic stays at the algorithmic 16 B/px when the level's L and c stay in L2 between the first and last
+// pass (they are re-read there).
+template <int M>
+__global__ void __launch_bounds__(256) k_cols_reduce(const float* __restrict__ L, const float* __restrict__ c,
+                                                     float* __restrict__ red, Strides st, Geom g, float tau, int T,
+                                                     size_t red_img_stride) {
     constexpr int MC = M + 1;
-    extern __shared__ float sm[];
-    const int NTOT = CW * TP;
-    float* sa = sm;
-    float* sb = sa + NTOT;
-    float* sc = sb + NTOT;
-    float* sd = sc + NTOT;
-    float* sla = sd + NTOT;  // last-equation exchange
-    float* slg = sla + NTOT;
-    float* sld = slg + NTOT;
-    float* sv = sld + NTOT;  // V chunk, prefetched with cp.async while the solve runs: [MC][NTOT]
-    const int cx = threadIdx.x % CW, p = threadIdx.x / CW;
-    const int x = blockIdx.x * CW + cx;
-    const bool active = (p < T) && (x < g.W);
+    const int x = blockIdx.x * 32 + threadIdx.x;
+    const int p = blockIdx.y * 8 + threadIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.W || p >= T) return;
     const int n = g.H;
-    const int j0 = p * M;
-    const int j1 = (p == T - 1) ? n : j0 + M;
-    const int m = active ? j1 - j0 : 0;
-
-    Chunk<MC> ch;
-    if (active) {  // the V chunk streams into shared memory behind the solve
-        const float* Vg = U + blockIdx.z * st.U + (size_t)j0 * g.P + x;
+    const int j0 = p * M, j1 = (p == T - 1) ? n : j0 + M, m = j1 - j0;
+    const float* Lc = L + z * st.L + (size_t)j0 * g.P + x;
+    const float* cc = c + z * st.c + (size_t)j0 * g.P + x;
+    float dv[MC], tq[MC + 1];  // tq[i] = τ(c_{i-1} + c_i) for i = 0..m (0 at the line ends)
+    float cv[MC];
 #pragma unroll
-        for (int i = 0; i < MC; ++i)
-            if (i < m) cp_async4(sv + i * NTOT + threadIdx.x, Vg + (size_t)i * g.P);
+    for (int i = 0; i < MC; ++i) {
+        dv[i] = i < m ? __ldg(Lc + (size_t)i * g.P) : 0.f;
+        cv[i] = i < m ? __ldg(cc + (size_t)i * g.P) : 0.f;
     }
-    if (active) {
-        float dv[MC], cv[MC];
-        const float* Lc = L + blockIdx.z * st.L + (size_t)j0 * g.P + x;
-        const float* cc = c + blockIdx.z * st.c + (size_t)j0 * g.P + x;
+    const float cprev = j0 > 0 ? __ldg(cc - g.P) : 0.f;
+    const float cnext = j1 < n ? __ldg(cc + (size_t)m * g.P) : 0.f;
+    tq[0] = j0 > 0 ? tau * (cprev + cv[0]) : 0.f;
 #pragma unroll
-        for (int i = 0; i < MC; ++i) {
-            if (i < m) {
-                dv[i] = __ldg(Lc + (size_t)i * g.P);
-                cv[i] = __ldg(cc + (size_t)i * g.P);
-            } else {
-                dv[i] = 0.f;
-                cv[i] = 0.f;
-            }
-        }
-        const float cprev = j0 > 0 ? __ldg(cc - g.P) : 0.f;
-        const float cnext = j1 < n ? __ldg(cc + (size_t)m * g.P) : 0.f;
-        if (m == M) eliminate_full<M>(ch, dv, cv, cprev, cnext, j0 == 0, j1 == n, tau);
-        else eliminate<MC>(ch, dv, cv, cprev, cnext, m, j0 == 0, j1 == n, tau);
-    } else {
-        ch.A = ch.C = ch.D = 0.f;
-        ch.lA = ch.lG = ch.lD = 0.f;
+    for (int i = 1; i <= MC; ++i) {
+        float v;
+        if (i < m) v = tau * (cv[i - 1] + cv[i]);
+        else if (i == m) v = j1 < n ? tau * (cv[i - 1 < MC ? i - 1 : 0] + cnext) : 0.f;
+        else v = 0.f;
+        tq[i] = v;
     }
-    const int idx = p * CW + cx;
-    sla[idx] = ch.lA;
-    slg[idx] = ch.lG;
-    sld[idx] = ch.lD;
-    __syncthreads();
-    float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
-    if (active) {
-        float pA = 0.f, pG = 0.f, pD = 0.f;
-        if (p > 0) {
-            pA = sla[idx - CW];
-            pG = slg[idx - CW];
-            pD = sld[idx - CW];
-        }
-        af = -ch.A * pA;
-        bf = 1.f - ch.A * pG - ch.C * ch.lA;
-        cf = -ch.C * ch.lG;
-        df = ch.D - ch.A * pD - ch.C * ch.lD;
-    }
-    const float xf = pcr_solve(af, bf, cf, df, p, TP, CW, idx, sa, sb, sc, sd);
-    sa[idx] = xf;
-    __syncthreads();
-    if (!active) return;
-    const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
-    const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
-    // L_i = ½(U + V): the row pass already wrote V (prefetched into sv); the average is formed here.
-    cp_async_wait_all();
-    const float* vv = sv + threadIdx.x;
-    float* Oc = Lout + blockIdx.z * st.out + (size_t)j0 * g.P + x;
-    Oc[0] = 0.5f * (xf + vv[0]);
+    // row i: a_i = -tq[i], cc_i = -tq[i+1], b_i = 1 + tq[i] + tq[i+1]
+    float pa = -1.f, pg = 0.f, pd = 0.f;  // downward, virtual row 0
 #pragma unroll
     for (int i = 1; i < MC; ++i) {
-        if (i < m - 1) Oc[(size_t)i * g.P] = 0.5f * (ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl + vv[i * NTOT]);
+        if (i < m) {
+            const float r = frcp(1.f + tq[i] + tq[i + 1] + tq[i] * pg);
+            pa = tq[i] * pa * r;
+            pg = -tq[i + 1] * r;
+            pd = fmaf(tq[i], pd, dv[i]) * r;
+        }
     }
-    Oc[(size_t)(m - 1) * g.P] = 0.5f * (xl + vv[(m - 1) * NTOT]);
+    float qa = 0.f, qg = -1.f, qd = 0.f;  // upward, virtual row m-1: x_i + qa x_{i-1} + qg x_last = qd
+#pragma unroll
+    for (int i = MC - 1; i >= 0; --i) {
+        if (i <= m - 2) {
+            const float r = frcp(1.f + tq[i] + tq[i + 1] + tq[i + 1] * qa);  // b_i - cc_i α~_{i+1}
+            qa = -tq[i] * r;
+            qg = tq[i + 1] * qg * r;
+            qd = fmaf(tq[i + 1], qd, dv[i]) * r;
+        }
+    }
+    // [z][p][6][W]: first (α~, γ~, δ~), last (α, γ, δ)
+    float* o = red + z * red_img_stride + (size_t)p * 6 * g.W + x;
+    o[0] = qa;
+    o[(size_t)g.W] = qg;
+    o[(size_t)2 * g.W] = qd;
+    o[(size_t)3 * g.W] = pa;
+    o[(size_t)4 * g.W] = pg;
+    o[(size_t)5 * g.W] = pd;
+}
+
+// One thread per column: Thomas on u = (f_0, l_0, f_1, l_1, ...),
+//   f_p:  α~_p l_{p-1} + f_p + γ~_p l_p = δ~_p,      l_p:  α_p f_p + l_p + γ_p f_{p+1} = δ_p.
+// The forward sweep's (c', d') are kept in the output slots; the backward sweep overwrites them with u.
+__global__ void __launch_bounds__(128) k_cols_solve(float* __restrict__ red, float* __restrict__ sol, Geom g, int T,
+                                                    size_t red_img_stride, size_t sol_img_stride) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, z = blockIdx.y;
+    if (x >= g.W) return;
+    const float* e = red + z * red_img_stride + x;
+    float* u = sol + z * sol_img_stride + x;  // [z][2T][2][W]: (c', d') then u
+    const size_t W = g.W;
+    float cp = 0.f, dp = 0.f;
+    for (int k = 0; k < 2 * T; ++k) {
+        const int pp = k >> 1;
+        const float* q = e + (size_t)pp * 6 * W + ((k & 1) ? 3 * W : 0);
+        const float sub = q[0], sup = q[W], rhs = q[2 * W];  // diag = 1
+        const float r = frcp(1.f - sub * cp);
+        cp = sup * r;
+        dp = (rhs - sub * dp) * r;
+        u[(size_t)k * 2 * W] = cp;
+        u[(size_t)k * 2 * W + W] = dp;
+    }
+    float xn = 0.f;
+    for (int k = 2 * T - 1; k >= 0; --k) {
+        xn = u[(size_t)k * 2 * W + W] - u[(size_t)k * 2 * W] * xn;
+        u[(size_t)k * 2 * W + W] = xn;
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) k_cols_final(const float* __restrict__ L, const float* __restrict__ c,
+                                                    const float* __restrict__ V, const float* __restrict__ sol,
+                                                    float* __restrict__ Lout, Strides st, Geom g, float tau, int T,
+                                                    size_t sol_img_stride) {
+    constexpr int MC = M + 1;
+    const int x = blockIdx.x * 32 + threadIdx.x;
+    const int p = blockIdx.y * 8 + threadIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.W || p >= T) return;
+    const int n = g.H;
+    const int j0 = p * M, j1 = (p == T - 1) ? n : j0 + M, m = j1 - j0;
+    const size_t W = g.W;
+    const float* u = sol + z * sol_img_stride + x;
+    const float xf = u[(size_t)(2 * p) * 2 * W + W], xl = u[(size_t)(2 * p + 1) * 2 * W + W];
+    const float* Lc = L + z * st.L + (size_t)j0 * g.P + x;
+    const float* cc = c + z * st.c + (size_t)j0 * g.P + x;
+    const float* Vc = V + z * st.U + (size_t)j0 * g.P + x;
+    float dv[MC], cv[MC], vv[MC];
+#pragma unroll
+    for (int i = 0; i < MC; ++i) {
+        dv[i] = i < m ? __ldg(Lc + (size_t)i * g.P) : 0.f;
+        cv[i] = i < m ? __ldg(cc + (size_t)i * g.P) : 0.f;
+        vv[i] = i < m ? __ldg(Vc + (size_t)i * g.P) : 0.f;
+    }
+    // interior rows 1..m-2 with x_0 = xf and x_{m-1} = xl known; τ(c_{i-1}+c_i) for i = 1..m-1 (interior only)
+    float cpv[MC], dpv[MC];
+    float cp = 0.f, dp = 0.f;
+#pragma unroll
+    for (int i = 1; i < MC; ++i) {
+        if (i <= m - 2) {
+            const float ta = tau * (cv[i - 1] + cv[i]), tb = tau * (cv[i] + cv[i + 1 < MC ? i + 1 : 0]);
+            float rhs = dv[i];
+            if (i == 1) rhs += ta * xf;          // -a_1 x_0
+            if (i == m - 2) rhs += tb * xl;      // -cc_{m-2} x_{m-1}
+            const float sub = (i == 1) ? 0.f : -ta;
+            const float sup = (i == m - 2) ? 0.f : -tb;
+            const float r = frcp(1.f + ta + tb - sub * cp);
+            cp = sup * r;
+            dp = (rhs - sub * dp) * r;
+            cpv[i] = cp;
+            dpv[i] = dp;
+        }
+    }
+    float* Oc = Lout + z * st.out + (size_t)j0 * g.P + x;
+    float xn = xl;
+#pragma unroll
+    for (int i = MC - 1; i >= 0; --i) {
+        if (i == m - 1) Oc[(size_t)i * g.P] = 0.5f * (xl + vv[i]);
+        else if (i >= 1 && i <= m - 2) {
+            xn = dpv[i] - cpv[i] * xn;
+            Oc[(size_t)i * g.P] = 0.5f * (xn + vv[i]);
+        }
+    }
+    Oc[0] = 0.5f * (xf + vv[0]);
 }
 
 // -------------------------------------------------------------------------------------------------------------
@@ -418,35 +461,25 @@ void run_rows_cta(const float* L, const float* c, float* V, Strides st, Geom g, 
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
-template <int CW, int M, int NT>
-void run_cols(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg, float tau,
-              cudaStream_t s) {
-    const int T = n_chunks(g.H, M);
-    const int TP = round_up(T, 32 / CW);
-    const size_t smem = sizeof(float) * (7 + M + 1) * CW * TP;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_aos_cols<CW, M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    dim3 grid((g.W + CW - 1) / CW, 1, nimg);
-    k_aos_cols<CW, M, NT><<<grid, CW * TP, smem, s>>>(L, c, U, Lout, st, g, tau, T, TP);
-}
-
 }  // namespace
 
-// Column chunk length: T = n_chunks(H, M) must fit the CTA (CW*TP <= NT).
+template <int M>
+void run_cols3(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg, float tau,
+               float* red, float* sol, cudaStream_t s) {
+    const int T = n_chunks(g.H, M);
+    const size_t red_stride = (size_t)T * 6 * g.W, sol_stride = (size_t)T * 4 * g.W;
+    dim3 blk(32, 8), grd((g.W + 31) / 32, (T + 7) / 8, nimg);
+    k_cols_reduce<M><<<grd, blk, 0, s>>>(L, c, red, st, g, tau, T, red_stride);
+    k_cols_solve<<<dim3((g.W + 127) / 128, nimg), 128, 0, s>>>(red, sol, g, T, red_stride, sol_stride);
+    k_cols_final<M><<<grd, blk, 0, s>>>(L, c, V, sol, Lout, st, g, tau, T, sol_stride);
+}
+
+// Columns: three-pass register-light scheme (chunk M = 16 rows, 8 for short columns).  red / sol: scratch of at
+// least 6·T·W and 4·T·W floats per image.
 bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
-                     float tau, cudaStream_t s) {
-    const int H = g.H;
-    if (H <= 128 * 4) run_cols<8, 4, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 6) run_cols<8, 6, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 8) run_cols<8, 8, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 10) run_cols<8, 10, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 12) run_cols<8, 12, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 256 * 16) run_cols<2, 16, 512>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 256 * 32) run_cols<2, 32, 512>(L, c, V, Lout, st, g, nimg, tau, s);
-    else return false;
+                     float tau, float* red, float* sol, cudaStream_t s) {
+    if (g.H >= 256) run_cols3<16>(L, c, V, Lout, st, g, nimg, tau, red, sol, s);
+    else run_cols3<8>(L, c, V, Lout, st, g, nimg, tau, red, sol, s);
     return true;
 }
 

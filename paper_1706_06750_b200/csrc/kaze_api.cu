@@ -55,7 +55,7 @@ struct kaze_ctx {
     // arena
     int Pmax = 0;
     size_t plane_max = 0;
-    float *Lt = nullptr, *Ldet = nullptr, *cbuf = nullptr, *ubuf = nullptr;
+    float *Lt = nullptr, *Ldet = nullptr, *cbuf = nullptr, *ubuf = nullptr, *redbuf = nullptr, *solbuf = nullptr;
     float2* Lxy = nullptr;  // interleaved (Lx, Ly)
     float* kval = nullptr;
     unsigned* hmax = nullptr;
@@ -118,15 +118,17 @@ struct Launch {
     int kc;
     double bytes;
     cudaStream_t s;
+    int nk;  // kernels launched inside this scope
     cudaEvent_t e0 = nullptr;
-    Launch(kaze_ctx* c_, int kc_, double bytes_, cudaStream_t s_) : c(c_), kc(kc_), bytes(bytes_), s(s_) {
+    Launch(kaze_ctx* c_, int kc_, double bytes_, cudaStream_t s_, int nk_ = 1)
+        : c(c_), kc(kc_), bytes(bytes_), s(s_), nk(nk_) {
         if (c->prof) {
             e0 = get_event(c);
             cudaEventRecord(e0, s);
         }
     }
     ~Launch() {
-        c->launches++;
+        c->launches += nk;
         if (c->prof) {
             cudaEvent_t e1 = get_event(c);
             cudaEventRecord(e1, s);
@@ -189,7 +191,7 @@ kaze_status validate_params(const kaze_params* p) {
 }
 
 void free_arena(kaze_ctx* c) {
-    void* ptrs[] = {c->Lt, c->Lxy, c->Ldet, c->cbuf, c->ubuf, c->kval, c->hmax, c->hist, c->fallback,
+    void* ptrs[] = {c->Lt, c->Lxy, c->Ldet, c->cbuf, c->ubuf, c->redbuf, c->solbuf, c->kval, c->hmax, c->hist, c->fallback,
                     c->bitmap, c->rowcnt, c->rowoff, c->hin[0], c->hin[1], c->hkps[0], c->hkps[1],
                     c->hcnt[0], c->hcnt[1], c->hdesc[0], c->hdesc[1]};
     for (void* q : ptrs)
@@ -264,8 +266,8 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
         }
         KZ_CHECK_LAUNCH(c, "aos_rows");
         {   // L_i = ½(U + V), U = column solves
-            Launch L(c, KC_AOS_COLS, 16.0 * px, s);
-            if (!launch_aos_cols(prev, c->cbuf, c->ubuf, cur, Strides{SL, SP, SP, SL}, g, n, tau, s))
+            Launch L(c, KC_AOS_COLS, 16.0 * px, s, 3);
+            if (!launch_aos_cols(prev, c->cbuf, c->ubuf, cur, Strides{SL, SP, SP, SL}, g, n, tau, c->redbuf, c->solbuf, s))
                 return KAZE_ERR_INVALID_ARGUMENT;
         }
         KZ_CHECK_LAUNCH(c, "aos_cols");
@@ -298,7 +300,7 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     }
     if (big.n > 0) {
         const size_t lo = (size_t)first_big * g.plane;
-        Launch L(c, KC_HESSIAN, 24.0 * px * big.n, s);
+        Launch L(c, KC_HESSIAN, 24.0 * px * big.n, s, 2);
         launch_hess_first(c->Lt + lo, c->Lxy + lo, c->img_stride, g, n, big, s);
         launch_hess_det(c->Lxy + lo, c->Ldet + lo, c->img_stride, g, n, big, s);
     }
@@ -308,7 +310,7 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     } else {
         DetectParams dp{(float)c->p.threshold, (float)c->p.edge_ratio, c->p.max_keypoints};
         {
-            Launch L(c, KC_NMS_MARK, 4.0 * px * N, s);
+            Launch L(c, KC_NMS_MARK, 4.0 * px * N, s);  // (+ one memset of the row counters)
             launch_nms_mark(c->Ldet, c->img_stride, g, n, N, dp, c->bitmap, c->rowcnt, s);
         }
         KZ_CHECK_LAUNCH(c, "nms_mark");
@@ -433,6 +435,8 @@ kaze_status kaze_create(const kaze_params* p, int device, kaze_ctx** out) {
               cudaMalloc(&c->Ldet, pyr) == cudaSuccess &&
               cudaMalloc(&c->cbuf, sizeof(float) * c->plane_max * B) == cudaSuccess &&
               cudaMalloc(&c->ubuf, sizeof(float) * c->plane_max * B) == cudaSuccess &&
+              cudaMalloc(&c->redbuf, sizeof(float) * 6 * ((size_t)p->max_height / 8 + 2) * p->max_width * B) == cudaSuccess &&
+              cudaMalloc(&c->solbuf, sizeof(float) * 4 * ((size_t)p->max_height / 8 + 2) * p->max_width * B) == cudaSuccess &&
               cudaMalloc(&c->kval, sizeof(float) * B) == cudaSuccess &&
               cudaMalloc(&c->hmax, sizeof(unsigned) * B) == cudaSuccess &&
               cudaMalloc(&c->hist, sizeof(int) * B * p->k_bins) == cudaSuccess &&
