@@ -176,10 +176,11 @@ __global__ void __launch_bounds__(256) k_cols_reduce(const float* __restrict__ L
     const float* cc = c + z * st.c + (size_t)j0 * g.P + x;
     float dv[MC], tq[MC + 1];  // tq[i] = τ(c_{i-1} + c_i) for i = 0..m (0 at the line ends)
     float cv[MC];
+    const uint64_t keep = l2_policy_evict_last();  // L and c are read again by k_cols_final: keep them in L2
 #pragma unroll
     for (int i = 0; i < MC; ++i) {
-        dv[i] = i < m ? __ldg(Lc + (size_t)i * g.P) : 0.f;
-        cv[i] = i < m ? __ldg(cc + (size_t)i * g.P) : 0.f;
+        dv[i] = i < m ? ld_policy(Lc + (size_t)i * g.P, keep) : 0.f;
+        cv[i] = i < m ? ld_policy(cc + (size_t)i * g.P, keep) : 0.f;
     }
     const float cprev = j0 > 0 ? __ldg(cc - g.P) : 0.f;
     const float cnext = j1 < n ? __ldg(cc + (size_t)m * g.P) : 0.f;
@@ -233,21 +234,51 @@ __global__ void __launch_bounds__(128) k_cols_solve(float* __restrict__ red, flo
     const float* e = red + z * red_img_stride + x;
     float* u = sol + z * sol_img_stride + x;  // [z][2T][2][W]: (c', d') then u
     const size_t W = g.W;
+    // the coefficients of 4 chunks (8 equations) are fetched one batch ahead of the recurrence
+    constexpr int KB = 4;
+    float cur[KB * 6], nxt[KB * 6];
+#pragma unroll
+    for (int i = 0; i < KB * 6; ++i) cur[i] = (i / 6) < T ? __ldg(e + (size_t)i * W) : 0.f;
     float cp = 0.f, dp = 0.f;
-    for (int k = 0; k < 2 * T; ++k) {
-        const int pp = k >> 1;
-        const float* q = e + (size_t)pp * 6 * W + ((k & 1) ? 3 * W : 0);
-        const float sub = q[0], sup = q[W], rhs = q[2 * W];  // diag = 1
-        const float r = frcp(1.f - sub * cp);
-        cp = sup * r;
-        dp = (rhs - sub * dp) * r;
-        u[(size_t)k * 2 * W] = cp;
-        u[(size_t)k * 2 * W + W] = dp;
+    for (int p0 = 0; p0 < T; p0 += KB) {
+#pragma unroll
+        for (int i = 0; i < KB * 6; ++i) nxt[i] = (p0 + KB + i / 6) < T ? __ldg(e + (size_t)(p0 * 6 + KB * 6 + i) * W) : 0.f;
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+            if (p0 + q < T) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {  // f then l equation of chunk p0+q
+                    const float sub = cur[q * 6 + 3 * h], sup = cur[q * 6 + 3 * h + 1], rhs = cur[q * 6 + 3 * h + 2];
+                    const float r = frcp(1.f - sub * cp);
+                    cp = sup * r;
+                    dp = (rhs - sub * dp) * r;
+                    const size_t k = (size_t)(2 * (p0 + q) + h);
+                    u[k * 2 * W] = cp;
+                    u[k * 2 * W + W] = dp;
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < KB * 6; ++i) cur[i] = nxt[i];
     }
+    // backward: u_k = d'_k - c'_k u_{k+1}; the (c', d') pairs are re-read a batch ahead as well
     float xn = 0.f;
-    for (int k = 2 * T - 1; k >= 0; --k) {
-        xn = u[(size_t)k * 2 * W + W] - u[(size_t)k * 2 * W] * xn;
-        u[(size_t)k * 2 * W + W] = xn;
+    for (int k0 = 2 * T - 1; k0 >= 0; k0 -= 8) {
+        float cc8[8], dd8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = k0 - i;
+            cc8[i] = k >= 0 ? u[(size_t)k * 2 * W] : 0.f;
+            dd8[i] = k >= 0 ? u[(size_t)k * 2 * W + W] : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = k0 - i;
+            if (k >= 0) {
+                xn = dd8[i] - cc8[i] * xn;
+                u[(size_t)k * 2 * W + W] = xn;
+            }
+        }
     }
 }
 
@@ -270,11 +301,12 @@ __global__ void __launch_bounds__(256) k_cols_final(const float* __restrict__ L,
     const float* cc = c + z * st.c + (size_t)j0 * g.P + x;
     const float* Vc = V + z * st.U + (size_t)j0 * g.P + x;
     float dv[MC], cv[MC], vv[MC];
+    const uint64_t done = l2_policy_evict_first();  // last use of this level's L, c and V
 #pragma unroll
     for (int i = 0; i < MC; ++i) {
-        dv[i] = i < m ? __ldg(Lc + (size_t)i * g.P) : 0.f;
-        cv[i] = i < m ? __ldg(cc + (size_t)i * g.P) : 0.f;
-        vv[i] = i < m ? __ldg(Vc + (size_t)i * g.P) : 0.f;
+        dv[i] = i < m ? ld_policy(Lc + (size_t)i * g.P, done) : 0.f;
+        cv[i] = i < m ? ld_policy(cc + (size_t)i * g.P, done) : 0.f;
+        vv[i] = i < m ? ld_policy(Vc + (size_t)i * g.P, done) : 0.f;
     }
     // interior rows 1..m-2 with x_0 = xf and x_{m-1} = xl known; τ(c_{i-1}+c_i) for i = 1..m-1 (interior only)
     float cpv[MC], dpv[MC];

@@ -39,6 +39,7 @@ struct ProfRec {
     int kc;
     cudaEvent_t e0, e1;
     double bytes;
+    int nk;
 };
 
 }  // namespace
@@ -132,7 +133,7 @@ struct Launch {
         if (c->prof) {
             cudaEvent_t e1 = get_event(c);
             cudaEventRecord(e1, s);
-            c->recs.push_back({kc, e0, e1, bytes});
+            c->recs.push_back({kc, e0, e1, bytes, nk});
         }
     }
 };
@@ -682,7 +683,7 @@ kaze_status kaze_get_profile(kaze_ctx* c, kaze_kernel_stat* out, int32_t cap, in
     for (auto& r : c->recs) {
         float ms = 0.f;
         KZ_CUDA(c, cudaEventElapsedTime(&ms, r.e0, r.e1));
-        acc[r.kc].launches += 1;
+        acc[r.kc].launches += r.nk;
         acc[r.kc].total_ms += ms;
         acc[r.kc].algo_bytes += r.bytes;
     }
