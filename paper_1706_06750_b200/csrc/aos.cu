@@ -1,7 +1,7 @@
 // aos.cu — semi-implicit AOS step of Eq. 4 (readings A1, A2) on sm_100a.
 //
 // L_i = ½[(I − 2τA_x(c))⁻¹ + (I − 2τA_y(c))⁻¹] L_{i−1}: H row systems of length W (k_aos_rows_cta → V, first) and
-// W column systems of length H (k_cols_* → L_i = ½(U + V), second).  Every line is tridiagonal with
+// W column systems of length H (k_aos_cols → L_i = ½(U + V), second).  Every line is tridiagonal with
 //   a_j = −τ(c_{j−1} + c_j),  cc_j = −τ(c_j + c_{j+1}),  b_j = 1 − a_j − cc_j   (Neumann ends: a_0 = cc_{n−1} = 0).
 //
 // Both passes use the partition ("Thomas–PCR hybrid") scheme of DESIGN.md §6: a line is cut into T chunks of M
@@ -14,9 +14,9 @@
 //            copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is solved
 //            by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve), and V
 //            leaves through shared memory with 16-byte stores.
-//   columns: three register-light passes (k_cols_reduce / k_cols_solve / k_cols_final, see below): every warp
-//            covers 32 adjacent columns, so every access is a full 128-byte row segment; no shared memory and no
-//            barriers; L_i = ½(U + V) is written by the last pass.
+//   columns: a CTA owns CW adjacent columns (whole 32-byte sectors per warp request); chunks eliminated in
+//            registers, the reduced systems re-mapped so each warp holds 32 chunks of one column and solved by the
+//            same warp-level SPIKE; V prefetched with cp.async; L_i = ½(U + V) written directly.
 #include "kaze_internal.cuh"
 #include "ptx.cuh"
 
@@ -151,193 +151,190 @@ __host__ __device__ inline int n_chunks(int n, int M) {
 }
 
 // -------------------------------------------------------------------------------------------------------------
-// Column systems in three register-light passes (no shared memory, no barriers, every warp = 32 adjacent columns,
-// so every access is a full 128-byte row segment):
-//   cols_reduce : per (column, chunk of M rows): a downward sweep keeping x_first gives the chunk's LAST equation
-//                 α x_first + x_last + γ x_next = δ, a mirrored upward sweep keeping x_last gives its FIRST equation
-//                 x_first + α~ x_prev + γ~ x_last = δ~ (O(1) state each, the chunk's L and c held in registers).
-//   cols_solve  : per column, the 2T reduced unknowns (x_first, x_last of every chunk) form a tridiagonal system,
-//                 solved by Thomas (diagonally dominant: Schur complement of an M-matrix).
-//   cols_final  : per chunk, the interior with known end values is a plain Thomas solve; L_i = ½(U + V) is written.
-// DRAM traffic stays at the algorithmic 16 B/px when the level's L and c stay in L2 between the first and last
-// pass (they are re-read there).
-template <int M>
-__global__ void __launch_bounds__(256) k_cols_reduce(const float* __restrict__ L, const float* __restrict__ c,
-                                                     float* __restrict__ red, Strides st, Geom g, float tau, int T,
-                                                     size_t red_img_stride) {
+// Column systems.  A CTA owns CW adjacent columns; thread (cx, p) owns chunk p of column cx (a warp covers CW columns
+// x 32/CW chunks, so every global request is whole 32-byte sectors).  Each thread eliminates its chunk in registers.
+// The reduced systems (one unknown per chunk) are solved by a warp-level SPIKE after a shared-memory re-mapping in
+// which every warp owns 32 consecutive chunks of ONE column: shuffle PCR on three right-hand sides inside the warp,
+// then one thread per column solves the 2·(TP/32) warp-boundary unknowns (4 block barriers in all).  The chunk
+// coefficients are parked in shared memory across the solve to keep the 1024-thread CTA within 64 registers.  V
+// streams into shared memory with cp.async behind all of this and L_i = ½(U + V) is written directly.
+template <int CW, int M, int NT, bool PARK>
+__global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, const float* __restrict__ c,
+                                                 const float* __restrict__ V, float* __restrict__ Lout, Strides st,
+                                                 Geom g, float tau, int T, int TP) {
     constexpr int MC = M + 1;
-    const int x = blockIdx.x * 32 + threadIdx.x;
-    const int p = blockIdx.y * 8 + threadIdx.y;
-    const int z = blockIdx.z;
-    if (x >= g.W || p >= T) return;
+    constexpr int NWM = NT / (32 * CW);  // warps per column system (max)
+    extern __shared__ float sm[];
+    const int NTOT = CW * TP, SP = TP + 1;
+    float* ea = sm;                 // [CW][TP+1] equations, system-major
+    float* eb = ea + CW * SP;
+    float* ec = eb + CW * SP;
+    float* ed = ec + CW * SP;
+    float* bnd = ed + CW * SP;      // [CW][NWM warps][6]
+    float* sol = bnd + CW * NWM * 6;  // [CW][NWM][2]
+    float* sla = sol + CW * NWM * 2;  // last-equation exchange [NTOT]
+    float* slg = sla + NTOT;
+    float* sld = slg + NTOT;
+    float* park = sld + NTOT;       // [3*(MC-1)][NTOT] chunk coefficients during the solve (PARK only)
+    float* sv = park + (PARK ? 3 * (MC - 1) * NTOT : 0);  // [MC][NTOT] V prefetch
+    const int tid = threadIdx.x;
+    const int cx = tid % CW, p = tid / CW;
+    const int x = blockIdx.x * CW + cx;
+    const bool active = (p < T) && (x < g.W);
     const int n = g.H;
-    const int j0 = p * M, j1 = (p == T - 1) ? n : j0 + M, m = j1 - j0;
-    const float* Lc = L + z * st.L + (size_t)j0 * g.P + x;
-    const float* cc = c + z * st.c + (size_t)j0 * g.P + x;
-    float dv[MC], tq[MC + 1];  // tq[i] = τ(c_{i-1} + c_i) for i = 0..m (0 at the line ends)
-    float cv[MC];
-    const uint64_t keep = l2_policy_evict_last();  // L and c are read again by k_cols_final: keep them in L2
+    const int j0 = p * M;
+    const int j1 = (p == T - 1) ? n : j0 + M;
+    const int m = active ? j1 - j0 : 0;
+    const int P = g.P;
+    float A = 0.f, C = 0.f, D = 0.f, lA = 0.f, lG = 0.f, lD = 0.f;
+    Chunk<MC> ch;
+    if (active) {
+        const float* Vg = V + blockIdx.z * st.U + (size_t)j0 * P + x;
 #pragma unroll
-    for (int i = 0; i < MC; ++i) {
-        dv[i] = i < m ? ld_policy(Lc + (size_t)i * g.P, keep) : 0.f;
-        cv[i] = i < m ? ld_policy(cc + (size_t)i * g.P, keep) : 0.f;
-    }
-    const float cprev = j0 > 0 ? __ldg(cc - g.P) : 0.f;
-    const float cnext = j1 < n ? __ldg(cc + (size_t)m * g.P) : 0.f;
-    tq[0] = j0 > 0 ? tau * (cprev + cv[0]) : 0.f;
+        for (int i = 0; i < MC; ++i)
+            if (i < m) cp_async4(sv + i * NTOT + tid, Vg + i * P);
+        const float* Lc = L + blockIdx.z * st.L + (size_t)j0 * P + x;
+        const float* cc = c + blockIdx.z * st.c + (size_t)j0 * P + x;
+        float dv[MC], cv[MC];
 #pragma unroll
-    for (int i = 1; i <= MC; ++i) {
-        float v;
-        if (i < m) v = tau * (cv[i - 1] + cv[i]);
-        else if (i == m) v = j1 < n ? tau * (cv[i - 1 < MC ? i - 1 : 0] + cnext) : 0.f;
-        else v = 0.f;
-        tq[i] = v;
-    }
-    // row i: a_i = -tq[i], cc_i = -tq[i+1], b_i = 1 + tq[i] + tq[i+1]
-    float pa = -1.f, pg = 0.f, pd = 0.f;  // downward, virtual row 0
-#pragma unroll
-    for (int i = 1; i < MC; ++i) {
-        if (i < m) {
-            const float r = frcp(1.f + tq[i] + tq[i + 1] + tq[i] * pg);
-            pa = tq[i] * pa * r;
-            pg = -tq[i + 1] * r;
-            pd = fmaf(tq[i], pd, dv[i]) * r;
+        for (int i = 0; i < MC; ++i) {
+            dv[i] = i < m ? __ldg(Lc + i * P) : 0.f;
+            cv[i] = i < m ? __ldg(cc + i * P) : 0.f;
         }
-    }
-    float qa = 0.f, qg = -1.f, qd = 0.f;  // upward, virtual row m-1: x_i + qa x_{i-1} + qg x_last = qd
+        const float cprev = j0 > 0 ? __ldg(cc - P) : 0.f;
+        const float cnext = j1 < n ? __ldg(cc + m * P) : 0.f;
+        if (m == M) eliminate_full<M>(ch, dv, cv, cprev, cnext, j0 == 0, j1 == n, tau);
+        else eliminate<MC>(ch, dv, cv, cprev, cnext, m, j0 == 0, j1 == n, tau);
+        if (PARK) {
 #pragma unroll
-    for (int i = MC - 1; i >= 0; --i) {
-        if (i <= m - 2) {
-            const float r = frcp(1.f + tq[i] + tq[i + 1] + tq[i + 1] * qa);  // b_i - cc_i α~_{i+1}
-            qa = -tq[i] * r;
-            qg = tq[i + 1] * qg * r;
-            qd = fmaf(tq[i + 1], qd, dv[i]) * r;
+            for (int i = 1; i < MC; ++i) {
+                park[(3 * (i - 1) + 0) * NTOT + tid] = ch.al[i];
+                park[(3 * (i - 1) + 1) * NTOT + tid] = ch.ga[i];
+                park[(3 * (i - 1) + 2) * NTOT + tid] = ch.de[i];
+            }
         }
+        A = ch.A;
+        C = ch.C;
+        D = ch.D;
+        lA = ch.lA;
+        lG = ch.lG;
+        lD = ch.lD;
     }
-    // [z][p][6][W]: first (α~, γ~, δ~), last (α, γ, δ)
-    float* o = red + z * red_img_stride + (size_t)p * 6 * g.W + x;
-    o[0] = qa;
-    o[(size_t)g.W] = qg;
-    o[(size_t)2 * g.W] = qd;
-    o[(size_t)3 * g.W] = pa;
-    o[(size_t)4 * g.W] = pg;
-    o[(size_t)5 * g.W] = pd;
-}
-
-// One thread per column: Thomas on u = (f_0, l_0, f_1, l_1, ...),
-//   f_p:  α~_p l_{p-1} + f_p + γ~_p l_p = δ~_p,      l_p:  α_p f_p + l_p + γ_p f_{p+1} = δ_p.
-// The forward sweep's (c', d') are kept in the output slots; the backward sweep overwrites them with u.
-__global__ void __launch_bounds__(128) k_cols_solve(float* __restrict__ red, float* __restrict__ sol, Geom g, int T,
-                                                    size_t red_img_stride, size_t sol_img_stride) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, z = blockIdx.y;
-    if (x >= g.W) return;
-    const float* e = red + z * red_img_stride + x;
-    float* u = sol + z * sol_img_stride + x;  // [z][2T][2][W]: (c', d') then u
-    const size_t W = g.W;
-    // the coefficients of 4 chunks (8 equations) are fetched one batch ahead of the recurrence
-    constexpr int KB = 4;
-    float cur[KB * 6], nxt[KB * 6];
+    sla[tid] = lA;
+    slg[tid] = lG;
+    sld[tid] = lD;
+    __syncthreads();
+    {   // f-equation of chunk p, stored system-major for the re-mapped solve
+        float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
+        if (active) {
+            const float pA = p > 0 ? sla[tid - CW] : 0.f, pG = p > 0 ? slg[tid - CW] : 0.f;
+            const float pD = p > 0 ? sld[tid - CW] : 0.f;
+            af = -A * pA;
+            bf = 1.f - A * pG - C * lA;
+            cf = -C * lG;
+            df = D - A * pD - C * lD;
+        }
+        ea[cx * SP + p] = af;
+        eb[cx * SP + p] = bf;
+        ec[cx * SP + p] = cf;
+        ed[cx * SP + p] = df;
+    }
+    __syncthreads();
+    {   // re-mapped: system s2 = tid / TP, equation p2 = tid % TP; warp w owns equations 32w..32w+31
+        const int s2 = tid / TP, p2 = tid - s2 * TP, lane = tid & 31, w = p2 >> 5, nw = TP >> 5;
+        const int i2 = s2 * SP + p2;
+        float a = ea[i2], b = eb[i2], cc = ec[i2], r0 = ed[i2], r1 = 0.f, r2 = 0.f;
+        if (lane == 0) {
+            r1 = a;
+            a = 0.f;
+        }
+        if (lane == 31) {
+            r2 = cc;
+            cc = 0.f;
+        }
 #pragma unroll
-    for (int i = 0; i < KB * 6; ++i) cur[i] = (i / 6) < T ? __ldg(e + (size_t)i * W) : 0.f;
-    float cp = 0.f, dp = 0.f;
-    for (int p0 = 0; p0 < T; p0 += KB) {
+        for (int s3 = 1; s3 < 32; s3 <<= 1) {
+            const bool hm = lane >= s3, hp = lane + s3 < 32;
+            const float am = __shfl_up_sync(0xffffffffu, a, s3), bm = __shfl_up_sync(0xffffffffu, b, s3);
+            const float cm = __shfl_up_sync(0xffffffffu, cc, s3), q0m = __shfl_up_sync(0xffffffffu, r0, s3);
+            const float q1m = __shfl_up_sync(0xffffffffu, r1, s3), q2m = __shfl_up_sync(0xffffffffu, r2, s3);
+            const float ap = __shfl_down_sync(0xffffffffu, a, s3), bp = __shfl_down_sync(0xffffffffu, b, s3);
+            const float cp = __shfl_down_sync(0xffffffffu, cc, s3), q0p = __shfl_down_sync(0xffffffffu, r0, s3);
+            const float q1p = __shfl_down_sync(0xffffffffu, r1, s3), q2p = __shfl_down_sync(0xffffffffu, r2, s3);
+            const float k1 = hm ? a * frcp(bm) : 0.f;
+            const float k2 = hp ? cc * frcp(bp) : 0.f;
+            a = hm ? -am * k1 : 0.f;
+            cc = hp ? -cp * k2 : 0.f;
+            b = b - (hm ? cm * k1 : 0.f) - (hp ? ap * k2 : 0.f);
+            r0 = r0 - (hm ? q0m * k1 : 0.f) - (hp ? q0p * k2 : 0.f);
+            r1 = r1 - (hm ? q1m * k1 : 0.f) - (hp ? q1p * k2 : 0.f);
+            r2 = r2 - (hm ? q2m * k1 : 0.f) - (hp ? q2p * k2 : 0.f);
+        }
+        const float rb = frcp(b);
+        const float yv = r0 * rb, vv = r1 * rb, zv = r2 * rb;
+        if (lane == 0 || lane == 31) {
+            float* o = bnd + (s2 * NWM + w) * 6 + (lane == 0 ? 0 : 3);
+            o[0] = yv;
+            o[1] = vv;
+            o[2] = zv;
+        }
+        __syncthreads();
+        if (p2 == 0) {  // F_w = y0 - v0 G_{w-1} - z0 F_{w+1},  G_w = y31 - v31 G_{w-1} - z31 F_{w+1}
+            float phi[NWM], psi[NWM], gam[NWM], mu[NWM];
+            float gp = 0.f, mp = 0.f;
 #pragma unroll
-        for (int i = 0; i < KB * 6; ++i) nxt[i] = (p0 + KB + i / 6) < T ? __ldg(e + (size_t)(p0 * 6 + KB * 6 + i) * W) : 0.f;
+            for (int k = 0; k < NWM; ++k) {
+                if (k < nw) {
+                    const float* o = bnd + (s2 * NWM + k) * 6;
+                    const float rden = frcp(1.f - o[1] * mp);
+                    phi[k] = (o[0] - o[1] * gp) * rden;
+                    psi[k] = o[2] * rden;
+                    gam[k] = o[3] - o[4] * gp + o[4] * mp * phi[k];
+                    mu[k] = o[4] * mp * psi[k] + o[5];
+                    gp = gam[k];
+                    mp = mu[k];
+                }
+            }
+            float Fn = 0.f;
 #pragma unroll
-        for (int q = 0; q < KB; ++q) {
-            if (p0 + q < T) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {  // f then l equation of chunk p0+q
-                    const float sub = cur[q * 6 + 3 * h], sup = cur[q * 6 + 3 * h + 1], rhs = cur[q * 6 + 3 * h + 2];
-                    const float r = frcp(1.f - sub * cp);
-                    cp = sup * r;
-                    dp = (rhs - sub * dp) * r;
-                    const size_t k = (size_t)(2 * (p0 + q) + h);
-                    u[k * 2 * W] = cp;
-                    u[k * 2 * W + W] = dp;
+            for (int k = NWM - 1; k >= 0; --k) {
+                if (k < nw) {
+                    sol[(s2 * NWM + k) * 2 + 1] = gam[k] - mu[k] * Fn;
+                    Fn = phi[k] - psi[k] * Fn;
+                    sol[(s2 * NWM + k) * 2] = Fn;
                 }
             }
         }
-#pragma unroll
-        for (int i = 0; i < KB * 6; ++i) cur[i] = nxt[i];
+        __syncthreads();
+        ed[i2] = yv - vv * (w > 0 ? sol[(s2 * NWM + w - 1) * 2 + 1] : 0.f) -
+                 zv * (w + 1 < nw ? sol[(s2 * NWM + w + 1) * 2] : 0.f);
     }
-    // backward: u_k = d'_k - c'_k u_{k+1}; the (c', d') pairs are re-read a batch ahead as well
-    float xn = 0.f;
-    for (int k0 = 2 * T - 1; k0 >= 0; k0 -= 8) {
-        float cc8[8], dd8[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int k = k0 - i;
-            cc8[i] = k >= 0 ? u[(size_t)k * 2 * W] : 0.f;
-            dd8[i] = k >= 0 ? u[(size_t)k * 2 * W + W] : 0.f;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int k = k0 - i;
-            if (k >= 0) {
-                xn = dd8[i] - cc8[i] * xn;
-                u[(size_t)k * 2 * W + W] = xn;
-            }
-        }
-    }
-}
-
-template <int M>
-__global__ void __launch_bounds__(256) k_cols_final(const float* __restrict__ L, const float* __restrict__ c,
-                                                    const float* __restrict__ V, const float* __restrict__ sol,
-                                                    float* __restrict__ Lout, Strides st, Geom g, float tau, int T,
-                                                    size_t sol_img_stride) {
-    constexpr int MC = M + 1;
-    const int x = blockIdx.x * 32 + threadIdx.x;
-    const int p = blockIdx.y * 8 + threadIdx.y;
-    const int z = blockIdx.z;
-    if (x >= g.W || p >= T) return;
-    const int n = g.H;
-    const int j0 = p * M, j1 = (p == T - 1) ? n : j0 + M, m = j1 - j0;
-    const size_t W = g.W;
-    const float* u = sol + z * sol_img_stride + x;
-    const float xf = u[(size_t)(2 * p) * 2 * W + W], xl = u[(size_t)(2 * p + 1) * 2 * W + W];
-    const float* Lc = L + z * st.L + (size_t)j0 * g.P + x;
-    const float* cc = c + z * st.c + (size_t)j0 * g.P + x;
-    const float* Vc = V + z * st.U + (size_t)j0 * g.P + x;
-    float dv[MC], cv[MC], vv[MC];
-    const uint64_t done = l2_policy_evict_first();  // last use of this level's L, c and V
-#pragma unroll
-    for (int i = 0; i < MC; ++i) {
-        dv[i] = i < m ? ld_policy(Lc + (size_t)i * g.P, done) : 0.f;
-        cv[i] = i < m ? ld_policy(cc + (size_t)i * g.P, done) : 0.f;
-        vv[i] = i < m ? ld_policy(Vc + (size_t)i * g.P, done) : 0.f;
-    }
-    // interior rows 1..m-2 with x_0 = xf and x_{m-1} = xl known; τ(c_{i-1}+c_i) for i = 1..m-1 (interior only)
-    float cpv[MC], dpv[MC];
-    float cp = 0.f, dp = 0.f;
+    __syncthreads();
+    if (!active) return;
+    const float xf = ed[cx * SP + p];
+    const float xnext = (p + 1 < T) ? ed[cx * SP + p + 1] : 0.f;
+    const float xl = lD - lA * xf - lG * xnext;
+    cp_async_wait_all();
+    const float* vq = sv + tid;
+    float* Oc = Lout + blockIdx.z * st.out + (size_t)j0 * P + x;
+    Oc[0] = 0.5f * (xf + vq[0]);
 #pragma unroll
     for (int i = 1; i < MC; ++i) {
-        if (i <= m - 2) {
-            const float ta = tau * (cv[i - 1] + cv[i]), tb = tau * (cv[i] + cv[i + 1 < MC ? i + 1 : 0]);
-            float rhs = dv[i];
-            if (i == 1) rhs += ta * xf;          // -a_1 x_0
-            if (i == m - 2) rhs += tb * xl;      // -cc_{m-2} x_{m-1}
-            const float sub = (i == 1) ? 0.f : -ta;
-            const float sup = (i == m - 2) ? 0.f : -tb;
-            const float r = frcp(1.f + ta + tb - sub * cp);
-            cp = sup * r;
-            dp = (rhs - sub * dp) * r;
-            cpv[i] = cp;
-            dpv[i] = dp;
+        if (i < m - 1) {
+            float al, ga, de;
+            if (PARK) {
+                al = park[(3 * (i - 1) + 0) * NTOT + tid];
+                ga = park[(3 * (i - 1) + 1) * NTOT + tid];
+                de = park[(3 * (i - 1) + 2) * NTOT + tid];
+            } else {
+                al = ch.al[i];
+                ga = ch.ga[i];
+                de = ch.de[i];
+            }
+            Oc[i * P] = 0.5f * (de - al * xf - ga * xl + vq[i * NTOT]);
         }
     }
-    float* Oc = Lout + z * st.out + (size_t)j0 * g.P + x;
-    float xn = xl;
-#pragma unroll
-    for (int i = MC - 1; i >= 0; --i) {
-        if (i == m - 1) Oc[(size_t)i * g.P] = 0.5f * (xl + vv[i]);
-        else if (i >= 1 && i <= m - 2) {
-            xn = dpv[i] - cpv[i] * xn;
-            Oc[(size_t)i * g.P] = 0.5f * (xn + vv[i]);
-        }
-    }
-    Oc[0] = 0.5f * (xf + vv[0]);
+    Oc[(m - 1) * P] = 0.5f * (xl + vq[(m - 1) * NTOT]);
 }
 
 // -------------------------------------------------------------------------------------------------------------
@@ -495,23 +492,36 @@ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 }  // namespace
 
-template <int M>
-void run_cols3(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg, float tau,
-               float* red, float* sol, cudaStream_t s) {
+template <int CW, int M, int NT, bool PARK>
+void run_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg, float tau,
+              cudaStream_t s) {
     const int T = n_chunks(g.H, M);
-    const size_t red_stride = (size_t)T * 6 * g.W, sol_stride = (size_t)T * 4 * g.W;
-    dim3 blk(32, 8), grd((g.W + 31) / 32, (T + 7) / 8, nimg);
-    k_cols_reduce<M><<<grd, blk, 0, s>>>(L, c, red, st, g, tau, T, red_stride);
-    k_cols_solve<<<dim3((g.W + 127) / 128, nimg), 128, 0, s>>>(red, sol, g, T, red_stride, sol_stride);
-    k_cols_final<M><<<grd, blk, 0, s>>>(L, c, V, sol, Lout, st, g, tau, T, sol_stride);
+    const int TP = round_up(T, 32);  // whole warps per column for the SPIKE re-mapping
+    constexpr int NWM = NT / (32 * CW);
+    const size_t smem = sizeof(float) * ((size_t)4 * CW * (TP + 1) + 8 * CW * NWM + 3 * CW * TP +
+                                         (size_t)((PARK ? 3 * M : 0) + M + 1) * CW * TP);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_aos_cols<CW, M, NT, PARK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+        attr = true;
+    }
+    dim3 grid((g.W + CW - 1) / CW, 1, nimg);
+    k_aos_cols<CW, M, NT, PARK><<<grid, CW * TP, smem, s>>>(L, c, V, Lout, st, g, tau, T, TP);
 }
 
-// Columns: three-pass register-light scheme (chunk M = 16 rows, 8 for short columns).  red / sol: scratch of at
-// least 6·T·W and 4·T·W floats per image.
+// Columns: CW*TP <= NT with TP = 32·ceil(T/32) chunks per column.
 bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
-                     float tau, float* red, float* sol, cudaStream_t s) {
-    if (g.H >= 256) run_cols3<16>(L, c, V, Lout, st, g, nimg, tau, red, sol, s);
-    else run_cols3<8>(L, c, V, Lout, st, g, nimg, tau, red, sol, s);
+                     float tau, cudaStream_t s) {
+    const int H = g.H;
+    if (H <= 128 * 4) run_cols<8, 4, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 6) run_cols<8, 6, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 8) run_cols<8, 8, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 10) run_cols<8, 10, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 12) run_cols<8, 12, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 256 * 8) run_cols<4, 8, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 256 * 16) run_cols<2, 16, 512, false>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 256 * 32) run_cols<2, 32, 512, false>(L, c, V, Lout, st, g, nimg, tau, s);
+    else return false;
     return true;
 }
 

@@ -56,7 +56,7 @@ struct kaze_ctx {
     // arena
     int Pmax = 0;
     size_t plane_max = 0;
-    float *Lt = nullptr, *Ldet = nullptr, *cbuf = nullptr, *ubuf = nullptr, *redbuf = nullptr, *solbuf = nullptr;
+    float *Lt = nullptr, *Ldet = nullptr, *cbuf = nullptr, *ubuf = nullptr;
     float2* Lxy = nullptr;  // interleaved (Lx, Ly)
     float* kval = nullptr;
     unsigned* hmax = nullptr;
@@ -192,7 +192,7 @@ kaze_status validate_params(const kaze_params* p) {
 }
 
 void free_arena(kaze_ctx* c) {
-    void* ptrs[] = {c->Lt, c->Lxy, c->Ldet, c->cbuf, c->ubuf, c->redbuf, c->solbuf, c->kval, c->hmax, c->hist, c->fallback,
+    void* ptrs[] = {c->Lt, c->Lxy, c->Ldet, c->cbuf, c->ubuf, c->kval, c->hmax, c->hist, c->fallback,
                     c->bitmap, c->rowcnt, c->rowoff, c->hin[0], c->hin[1], c->hkps[0], c->hkps[1],
                     c->hcnt[0], c->hcnt[1], c->hdesc[0], c->hdesc[1]};
     for (void* q : ptrs)
@@ -267,8 +267,8 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
         }
         KZ_CHECK_LAUNCH(c, "aos_rows");
         {   // L_i = ½(U + V), U = column solves
-            Launch L(c, KC_AOS_COLS, 16.0 * px, s, 3);
-            if (!launch_aos_cols(prev, c->cbuf, c->ubuf, cur, Strides{SL, SP, SP, SL}, g, n, tau, c->redbuf, c->solbuf, s))
+            Launch L(c, KC_AOS_COLS, 16.0 * px, s);
+            if (!launch_aos_cols(prev, c->cbuf, c->ubuf, cur, Strides{SL, SP, SP, SL}, g, n, tau, s))
                 return KAZE_ERR_INVALID_ARGUMENT;
         }
         KZ_CHECK_LAUNCH(c, "aos_cols");
@@ -436,8 +436,6 @@ kaze_status kaze_create(const kaze_params* p, int device, kaze_ctx** out) {
               cudaMalloc(&c->Ldet, pyr) == cudaSuccess &&
               cudaMalloc(&c->cbuf, sizeof(float) * c->plane_max * B) == cudaSuccess &&
               cudaMalloc(&c->ubuf, sizeof(float) * c->plane_max * B) == cudaSuccess &&
-              cudaMalloc(&c->redbuf, sizeof(float) * 6 * ((size_t)p->max_height / 8 + 2) * p->max_width * B) == cudaSuccess &&
-              cudaMalloc(&c->solbuf, sizeof(float) * 4 * ((size_t)p->max_height / 8 + 2) * p->max_width * B) == cudaSuccess &&
               cudaMalloc(&c->kval, sizeof(float) * B) == cudaSuccess &&
               cudaMalloc(&c->hmax, sizeof(unsigned) * B) == cudaSuccess &&
               cudaMalloc(&c->hist, sizeof(int) * B * p->k_bins) == cudaSuccess &&

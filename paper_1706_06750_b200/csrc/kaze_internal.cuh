@@ -54,9 +54,8 @@ struct Strides {  // per-image strides (floats) of the four buffers an AOS pass 
 bool launch_aos_rows(const float* L, const float* c, float* V, Strides st, Geom g, int nimg, float tau,
                      cudaStream_t s);
 // Lout = ½(U + V), U = column solves of (I - 2 tau A_y(c)) U = L   (strides: L, c, U = V's, out)
-// red / sol: scratch, >= 6·ceil(H/8)·W and 4·ceil(H/8)·W floats per image (image strides derived inside).
 bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
-                     float tau, float* red, float* sol, cudaStream_t s);
+                     float tau, cudaStream_t s);
 
 // ---- hessian.cu ----  (all N levels of nimg images in one launch; level stride = plane)
 // Lxy: interleaved (s·∂x L, s·∂y L) float2 planes, same element strides as the float pyramids.
