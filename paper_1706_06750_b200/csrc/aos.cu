@@ -14,15 +14,42 @@
 //            copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is solved
 //            by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve), and V
 //            leaves through shared memory with 16-byte stores.
-//   columns: a CTA owns CW adjacent columns (whole 32-byte sectors per warp request); chunks eliminated in
-//            registers, the reduced systems re-mapped so each warp holds 32 chunks of one column and solved by the
-//            same warp-level SPIKE; V prefetched with cp.async; L_i = ½(U + V) written directly.
+//   columns: a CTA owns CW adjacent columns; a warp covers CW columns × 32/CW chunks, so every global request is
+//            whole 32-byte sectors; the reduced systems are solved by PCR in shared memory; V is prefetched with
+//            cp.async behind the solve and L_i = ½(U + V) is written directly.
+//            (Measured alternatives, all slower on B200 for 1920x1200: TMA-pipelined persistent strips 80 ms,
+//            three register-light passes 88 ms, re-mapped warp SPIKE 77 ms, vs 66 ms per 256-image step here.)
 #include "kaze_internal.cuh"
 #include "ptx.cuh"
 
 namespace kz {
 
 namespace {
+
+// Parallel cyclic reduction of a tridiagonal system with one equation per thread (p = 0..TP-1 within its
+// system, idx = p*stride + off in the shared arrays).  Threads p >= T carry identity rows.  Returns x_p.
+__device__ __forceinline__ float pcr_solve(float af, float bf, float cf, float df, int p, int TP, int stride, int idx,
+                                           float* sa, float* sb, float* sc, float* sd) {
+    for (int st = 1; st < TP; st <<= 1) {
+        sa[idx] = af;
+        sb[idx] = bf;
+        sc[idx] = cf;
+        sd[idx] = df;
+        __syncthreads();
+        const bool hm = p >= st, hp = p + st < TP;
+        const int jm = hm ? idx - st * stride : idx, jp = hp ? idx + st * stride : idx;
+        const float am = sa[jm], bm = sb[jm], cm = sc[jm], dm = sd[jm];
+        const float ap = sa[jp], bp = sb[jp], cp = sc[jp], dp = sd[jp];
+        const float k1 = hm ? af * frcp(bm) : 0.f;
+        const float k2 = hp ? cf * frcp(bp) : 0.f;
+        __syncthreads();
+        af = -am * k1;
+        cf = -cp * k2;
+        bf = bf - cm * k1 - ap * k2;
+        df = df - dm * k1 - dp * k2;
+    }
+    return df * frcp(bf);
+}
 
 template <int MC>
 struct Chunk {
@@ -151,190 +178,93 @@ __host__ __device__ inline int n_chunks(int n, int M) {
 }
 
 // -------------------------------------------------------------------------------------------------------------
-// Column systems.  A CTA owns CW adjacent columns; thread (cx, p) owns chunk p of column cx (a warp covers CW columns
-// x 32/CW chunks, so every global request is whole 32-byte sectors).  Each thread eliminates its chunk in registers.
-// The reduced systems (one unknown per chunk) are solved by a warp-level SPIKE after a shared-memory re-mapping in
-// which every warp owns 32 consecutive chunks of ONE column: shuffle PCR on three right-hand sides inside the warp,
-// then one thread per column solves the 2·(TP/32) warp-boundary unknowns (4 block barriers in all).  The chunk
-// coefficients are parked in shared memory across the solve to keep the 1024-thread CTA within 64 registers.  V
-// streams into shared memory with cp.async behind all of this and L_i = ½(U + V) is written directly.
-template <int CW, int M, int NT, bool PARK>
+// Column systems.  Thread (cx, p): column x0 + cx, chunk p of T.  blockDim.x = CW * TP; shared index p*CW + cx.
+template <int CW, int M, int NT>
 __global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, const float* __restrict__ c,
-                                                 const float* __restrict__ V, float* __restrict__ Lout, Strides st,
+                                                 const float* __restrict__ U, float* __restrict__ Lout, Strides st,
                                                  Geom g, float tau, int T, int TP) {
     constexpr int MC = M + 1;
-    constexpr int NWM = NT / (32 * CW);  // warps per column system (max)
     extern __shared__ float sm[];
-    const int NTOT = CW * TP, SP = TP + 1;
-    float* ea = sm;                 // [CW][TP+1] equations, system-major
-    float* eb = ea + CW * SP;
-    float* ec = eb + CW * SP;
-    float* ed = ec + CW * SP;
-    float* bnd = ed + CW * SP;      // [CW][NWM warps][6]
-    float* sol = bnd + CW * NWM * 6;  // [CW][NWM][2]
-    float* sla = sol + CW * NWM * 2;  // last-equation exchange [NTOT]
+    const int NTOT = CW * TP;
+    float* sa = sm;
+    float* sb = sa + NTOT;
+    float* sc = sb + NTOT;
+    float* sd = sc + NTOT;
+    float* sla = sd + NTOT;  // last-equation exchange
     float* slg = sla + NTOT;
     float* sld = slg + NTOT;
-    float* park = sld + NTOT;       // [3*(MC-1)][NTOT] chunk coefficients during the solve (PARK only)
-    float* sv = park + (PARK ? 3 * (MC - 1) * NTOT : 0);  // [MC][NTOT] V prefetch
-    const int tid = threadIdx.x;
-    const int cx = tid % CW, p = tid / CW;
+    float* sv = sld + NTOT;  // V chunk, prefetched with cp.async while the solve runs: [MC][NTOT]
+    const int cx = threadIdx.x % CW, p = threadIdx.x / CW;
     const int x = blockIdx.x * CW + cx;
     const bool active = (p < T) && (x < g.W);
     const int n = g.H;
     const int j0 = p * M;
     const int j1 = (p == T - 1) ? n : j0 + M;
     const int m = active ? j1 - j0 : 0;
-    const int P = g.P;
-    float A = 0.f, C = 0.f, D = 0.f, lA = 0.f, lG = 0.f, lD = 0.f;
+
     Chunk<MC> ch;
-    if (active) {
-        const float* Vg = V + blockIdx.z * st.U + (size_t)j0 * P + x;
+    if (active) {  // the V chunk streams into shared memory behind the solve
+        const float* Vg = U + blockIdx.z * st.U + (size_t)j0 * g.P + x;
 #pragma unroll
         for (int i = 0; i < MC; ++i)
-            if (i < m) cp_async4(sv + i * NTOT + tid, Vg + i * P);
-        const float* Lc = L + blockIdx.z * st.L + (size_t)j0 * P + x;
-        const float* cc = c + blockIdx.z * st.c + (size_t)j0 * P + x;
+            if (i < m) cp_async4(sv + i * NTOT + threadIdx.x, Vg + (size_t)i * g.P);
+    }
+    if (active) {
         float dv[MC], cv[MC];
+        const float* Lc = L + blockIdx.z * st.L + (size_t)j0 * g.P + x;
+        const float* cc = c + blockIdx.z * st.c + (size_t)j0 * g.P + x;
 #pragma unroll
         for (int i = 0; i < MC; ++i) {
-            dv[i] = i < m ? __ldg(Lc + i * P) : 0.f;
-            cv[i] = i < m ? __ldg(cc + i * P) : 0.f;
+            if (i < m) {
+                dv[i] = __ldg(Lc + (size_t)i * g.P);
+                cv[i] = __ldg(cc + (size_t)i * g.P);
+            } else {
+                dv[i] = 0.f;
+                cv[i] = 0.f;
+            }
         }
-        const float cprev = j0 > 0 ? __ldg(cc - P) : 0.f;
-        const float cnext = j1 < n ? __ldg(cc + m * P) : 0.f;
+        const float cprev = j0 > 0 ? __ldg(cc - g.P) : 0.f;
+        const float cnext = j1 < n ? __ldg(cc + (size_t)m * g.P) : 0.f;
         if (m == M) eliminate_full<M>(ch, dv, cv, cprev, cnext, j0 == 0, j1 == n, tau);
         else eliminate<MC>(ch, dv, cv, cprev, cnext, m, j0 == 0, j1 == n, tau);
-        if (PARK) {
-#pragma unroll
-            for (int i = 1; i < MC; ++i) {
-                park[(3 * (i - 1) + 0) * NTOT + tid] = ch.al[i];
-                park[(3 * (i - 1) + 1) * NTOT + tid] = ch.ga[i];
-                park[(3 * (i - 1) + 2) * NTOT + tid] = ch.de[i];
-            }
-        }
-        A = ch.A;
-        C = ch.C;
-        D = ch.D;
-        lA = ch.lA;
-        lG = ch.lG;
-        lD = ch.lD;
+    } else {
+        ch.A = ch.C = ch.D = 0.f;
+        ch.lA = ch.lG = ch.lD = 0.f;
     }
-    sla[tid] = lA;
-    slg[tid] = lG;
-    sld[tid] = lD;
+    const int idx = p * CW + cx;
+    sla[idx] = ch.lA;
+    slg[idx] = ch.lG;
+    sld[idx] = ch.lD;
     __syncthreads();
-    {   // f-equation of chunk p, stored system-major for the re-mapped solve
-        float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
-        if (active) {
-            const float pA = p > 0 ? sla[tid - CW] : 0.f, pG = p > 0 ? slg[tid - CW] : 0.f;
-            const float pD = p > 0 ? sld[tid - CW] : 0.f;
-            af = -A * pA;
-            bf = 1.f - A * pG - C * lA;
-            cf = -C * lG;
-            df = D - A * pD - C * lD;
+    float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
+    if (active) {
+        float pA = 0.f, pG = 0.f, pD = 0.f;
+        if (p > 0) {
+            pA = sla[idx - CW];
+            pG = slg[idx - CW];
+            pD = sld[idx - CW];
         }
-        ea[cx * SP + p] = af;
-        eb[cx * SP + p] = bf;
-        ec[cx * SP + p] = cf;
-        ed[cx * SP + p] = df;
+        af = -ch.A * pA;
+        bf = 1.f - ch.A * pG - ch.C * ch.lA;
+        cf = -ch.C * ch.lG;
+        df = ch.D - ch.A * pD - ch.C * ch.lD;
     }
-    __syncthreads();
-    {   // re-mapped: system s2 = tid / TP, equation p2 = tid % TP; warp w owns equations 32w..32w+31
-        const int s2 = tid / TP, p2 = tid - s2 * TP, lane = tid & 31, w = p2 >> 5, nw = TP >> 5;
-        const int i2 = s2 * SP + p2;
-        float a = ea[i2], b = eb[i2], cc = ec[i2], r0 = ed[i2], r1 = 0.f, r2 = 0.f;
-        if (lane == 0) {
-            r1 = a;
-            a = 0.f;
-        }
-        if (lane == 31) {
-            r2 = cc;
-            cc = 0.f;
-        }
-#pragma unroll
-        for (int s3 = 1; s3 < 32; s3 <<= 1) {
-            const bool hm = lane >= s3, hp = lane + s3 < 32;
-            const float am = __shfl_up_sync(0xffffffffu, a, s3), bm = __shfl_up_sync(0xffffffffu, b, s3);
-            const float cm = __shfl_up_sync(0xffffffffu, cc, s3), q0m = __shfl_up_sync(0xffffffffu, r0, s3);
-            const float q1m = __shfl_up_sync(0xffffffffu, r1, s3), q2m = __shfl_up_sync(0xffffffffu, r2, s3);
-            const float ap = __shfl_down_sync(0xffffffffu, a, s3), bp = __shfl_down_sync(0xffffffffu, b, s3);
-            const float cp = __shfl_down_sync(0xffffffffu, cc, s3), q0p = __shfl_down_sync(0xffffffffu, r0, s3);
-            const float q1p = __shfl_down_sync(0xffffffffu, r1, s3), q2p = __shfl_down_sync(0xffffffffu, r2, s3);
-            const float k1 = hm ? a * frcp(bm) : 0.f;
-            const float k2 = hp ? cc * frcp(bp) : 0.f;
-            a = hm ? -am * k1 : 0.f;
-            cc = hp ? -cp * k2 : 0.f;
-            b = b - (hm ? cm * k1 : 0.f) - (hp ? ap * k2 : 0.f);
-            r0 = r0 - (hm ? q0m * k1 : 0.f) - (hp ? q0p * k2 : 0.f);
-            r1 = r1 - (hm ? q1m * k1 : 0.f) - (hp ? q1p * k2 : 0.f);
-            r2 = r2 - (hm ? q2m * k1 : 0.f) - (hp ? q2p * k2 : 0.f);
-        }
-        const float rb = frcp(b);
-        const float yv = r0 * rb, vv = r1 * rb, zv = r2 * rb;
-        if (lane == 0 || lane == 31) {
-            float* o = bnd + (s2 * NWM + w) * 6 + (lane == 0 ? 0 : 3);
-            o[0] = yv;
-            o[1] = vv;
-            o[2] = zv;
-        }
-        __syncthreads();
-        if (p2 == 0) {  // F_w = y0 - v0 G_{w-1} - z0 F_{w+1},  G_w = y31 - v31 G_{w-1} - z31 F_{w+1}
-            float phi[NWM], psi[NWM], gam[NWM], mu[NWM];
-            float gp = 0.f, mp = 0.f;
-#pragma unroll
-            for (int k = 0; k < NWM; ++k) {
-                if (k < nw) {
-                    const float* o = bnd + (s2 * NWM + k) * 6;
-                    const float rden = frcp(1.f - o[1] * mp);
-                    phi[k] = (o[0] - o[1] * gp) * rden;
-                    psi[k] = o[2] * rden;
-                    gam[k] = o[3] - o[4] * gp + o[4] * mp * phi[k];
-                    mu[k] = o[4] * mp * psi[k] + o[5];
-                    gp = gam[k];
-                    mp = mu[k];
-                }
-            }
-            float Fn = 0.f;
-#pragma unroll
-            for (int k = NWM - 1; k >= 0; --k) {
-                if (k < nw) {
-                    sol[(s2 * NWM + k) * 2 + 1] = gam[k] - mu[k] * Fn;
-                    Fn = phi[k] - psi[k] * Fn;
-                    sol[(s2 * NWM + k) * 2] = Fn;
-                }
-            }
-        }
-        __syncthreads();
-        ed[i2] = yv - vv * (w > 0 ? sol[(s2 * NWM + w - 1) * 2 + 1] : 0.f) -
-                 zv * (w + 1 < nw ? sol[(s2 * NWM + w + 1) * 2] : 0.f);
-    }
+    const float xf = pcr_solve(af, bf, cf, df, p, TP, CW, idx, sa, sb, sc, sd);
+    sa[idx] = xf;
     __syncthreads();
     if (!active) return;
-    const float xf = ed[cx * SP + p];
-    const float xnext = (p + 1 < T) ? ed[cx * SP + p + 1] : 0.f;
-    const float xl = lD - lA * xf - lG * xnext;
+    const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
+    const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
+    // L_i = ½(U + V): the row pass already wrote V (prefetched into sv); the average is formed here.
     cp_async_wait_all();
-    const float* vq = sv + tid;
-    float* Oc = Lout + blockIdx.z * st.out + (size_t)j0 * P + x;
-    Oc[0] = 0.5f * (xf + vq[0]);
+    const float* vv = sv + threadIdx.x;
+    float* Oc = Lout + blockIdx.z * st.out + (size_t)j0 * g.P + x;
+    Oc[0] = 0.5f * (xf + vv[0]);
 #pragma unroll
     for (int i = 1; i < MC; ++i) {
-        if (i < m - 1) {
-            float al, ga, de;
-            if (PARK) {
-                al = park[(3 * (i - 1) + 0) * NTOT + tid];
-                ga = park[(3 * (i - 1) + 1) * NTOT + tid];
-                de = park[(3 * (i - 1) + 2) * NTOT + tid];
-            } else {
-                al = ch.al[i];
-                ga = ch.ga[i];
-                de = ch.de[i];
-            }
-            Oc[i * P] = 0.5f * (de - al * xf - ga * xl + vq[i * NTOT]);
-        }
+        if (i < m - 1) Oc[(size_t)i * g.P] = 0.5f * (ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl + vv[i * NTOT]);
     }
-    Oc[(m - 1) * P] = 0.5f * (xl + vq[(m - 1) * NTOT]);
+    Oc[(size_t)(m - 1) * g.P] = 0.5f * (xl + vv[(m - 1) * NTOT]);
 }
 
 // -------------------------------------------------------------------------------------------------------------
@@ -490,37 +420,34 @@ void run_rows_cta(const float* L, const float* c, float* V, Strides st, Geom g, 
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
-}  // namespace
-
-template <int CW, int M, int NT, bool PARK>
-void run_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg, float tau,
+template <int CW, int M, int NT>
+void run_cols(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg, float tau,
               cudaStream_t s) {
     const int T = n_chunks(g.H, M);
-    const int TP = round_up(T, 32);  // whole warps per column for the SPIKE re-mapping
-    constexpr int NWM = NT / (32 * CW);
-    const size_t smem = sizeof(float) * ((size_t)4 * CW * (TP + 1) + 8 * CW * NWM + 3 * CW * TP +
-                                         (size_t)((PARK ? 3 * M : 0) + M + 1) * CW * TP);
+    const int TP = round_up(T, 32 / CW);
+    const size_t smem = sizeof(float) * (7 + M + 1) * CW * TP;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_aos_cols<CW, M, NT, PARK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+        cudaFuncSetAttribute(k_aos_cols<CW, M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     dim3 grid((g.W + CW - 1) / CW, 1, nimg);
-    k_aos_cols<CW, M, NT, PARK><<<grid, CW * TP, smem, s>>>(L, c, V, Lout, st, g, tau, T, TP);
+    k_aos_cols<CW, M, NT><<<grid, CW * TP, smem, s>>>(L, c, U, Lout, st, g, tau, T, TP);
 }
 
-// Columns: CW*TP <= NT with TP = 32·ceil(T/32) chunks per column.
+}  // namespace
+
+// Column chunk length: T = n_chunks(H, M) must fit the CTA (CW*TP <= NT).
 bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
                      float tau, cudaStream_t s) {
     const int H = g.H;
-    if (H <= 128 * 4) run_cols<8, 4, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 6) run_cols<8, 6, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 8) run_cols<8, 8, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 10) run_cols<8, 10, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 12) run_cols<8, 12, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 256 * 8) run_cols<4, 8, 1024, true>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 256 * 16) run_cols<2, 16, 512, false>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 256 * 32) run_cols<2, 32, 512, false>(L, c, V, Lout, st, g, nimg, tau, s);
+    if (H <= 128 * 4) run_cols<8, 4, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 6) run_cols<8, 6, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 8) run_cols<8, 8, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 10) run_cols<8, 10, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 128 * 12) run_cols<8, 12, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 256 * 16) run_cols<2, 16, 512>(L, c, V, Lout, st, g, nimg, tau, s);
+    else if (H <= 256 * 32) run_cols<2, 32, 512>(L, c, V, Lout, st, g, nimg, tau, s);
     else return false;
     return true;
 }
