@@ -1,8 +1,8 @@
 // stencil.cu — Gaussian prefilter, gradient / conductivity and the contrast factor k (sm_100a).
 //
 //  * prefilter: L0 = G(σ0) * I, separable tile kernel, replicate border (A6, A16).
-//  * cond:      c = g(|∇(G(1) * L)|) with ∇ = Scharr step 1 (Eqs. 2-3, A5, A8); one warp-streaming
-//               pass computes the σ=1 smoothing at clamped coordinates in registers, then the 3x3 Scharr.
+//  * cond:      c = g(|∇(G(1) * L)|) with ∇ = Scharr step 1 (Eqs. 2-3, A5, A8); one tiled pass
+//               computes the σ=1 smoothing at clamped coordinates in shared memory, then the 3x3 Scharr.
 //               Mode 0 (level 1) writes |∇|² and the image maximum of |∇| for the k histogram.
 //  * khist / kfinal: 300-bin histogram of |∇| over the interior, percentile → k on the device
 //               (A7), no host round trip.
@@ -78,105 +78,134 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ in,
     }
 }
 
-// G(σ=1) has radius 3 (A6).
-constexpr int R1 = 3;
-
 // -------------------------------------------------------------------------------------------------
-// |∇(G1 * L)|² → c (mode 1) or |∇|² + max|∇| (mode 0), warp-streaming: a warp owns 30 output columns — lane l holds the
-// Ls column x0-1+l, so lanes 1..30 produce outputs and lanes 0 / 31 are the Ls halo — and walks CS_SEG output rows
-// top to bottom.  Per input row it loads the 38-column L segment (clamped) into a per-warp shared row, forms the
-// horizontal G1 for its column, keeps the last 7 horizontal results in registers for the vertical G1, keeps the
-// last 3 Ls rows for the Scharr, and reads the Ls of its neighbour columns with shuffles.  Every L value is read
-// from HBM ~1.1 times; ~50 instructions per 30 pixels per row.  Border semantics (A16): Ls is evaluated at clamped
-// coordinates (its window rows/columns are L at clamped indices), and the Scharr reads Ls at clamp(x±1),
-// clamp(y±1) — the column-neighbour and first/last-row selects below.
-constexpr int CS_SEG = 64;
-
+// |∇(G1 * L)|² → c (mode 1) or |∇|² + max|∇| (mode 0).  G(σ=1) has radius 3 (A6).
+// Shared-memory traffic is kept to ~12 accesses per pixel with register sliding windows:
+//   L tile  tL[u]  = L(clamp(u)) for u in [x0-4, x0+35]²   (odd pitch 41: per-row sweeps are conflict free)
+//   tH[r][v]       = Σ_d g_d tL[r][v+d]      horizontal G1, one thread per tile row (two halves)
+//   tS[v][v']      = Σ_d g_d tH[v+d][v']     vertical G1, one thread per column (four row groups)
+// tS holds Ls at the virtual coordinates [x0-1, x0+32]²; it equals Ls(clamp(v)) wherever v is inside the
+// image, and the Scharr reads Ls at clamped coordinates only (A16), so border tiles need no special path.
+constexpr int R1 = 3;
 template <int MODE>
-__global__ void __launch_bounds__(256) k_cond_stream(const float* __restrict__ L, size_t in_img_stride,
-                                                     float* __restrict__ out, size_t out_img_stride, Geom g,
-                                                     GaussTaps t, int diffusivity, const float* __restrict__ kval,
-                                                     unsigned* __restrict__ hmax_bits) {
-    __shared__ float rowbuf[8][2][40];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int x0 = (blockIdx.x * 8 + warp) * 30;
-    if (x0 >= g.W) return;  // warp-uniform
-    const int y0 = blockIdx.y * CS_SEG, img = blockIdx.z;
+__global__ void __launch_bounds__(256) k_cond(const float* __restrict__ L, size_t in_img_stride,
+                                              float* __restrict__ out, size_t out_img_stride, Geom g,
+                                              GaussTaps t, int diffusivity, const float* __restrict__ kval,
+                                              unsigned* __restrict__ hmax_bits) {
+    constexpr int H0 = R1 + 1;              // halo of the L tile
+    constexpr int LN = TW + 2 * H0;         // 40 (square tile, TW == TH)
+    constexpr int SN = TW + 2;              // 34
+    __shared__ float tL[LN][LN + 1];
+    __shared__ float tH[LN][SN + 1];
+    __shared__ float tS[SN][SN + 1];
+    __shared__ float red[8];
+    static_assert(TW == TH, "square tiles");
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, img = blockIdx.z;
     const float* src = L + img * in_img_stride;
-    const int W = g.W, H = g.H;
-    const int xcol = x0 - 1 + lane;                   // this lane's Ls column (virtual)
-    const int hb = clampi(xcol, 0, W - 1) - (x0 - 4) - R1;  // row-buffer index of tap d = -3
-    const int gxa = clampi(x0 - 4 + lane, 0, W - 1), gxb = clampi(x0 + 28 + lane, 0, W - 1);
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+    {   // all tile loads issued before any shared store (LN = 40 rows: 5 per warp; 40 columns: 32 + 8 lanes)
+        constexpr int KR = LN / 8;
+        const int gx0 = clampi(x0 - H0 + tx, 0, g.W - 1), gx1 = clampi(x0 - H0 + 32 + tx, 0, g.W - 1);
+        float v0[KR], v1[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const float* row = src + (size_t)clampi(y0 - H0 + ty + 8 * k, 0, g.H - 1) * g.P;
+            v0[k] = __ldg(row + gx0);
+            v1[k] = tx < LN - 32 ? __ldg(row + gx1) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            tL[ty + 8 * k][tx] = v0[k];
+            if (tx < LN - 32) tL[ty + 8 * k][32 + tx] = v1[k];
+        }
+    }
     float w[2 * R1 + 1];
 #pragma unroll
     for (int d = 0; d <= 2 * R1; ++d) w[d] = t.w[d];
+    __syncthreads();
+    if (tid < 2 * LN) {  // horizontal: row r, output columns [17h, 17h+17)
+        constexpr int NO = SN / 2;  // 17
+        const int r = tid % LN, h = tid / LN;
+        float win[NO + 2 * R1];
+#pragma unroll
+        for (int i = 0; i < NO + 2 * R1; ++i) win[i] = tL[r][NO * h + i];
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
+            float acc = 0.f;
+#pragma unroll
+            for (int d = 0; d <= 2 * R1; ++d) acc = fmaf(w[d], win[o + d], acc);
+            tH[r][NO * h + o] = acc;
+        }
+    }
+    __syncthreads();
+    if (tid < 4 * SN) {  // vertical: column v, output rows [9q, min(9q+9, 34))
+        constexpr int NO = 9;
+        const int v = tid % SN, q = tid / SN;
+        const int r0 = NO * q;
+        float win[NO + 2 * R1];
+#pragma unroll
+        for (int i = 0; i < NO + 2 * R1; ++i) win[i] = (r0 + i < LN) ? tH[r0 + i][v] : 0.f;
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
+            if (r0 + o < SN) {
+                float acc = 0.f;
+#pragma unroll
+                for (int d = 0; d <= 2 * R1; ++d) acc = fmaf(w[d], win[o + d], acc);
+                tS[r0 + o][v] = acc;
+            }
+        }
+    }
+    __syncthreads();
     float ik2 = 1.f;
     if (MODE == 1) {
         const float k = kval[img];
         ik2 = frcp(k * k);
     }
-    float hw[2 * R1 + 1];
-#pragma unroll
-    for (int d = 0; d <= 2 * R1; ++d) hw[d] = 0.f;
-    float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, lmax = 0.f;
+    float lmax = 0.f;
     float* dst = out + img * out_img_stride;
-    const bool outcol = lane >= 1 && lane <= 30 && xcol < W;
-    const bool at_left = xcol == 0, at_right = xcol == W - 1;
-    const int u0 = y0 - 4, u1 = y0 + CS_SEG + 3;
-    // software pipeline: the next row's two loads are in flight while the current row is processed
-    const float* r0 = src + (size_t)clampi(u0, 0, H - 1) * g.P;
-    float na = __ldg(r0 + gxa), nb = lane < 6 ? __ldg(r0 + gxb) : 0.f;
-    int buf = 0;
-    for (int u = u0; u <= u1; ++u) {
-        rowbuf[warp][buf][lane] = na;
-        if (lane < 6) rowbuf[warp][buf][32 + lane] = nb;
-        if (u < u1) {
-            const float* rn = src + (size_t)clampi(u + 1, 0, H - 1) * g.P;
-            na = __ldg(rn + gxa);
-            nb = lane < 6 ? __ldg(rn + gxb) : 0.f;
-        }
-        __syncwarp();
-        float hh = 0.f;
+    const int x = x0 + tx;
+    // tS index of virtual coordinate v is v - (x0 - 1); the Scharr reads Ls(clamp(x±1), clamp(y±1))
+    const int xm = clampi(x - 1, 0, g.W - 1) - (x0 - 1), xp = clampi(x + 1, 0, g.W - 1) - (x0 - 1), xc = tx + 1;
+    const int yb = y0 + 4 * ty;  // four output rows per thread
+    float cm[6], cc[6], cp[6];
 #pragma unroll
-        for (int d = 0; d <= 2 * R1; ++d) hh = fmaf(w[d], rowbuf[warp][buf][hb + d], hh);
-        buf ^= 1;  // the other buffer is refilled next iteration; this one is not written again until then
+    for (int i = 0; i < 6; ++i) {
+        const int yy = clampi(yb - 1 + i, 0, g.H - 1) - (y0 - 1);
+        cm[i] = tS[yy][xm];
+        cc[i] = tS[yy][xc];
+        cp[i] = tS[yy][xp];
+    }
 #pragma unroll
-        for (int d = 0; d < 2 * R1; ++d) hw[d] = hw[d + 1];
-        hw[2 * R1] = hh;
-        if (u < y0 + 2) continue;  // window rows u-6..u not yet complete for Ls(u-3), v >= y0-1
-        float lsv = 0.f;
-#pragma unroll
-        for (int d = 0; d <= 2 * R1; ++d) lsv = fmaf(w[d], hw[d], lsv);
-        ls0 = ls1;
-        ls1 = ls2;
-        ls2 = lsv;
-        if (u < y0 + 4) continue;
-        const int y = u - 4;
-        if (y >= H) break;
-        const float lm = (y == 0) ? ls1 : ls0, lp = (y == H - 1) ? ls1 : ls2;
-        // vertical (3,10,3)/16 smoothing and vertical difference of this column, neighbours by shuffles
-        const float sv = 0.1875f * lm + 0.625f * ls1 + 0.1875f * lp;
-        const float dv = lp - lm;
-        float svl = __shfl_up_sync(0xffffffffu, sv, 1), svr = __shfl_down_sync(0xffffffffu, sv, 1);
-        float dvl = __shfl_up_sync(0xffffffffu, dv, 1), dvr = __shfl_down_sync(0xffffffffu, dv, 1);
-        if (at_left) { svl = sv; dvl = dv; }
-        if (at_right) { svr = sv; dvr = dv; }
-        const float gx = 0.5f * (svr - svl);
-        const float gy = 0.5f * (0.1875f * dvl + 0.625f * dv + 0.1875f * dvr);
+    for (int k = 0; k < 4; ++k) {
+        const int y = yb + k;
+        // window rows k, k+1, k+2 hold clamp(y-1), y, clamp(y+1) unless y is the first/last image row
+        const bool top = (y == 0), bot = (y == g.H - 1);
+        const float mm = top ? cm[k + 1] : cm[k], mc = top ? cc[k + 1] : cc[k], mp = top ? cp[k + 1] : cp[k];
+        const float pm = bot ? cm[k + 1] : cm[k + 2], pc = bot ? cc[k + 1] : cc[k + 2], pp = bot ? cp[k + 1] : cp[k + 2];
+        float gx = 0.1875f * (mp - mm) + 0.625f * (cp[k + 1] - cm[k + 1]) + 0.1875f * (pp - pm);
+        float gy = 0.1875f * (pm - mm) + 0.625f * (pc - mc) + 0.1875f * (pp - mp);
+        gx *= 0.5f;
+        gy *= 0.5f;
         const float g2 = gx * gx + gy * gy;
-        if (outcol) {
+        if (x < g.W && y < g.H) {
             if (MODE == 0) {
-                dst[(size_t)y * g.P + xcol] = g2;
-                if (xcol >= 1 && xcol <= W - 2 && y >= 1 && y <= H - 2) lmax = fmaxf(lmax, sqrtf(g2));
+                dst[(size_t)y * g.P + x] = g2;
+                if (x >= 1 && x <= g.W - 2 && y >= 1 && y <= g.H - 2) lmax = fmaxf(lmax, sqrtf(g2));
             } else {
                 const float q = g2 * ik2;
-                dst[(size_t)y * g.P + xcol] = diffusivity == 2 ? frcp(1.f + q) : __expf(-q);
+                dst[(size_t)y * g.P + x] = diffusivity == 2 ? frcp(1.f + q) : __expf(-q);
             }
         }
     }
     if (MODE == 0) {
         for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-        if (lane == 0) atomicMax(hmax_bits + img, __float_as_uint(lmax));
+        if (tx == 0) red[ty] = lmax;
+        __syncthreads();
+        if (tid == 0) {
+            float m = 0.f;
+            for (int wv = 0; wv < 8; ++wv) m = fmaxf(m, red[wv]);
+            atomicMax(hmax_bits + img, __float_as_uint(m));  // non-negative floats order as uints
+        }
     }
 }
 
@@ -272,14 +301,13 @@ void launch_prefilter(const float* img, int64_t in_pitch, size_t in_img_stride, 
 void launch_cond(const float* L, size_t in_img_stride, float* out, size_t out_img_stride, Geom g, int nimg,
                  const GaussTaps& t1, int mode, int diffusivity, const float* kval, unsigned* hmax_bits,
                  cudaStream_t s) {
-    const int strips = (g.W + 29) / 30;
-    dim3 grid((strips + 7) / 8, (g.H + CS_SEG - 1) / CS_SEG, nimg);
+    dim3 grid((g.W + TW - 1) / TW, (g.H + TH - 1) / TH, nimg);
     if (mode == 0)
-        k_cond_stream<0><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval,
-                                              hmax_bits);
+        k_cond<0><<<grid, dim3(32, 8), 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval,
+                                               hmax_bits);
     else
-        k_cond_stream<1><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval,
-                                              hmax_bits);
+        k_cond<1><<<grid, dim3(32, 8), 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval,
+                                               hmax_bits);
 }
 
 void launch_khist(const float* g2, size_t img_stride, Geom g, int nimg, int bins, const unsigned* hmax_bits, int* hist,
