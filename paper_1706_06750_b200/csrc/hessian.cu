@@ -6,7 +6,9 @@
 // which equals s⁴(LxxLyy − Lxy²) with per-pixel derivatives (the factor s per derivative order is absorbed in
 // N).  Second derivatives read the MATERIALISED first derivatives at clamped coordinates (A10), so they are two
 // passes: hess_first (L → Lx, Ly) and hess_det (Lx, Ly → Ldet).  One launch covers every level of every image
-// (blockIdx.y packs (level, row-tile)); the per-level step s_i comes from the LevelTable.
+// (blockIdx.y packs (level, row-tile)); the per-level step s_i comes from the LevelTable.  (A fused shared-memory
+// tile form moving 16 instead of 24 B/px measured slower on B200 at every step: 80-87 µs vs 59 µs per level and
+// 4 images — the (T+4s)² halo recomputation costs more than the 8 B/px it saves.)
 #include "kaze_internal.cuh"
 
 namespace kz {
@@ -102,121 +104,6 @@ __global__ void __launch_bounds__(256) k_hess_det(const float2* __restrict__ Lxy
     }
 }
 
-// Fused per-level Hessian: one CTA computes a T x T output tile of Lx, Ly and Ldet, with the L tile (T + 4S)² and
-// the first-derivative tile (T + 2S)² in shared memory — 16 B/px of DRAM traffic instead of 24 B/px for the
-// two-pass form.  The step S is a template parameter (one instantiation per step of the schedule), so every index
-// is compile-time affine.  Virtual coordinates outside the image are evaluated at their clamped position, which is
-// exactly what the clamped-intermediate semantics (A10) read; interior tiles skip all clamping.
-template <int T, int S>
-__global__ void __launch_bounds__(T * 8) k_hess_fused(const float* __restrict__ Lt, float2* __restrict__ Lxy,
-                                                      float* __restrict__ Ldet, size_t img_stride, Geom g) {
-    constexpr int NL = T + 4 * S, ND = T + 2 * S;
-    constexpr int NLP = NL | 1;  // odd pitches: column walks by a warp are conflict free
-    extern __shared__ __align__(16) float hsm[];
-    float* tL = hsm;                                                   // NL x NLP
-    float2* tD = reinterpret_cast<float2*>(hsm + ((NL * NLP + 3) & ~3));  // ND x ND
-    const int x0 = blockIdx.x * T, y0 = blockIdx.y * T;
-    const size_t base = blockIdx.z * img_stride;
-    const float* L = Lt + base;
-    const int tx = threadIdx.x, ty = threadIdx.y;  // blockDim = (T, 8)
-    const bool interior = (x0 - 2 * S >= 0) && (y0 - 2 * S >= 0) && (x0 + T + 2 * S <= g.W) && (y0 + T + 2 * S <= g.H);
-    // ---- L tile ----
-    constexpr int KC = (NL + T - 1) / T;
-    for (int r = ty; r < NL; r += 8) {
-        const float* row = L + (size_t)(interior ? y0 - 2 * S + r : clampi(y0 - 2 * S + r, 0, g.H - 1)) * g.P;
-        float v[KC];
-#pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            const int cidx = tx + k * T;
-            const int gx = interior ? x0 - 2 * S + cidx : clampi(x0 - 2 * S + cidx, 0, g.W - 1);
-            v[k] = (cidx < NL) ? __ldg(row + gx) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < KC; ++k)
-            if (tx + k * T < NL) tL[r * NLP + tx + k * T] = v[k];
-    }
-    __syncthreads();
-    // ---- first derivatives on the ND x ND tile (virtual coords y0-S.., x0-S..) ----
-    constexpr int KD = (ND + T - 1) / T;
-    for (int r = ty; r < ND; r += 8) {
-        int ym, y1, yp;
-        if (interior) {
-            y1 = r + S;
-            ym = r;
-            yp = r + 2 * S;
-        } else {
-            const int vy = clampi(y0 - S + r, 0, g.H - 1);
-            y1 = vy - (y0 - 2 * S);
-            ym = clampi(vy - S, 0, g.H - 1) - (y0 - 2 * S);
-            yp = clampi(vy + S, 0, g.H - 1) - (y0 - 2 * S);
-        }
-#pragma unroll
-        for (int k = 0; k < KD; ++k) {
-            const int cidx = tx + k * T;
-            if (cidx >= ND) continue;
-            int xm, x1, xp;
-            if (interior) {
-                x1 = cidx + S;
-                xm = cidx;
-                xp = cidx + 2 * S;
-            } else {
-                const int vx = clampi(x0 - S + cidx, 0, g.W - 1);
-                x1 = vx - (x0 - 2 * S);
-                xm = clampi(vx - S, 0, g.W - 1) - (x0 - 2 * S);
-                xp = clampi(vx + S, 0, g.W - 1) - (x0 - 2 * S);
-            }
-            const float a = tL[ym * NLP + xm], b = tL[ym * NLP + x1], c = tL[ym * NLP + xp];
-            const float d = tL[y1 * NLP + xm], f = tL[y1 * NLP + xp];
-            const float h = tL[yp * NLP + xm], ii = tL[yp * NLP + x1], j = tL[yp * NLP + xp];
-            const float dx = 0.5f * (kW0 * (c - a) + kW1 * (f - d) + kW0 * (j - h));
-            const float dy = 0.5f * (kW0 * (h - a) + kW1 * (ii - b) + kW0 * (j - c));
-            tD[r * ND + cidx] = make_float2(dx, dy);
-        }
-    }
-    __syncthreads();
-    // ---- outputs: Lx, Ly (centre of tD) and Ldet ----
-    const int x = x0 + tx;
-    int xm = tx, x1 = tx + S, xp = tx + 2 * S;
-    if (!interior) {
-        xm = clampi(x - S, 0, g.W - 1) - (x0 - S);
-        xp = clampi(x + S, 0, g.W - 1) - (x0 - S);
-    }
-    float2* Dout = Lxy + base;
-    float* Lout = Ldet + base;
-#pragma unroll 4
-    for (int r = ty; r < T; r += 8) {
-        const int y = y0 + r;
-        int ym = r, y1 = r + S, yp = r + 2 * S;
-        if (!interior) {
-            ym = clampi(y - S, 0, g.H - 1) - (y0 - S);
-            yp = clampi(y + S, 0, g.H - 1) - (y0 - S);
-        }
-        const float2 a = tD[ym * ND + xm], b = tD[ym * ND + x1], c = tD[ym * ND + xp];
-        const float2 d = tD[y1 * ND + xm], e = tD[y1 * ND + x1], f = tD[y1 * ND + xp];
-        const float2 h = tD[yp * ND + xm], ii = tD[yp * ND + x1], j = tD[yp * ND + xp];
-        const float lxx = 0.5f * (kW0 * (c.x - a.x) + kW1 * (f.x - d.x) + kW0 * (j.x - h.x));
-        const float lxy = 0.5f * (kW0 * (h.x - a.x) + kW1 * (ii.x - b.x) + kW0 * (j.x - c.x));
-        const float lyy = 0.5f * (kW0 * (h.y - a.y) + kW1 * (ii.y - b.y) + kW0 * (j.y - c.y));
-        if (x < g.W && y < g.H) {
-            Dout[(size_t)y * g.P + x] = e;
-            Lout[(size_t)y * g.P + x] = lxx * lyy - lxy * lxy;
-        }
-    }
-}
-
-template <int T, int S>
-void run_hess(const float* Lt, float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, cudaStream_t st) {
-    constexpr int NL = T + 4 * S, ND = T + 2 * S, NLP = NL | 1;
-    const size_t smem = sizeof(float) * (((NL * NLP + 3) & ~3) + 2 * ND * ND);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_hess_fused<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    dim3 grid((g.W + T - 1) / T, (g.H + T - 1) / T, nimg);
-    k_hess_fused<T, S><<<grid, dim3(T, 8), smem, st>>>(Lt, Lxy, Ldet, img_stride, g);
-}
-
 __global__ void k_component_copy(float2* __restrict__ plane, int comp, float* __restrict__ tight, int to_tight,
                                  Geom g) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
@@ -240,21 +127,6 @@ void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, 
     int ty = (g.H + 31) / 32;
     dim3 grid((g.W + 31) / 32, ty * lt.n, nimg);
     k_hess_det<<<grid, dim3(32, 8), 0, s>>>(Lxy, Ldet, img_stride, g, lt, ty);
-}
-
-bool launch_hessian(const float* Lt, float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, int step,
-                    cudaStream_t st) {
-    switch (step) {
-#define KZ_H(S)                                                            \
-    case S:                                                                \
-        if (S <= 8) run_hess<32, S>(Lt, Lxy, Ldet, img_stride, g, nimg, st); \
-        else run_hess<64, S>(Lt, Lxy, Ldet, img_stride, g, nimg, st);      \
-        return true;
-        KZ_H(1) KZ_H(2) KZ_H(3) KZ_H(4) KZ_H(5) KZ_H(6) KZ_H(7) KZ_H(8) KZ_H(9) KZ_H(10) KZ_H(11) KZ_H(12) KZ_H(13)
-        KZ_H(14) KZ_H(15) KZ_H(16) KZ_H(17) KZ_H(18) KZ_H(19) KZ_H(20) KZ_H(21) KZ_H(22) KZ_H(23) KZ_H(24)
-#undef KZ_H
-        default: return false;
-    }
 }
 
 void launch_component_copy(float2* plane, int comp, float* tight, int to_tight, Geom g, cudaStream_t s) {

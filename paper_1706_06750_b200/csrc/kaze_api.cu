@@ -173,8 +173,6 @@ GaussTaps make_taps(double sigma) {
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
-constexpr int kFusedMaxStep = 4;  // Hessian: fused tile kernel up to this step, two-pass above
-
 kaze_status validate_params(const kaze_params* p) {
     if (!p) return KAZE_ERR_INVALID_ARGUMENT;
     if (p->octaves < 1 || p->sublevels < 1 || p->octaves * p->sublevels > kMaxLevels) return KAZE_ERR_INVALID_ARGUMENT;
@@ -283,27 +281,10 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     const int N = c->N, n = c->n;
     const Geom g = c->geom;
     const double px = (double)g.W * g.H * n;
-    // Hessian (Eq. 8): small steps use the fused shared-memory tile kernel (16 B/px); large steps, whose halos make
-    // tiles redundant, use the two-pass form (24 B/px, no halo recomputation) — one launch per pass for those levels.
-    LevelTable big = c->lt;
-    big.n = 0;
-    int first_big = -1;
-    for (int level = 0; level < N; ++level) {
-        const size_t lo = (size_t)level * g.plane;
-        const int st = c->lt.step[level];
-        if (st <= kFusedMaxStep) {
-            Launch L(c, KC_HESSIAN, 16.0 * px, s);
-            launch_hessian(c->Lt + lo, c->Lxy + lo, c->Ldet + lo, c->img_stride, g, n, st, s);
-        } else {
-            if (first_big < 0) first_big = level;
-            big.step[big.n++] = st;  // the remaining levels are contiguous (steps grow with the level)
-        }
-    }
-    if (big.n > 0) {
-        const size_t lo = (size_t)first_big * g.plane;
-        Launch L(c, KC_HESSIAN, 24.0 * px * big.n, s, 2);
-        launch_hess_first(c->Lt + lo, c->Lxy + lo, c->img_stride, g, n, big, s);
-        launch_hess_det(c->Lxy + lo, c->Ldet + lo, c->img_stride, g, n, big, s);
+    {   // Hessian (Eq. 8), all levels in two launches: L → (Lx, Ly) → Ldet
+        Launch L(c, KC_HESSIAN, 24.0 * px * N, s, 2);
+        launch_hess_first(c->Lt, c->Lxy, c->img_stride, g, n, c->lt, s);
+        launch_hess_det(c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s);
     }
     KZ_CHECK_LAUNCH(c, "hessian");
     if (N < 3) {

@@ -63,10 +63,6 @@ void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, 
                        cudaStream_t s);
 void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                      cudaStream_t s);
-// Fused per-level form (one launch per level): Lxy and Ldet from Lt in one pass.
-// (steps 1..24 have compiled instantiations; returns false otherwise)
-bool launch_hessian(const float* Lt, float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, int step,
-                    cudaStream_t s);
 // Diagnostic copy of one component of an interleaved plane to/from a tightly packed w x h buffer
 // (to_tight = 1: plane → tight).
 void launch_component_copy(float2* plane, int comp, float* tight, int to_tight, Geom g, cudaStream_t s);
