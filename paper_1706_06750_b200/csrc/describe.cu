@@ -39,9 +39,10 @@ __device__ __forceinline__ float2 bilinear2(const float2* __restrict__ img, int 
 
 constexpr int kWarps = 8;
 
-__global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy, size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
+__global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy,
+                                                  const cudaTextureObject_t* __restrict__ texs, size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
                                                   const int* __restrict__ counts, int cap, float* __restrict__ desc,
-                                                  int nwin, int keep_angle) {
+                                                  int nwin, int keep_angle, int N) {
     __shared__ int pre[kMaxBatch + 1];
     __shared__ __align__(16) float sbuf[kWarps][2 * 576];
     if (threadIdx.x == 0) {
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
         const float x = kp->x, y = kp->y, sigma = kp->sigma;
         const int level = kp->level;
         const float2* lxy = Lxy + img * img_stride + (size_t)level * g.plane;
+        const cudaTextureObject_t tex = texs[img * N + level];
         float angle;
         int flags = 0;
         if (keep_angle) {
@@ -141,7 +143,8 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
             const float u = (float)p - 11.5f, v = (float)q - 11.5f;
             const float px = x + sigma * (u * co - v * si);
             const float py = y + sigma * (u * si + v * co);
-            const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);
+            // hardware bilinear filtering (texel centres at +0.5; clamped addressing = clamped taps, A14/A16)
+            const float2 gv = tex2D<float2>(tex, px + 0.5f, py + 0.5f);
             const float gx = gv.x, gy = gv.y;
             sx[p * 24 + q] = gx * co + gy * si;
             sy[p * 24 + q] = -gx * si + gy * co;
@@ -212,10 +215,10 @@ void init_describe_tables() {
     cudaMemcpyToSymbol(c_w2, w2, sizeof(w2));
 }
 
-void launch_describe(const float2* Lxy, size_t img_stride, Geom g, int nimg, int N, kaze_keypoint* kps,
-                     const int* counts, int cap, float* desc, int nwin, int keep_angle, cudaStream_t s) {
-    (void)N;
-    k_describe<<<148 * 5, 256, 0, s>>>(Lxy, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle);
+void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t img_stride, Geom g, int nimg, int N,
+                     kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
+                     cudaStream_t s) {
+    k_describe<<<148 * 5, 256, 0, s>>>(Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N);
 }
 
 }  // namespace kz

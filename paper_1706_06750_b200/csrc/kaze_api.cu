@@ -79,6 +79,10 @@ struct kaze_ctx {
     int* pinned_counts = nullptr;  // 2 * max_batch
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_cnt[2] = {}, ev_d2h[2] = {};
+    // descriptor texture objects over the Lxy planes, [max_batch][N], rebuilt when the geometry changes
+    std::vector<cudaTextureObject_t> texs;
+    cudaTextureObject_t* d_texs = nullptr;
+    int tex_W = 0, tex_H = 0;
     // profiling
     bool prof = false;
     std::vector<ProfRec> recs;
@@ -196,9 +200,14 @@ void free_arena(kaze_ctx* c) {
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (c->pinned_counts) cudaFreeHost(c->pinned_counts);
+    for (auto t : c->texs) cudaDestroyTextureObject(t);
+    c->texs.clear();
+    if (c->d_texs) cudaFree(c->d_texs);
 }
 
-size_t plane_of(int W, int H) { return (size_t)round_up(W, 32) * H; }
+// Plane size in floats: pitch x H rounded to 128 floats, so every (image, level) plane of the interleaved float2
+// derivative array starts 1024-byte aligned (texture base alignment for the descriptor's filtered fetches).
+size_t plane_of(int W, int H) { return ((size_t)round_up(W, 32) * H + 127) / 128 * 128; }
 
 // ---- the three steps, on one chunk of n <= max_batch images ----
 void set_geometry(kaze_ctx* c, int n, int w, int h) {
@@ -313,12 +322,45 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     return KAZE_OK;
 }
 
+// Texture objects (bilinear filtering, clamped addressing, unnormalised coordinates) over every (image, level)
+// Lxy plane of the current geometry, for the descriptor's 576 filtered samples per keypoint.
+kaze_status ensure_textures(kaze_ctx* c) {
+    if (c->tex_W == c->W && c->tex_H == c->H && !c->texs.empty()) return KAZE_OK;
+    for (auto t : c->texs) cudaDestroyTextureObject(t);
+    c->texs.clear();
+    const int B = c->p.max_batch, N = c->N;
+    if (!c->d_texs && cudaMalloc(&c->d_texs, sizeof(cudaTextureObject_t) * B * N) != cudaSuccess) return KAZE_ERR_OOM;
+    c->texs.resize((size_t)B * N);
+    for (int b = 0; b < B; ++b)
+        for (int l = 0; l < N; ++l) {
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypePitch2D;
+            rd.res.pitch2D.devPtr = c->Lxy + (size_t)b * c->img_stride + (size_t)l * c->geom.plane;
+            rd.res.pitch2D.desc = cudaCreateChannelDesc<float2>();
+            rd.res.pitch2D.width = c->W;
+            rd.res.pitch2D.height = c->H;
+            rd.res.pitch2D.pitchInBytes = sizeof(float2) * c->geom.P;
+            cudaTextureDesc td{};
+            td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+            td.filterMode = cudaFilterModeLinear;
+            td.readMode = cudaReadModeElementType;
+            td.normalizedCoords = 0;
+            KZ_CUDA(c, cudaCreateTextureObject(&c->texs[(size_t)b * N + l], &rd, &td, nullptr));
+        }
+    KZ_CUDA(c, cudaMemcpy(c->d_texs, c->texs.data(), sizeof(cudaTextureObject_t) * B * N, cudaMemcpyHostToDevice));
+    c->tex_W = c->W;
+    c->tex_H = c->H;
+    return KAZE_OK;
+}
+
 // Step 3.
 kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_counts, float* d_desc, cudaStream_t s) {
+    kaze_status st = ensure_textures(c);
+    if (st != KAZE_OK) return st;
     {
         Launch L(c, KC_DESCRIBE, 0.0, s);
-        launch_describe(c->Lxy, c->img_stride, c->geom, c->n, c->N, d_kps, d_counts, c->p.max_keypoints, d_desc,
-                        c->p.ori_windows, (c->p.flags & KAZE_FLAG_KEEP_ANGLE) ? 1 : 0, s);
+        launch_describe(c->Lxy, c->d_texs, c->img_stride, c->geom, c->n, c->N, d_kps, d_counts, c->p.max_keypoints,
+                        d_desc, c->p.ori_windows, (c->p.flags & KAZE_FLAG_KEEP_ANGLE) ? 1 : 0, s);
     }
     KZ_CHECK_LAUNCH(c, "describe");
     c->last_stream = s;

@@ -82,7 +82,8 @@ void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, cons
 
 // ---- describe.cu ----
 void init_describe_tables();
-void launch_describe(const float2* Lxy, size_t img_stride, Geom g, int nimg, int N,
+// texs: [nimg][N] texture objects over the Lxy planes (linear filtering, clamp) for the M-SURF samples.
+void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t img_stride, Geom g, int nimg, int N,
                      kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
                      cudaStream_t s);
 
