@@ -450,7 +450,7 @@ kaze_status kaze_create(const kaze_params* p, int device, kaze_ctx** out) {
     c->g0 = make_taps(p->sigma0);
     c->g1 = make_taps(1.0);
     c->Pmax = round_up(p->max_width, 32);
-    c->plane_max = (size_t)c->Pmax * p->max_height;
+    c->plane_max = plane_of(p->max_width, p->max_height);  // >= every build's plane (see plane_of)
     const size_t B = p->max_batch, N = c->N;
     const size_t pyr = sizeof(float) * c->plane_max * N * B;
     const int words = (p->max_width + 31) / 32;
