@@ -9,7 +9,7 @@
 //   nms_mark : one CTA per (image, level, row) — warp ballots produce a 1-bit-per-pixel candidate bitmap and the
 //              row's candidate count;
 //   kp_scan  : one CTA per image — exclusive scan of the row counts → row offsets, total → d_counts;
-//   kp_emit  : one CTA per (image, level, row) — rank of each set bit = row offset + popcounts before it; the
+//   kp_emit  : one warp per (image, level, row) — rank of each set bit = row offset + popcounts before it; the
 //              sub-pixel fit is re-evaluated (same fp32 code as the mark pass, so the same decision) and the
 //              32-byte keypoint is written if its rank is below the capacity.
 #include "kaze_internal.cuh"
@@ -174,62 +174,53 @@ __global__ void __launch_bounds__(1024) k_kp_scan(const int* __restrict__ rowcnt
     if (threadIdx.x == blockDim.x - 1) counts[img] = run;
 }
 
+// One WARP per (image, level, row); 8 rows per CTA.  Lane w of a 32-word step owns bitmap word w: an inclusive warp
+// scan of the word popcounts gives each word's rank base, and the lane walks its set bits in x order.
 __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet, size_t img_stride, Geom g,
                                                  LevelTable lt, DetectParams dp, const uint32_t* __restrict__ bitmap,
                                                  const int* __restrict__ rowcnt, const int* __restrict__ rowoff,
-                                                 kaze_keypoint* __restrict__ kps) {
-    __shared__ int wpre[129];
+                                                 kaze_keypoint* __restrict__ kps, int total_rows) {
+    const int lane = threadIdx.x & 31;
+    const int q = blockIdx.x * 8 + (threadIdx.x >> 5);  // flat row id over (img, level-1, y)
+    if (q >= total_rows) return;
+    if (rowcnt[q] == 0) return;  // warp-uniform
     const int N = lt.n;
-    const int y = blockIdx.x, li = blockIdx.y, level = li + 1, img = blockIdx.z;
+    const int y = q % g.H, rest = q / g.H, li = rest % (N - 2), img = rest / (N - 2), level = li + 1;
     const int words = (g.W + 31) / 32;
-    const size_t row = ((size_t)img * (N - 2) + li) * g.H + y;
-    const uint32_t* bm = bitmap + row * words;
-    if (rowcnt[row] == 0) return;
-    const int base = rowoff[row];
-    // word prefix (words <= 128 for W <= 4096; larger rows handled in passes of 128 words)
-    int carry = 0;
-    for (int w0 = 0; w0 < words; w0 += 128) {
-        const int nw = min(128, words - w0);
-        __syncthreads();
-        if (threadIdx.x < 32) {  // warp 0: exclusive prefix of word popcounts, 32 words per step
-            const int lane = threadIdx.x;
-            int r = carry;
-            for (int k0 = 0; k0 < nw; k0 += 32) {
-                const int c = (k0 + lane < nw) ? __popc(bm[w0 + k0 + lane]) : 0;
-                int incl = c;
-                for (int o = 1; o < 32; o <<= 1) {
-                    int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                if (k0 + lane < nw) wpre[k0 + lane] = r + incl - c;
-                r += __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t* bm = bitmap + (size_t)q * words;
+    const float* D0 = Ldet + img * img_stride + (size_t)level * g.plane;
+    int run = rowoff[q];
+    for (int w0 = 0; w0 < words; w0 += 32) {
+        uint32_t word = (w0 + lane < words) ? bm[w0 + lane] : 0u;
+        const int c = __popc(word);
+        int incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        int rank = run + incl - c;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+        while (word) {
+            const int bit = __ffs(word) - 1;
+            word &= word - 1;
+            if (rank < dp.cap) {
+                const int x = (w0 + lane) * 32 + bit;
+                float ox = 0.f, oy = 0.f, v = 0.f;
+                is_keypoint(D0 - g.plane, D0, D0 + g.plane, g.P, x, y, dp.threshold, dp.edge_ratio, ox, oy, v);
+                kaze_keypoint kp;
+                kp.x = (float)x + ox;
+                kp.y = (float)y + oy;
+                kp.sigma = lt.sigma[level];
+                kp.response = v;
+                kp.angle = 0.f;
+                kp.level = level;
+                kp.octave = (int16_t)(level / lt.S);
+                kp.sublevel = (int16_t)(level % lt.S);
+                kp.flags = 0;
+                kps[(size_t)img * dp.cap + rank] = kp;
             }
-            if (lane == 0) wpre[128] = r;
+            ++rank;
         }
-        __syncthreads();
-        const float* D0 = Ldet + img * img_stride + (size_t)level * g.plane;
-        for (int k = threadIdx.x; k < nw * 32; k += blockDim.x) {
-            const int w = k >> 5, bit = k & 31;
-            const uint32_t word = bm[w0 + w];
-            if (!((word >> bit) & 1u)) continue;
-            const int rank = base + wpre[w] + __popc(word & ((1u << bit) - 1u));
-            if (rank >= dp.cap) continue;
-            const int x = (w0 + w) * 32 + bit;
-            float ox = 0.f, oy = 0.f, v = 0.f;
-            is_keypoint(D0 - g.plane, D0, D0 + g.plane, g.P, x, y, dp.threshold, dp.edge_ratio, ox, oy, v);
-            kaze_keypoint kp;
-            kp.x = (float)x + ox;
-            kp.y = (float)y + oy;
-            kp.sigma = lt.sigma[level];
-            kp.response = v;
-            kp.angle = 0.f;
-            kp.level = level;
-            kp.octave = (int16_t)(level / lt.S);
-            kp.sublevel = (int16_t)(level % lt.S);
-            kp.flags = 0;
-            kps[(size_t)img * dp.cap + rank] = kp;
-        }
-        carry = wpre[128];
     }
 }
 
@@ -248,8 +239,8 @@ void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, 
 
 void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
                     const uint32_t* bitmap, const int* rowcnt, const int* rowoff, kaze_keypoint* kps, cudaStream_t s) {
-    dim3 grid(g.H, lt.n - 2, nimg);
-    k_kp_emit<<<grid, 256, 0, s>>>(Ldet, img_stride, g, lt, dp, bitmap, rowcnt, rowoff, kps);
+    const int total = g.H * (lt.n - 2) * nimg;
+    k_kp_emit<<<(total + 7) / 8, 256, 0, s>>>(Ldet, img_stride, g, lt, dp, bitmap, rowcnt, rowoff, kps, total);
 }
 
 }  // namespace kz
