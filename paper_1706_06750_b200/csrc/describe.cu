@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
             for (int j = lane; j < kOriSamples; j += 32) {
                 const float px = x + sigma * c_ori_u[j], py = y + sigma * c_ori_v[j];
                 const float w = c_ori_w[j];
-                const float2 gv = tex2D<float2>(tex, px + 0.5f, py + 0.5f);
+                const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);  // exact: the window choice is an argmax
                 const float rx = w * gv.x, ry = w * gv.y;
                 float ph = atan2f(ry, rx);
                 if (ph < 0.f) ph += kTwoPi;
