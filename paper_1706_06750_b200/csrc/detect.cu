@@ -6,8 +6,8 @@
 // the quadratic fit offset δ = −H⁻¹∇D has |δx|, |δy| <= 1.
 //
 // Compaction is deterministic and ordered by (level, y, x) without a sort:
-//   nms_mark : one CTA per (image, level, row) — warp ballots produce a 1-bit-per-pixel candidate bitmap and the
-//              row's candidate count;
+//   nms_mark : warps streaming 32-column strips down the rows — ballots produce a 1-bit-per-pixel candidate bitmap;
+//              k_rowcount turns it into per-row candidate counts;
 //   kp_scan  : one CTA per image — exclusive scan of the row counts → row offsets, total → d_counts;
 //   kp_emit  : one warp per (image, level, row) — rank of each set bit = row offset + popcounts before it; the
 //              sub-pixel fit is re-evaluated (same fp32 code as the mark pass, so the same decision) and the
@@ -62,79 +62,93 @@ __device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const 
     return refine(patch, er, ox, oy);
 }
 
-// nms_mark tile: 256 columns x NY rows of one level of one image, one thread per column.  Each thread loads its
-// column of the three levels (NY+2 rows each) into registers with coalesced row loads, forms the vertical 3-maxima
-// in registers and publishes them in shared memory; the 26-neighbour maximum of a pixel is then
-//   max( V_{i-1}[c-1..c+1][r], V_{i+1}[c-1..c+1][r], V_i[c±1][r], D_i[c][r±1] )
-// (V = vertical 3-max), a handful of operations per pixel.  Only candidates run the edge test / sub-pixel fit.
-constexpr int NX = 256, NY = 8;
+// nms_mark: one WARP per (32-column strip, NSEG-row segment, level, image), streaming down the rows.  Lane l owns
+// column x0+l and keeps, for each of the levels i-1, i, i+1, the last three rows of its column in registers (lanes 0
+// and 31 also keep the halo columns x0-1 / x0+32).  The 26-neighbour maximum is
+//   max(vmax_{i-1}, vmax_{i+1} over columns x-1..x+1;  vmax_i over x-1, x+1;  D_i(x, y±1))
+// with vmax = vertical 3-maximum, the column neighbours coming from shuffles: ~30 instructions per pixel, 3
+// coalesced loads per pixel, no shared memory, no barriers.  Only candidates run the edge test / sub-pixel fit.
+// The warp writes the row's 32-bit candidate word; row counts come from k_rowcount.
+constexpr int NSEG = 64;
 
 __global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
-                                                  DetectParams dp, uint32_t* __restrict__ bitmap,
-                                                  int* __restrict__ rowcnt) {
-    __shared__ float V[3][NY][NX + 2];   // vertical 3-max per level, row r (output rows), column c (tile coords)
-    __shared__ float C1[NY + 2][NX + 2]; // level-i values (for the 3x3 patch of candidates)
-    __shared__ int rc[NY];
-    const int x0 = blockIdx.x * NX, y0 = blockIdx.y * NY;
-    const int li = blockIdx.z % (N - 2), img = blockIdx.z / (N - 2), level = li + 1;
-    const float* D0 = Ldet + img * img_stride + (size_t)level * g.plane;
-    const int tid = threadIdx.x;
-    if (tid < NY) rc[tid] = 0;
-    // columns handled by this thread: its own (tile column tid+1) and, for threads 0 / 1, the halo columns 0 / NX+1
-    for (int pass = 0; pass < 2; ++pass) {
-        int col;
-        if (pass == 0) col = tid + 1;
-        else if (tid == 0) col = 0;
-        else if (tid == 1) col = NX + 1;
-        else break;
-        const int gx = clampi(x0 - 1 + col, 0, g.W - 1);
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-            const float* Dl = D0 + (ptrdiff_t)(l - 1) * (ptrdiff_t)g.plane + gx;
-            float v[NY + 2];
-#pragma unroll
-            for (int r = 0; r < NY + 2; ++r) v[r] = __ldg(Dl + (size_t)clampi(y0 - 1 + r, 0, g.H - 1) * g.P);
-#pragma unroll
-            for (int r = 0; r < NY; ++r) V[l][r][col] = fmaxf(v[r], fmaxf(v[r + 1], v[r + 2]));
-            if (l == 1) {
-#pragma unroll
-                for (int r = 0; r < NY + 2; ++r) C1[r][col] = v[r];
-            }
-        }
-    }
-    __syncthreads();
+                                                  DetectParams dp, uint32_t* __restrict__ bitmap) {
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int words = (g.W + 31) / 32;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int x = x0 + tid, c = tid + 1;
-#pragma unroll 1
-    for (int r = 0; r < NY; ++r) {
-        const int y = y0 + r;
-        bool k = false;
-        if (y >= 1 && y <= g.H - 2 && x >= 1 && x <= g.W - 2) {
-            const float v = C1[r + 1][c];
-            float m = fmaxf(fmaxf(V[0][r][c - 1], V[0][r][c]), V[0][r][c + 1]);
-            m = fmaxf(m, fmaxf(fmaxf(V[2][r][c - 1], V[2][r][c]), V[2][r][c + 1]));
-            m = fmaxf(m, fmaxf(V[1][r][c - 1], V[1][r][c + 1]));
-            m = fmaxf(m, fmaxf(C1[r][c], C1[r + 2][c]));
-            if (v > dp.threshold && v > m) {
-                float patch[3][3];
-#pragma unroll
-                for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-                    for (int dx = 0; dx < 3; ++dx) patch[dy][dx] = C1[r + dy][c - 1 + dx];
+    if (strip >= words) return;  // warp-uniform
+    const int x0 = strip * 32, x = x0 + lane;
+    const int y0 = blockIdx.y * NSEG;
+    const int li = blockIdx.z % (N - 2), img = blockIdx.z / (N - 2), level = li + 1;
+    const int W = g.W, H = g.H;
+    const float* D1 = Ldet + img * img_stride + (size_t)level * g.plane;
+    const float* D0 = D1 - g.plane;
+    const float* D2 = D1 + g.plane;
+    const int xc = min(x, W - 1);
+    const bool halo = lane == 0 || lane == 31;
+    const int xh = lane == 0 ? max(x0 - 1, 0) : min(x0 + 32, W - 1);
+    // windows: [0] = row y-1, [1] = y, [2] = y+1 (own column), h* = halo column
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
+    float ha0 = 0.f, ha1 = 0.f, ha2 = 0.f, hb0 = 0.f, hb1 = 0.f, hb2 = 0.f, hc0 = 0.f, hc1 = 0.f, hc2 = 0.f;
+    const int ylast = min(y0 + NSEG, H - 1);  // last row loaded (the row below the last output row)
+    uint32_t* bm = bitmap + (((size_t)img * (N - 2) + li) * H) * words + strip;
+    for (int r = y0 - 1; r <= ylast; ++r) {
+        const size_t ro = (size_t)max(r, 0) * g.P;
+        a0 = a1; a1 = a2; a2 = __ldg(D0 + ro + xc);
+        b0 = b1; b1 = b2; b2 = __ldg(D1 + ro + xc);
+        c0 = c1; c1 = c2; c2 = __ldg(D2 + ro + xc);
+        if (halo) {
+            ha0 = ha1; ha1 = ha2; ha2 = __ldg(D0 + ro + xh);
+            hb0 = hb1; hb1 = hb2; hb2 = __ldg(D1 + ro + xh);
+            hc0 = hc1; hc1 = hc2; hc2 = __ldg(D2 + ro + xh);
+        }
+        const int y = r - 1;  // the window now holds rows y-1, y, y+1
+        if (y < y0) continue;
+        const float va = fmaxf(a0, fmaxf(a1, a2)), vc = fmaxf(c0, fmaxf(c1, c2)), vb = fmaxf(b0, fmaxf(b1, b2));
+        float val = __shfl_up_sync(0xffffffffu, va, 1), var = __shfl_down_sync(0xffffffffu, va, 1);
+        float vcl = __shfl_up_sync(0xffffffffu, vc, 1), vcr = __shfl_down_sync(0xffffffffu, vc, 1);
+        float vbl = __shfl_up_sync(0xffffffffu, vb, 1), vbr = __shfl_down_sync(0xffffffffu, vb, 1);
+        if (halo) {
+            const float hva = fmaxf(ha0, fmaxf(ha1, ha2)), hvc = fmaxf(hc0, fmaxf(hc1, hc2));
+            const float hvb = fmaxf(hb0, fmaxf(hb1, hb2));
+            if (lane == 0) { val = hva; vcl = hvc; vbl = hvb; }
+            else { var = hva; vcr = hvc; vbr = hvb; }
+        }
+        float m = fmaxf(fmaxf(val, va), fmaxf(var, vc));
+        m = fmaxf(m, fmaxf(fmaxf(vcl, vcr), fmaxf(vbl, vbr)));
+        m = fmaxf(m, fmaxf(b0, b2));
+        bool k = (x >= 1 && x <= W - 2 && y >= 1 && y <= H - 2) && b1 > dp.threshold && b1 > m;
+        if (__any_sync(0xffffffffu, k)) {  // rare: gather the level-i 3x3 patch and fit
+            float l0 = __shfl_up_sync(0xffffffffu, b0, 1), l1 = __shfl_up_sync(0xffffffffu, b1, 1);
+            float l2 = __shfl_up_sync(0xffffffffu, b2, 1);
+            float q0 = __shfl_down_sync(0xffffffffu, b0, 1), q1 = __shfl_down_sync(0xffffffffu, b1, 1);
+            float q2 = __shfl_down_sync(0xffffffffu, b2, 1);
+            if (lane == 0) { l0 = hb0; l1 = hb1; l2 = hb2; }
+            if (lane == 31) { q0 = hb0; q1 = hb1; q2 = hb2; }
+            if (k) {
+                const float patch[3][3] = {{l0, b0, q0}, {l1, b1, q1}, {l2, b2, q2}};
                 float ox, oy;
                 k = refine(patch, dp.edge_ratio, ox, oy);
             }
         }
         const uint32_t bits = __ballot_sync(0xffffffffu, k);
-        if (lane == 0 && y < g.H && x0 + warp * 32 < g.W) {
-            const size_t row = ((size_t)img * (N - 2) + li) * g.H + y;
-            bitmap[row * words + (x0 >> 5) + warp] = bits;
-            if (bits) atomicAdd(&rc[r], __popc(bits));
-        }
+        if (lane == 0 && y < H) bm[(size_t)y * words] = bits;
     }
-    __syncthreads();
-    if (tid < NY && y0 + tid < g.H && rc[tid]) atomicAdd(&rowcnt[((size_t)img * (N - 2) + li) * g.H + y0 + tid], rc[tid]);
+    // the last image row is never a window centre above; it has no candidates (border)
+    if (lane == 0 && y0 + NSEG >= H && H - 1 >= y0) bm[(size_t)(H - 1) * words] = 0u;
+}
+
+// Row candidate counts from the bitmap: one warp per (image, level, row).
+__global__ void __launch_bounds__(256) k_rowcount(const uint32_t* __restrict__ bitmap, int words, int total_rows,
+                                                  int* __restrict__ rowcnt) {
+    const int lane = threadIdx.x & 31;
+    const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (q >= total_rows) return;
+    const uint32_t* bm = bitmap + (size_t)q * words;
+    int c = 0;
+    for (int w = lane; w < words; w += 32) c += __popc(bm[w]);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) rowcnt[q] = c;
 }
 
 // One CTA per image: exclusive scan of R row counts.
@@ -228,9 +242,11 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
 
 void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, int N, DetectParams dp, uint32_t* bitmap,
                      int* rowcnt, cudaStream_t s) {
-    cudaMemsetAsync(rowcnt, 0, sizeof(int) * (size_t)nimg * (N - 2) * g.H, s);
-    dim3 grid((g.W + NX - 1) / NX, (g.H + NY - 1) / NY, nimg * (N - 2));
-    k_nms_mark<<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, bitmap, rowcnt);
+    const int words = (g.W + 31) / 32;
+    dim3 grid((words + 7) / 8, (g.H + NSEG - 1) / NSEG, nimg * (N - 2));
+    k_nms_mark<<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, bitmap);
+    const int total = g.H * (N - 2) * nimg;
+    k_rowcount<<<(total + 7) / 8, 256, 0, s>>>(bitmap, words, total, rowcnt);
 }
 
 void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, int* counts, cudaStream_t s) {

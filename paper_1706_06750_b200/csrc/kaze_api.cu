@@ -301,7 +301,7 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     } else {
         DetectParams dp{(float)c->p.threshold, (float)c->p.edge_ratio, c->p.max_keypoints};
         {
-            Launch L(c, KC_NMS_MARK, 4.0 * px * N, s);  // (+ one memset of the row counters)
+            Launch L(c, KC_NMS_MARK, 4.0 * px * N, s, 2);  // nms_mark + rowcount
             launch_nms_mark(c->Ldet, c->img_stride, g, n, N, dp, c->bitmap, c->rowcnt, s);
         }
         KZ_CHECK_LAUNCH(c, "nms_mark");
