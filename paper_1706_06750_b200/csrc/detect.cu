@@ -92,15 +92,34 @@ __global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet
     float ha0 = 0.f, ha1 = 0.f, ha2 = 0.f, hb0 = 0.f, hb1 = 0.f, hb2 = 0.f, hc0 = 0.f, hc1 = 0.f, hc2 = 0.f;
     const int ylast = min(y0 + NSEG, H - 1);  // last row loaded (the row below the last output row)
     uint32_t* bm = bitmap + (((size_t)img * (N - 2) + li) * H) * words + strip;
+    // software pipeline: the next row's loads are issued before the current row is consumed
+    size_t ro = (size_t)max(y0 - 1, 0) * g.P;
+    float na = __ldg(D0 + ro + xc), nb = __ldg(D1 + ro + xc), nc = __ldg(D2 + ro + xc);
+    float nha = 0.f, nhb = 0.f, nhc = 0.f;
+    if (halo) {
+        nha = __ldg(D0 + ro + xh);
+        nhb = __ldg(D1 + ro + xh);
+        nhc = __ldg(D2 + ro + xh);
+    }
     for (int r = y0 - 1; r <= ylast; ++r) {
-        const size_t ro = (size_t)max(r, 0) * g.P;
-        a0 = a1; a1 = a2; a2 = __ldg(D0 + ro + xc);
-        b0 = b1; b1 = b2; b2 = __ldg(D1 + ro + xc);
-        c0 = c1; c1 = c2; c2 = __ldg(D2 + ro + xc);
+        a0 = a1; a1 = a2; a2 = na;
+        b0 = b1; b1 = b2; b2 = nb;
+        c0 = c1; c1 = c2; c2 = nc;
         if (halo) {
-            ha0 = ha1; ha1 = ha2; ha2 = __ldg(D0 + ro + xh);
-            hb0 = hb1; hb1 = hb2; hb2 = __ldg(D1 + ro + xh);
-            hc0 = hc1; hc1 = hc2; hc2 = __ldg(D2 + ro + xh);
+            ha0 = ha1; ha1 = ha2; ha2 = nha;
+            hb0 = hb1; hb1 = hb2; hb2 = nhb;
+            hc0 = hc1; hc1 = hc2; hc2 = nhc;
+        }
+        if (r < ylast) {
+            ro = (size_t)(r + 1) * g.P;
+            na = __ldg(D0 + ro + xc);
+            nb = __ldg(D1 + ro + xc);
+            nc = __ldg(D2 + ro + xc);
+            if (halo) {
+                nha = __ldg(D0 + ro + xh);
+                nhb = __ldg(D1 + ro + xh);
+                nhc = __ldg(D2 + ro + xh);
+            }
         }
         const int y = r - 1;  // the window now holds rows y-1, y, y+1
         if (y < y0) continue;
