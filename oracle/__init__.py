@@ -43,6 +43,8 @@ class Params(C.Structure):
         ("edge_ratio", C.c_double),
         ("ori_windows", C.c_int32),
         ("keep_angle", C.c_int32),
+        ("scheme", C.c_int32),
+        ("tau_max", C.c_double),
     ]
 
 
@@ -107,6 +109,9 @@ def lib():
         L.kazeref_run.argtypes = [_fp, C.c_int, C.c_int, C.POINTER(Params), C.POINTER(KP),
                                   C.c_int64, _dp, _dp, C.POINTER(C.c_int32), _dp, _dp, _dp, _dp]
         L.kazeref_run.restype = C.c_int64
+        L.kazeref_fed_taus.argtypes = [C.c_int, C.c_double, _dp]
+        L.kazeref_fed_cycle.argtypes = [C.c_double, C.c_double, _dp, C.c_int]
+        L.kazeref_fed_step.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, _dp]
         L.kazeref_run_batch.argtypes = [_fp, C.c_int, C.c_int, C.c_int, C.POINTER(Params),
                                         C.c_int64, C.c_int, C.POINTER(C.c_int64)]
     return _lib
@@ -209,6 +214,26 @@ def scale_space(img, **kw):
     fb = C.c_int32()
     _chk(lib().kazeref_scale_space(im.ctypes.data_as(_fp), W, H, C.byref(p), _d(lv), C.byref(k), C.byref(fb)))
     return lv, k.value, bool(fb.value)
+
+
+def fed_taus(n: int, tau_max: float = 0.25) -> np.ndarray:
+    t = np.zeros(n)
+    _chk(lib().kazeref_fed_taus(n, tau_max, _d(t)))
+    return t
+
+
+def fed_cycle(T: float, tau_max: float = 0.25) -> np.ndarray:
+    n = _chk(lib().kazeref_fed_cycle(T, tau_max, None, 0))
+    t = np.zeros(n)
+    lib().kazeref_fed_cycle(T, tau_max, _d(t), n)
+    return t
+
+
+def fed_step(L, c, tau: float) -> np.ndarray:
+    a, b = _f64(L), _f64(c)
+    out = np.empty_like(a)
+    _chk(lib().kazeref_fed_step(_d(a), _d(b), a.shape[1], a.shape[0], tau, _d(out)))
+    return out
 
 
 def hessian(L, s: int):

@@ -38,6 +38,8 @@ void kazeref_default_params(kazeref_params* p) {
     p->edge_ratio = 10.0;
     p->ori_windows = 42;
     p->keep_angle = 0;
+    p->scheme = 0;
+    p->tau_max = 0.25;  /* S:L118 */
 }
 
 /* ---------------------------------------------------------------------------------------
@@ -257,9 +259,57 @@ int kazeref_aos_step(const double* L, const double* c, int W, int H, double tau,
     return 0;
 }
 
-/* Nonlinear scale space (P:L255-260 with the AOS solver of Eq. 4 [A1]):
+/* FED (Eq. 5; reading A20): "perform M cycles of n explicit diffusion steps with varying step sizes". */
+int kazeref_fed_taus(int n, double tau_max, double* taus) {
+    if (n < 1 || !(tau_max > 0) || !taus) return -1;
+    for (int j = 0; j < n; ++j) {
+        double cj = cos(KR_PI * (double)(2 * j + 1) / (double)(4 * n + 2));
+        taus[j] = tau_max / (2.0 * cj * cj);
+    }
+    return 0;
+}
+
+/* A20: n = smallest integer with τ_max·n(n+1)/3 >= T (the closed-form sum of Eq. 5's steps), i.e.
+ * n = ceil(−1/2 + 1/2·sqrt(1 + 12 T / τ_max)); the steps are scaled by q = T / (τ_max·n(n+1)/3). */
+int kazeref_fed_cycle(double T, double tau_max, double* taus, int cap) {
+    if (!(T > 0) || !(tau_max > 0)) return -1;
+    int n = (int)ceil(-0.5 + 0.5 * sqrt(1.0 + 12.0 * T / tau_max) - 1e-12);
+    if (n < 1) n = 1;
+    while (tau_max * n * (n + 1) / 3.0 < T) ++n;  /* guard the ceiling against rounding */
+    if (taus) {
+        double* t = (double*)malloc(sizeof(double) * n);
+        kazeref_fed_taus(n, tau_max, t);
+        double q = T / (tau_max * n * (n + 1) / 3.0);
+        for (int j = 0; j < n && j < cap; ++j) taus[j] = q * t[j];
+        free(t);
+    }
+    return n;
+}
+
+/* One explicit step of Eq. 1 with the conductivities held fixed (A20): the flux through the face
+ * between p and its 4-neighbour q is ½(c_p + c_q)(L_q − L_p); faces on the image border carry no flux (Neumann). */
+int kazeref_fed_step(const double* L, const double* c, int W, int H, double tau, double* out) {
+    if (!L || !c || !out || W < 1 || H < 1) return -1;
+    static const int dx[4] = {1, -1, 0, 0}, dy[4] = {0, 0, 1, -1};
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            size_t p = (size_t)y * W + x;
+            double flux = 0.0;
+            for (int k = 0; k < 4; ++k) {
+                int qx = x + dx[k], qy = y + dy[k];
+                if (qx < 0 || qx >= W || qy < 0 || qy >= H) continue;
+                size_t q = (size_t)qy * W + qx;
+                flux += 0.5 * (c[p] + c[q]) * (L[q] - L[p]);
+            }
+            out[p] = L[p] + tau * flux;
+        }
+    return 0;
+}
+
+/* Nonlinear scale space (P:L255-260 with the AOS solver of Eq. 4 [A1], or the FED cycles of Eq. 5 [A20]):
  *   L_0 = G(σ0) * I  (t_0 = σ0²/2);   k from L_0 (A7) unless overridden;
- *   for i = 1..N−1:  c_i = g(|∇ G(1)*L_{i−1}|),  τ_i = t_i − t_{i−1},  L_i = AOS(L_{i−1}, c_i, τ_i). */
+ *   for i = 1..N−1:  c_i = g(|∇ G(1)*L_{i−1}|),  τ_i = t_i − t_{i−1},  L_i = AOS(L_{i−1}, c_i, τ_i)  or
+ *                    L_i = FED cycle of total time τ_i applied to L_{i−1} with c_i fixed. */
 int kazeref_scale_space(const float* img, int W, int H, const kazeref_params* p,
                         double* levels, double* k_out, int32_t* fallback) {
     if (!img || !p || !levels || W < 3 || H < 3) return -1;
@@ -281,12 +331,27 @@ int kazeref_scale_space(const float* img, int W, int H, const kazeref_params* p,
     if (k_out) *k_out = k;
     if (fallback) *fallback = fb;
     double* c = (double*)malloc(sizeof(double) * np);
+    double* tmp = p->scheme == 1 ? (double*)malloc(sizeof(double) * np) : NULL;
     for (int i = 1; i < N; ++i) {
         const double* prev = levels + (size_t)(i - 1) * np;
+        double* cur = levels + (size_t)i * np;
         kazeref_conductivity(prev, W, H, k, p->diffusivity, c);
-        kazeref_aos_step(prev, c, W, H, t[i] - t[i - 1], levels + (size_t)i * np, NULL, NULL);
+        if (p->scheme == 1) {  /* FED cycle from t_{i-1} to t_i with c held fixed (A20) */
+            int n = kazeref_fed_cycle(t[i] - t[i - 1], p->tau_max, NULL, 0);
+            double* taus = (double*)malloc(sizeof(double) * n);
+            kazeref_fed_cycle(t[i] - t[i - 1], p->tau_max, taus, n);
+            memcpy(cur, prev, sizeof(double) * np);
+            for (int j = 0; j < n; ++j) {
+                kazeref_fed_step(cur, c, W, H, taus[j], tmp);
+                memcpy(cur, tmp, sizeof(double) * np);
+            }
+            free(taus);
+        } else {
+            kazeref_aos_step(prev, c, W, H, t[i] - t[i - 1], cur, NULL, NULL);
+        }
     }
     free(c); free(I); free(t);
+    if (tmp) free(tmp);
     return 0;
 }
 

@@ -34,6 +34,8 @@ typedef struct {
     double  edge_ratio;     /* r of Eq. 12; <= 0 disables the test */
     int32_t ori_windows;    /* number of sliding-window centres (A14), default 42 */
     int32_t keep_angle;     /* 1: describe with the angles already in kps (stage-isolated use) */
+    int32_t scheme;         /* 0 = AOS (Eq. 4, BASELINE north_star, A1); 1 = FED cycles (Eq. 5, A20) */
+    double  tau_max;        /* FED stability bound of one explicit step (A20), default 0.25 */
 } kazeref_params;
 
 typedef struct {
@@ -76,7 +78,18 @@ int kazeref_thomas(int n, const double* a, const double* b, const double* c, con
 int kazeref_aos_step(const double* L, const double* c, int W, int H, double tau,
                      double* Lnew, double* U, double* V);
 
-/* Nonlinear scale space: L_0 = G(σ0)*I, then N−1 AOS steps (A1).
+/* FED step sizes of Eq. 5: τ_j = τ_max / (2 cos²(π (2j+1)/(4n+2))), j = 0..n−1. */
+int kazeref_fed_taus(int n, double tau_max, double* taus);
+
+/* One FED cycle reaching time T exactly (A20): the smallest n with τ_max·n(n+1)/3 >= T, the Eq. 5 steps scaled by
+ * q = T / (τ_max·n(n+1)/3).  Writes at most cap steps; returns n (< 0 on error). */
+int kazeref_fed_cycle(double T, double tau_max, double* taus, int cap);
+
+/* One explicit diffusion step (A20): L⁺(p) = L(p) + τ Σ_{q ∈ N4(p)} ½(c(p) + c(q)) (L(q) − L(p)), neighbours outside
+ * the image contribute nothing (Neumann). */
+int kazeref_fed_step(const double* L, const double* c, int W, int H, double tau, double* out);
+
+/* Nonlinear scale space: L_0 = G(σ0)*I, then N−1 AOS steps (A1) or FED cycles (scheme 1, A20).
  * levels: N*H*W doubles.  k_out / fallback may be NULL. */
 int kazeref_scale_space(const float* img, int W, int H, const kazeref_params* p,
                         double* levels, double* k_out, int32_t* fallback);

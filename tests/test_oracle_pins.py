@@ -490,3 +490,106 @@ def test_bilinear_exact_on_planes(O):
     for (x, y) in [(3.25, 4.75), (0.0, 0.0), (10.9, 8.1)]:
         assert O.bilinear(img, x, y) == pytest.approx(0.7 * x - 1.3 * y + 2.0, abs=1e-13)
     assert O.bilinear(img, -5.0, 4.0) == pytest.approx(img[4, 0])  # clamped
+
+
+# ----------------------------------------------------------------------------- P22 FED (Eq. 5, A20)
+def test_fed_taus_spec_and_closed_form(O):
+    for e in GOLD["fed"]["taus"]:
+        np.testing.assert_allclose(O.fed_taus(e["n"], e["tau_max"]), e["taus"], rtol=1e-14)
+    for n in range(1, 51):  # Σ τ_j = τ_max n(n+1)/3, all positive
+        t = O.fed_taus(n, 0.25)
+        assert (t > 0).all()
+        assert t.sum() == pytest.approx(0.25 * n * (n + 1) / 3, rel=1e-9)
+
+
+def test_fed_cycle_spec_and_exact_arrival(O):
+    for e in GOLD["fed"]["cycle"]:
+        t = O.fed_cycle(e["T"], e["tau_max"])
+        assert len(t) == e["n"] and t.sum() == pytest.approx(e["T"], rel=1e-12)
+    sg, tt, _ = O.schedule(4, 4, 1.6)
+    for T in np.diff(tt):
+        t = O.fed_cycle(T, 0.25)
+        n = len(t)
+        assert 0.25 * n * (n + 1) / 3 >= T * (1 - 1e-12) and 0.25 * (n - 1) * n / 3 < T  # smallest such n
+        assert t.sum() == pytest.approx(T, rel=1e-12)
+
+
+def test_fed_cycle_is_stable_polynomial(O):
+    """Eq. 5's point: the whole cycle's amplification prod(1 - τ_j μ) stays in [-1, 1] for every Laplacian
+    eigenvalue μ in [0, 2/τ_max] (2-D 4-neighbour, c <= 1) although single steps exceed the explicit limit."""
+    for n in (1, 2, 5, 17, 40):
+        t = O.fed_taus(n, 0.25)
+        assert t.max() > 0.25 or n == 1
+        mu = np.linspace(0, 8.0, 20001)
+        amp = np.prod(1 - t[:, None] * mu[None, :], axis=0)
+        assert np.abs(amp).max() <= 1 + 1e-9
+
+
+def test_fed_step_dct_closed_form_and_invariants(O):
+    """c = 1: every Neumann DCT-II mode is an eigenvector of the 4-neighbour step, eigenvalue
+    1 − τ(4 sin²(πk/2W) + 4 sin²(πl/2H)); mass is conserved and the max principle holds for τ ≤ 1/4."""
+    H, W = 24, 40
+    yy, xx = np.mgrid[0:H, 0:W].astype(float)
+    c = np.ones((H, W))
+    for (k, l, tau) in [(3, 2, 0.2), (7, 0, 0.25), (0, 5, 0.1), (13, 11, 1.7)]:
+        mode = np.cos(np.pi * k * (xx + 0.5) / W) * np.cos(np.pi * l * (yy + 0.5) / H)
+        lam = 1 - tau * (4 * np.sin(np.pi * k / (2 * W)) ** 2 + 4 * np.sin(np.pi * l / (2 * H)) ** 2)
+        np.testing.assert_allclose(O.fed_step(mode, c, tau), lam * mode, atol=1e-13)
+    rng = np.random.default_rng(22)
+    L = rng.random((H, W))
+    cr = rng.uniform(0.0, 1.0, (H, W))
+    np.testing.assert_allclose(O.fed_step(np.full((H, W), 0.3), cr, 0.25), 0.3, rtol=1e-15)
+    for tau in (0.05, 0.25, 3.0):
+        out = O.fed_step(L, cr, tau)
+        assert out.sum() == pytest.approx(L.sum(), rel=1e-13)
+        if tau <= 0.25:
+            assert out.min() >= L.min() - 1e-14 and out.max() <= L.max() + 1e-14
+
+
+def test_fed_step_vs_dense_graph_laplacian(O):
+    """Brute force on a 5x4 grid: the step equals (I + τ A) L with A the weighted graph Laplacian of the
+    4-neighbour grid, edge weight ½(c_p + c_q), assembled edge by edge."""
+    H, W = 4, 5
+    rng = np.random.default_rng(23)
+    L, c = rng.random((H, W)), rng.uniform(0.1, 1, (H, W))
+    n = H * W
+    A = np.zeros((n, n))
+    for y in range(H):
+        for x in range(W):
+            for (yy, xx) in ((y, x + 1), (y + 1, x)):
+                if yy < H and xx < W:
+                    p, q = y * W + x, yy * W + xx
+                    w = 0.5 * (c[y, x] + c[yy, xx])
+                    A[p, q] += w
+                    A[q, p] += w
+                    A[p, p] -= w
+                    A[q, q] -= w
+    np.testing.assert_allclose(O.fed_step(L, c, 0.21), ((np.eye(n) + 0.21 * A) @ L.ravel()).reshape(H, W), atol=1e-14)
+
+
+def test_fed_unit_conductivity_is_gaussian(O):
+    """c = 1, FED evolution to time t ≈ G(sqrt(2t)), RMS < 1e-2 on a smooth 64×64 image."""
+    yy, xx = np.mgrid[0:64, 0:64].astype(float)
+    img = np.exp(-((xx - 32) ** 2 + (yy - 32) ** 2) / (2 * 4.0 ** 2))
+    t = 4.0
+    L = img.copy()
+    for tau in O.fed_cycle(t, 0.25):
+        L = O.fed_step(L, np.ones_like(L), tau)
+    ref = O.gaussian_blur(img, math.sqrt(2 * t))
+    assert np.sqrt(np.mean((L - ref) ** 2)) < 1e-2
+
+
+def test_fed_scale_space_mass_and_agreement_with_aos(O):
+    """mass conserved over a full g2 FED pyramid on 128×128; FED and AOS discretise the same PDE, so
+    their levels agree to within a fraction of how far each level has evolved."""
+    img = kaze_inputs.synth_image(128, 128, 3).astype(np.float64)
+    lf, kf, _ = O.scale_space(img, octaves=3, sublevels=4, scheme=1)
+    la, ka, _ = O.scale_space(img, octaves=3, sublevels=4, scheme=0)
+    assert kf == ka
+    m0 = lf[0].sum()
+    for i in range(1, lf.shape[0]):
+        assert lf[i].sum() == pytest.approx(m0, rel=1e-4)
+        # the two schemes differ by their splitting / time errors, far less than the evolution itself
+        rms = np.sqrt(np.mean((lf[i] - la[i]) ** 2))
+        assert rms < 0.25 * np.sqrt(np.mean((lf[i] - lf[0]) ** 2))
+    assert lf.min() >= lf[0].min() - 1e-12 and lf.max() <= lf[0].max() + 1e-12
