@@ -111,6 +111,7 @@ def lib():
         L.kazeref_run.restype = C.c_int64
         L.kazeref_fed_taus.argtypes = [C.c_int, C.c_double, _dp]
         L.kazeref_fed_cycle.argtypes = [C.c_double, C.c_double, _dp, C.c_int]
+        L.kazeref_fed_order.argtypes = [_dp, C.c_int, C.POINTER(C.c_int32)]
         L.kazeref_fed_step.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, _dp]
         L.kazeref_run_batch.argtypes = [_fp, C.c_int, C.c_int, C.c_int, C.POINTER(Params),
                                         C.c_int64, C.c_int, C.POINTER(C.c_int64)]
@@ -227,6 +228,13 @@ def fed_cycle(T: float, tau_max: float = 0.25) -> np.ndarray:
     t = np.zeros(n)
     lib().kazeref_fed_cycle(T, tau_max, _d(t), n)
     return t
+
+
+def fed_order(taus) -> np.ndarray:
+    t = _f64(taus)
+    o = np.zeros(len(t), np.int32)
+    _chk(lib().kazeref_fed_order(_d(t), len(t), o.ctypes.data_as(C.POINTER(C.c_int32))))
+    return o
 
 
 def fed_step(L, c, tau: float) -> np.ndarray:

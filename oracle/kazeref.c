@@ -286,6 +286,47 @@ int kazeref_fed_cycle(double T, double tau_max, double* taus, int cap) {
     return n;
 }
 
+static int kr_gcd(int a, int b) { while (b) { int t = a % b; a = b; b = t; } return a; }
+
+/* A21: choose κ by brute force over every admissible κ and every μ of the grid. */
+int kazeref_fed_order(const double* taus, int n, int32_t* order) {
+    if (n < 1 || !taus || !order) return -1;
+    enum { NMU = 1025 };
+    int best_k = 1;
+    double best_g = -1.0;
+    int32_t* ord = (int32_t*)malloc(sizeof(int32_t) * n);
+    double* pre = (double*)malloc(sizeof(double) * n);  /* max_μ |P_m| */
+    double* suf = (double*)malloc(sizeof(double) * (n + 1));  /* max_μ |S_m| (S_n = 1) */
+    for (int k = 1; k < (n > 1 ? n : 2); ++k) {
+        if (kr_gcd(k, n) != 1) continue;
+        for (int m = 0; m < n; ++m) ord[m] = (int32_t)(((long)k * m) % n);
+        for (int m = 0; m < n; ++m) pre[m] = 0.0;
+        for (int m = 0; m <= n; ++m) suf[m] = (m == n) ? 1.0 : 0.0;
+        for (int i = 0; i < NMU; ++i) {
+            double mu = 8.0 * i / (NMU - 1);
+            double p = 1.0;
+            for (int m = 0; m < n; ++m) {
+                p *= 1.0 - taus[ord[m]] * mu;
+                if (fabs(p) > pre[m]) pre[m] = fabs(p);
+            }
+            double s = 1.0;
+            for (int m = n - 1; m >= 0; --m) {
+                s *= 1.0 - taus[ord[m]] * mu;
+                if (fabs(s) > suf[m]) suf[m] = fabs(s);
+            }
+        }
+        double g = 0.0;
+        for (int m = 0; m < n; ++m) {
+            double v = pre[m] * suf[m + 1];
+            if (v > g) g = v;
+        }
+        if (best_g < 0 || g < best_g) { best_g = g; best_k = k; }
+    }
+    for (int m = 0; m < n; ++m) order[m] = (int32_t)(((long)best_k * m) % n);
+    free(ord); free(pre); free(suf);
+    return best_k;
+}
+
 /* One explicit step of Eq. 1 with the conductivities held fixed (A20): the flux through the face
  * between p and its 4-neighbour q is ½(c_p + c_q)(L_q − L_p); faces on the image border carry no flux (Neumann). */
 int kazeref_fed_step(const double* L, const double* c, int W, int H, double tau, double* out) {
@@ -309,7 +350,7 @@ int kazeref_fed_step(const double* L, const double* c, int W, int H, double tau,
 /* Nonlinear scale space (P:L255-260 with the AOS solver of Eq. 4 [A1], or the FED cycles of Eq. 5 [A20]):
  *   L_0 = G(σ0) * I  (t_0 = σ0²/2);   k from L_0 (A7) unless overridden;
  *   for i = 1..N−1:  c_i = g(|∇ G(1)*L_{i−1}|),  τ_i = t_i − t_{i−1},  L_i = AOS(L_{i−1}, c_i, τ_i)  or
- *                    L_i = FED cycle of total time τ_i applied to L_{i−1} with c_i fixed. */
+ *                    L_i = FED cycle of total time τ_i applied to L_{i−1} with c_i fixed, steps in the A21 order. */
 int kazeref_scale_space(const float* img, int W, int H, const kazeref_params* p,
                         double* levels, double* k_out, int32_t* fallback) {
     if (!img || !p || !levels || W < 3 || H < 3) return -1;
@@ -339,13 +380,15 @@ int kazeref_scale_space(const float* img, int W, int H, const kazeref_params* p,
         if (p->scheme == 1) {  /* FED cycle from t_{i-1} to t_i with c held fixed (A20) */
             int n = kazeref_fed_cycle(t[i] - t[i - 1], p->tau_max, NULL, 0);
             double* taus = (double*)malloc(sizeof(double) * n);
+            int32_t* order = (int32_t*)malloc(sizeof(int32_t) * n);
             kazeref_fed_cycle(t[i] - t[i - 1], p->tau_max, taus, n);
+            kazeref_fed_order(taus, n, order);  /* A21 */
             memcpy(cur, prev, sizeof(double) * np);
             for (int j = 0; j < n; ++j) {
-                kazeref_fed_step(cur, c, W, H, taus[j], tmp);
+                kazeref_fed_step(cur, c, W, H, taus[order[j]], tmp);
                 memcpy(cur, tmp, sizeof(double) * np);
             }
-            free(taus);
+            free(taus); free(order);
         } else {
             kazeref_aos_step(prev, c, W, H, t[i] - t[i - 1], cur, NULL, NULL);
         }

@@ -85,6 +85,13 @@ int kazeref_fed_taus(int n, double tau_max, double* taus);
  * q = T / (τ_max·n(n+1)/3).  Writes at most cap steps; returns n (< 0 on error). */
 int kazeref_fed_cycle(double T, double tau_max, double* taus, int cap);
 
+/* Rounding-stable application order of a cycle's steps (A21).  With c fixed every step is a polynomial in the
+ * same matrix A, so the cycle Π_j (I + τ_j A) does not depend on the order in exact arithmetic, but its rounding
+ * does (P_m, S_m below grow like 1e12 for n = 29 in natural order).  Order: j_m = (κ·m) mod n with κ ∈ [1, n),
+ * gcd(κ, n) = 1, minimising G(κ) = max_m max_μ |P_m(μ)| · max_μ |S_{m+1}(μ)|, P_m = Π_{i≤m}(1 − τ_{j_i} μ),
+ * S_{m+1} = Π_{i>m}(1 − τ_{j_i} μ), μ ∈ {8i/1024 : i = 0..1024}; ties → smallest κ.  Returns κ. */
+int kazeref_fed_order(const double* taus, int n, int32_t* order);
+
 /* One explicit diffusion step (A20): L⁺(p) = L(p) + τ Σ_{q ∈ N4(p)} ½(c(p) + c(q)) (L(q) − L(p)), neighbours outside
  * the image contribute nothing (Neumann). */
 int kazeref_fed_step(const double* L, const double* c, int W, int H, double tau, double* out);

@@ -593,3 +593,33 @@ def test_fed_scale_space_mass_and_agreement_with_aos(O):
         rms = np.sqrt(np.mean((lf[i] - la[i]) ** 2))
         assert rms < 0.25 * np.sqrt(np.mean((lf[i] - lf[0]) ** 2))
     assert lf.min() >= lf[0].min() - 1e-12 and lf.max() <= lf[0].max() + 1e-12
+
+
+def test_fed_order_is_permutation_and_stable(O):
+    """A21: the order is a κ-permutation; in exact arithmetic the cycle is order independent, so with c ≡ 1 a DCT
+    mode must come out scaled by Π_j(1 − τ_j μ) whatever the order — natural order loses ~1e-4 of it in fp64 at
+    n = 29 (partial products ~1e12), the chosen order keeps it to rounding."""
+    sg, t, _ = O.schedule(4, 4, 1.6)
+    for T in np.diff(t):
+        taus = O.fed_cycle(T)
+        o = O.fed_order(taus)
+        assert sorted(o.tolist()) == list(range(len(taus)))
+        if len(o) > 1:
+            kappa = int(o[1])
+            assert math.gcd(kappa, len(o)) == 1 and all(o[m] == (kappa * m) % len(o) for m in range(len(o)))
+    # exact spectral result: with c ≡ 1 and Neumann borders the orthonormal DCT-II diagonalises A (scipy.fft)
+    from scipy.fft import dctn, idctn
+    H, W = 16, 24
+    taus = O.fed_cycle(67.86)
+    assert len(taus) == 29
+    rng = np.random.default_rng(24)
+    L0 = rng.random((H, W))
+    mu = (4 * np.sin(np.pi * np.arange(H) / (2 * H)) ** 2)[:, None] + (4 * np.sin(np.pi * np.arange(W) / (2 * W)) ** 2)[None, :]
+    exact = idctn(dctn(L0, norm="ortho") * np.prod(1 - taus[:, None, None] * mu[None], axis=0), norm="ortho")
+    def cycle(order):
+        L = L0.copy()
+        for j in order:
+            L = O.fed_step(L, np.ones_like(L), taus[j])
+        return L
+    np.testing.assert_allclose(cycle(O.fed_order(taus)), exact, atol=1e-12)
+    assert np.abs(cycle(range(29)) - exact).max() > 1e-8  # the natural order is measurably worse
