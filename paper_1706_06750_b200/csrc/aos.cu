@@ -1,24 +1,28 @@
 // aos.cu — semi-implicit AOS step of Eq. 4 (readings A1, A2) on sm_100a.
 //
-// L_i = ½[(I − 2τA_x(c))⁻¹ + (I − 2τA_y(c))⁻¹] L_{i−1}: H row systems of length W (k_aos_rows_cta → V, first) and
-// W column systems of length H (k_aos_cols → L_i = ½(U + V), second).  Every line is tridiagonal with
+// L_i = ½[(I − 2τA_y(c))⁻¹ + (I − 2τA_x(c))⁻¹] L_{i−1}: W column systems of length H (k_aos_cols_u → U, first
+// pass, 12 B/px) and H row systems of length W (k_aos_rows_cta → L_i = ½(U + V), second pass, 16 B/px).  Every
+// line is tridiagonal with
 //   a_j = −τ(c_{j−1} + c_j),  cc_j = −τ(c_j + c_{j+1}),  b_j = 1 − a_j − cc_j   (Neumann ends: a_0 = cc_{n−1} = 0).
 //
 // Both passes use the partition ("Thomas–PCR hybrid") scheme of DESIGN.md §6: a line is cut into T chunks of M
-// samples (the last takes the remainder, 2..M+1), one thread per chunk.  Each thread eliminates its chunk in
-// registers (downward sweep keeping x_first, upward sweep keeping x_last), leaving x_i = δ'_i − α'_i x_first −
-// γ'_i x_last and two reduced equations; substituting the neighbour's last equation gives a tridiagonal system in
-// the T chunk-first unknowns; after it is solved every thread evaluates its samples.  One 1-ulp reciprocal per
-// sample.
-//   rows:    one CTA (4 or 8 warps) per row.  The TMA engine streams the row's L and c into shared memory (1-D bulk
-//            copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is solved
-//            by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve), and V
-//            leaves through shared memory with 16-byte stores.
+// samples, one thread per chunk.  Each thread eliminates its chunk in registers, leaving two reduced equations
+// (its first sample in terms of the previous chunk's last, its last in terms of the next chunk's first);
+// substituting the neighbour's last equation gives a tridiagonal system in the T chunk-first unknowns; after it
+// is solved every thread evaluates its samples.
 //   columns: a CTA owns CW adjacent columns; a warp covers CW columns × 32/CW chunks, so every global request is
-//            whole 32-byte sectors; the reduced systems are solved by PCR in shared memory; V is prefetched with
-//            cp.async behind the solve and L_i = ½(U + V) is written directly.
-//            (Measured alternatives, all slower on B200 for 1920x1200: TMA-pipelined persistent strips 80 ms,
-//            three register-light passes 88 ms, re-mapped warp SPIKE 77 ms, vs 66 ms per 256-image step here.)
+//            whole 32-byte sectors.  Register-light elimination (independent down and up sweeps, then a Dirichlet
+//            Thomas sweep in place: two live values per sample) lets two 480-thread CTAs share an SM, so one
+//            CTA's loads overlap the other's solve; the reduced systems are solved by PCR in shared memory.
+//            The ragged last chunk is padded with decoupled rows (zero edge weights), so there is one path.
+//            Columns run first because the row pass reads a third array almost for free: its TMA bulk copies
+//            stream L, c and U, and it writes L_i = ½(U + V) with 16-byte stores.  (Measured on B200, 256-image
+//            1920x1200 step: this order and kernel 34.7 + 25.0 ms vs 58.3 + 22.9 ms for rows-first with a
+//            three-value column kernel; earlier column variants — TMA-pipelined persistent strips, three
+//            register-light passes, re-mapped warp SPIKE — were slower still.)
+//   rows:    one CTA (4 or 8 warps) per row.  The TMA engine streams the row's L, c and U into shared memory (1-D
+//            bulk copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is
+//            solved by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve).
 #include "kaze_internal.cuh"
 #include "ptx.cuh"
 
@@ -178,93 +182,139 @@ __host__ __device__ inline int n_chunks(int n, int M) {
 }
 
 // -------------------------------------------------------------------------------------------------------------
-// Column systems.  Thread (cx, p): column x0 + cx, chunk p of T.  blockDim.x = CW * TP; shared index p*CW + cx.
-template <int CW, int M, int NT>
-__global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, const float* __restrict__ c,
-                                                 const float* __restrict__ U, float* __restrict__ Lout, Strides st,
-                                                 Geom g, float tau, int T, int TP) {
-    constexpr int MC = M + 1;
+// Column systems (first pass: U = column solves).  Thread (cx, p): column x0 + cx, chunk p of T; blockDim.x =
+// CW * TP, shared index p*CW + cx.  A warp covers CW adjacent columns x 32/CW chunks (whole 32-byte sectors).
+//
+// Register-light elimination (two values per sample stay live instead of three): with the chunk's samples
+// x_0..x_{m-1}, edge weights tq_i = τ(c_{i-1} + c_i) (a_i = −tq_i, cc_i = −tq_{i+1}, b_i = 1 + tq_i + tq_{i+1}),
+//   down sweep, x_0 symbolic:        x_{m-1} = F − G·x_m − Hh·x_0          (the chunk's "last equation")
+//   up sweep, x_{m-1} symbolic:      x_0 + A·x_{−1} + C·x_{m-1} = D        (its "first equation")
+// Both sweeps read only (L, tq) and keep O(1) state.  Substituting the neighbours' last equations gives a
+// tridiagonal system in the chunk-first unknowns X_k (PCR in shared memory); x_{m-1} follows from the last
+// equation, and the interior is a Dirichlet problem solved by a Thomas sweep that overwrites (L, tq) in place.
+struct ChunkEq {
+    float A, C, D;     // first equation
+    float lF, lG, lH;  // last equation
+};
+
+// Every chunk has exactly M samples: samples past the line end are padding rows decoupled by zero edge weights
+// (b = 1, d = 0), so one branch-free path serves the ragged last chunk too.
+template <int M>
+__device__ __forceinline__ void chunk_reduce(const float (&dv)[M], const float (&tq)[M + 1], ChunkEq& e) {
+    float F = 0.f, G = 0.f, Hh = -1.f;
+#pragma unroll
+    for (int i = 1; i < M; ++i) {
+        const float r = frcp(fmaf(tq[i], G, 1.f + tq[i] + tq[i + 1]));  // b_i − a_i G
+        F = fmaf(tq[i], F, dv[i]) * r;
+        Hh = tq[i] * Hh * r;
+        G = -tq[i + 1] * r;
+    }
+    e.lF = F;
+    e.lG = G;
+    e.lH = Hh;
+    float P = 0.f, Q = 0.f, S = -1.f;
+#pragma unroll
+    for (int i = M - 2; i >= 1; --i) {
+        const float r = frcp(fmaf(tq[i + 1], Q, 1.f + tq[i] + tq[i + 1]));  // b_i − cc_i Q
+        P = fmaf(tq[i + 1], P, dv[i]) * r;
+        S = tq[i + 1] * S * r;
+        Q = -tq[i] * r;
+    }
+    const float rB = frcp(fmaf(tq[1], Q, 1.f + tq[0] + tq[1]));
+    e.A = -tq[0] * rB;
+    e.C = tq[1] * S * rB;
+    e.D = fmaf(tq[1], P, dv[0]) * rB;
+}
+
+// Interior of the chunk with x_0 = x0 and x_{M-1} = xl known; writes the samples j0+i < n (stride P floats).
+template <int M>
+__device__ __forceinline__ void chunk_finish(float (&dv)[M], float (&tq)[M + 1], float x0, float xl,
+                                             float* __restrict__ out, int P, int nvalid) {
+    float Fp = x0, G = 0.f;
+#pragma unroll
+    for (int i = 1; i < M - 1; ++i) {
+        const float r = frcp(fmaf(tq[i], G, 1.f + tq[i] + tq[i + 1]));
+        Fp = fmaf(tq[i], Fp, dv[i]) * r;
+        G = -tq[i + 1] * r;
+        dv[i] = Fp;  // F'_i
+        tq[i] = G;   // G_i
+    }
+    out[0] = x0;
+    if (M - 1 < nvalid) out[(size_t)(M - 1) * P] = xl;
+    float xn = xl;
+#pragma unroll
+    for (int i = M - 2; i >= 1; --i) {
+        xn = fmaf(-tq[i], xn, dv[i]);
+        if (i < nvalid) out[(size_t)i * P] = xn;
+    }
+}
+
+template <int CW, int M, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_aos_cols_u(const float* __restrict__ L, const float* __restrict__ c,
+                                                         float* __restrict__ U, Strides st, Geom g, float tau, int T,
+                                                         int TP) {
     extern __shared__ float sm[];
     const int NTOT = CW * TP;
     float* sa = sm;
     float* sb = sa + NTOT;
     float* sc = sb + NTOT;
     float* sd = sc + NTOT;
-    float* sla = sd + NTOT;  // last-equation exchange
-    float* slg = sla + NTOT;
-    float* sld = slg + NTOT;
-    float* sv = sld + NTOT;  // V chunk, prefetched with cp.async while the solve runs: [MC][NTOT]
+    float* slF = sd + NTOT;  // last-equation exchange
+    float* slG = slF + NTOT;
+    float* slH = slG + NTOT;
     const int cx = threadIdx.x % CW, p = threadIdx.x / CW;
     const int x = blockIdx.x * CW + cx;
     const bool active = (p < T) && (x < g.W);
     const int n = g.H;
     const int j0 = p * M;
-    const int j1 = (p == T - 1) ? n : j0 + M;
-    const int m = active ? j1 - j0 : 0;
-
-    Chunk<MC> ch;
-    if (active) {  // the V chunk streams into shared memory behind the solve
-        const float* Vg = U + blockIdx.z * st.U + (size_t)j0 * g.P + x;
-#pragma unroll
-        for (int i = 0; i < MC; ++i)
-            if (i < m) cp_async4(sv + i * NTOT + threadIdx.x, Vg + (size_t)i * g.P);
-    }
+    const int nvalid = n - j0;  // samples of this chunk inside the line (>= 1 for p < T)
+    float dv[M], tq[M + 1];
+    ChunkEq e{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (active) {
-        float dv[MC], cv[MC];
         const float* Lc = L + blockIdx.z * st.L + (size_t)j0 * g.P + x;
         const float* cc = c + blockIdx.z * st.c + (size_t)j0 * g.P + x;
+        float cv[M];
 #pragma unroll
-        for (int i = 0; i < MC; ++i) {
-            if (i < m) {
-                dv[i] = __ldg(Lc + (size_t)i * g.P);
-                cv[i] = __ldg(cc + (size_t)i * g.P);
-            } else {
-                dv[i] = 0.f;
-                cv[i] = 0.f;
-            }
+        for (int i = 0; i < M; ++i) {
+            const bool in = i < nvalid;
+            dv[i] = in ? __ldg(Lc + (size_t)i * g.P) : 0.f;
+            cv[i] = in ? __ldg(cc + (size_t)i * g.P) : 0.f;
         }
         const float cprev = j0 > 0 ? __ldg(cc - g.P) : 0.f;
-        const float cnext = j1 < n ? __ldg(cc + (size_t)m * g.P) : 0.f;
-        if (m == M) eliminate_full<M>(ch, dv, cv, cprev, cnext, j0 == 0, j1 == n, tau);
-        else eliminate<MC>(ch, dv, cv, cprev, cnext, m, j0 == 0, j1 == n, tau);
-    } else {
-        ch.A = ch.C = ch.D = 0.f;
-        ch.lA = ch.lG = ch.lD = 0.f;
+        const float cnext = M < nvalid ? __ldg(cc + (size_t)M * g.P) : 0.f;
+        // edge i joins samples j0+i-1 and j0+i; it exists iff 1 <= j0+i <= n-1 (Neumann ends, padding decoupled)
+        tq[0] = j0 > 0 ? tau * (cprev + cv[0]) : 0.f;
+#pragma unroll
+        for (int i = 1; i < M; ++i) tq[i] = i < nvalid ? tau * (cv[i - 1] + cv[i]) : 0.f;
+        tq[M] = M < nvalid ? tau * (cv[M - 1] + cnext) : 0.f;
+        chunk_reduce<M>(dv, tq, e);
     }
     const int idx = p * CW + cx;
-    sla[idx] = ch.lA;
-    slg[idx] = ch.lG;
-    sld[idx] = ch.lD;
+    slF[idx] = e.lF;
+    slG[idx] = e.lG;
+    slH[idx] = e.lH;
     __syncthreads();
     float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
     if (active) {
-        float pA = 0.f, pG = 0.f, pD = 0.f;
+        float pF = 0.f, pG = 0.f, pH = 0.f;
         if (p > 0) {
-            pA = sla[idx - CW];
-            pG = slg[idx - CW];
-            pD = sld[idx - CW];
+            pF = slF[idx - CW];
+            pG = slG[idx - CW];
+            pH = slH[idx - CW];
         }
-        af = -ch.A * pA;
-        bf = 1.f - ch.A * pG - ch.C * ch.lA;
-        cf = -ch.C * ch.lG;
-        df = ch.D - ch.A * pD - ch.C * ch.lD;
+        // x_{-1} = pF − pG·X_k − pH·X_{k−1};  x_{M−1} = lF − lG·X_{k+1} − lH·X_k
+        af = -e.A * pH;
+        bf = 1.f - e.A * pG - e.C * e.lH;
+        cf = -e.C * e.lG;
+        df = e.D - e.A * pF - e.C * e.lF;
     }
     const float xf = pcr_solve(af, bf, cf, df, p, TP, CW, idx, sa, sb, sc, sd);
     sa[idx] = xf;
     __syncthreads();
     if (!active) return;
     const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
-    const float xl = ch.lD - ch.lA * xf - ch.lG * xnext;
-    // L_i = ½(U + V): the row pass already wrote V (prefetched into sv); the average is formed here.
-    cp_async_wait_all();
-    const float* vv = sv + threadIdx.x;
-    float* Oc = Lout + blockIdx.z * st.out + (size_t)j0 * g.P + x;
-    Oc[0] = 0.5f * (xf + vv[0]);
-#pragma unroll
-    for (int i = 1; i < MC; ++i) {
-        if (i < m - 1) Oc[(size_t)i * g.P] = 0.5f * (ch.de[i] - ch.al[i] * xf - ch.ga[i] * xl + vv[i * NTOT]);
-    }
-    Oc[(size_t)(m - 1) * g.P] = 0.5f * (xl + vv[(m - 1) * NTOT]);
+    const float xl = e.lF - e.lG * xnext - e.lH * xf;
+    chunk_finish<M>(dv, tq, xf, xl, U + blockIdx.z * st.out + (size_t)j0 * g.P + x, g.P, nvalid);
 }
 
 // -------------------------------------------------------------------------------------------------------------
@@ -275,7 +325,8 @@ __global__ void __launch_bounds__(NT) k_aos_cols(const float* __restrict__ L, co
 // then x = y − v·x_{prev warp} − z·x_{next warp}.  x goes back to shared memory and V leaves with 16-byte stores.
 template <int M, int NW>
 __global__ void __launch_bounds__(32 * NW) k_aos_rows_cta(const float* __restrict__ L, const float* __restrict__ c,
-                                                          float* __restrict__ V, Strides st, Geom g, float tau, int T) {
+                                                          const float* __restrict__ U, float* __restrict__ Lout,
+                                                          Strides st, Geom g, float tau, int T) {
     constexpr int MC = M + 1, TP = 32 * NW;
     extern __shared__ __align__(16) float rs[];
     __shared__ __align__(8) uint64_t bar;
@@ -284,15 +335,17 @@ __global__ void __launch_bounds__(32 * NW) k_aos_rows_cta(const float* __restric
     const int Wp = (n + 3) & ~3;
     float* sL = rs;
     float* sC = rs + Wp;
+    float* sU = rs + 2 * Wp;
     const int p = threadIdx.x, lane = p & 31, w = p >> 5;
     const int img = blockIdx.x / g.H, y = blockIdx.x - img * g.H;
     const size_t ry = (size_t)y * g.P;
     if (p == 0) {
         mbar_init(&bar, 1);
         fence_mbar_init();
-        mbar_arrive_expect_tx(&bar, 8u * (uint32_t)Wp);
+        mbar_arrive_expect_tx(&bar, 12u * (uint32_t)Wp);
         bulk_g2s(sL, L + img * st.L + ry, 4u * (uint32_t)Wp, &bar);
         bulk_g2s(sC, c + img * st.c + ry, 4u * (uint32_t)Wp, &bar);
+        bulk_g2s(sU, U + img * st.U + ry, 4u * (uint32_t)Wp, &bar);
     }
     __syncthreads();
     mbar_wait(&bar, 0);
@@ -401,70 +454,76 @@ __global__ void __launch_bounds__(32 * NW) k_aos_rows_cta(const float* __restric
         sL[j1 - 1] = xl;
     }
     __syncthreads();
-    float4* Vr = reinterpret_cast<float4*>(V + img * st.out + ry);
-    for (int v = p; v < (Wp >> 2); v += TP) Vr[v] = reinterpret_cast<const float4*>(sL)[v];
+    // L_i = ½(U + V), U from the column pass
+    float4* Or = reinterpret_cast<float4*>(Lout + img * st.out + ry);
+    for (int v = p; v < (Wp >> 2); v += TP) {
+        const float4 a = reinterpret_cast<const float4*>(sL)[v], b = reinterpret_cast<const float4*>(sU)[v];
+        Or[v] = make_float4(0.5f * (a.x + b.x), 0.5f * (a.y + b.y), 0.5f * (a.z + b.z), 0.5f * (a.w + b.w));
+    }
 }
 
 template <int M, int NW>
-void run_rows_cta(const float* L, const float* c, float* V, Strides st, Geom g, int nimg, float tau, cudaStream_t s) {
+void run_rows_cta(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg, float tau,
+                  cudaStream_t s) {
     int T = (g.W + M - 1) / M;
     if (T > 1 && g.W - (T - 1) * M == 1) --T;
-    const size_t smem = sizeof(float) * 2 * ((g.W + 3) & ~3);
+    const size_t smem = sizeof(float) * 3 * ((g.W + 3) & ~3);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_aos_rows_cta<M, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    k_aos_rows_cta<M, NW><<<g.H * nimg, 32 * NW, smem, s>>>(L, c, V, st, g, tau, T);
+    k_aos_rows_cta<M, NW><<<g.H * nimg, 32 * NW, smem, s>>>(L, c, U, Lout, st, g, tau, T);
 }
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
-template <int CW, int M, int NT>
-void run_cols(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg, float tau,
-              cudaStream_t s) {
-    const int T = n_chunks(g.H, M);
+template <int CW, int M, int NT, int MINB>
+void run_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau, cudaStream_t s) {
+    const int T = (g.H + M - 1) / M;  // the last chunk is padded (decoupled rows)
     const int TP = round_up(T, 32 / CW);
-    const size_t smem = sizeof(float) * (7 + M + 1) * CW * TP;
+    const size_t smem = sizeof(float) * 7 * CW * TP;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_aos_cols<CW, M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_aos_cols_u<CW, M, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     dim3 grid((g.W + CW - 1) / CW, 1, nimg);
-    k_aos_cols<CW, M, NT><<<grid, CW * TP, smem, s>>>(L, c, U, Lout, st, g, tau, T, TP);
+    k_aos_cols_u<CW, M, NT, MINB><<<grid, CW * TP, smem, s>>>(L, c, U, st, g, tau, T, TP);
 }
 
 }  // namespace
 
-// Column chunk length: T = n_chunks(H, M) must fit the CTA (CW*TP <= NT).
-bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
-                     float tau, cudaStream_t s) {
+// Column chunk length M: T = ceil(H/M) chunks per column, CW*TP <= NT threads; MINB = 2 keeps two CTAs resident
+// per SM so one CTA's loads overlap the other's solve.  At 1920x1200 (256-image step, 1 B200): M = 20 (480
+// threads, 64 registers) 34.7 ms, M = 24 (72 registers) 39.7 ms, M = 16 (608 threads, one CTA per SM) 45.8 ms.
+bool launch_aos_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau,
+                     cudaStream_t s) {
     const int H = g.H;
-    if (H <= 128 * 4) run_cols<8, 4, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 6) run_cols<8, 6, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 8) run_cols<8, 8, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 10) run_cols<8, 10, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 128 * 12) run_cols<8, 12, 1024>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 256 * 16) run_cols<2, 16, 512>(L, c, V, Lout, st, g, nimg, tau, s);
-    else if (H <= 256 * 32) run_cols<2, 32, 512>(L, c, V, Lout, st, g, nimg, tau, s);
+    if (H <= 8 * 64) run_cols<8, 8, 512, 2>(L, c, U, st, g, nimg, tau, s);
+    else if (H <= 12 * 64) run_cols<8, 12, 512, 2>(L, c, U, st, g, nimg, tau, s);
+    else if (H <= 16 * 64) run_cols<8, 16, 512, 2>(L, c, U, st, g, nimg, tau, s);
+    else if (H <= 20 * 64) run_cols<8, 20, 512, 2>(L, c, U, st, g, nimg, tau, s);
+    else if (H <= 32 * 64) run_cols<4, 32, 256, 2>(L, c, U, st, g, nimg, tau, s);
+    else if (H <= 32 * 128) run_cols<4, 32, 512, 1>(L, c, U, st, g, nimg, tau, s);
+    else if (H <= 32 * 256) run_cols<2, 32, 512, 1>(L, c, U, st, g, nimg, tau, s);
     else return false;
     return true;
 }
 
 // Row systems, one CTA per row: the smallest odd chunk M >= 5 with T = ceil(W/M) <= 32·NW threads.
-bool launch_aos_rows(const float* L, const float* c, float* V, Strides st, Geom g, int nimg, float tau,
-                     cudaStream_t s) {
+bool launch_aos_rows(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg,
+                     float tau, cudaStream_t s) {
     const int W = g.W;
-    if (W <= 128 * 5) run_rows_cta<5, 4>(L, c, V, st, g, nimg, tau, s);
-    else if (W <= 128 * 7) run_rows_cta<7, 4>(L, c, V, st, g, nimg, tau, s);
-    else if (W <= 128 * 9) run_rows_cta<9, 4>(L, c, V, st, g, nimg, tau, s);
-    else if (W <= 128 * 11) run_rows_cta<11, 4>(L, c, V, st, g, nimg, tau, s);
-    else if (W <= 128 * 13) run_rows_cta<13, 4>(L, c, V, st, g, nimg, tau, s);
-    else if (W <= 128 * 15) run_rows_cta<15, 4>(L, c, V, st, g, nimg, tau, s);
-    else if (W <= 256 * 11) run_rows_cta<11, 8>(L, c, V, st, g, nimg, tau, s);
-    else if (W <= 256 * 17) run_rows_cta<17, 8>(L, c, V, st, g, nimg, tau, s);
-    else if (W <= 256 * 33) run_rows_cta<33, 8>(L, c, V, st, g, nimg, tau, s);
+    if (W <= 128 * 5) run_rows_cta<5, 4>(L, c, U, Lout, st, g, nimg, tau, s);
+    else if (W <= 128 * 7) run_rows_cta<7, 4>(L, c, U, Lout, st, g, nimg, tau, s);
+    else if (W <= 128 * 9) run_rows_cta<9, 4>(L, c, U, Lout, st, g, nimg, tau, s);
+    else if (W <= 128 * 11) run_rows_cta<11, 4>(L, c, U, Lout, st, g, nimg, tau, s);
+    else if (W <= 128 * 13) run_rows_cta<13, 4>(L, c, U, Lout, st, g, nimg, tau, s);
+    else if (W <= 128 * 15) run_rows_cta<15, 4>(L, c, U, Lout, st, g, nimg, tau, s);
+    else if (W <= 256 * 11) run_rows_cta<11, 8>(L, c, U, Lout, st, g, nimg, tau, s);
+    else if (W <= 256 * 17) run_rows_cta<17, 8>(L, c, U, Lout, st, g, nimg, tau, s);
+    else if (W <= 256 * 33) run_rows_cta<33, 8>(L, c, U, Lout, st, g, nimg, tau, s);
     else return false;
     return true;
 }

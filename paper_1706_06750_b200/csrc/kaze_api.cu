@@ -267,18 +267,18 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
         }
         KZ_CHECK_LAUNCH(c, "cond");
         const float tau = (float)(c->t[i] - c->t[i - 1]);
-        {   // V = row solves (ubuf holds V)
-            Launch L(c, KC_AOS_ROWS, 12.0 * px, s);
-            if (!launch_aos_rows(prev, c->cbuf, c->ubuf, Strides{SL, SP, 0, SP}, g, n, tau, s))
-                return KAZE_ERR_INVALID_ARGUMENT;
-        }
-        KZ_CHECK_LAUNCH(c, "aos_rows");
-        {   // L_i = ½(U + V), U = column solves
-            Launch L(c, KC_AOS_COLS, 16.0 * px, s);
-            if (!launch_aos_cols(prev, c->cbuf, c->ubuf, cur, Strides{SL, SP, SP, SL}, g, n, tau, s))
+        {   // U = column solves (ubuf holds U)
+            Launch L(c, KC_AOS_COLS, 12.0 * px, s);
+            if (!launch_aos_cols(prev, c->cbuf, c->ubuf, Strides{SL, SP, 0, SP}, g, n, tau, s))
                 return KAZE_ERR_INVALID_ARGUMENT;
         }
         KZ_CHECK_LAUNCH(c, "aos_cols");
+        {   // L_i = ½(U + V), V = row solves
+            Launch L(c, KC_AOS_ROWS, 16.0 * px, s);
+            if (!launch_aos_rows(prev, c->cbuf, c->ubuf, cur, Strides{SL, SP, SP, SL}, g, n, tau, s))
+                return KAZE_ERR_INVALID_ARGUMENT;
+        }
+        KZ_CHECK_LAUNCH(c, "aos_rows");
     }
     c->built = true;
     c->last_stream = s;

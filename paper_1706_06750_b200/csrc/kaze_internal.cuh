@@ -50,11 +50,11 @@ void launch_c_from_g2(float* buf, size_t img_stride, Geom g, int nimg, int diffu
 struct Strides {  // per-image strides (floats) of the four buffers an AOS pass touches
     size_t L, c, U, out;
 };
-// V = row solves of (I - 2 tau A_x(c)) V = L                      (strides: L, c, -, out = V)
-bool launch_aos_rows(const float* L, const float* c, float* V, Strides st, Geom g, int nimg, float tau,
+// First pass: U = column solves of (I - 2 tau A_y(c)) U = L      (strides: L, c, -, out = U)
+bool launch_aos_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau,
                      cudaStream_t s);
-// Lout = ½(U + V), U = column solves of (I - 2 tau A_y(c)) U = L   (strides: L, c, U = V's, out)
-bool launch_aos_cols(const float* L, const float* c, const float* V, float* Lout, Strides st, Geom g, int nimg,
+// Second pass: Lout = ½(U + V), V = row solves of (I - 2 tau A_x(c)) V = L   (strides: L, c, U, out)
+bool launch_aos_rows(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg,
                      float tau, cudaStream_t s);
 
 // ---- hessian.cu ----  (all N levels of nimg images in one launch; level stride = plane)
