@@ -6,7 +6,8 @@
  * silent or garbled).  The method, in the paper's three steps:
  *   1. nonlinear scale space: Gaussian prefilter σ0, contrast k from the gradient histogram
  *      (A7), Perona–Malik g2 conductivity (Eqs. 2-3), and one semi-implicit
- *      AOS step of Eq. 4 per evolution time t_i = σ_i²/2 (Eqs. 6-7, A1-A3)
+ *      AOS step of Eq. 4 per evolution time t_i = σ_i²/2 (Eqs. 6-7, A1-A3) — or, with
+ *      scheme = KAZE_SCHEME_FED, one FED cycle of Eq. 5 per level (A20-A21)
  *      → kaze_build_scale_space;
  *   2. scale-normalised Hessian determinant (Eq. 8, A9-A10), 3x3x3 extrema above the
  *      threshold, edge test (Eqs. 9-12) and 2-D sub-pixel fit → kaze_detect;
@@ -35,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KAZE_ABI_VERSION 1
+#define KAZE_ABI_VERSION 2
 
 typedef struct kaze_ctx kaze_ctx;
 
@@ -64,7 +65,15 @@ typedef struct {
     int32_t max_keypoints; /* per-image capacity of the keypoint / descriptor outputs, >= 1       */
     int32_t ori_windows;   /* sliding-window centres for the orientation, default 42, 1..64 (A14) */
     int32_t flags;         /* KAZE_FLAG_* below                                                   */
+    int32_t scheme;        /* KAZE_SCHEME_AOS (default; Eq. 4, A1) or KAZE_SCHEME_FED (Eq. 5, A20) */
+    double  tau_max;       /* FED: stability bound of one explicit step, in (0, 0.25], default 0.25 */
 } kaze_params;
+
+/* Scale-space solver (kaze_params.scheme). */
+#define KAZE_SCHEME_AOS 0  /* one semi-implicit AOS step of Eq. 4 per level                  */
+#define KAZE_SCHEME_FED 1  /* one FED cycle per level: n explicit steps with Eq. 5 step sizes scaled to
+                              reach t_i exactly, n = min{n : τ_max n(n+1)/3 >= t_i − t_{i−1}}, in the
+                              κ-cycle order of A21                                          */
 
 /* kaze_describe uses the angles already stored in d_kps instead of computing them (stage-isolated
  * parity tests with pinned angles). */
@@ -162,6 +171,11 @@ kaze_status kaze_get_profile(kaze_ctx* ctx, kaze_kernel_stat* out, int32_t cap, 
 kaze_status kaze_reset_profile(kaze_ctx* ctx);
 /* Number of kernels this context has launched since creation (or the last reset). */
 int64_t kaze_launch_count(const kaze_ctx* ctx);
+
+/* Host-only: the FED cycle the context runs for a level transition of total time T (Eq. 5, A20) —
+ * step sizes in execution order (A21) written to taus[0 .. min(n, cap)); returns n (> 0), or
+ * KAZE_ERR_INVALID_ARGUMENT for T <= 0, tau_max outside (0, 0.25], or taus == NULL with cap > 0. */
+int32_t kaze_fed_cycle(double T, double tau_max, float* taus, int32_t cap);
 
 const char* kaze_status_string(kaze_status s);
 const char* kaze_last_error(const kaze_ctx* ctx);

@@ -20,7 +20,7 @@ __all__ = [
     "kaze_default_params", "kaze_create", "kaze_destroy", "kaze_build_scale_space", "kaze_detect",
     "kaze_describe", "kaze_extract", "kaze_extract_host", "kaze_get_k", "kaze_get_level", "kaze_set_level",
     "kaze_set_profiling", "kaze_get_profile", "kaze_reset_profile", "kaze_launch_count", "kaze_abi_version",
-    "Kaze", "PLANE_LT", "PLANE_LX", "PLANE_LY", "PLANE_LDET", "PLANE_COND", "FLAG_KEEP_ANGLE",
+    "kaze_fed_cycle", "Kaze", "PLANE_LT", "PLANE_LX", "PLANE_LY", "PLANE_LDET", "PLANE_COND", "FLAG_KEEP_ANGLE", "SCHEME_AOS", "SCHEME_FED",
     "EXPORTED_SYMBOLS",
 ]
 
@@ -29,6 +29,7 @@ lib_path = os.path.join(_HERE, "libkaze_b200.so")
 
 PLANE_LT, PLANE_LX, PLANE_LY, PLANE_LDET, PLANE_COND = 0, 1, 2, 3, 4
 FLAG_KEEP_ANGLE = 1
+SCHEME_AOS, SCHEME_FED = 0, 1
 
 STATUS = {
     0: "ok", -1: "invalid argument", -2: "image too small", -3: "capacity", -4: "state",
@@ -40,7 +41,7 @@ EXPORTED_SYMBOLS = [
     "kaze_default_params", "kaze_create", "kaze_destroy", "kaze_build_scale_space", "kaze_detect",
     "kaze_describe", "kaze_extract", "kaze_extract_host", "kaze_get_k", "kaze_get_level", "kaze_set_level",
     "kaze_set_profiling", "kaze_get_profile", "kaze_reset_profile", "kaze_launch_count",
-    "kaze_status_string", "kaze_last_error", "kaze_abi_version",
+    "kaze_status_string", "kaze_last_error", "kaze_abi_version", "kaze_fed_cycle",
 ]
 
 
@@ -58,6 +59,7 @@ class KazeParams(C.Structure):
         ("k_bins", C.c_int32), ("diffusivity", C.c_int32),
         ("k_override", C.c_double), ("threshold", C.c_double), ("edge_ratio", C.c_double),
         ("max_keypoints", C.c_int32), ("ori_windows", C.c_int32), ("flags", C.c_int32),
+        ("scheme", C.c_int32), ("tau_max", C.c_double),
     ]
 
 
@@ -117,8 +119,11 @@ def lib():
     L.kaze_last_error.argtypes = [_vp]
     L.kaze_last_error.restype = C.c_char_p
     L.kaze_abi_version.restype = C.c_int32
+    L.kaze_fed_cycle.argtypes = [C.c_double, C.c_double, _vp, C.c_int32]
+    L.kaze_fed_cycle.restype = C.c_int32
     for name in EXPORTED_SYMBOLS:
-        if name not in ("kaze_launch_count", "kaze_status_string", "kaze_last_error", "kaze_abi_version"):
+        if name not in ("kaze_launch_count", "kaze_status_string", "kaze_last_error", "kaze_abi_version",
+                        "kaze_fed_cycle"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -238,6 +243,16 @@ def kaze_launch_count(ctx: int) -> int:
 
 def kaze_abi_version() -> int:
     return int(lib().kaze_abi_version())
+
+
+def kaze_fed_cycle(T: float, tau_max: float = 0.25) -> np.ndarray:
+    """Host-only: the FED cycle's step sizes in execution order for a level transition of total time T."""
+    n = int(lib().kaze_fed_cycle(T, tau_max, None, 0))
+    if n <= 0:
+        raise KazeError(n, "kaze_fed_cycle")
+    out = np.zeros(n, np.float32)
+    lib().kaze_fed_cycle(T, tau_max, out.ctypes.data, n)
+    return out
 
 
 # ---- convenience wrapper ---------------------------------------------------------------------------------------

@@ -173,14 +173,6 @@ __device__ __forceinline__ void eliminate_full(Chunk<M + 1>& ch, const float (&d
     ch.D = fmaf(tq[1], nd, dv[0]) * rB;
 }
 
-// Chunking of a line of n samples into chunks of M: T chunks, chunk p = [p*M, p*M + size), the last one takes the
-// remainder; a remainder of 1 is merged into the previous chunk (so 2 <= size <= M+1).
-__host__ __device__ inline int n_chunks(int n, int M) {
-    int T = (n + M - 1) / M;
-    if (T > 1 && n - (T - 1) * M == 1) --T;
-    return T;
-}
-
 // -------------------------------------------------------------------------------------------------------------
 // Column systems (first pass: U = column solves).  Thread (cx, p): column x0 + cx, chunk p of T; blockDim.x =
 // CW * TP, shared index p*CW + cx.  A warp covers CW adjacent columns x 32/CW chunks (whole 32-byte sectors).

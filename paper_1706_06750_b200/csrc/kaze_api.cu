@@ -3,6 +3,7 @@
 //
 // Host-side arithmetic kept here (schedule, Gaussian taps, τ_i) is this product's own; it shares nothing with
 // oracle/ (DESIGN.md §2).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -29,11 +30,12 @@ enum KernelClass {
     KC_KP_SCAN,
     KC_KP_EMIT,
     KC_DESCRIBE,
+    KC_FED,
     KC_COUNT
 };
 const char* kKernelNames[KC_COUNT] = {"prefilter", "grad_l1",  "k_hist",   "k_final",  "c_from_g2",
                                       "cond",      "aos_cols", "aos_rows", "hessian",
-                                      "nms_mark",  "kp_scan",  "kp_emit",  "describe"};
+                                      "nms_mark",  "kp_scan",  "kp_emit",  "describe", "fed"};
 
 struct ProfRec {
     int kc;
@@ -53,6 +55,7 @@ struct kaze_ctx {
     int step[kMaxLevels];
     GaussTaps g0{}, g1{};
     LevelTable lt{};
+    std::vector<std::vector<float>> fed;  // scheme FED: level i's cycle step sizes in execution order (A20, A21)
     // arena
     int Pmax = 0;
     size_t plane_max = 0;
@@ -177,6 +180,62 @@ GaussTaps make_taps(double sigma) {
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+// One FED cycle of total time T (Eq. 5; A20, A21), as the product computes it:
+//  * n = the smallest integer with τ_max·n(n+1)/3 >= T (the sum of Eq. 5's n steps is τ_max·n(n+1)/3);
+//  * τ_j = q·τ_max / (2cos²(π(2j+1)/(4n+2))), j = 0..n−1, with q = T / (τ_max·n(n+1)/3) so the cycle ends at T;
+//  * execution order j_m = (κ·m) mod n, κ coprime to n, minimising max_m max_μ|Π_{l<=m}(1 − τ_{j_l}μ)| ·
+//    max_μ|Π_{l>m}(1 − τ_{j_l}μ)| over μ on 1025 points of [0, 8] (the spectrum of the 5-point operator with
+//    c <= 1); ties → the smallest κ.  In fp32 the natural (increasing) order amplifies rounding by ~1e12 at
+//    n = 29; this order keeps the cycle at the rounding level of a single step.
+std::vector<float> fed_cycle(double T, double tau_max) {
+    int n = 1;
+    while (tau_max * n * (n + 1) / 3.0 < T) ++n;
+    const double q = T / (tau_max * n * (n + 1) / 3.0);
+    std::vector<double> tau(n);
+    for (int j = 0; j < n; ++j) {
+        const double cj = std::cos(M_PI * (2.0 * j + 1.0) / (4.0 * n + 2.0));
+        tau[j] = q * tau_max / (2.0 * cj * cj);
+    }
+    auto gcd = [](int a, int b) {
+        while (b) {
+            const int r = a % b;
+            a = b;
+            b = r;
+        }
+        return a;
+    };
+    constexpr int kMu = 1025;
+    int best = 1;
+    double best_g = INFINITY;
+    std::vector<double> fwd(n), bwd(n + 1);
+    for (int kap = 1; kap < std::max(n, 2); ++kap) {
+        if (gcd(kap, n) != 1) continue;
+        std::fill(fwd.begin(), fwd.end(), 0.0);
+        std::fill(bwd.begin(), bwd.end(), 0.0);
+        bwd[n] = 1.0;
+        for (int u = 0; u < kMu; ++u) {
+            const double mu = 8.0 * u / (kMu - 1);
+            double pf = 1.0, pb = 1.0;
+            for (int m = 0; m < n; ++m) {
+                pf *= 1.0 - tau[(size_t)((long)kap * m % n)] * mu;
+                fwd[m] = std::max(fwd[m], std::fabs(pf));
+                const int mb = n - 1 - m;
+                pb *= 1.0 - tau[(size_t)((long)kap * mb % n)] * mu;
+                bwd[mb] = std::max(bwd[mb], std::fabs(pb));
+            }
+        }
+        double gk = 0.0;
+        for (int m = 0; m < n; ++m) gk = std::max(gk, fwd[m] * bwd[m + 1]);
+        if (gk < best_g) {
+            best_g = gk;
+            best = kap;
+        }
+    }
+    std::vector<float> out(n);
+    for (int m = 0; m < n; ++m) out[m] = (float)tau[(size_t)((long)best * m % n)];
+    return out;
+}
+
 kaze_status validate_params(const kaze_params* p) {
     if (!p) return KAZE_ERR_INVALID_ARGUMENT;
     if (p->octaves < 1 || p->sublevels < 1 || p->octaves * p->sublevels > kMaxLevels) return KAZE_ERR_INVALID_ARGUMENT;
@@ -190,6 +249,8 @@ kaze_status validate_params(const kaze_params* p) {
     if (p->max_batch < 1 || p->max_batch > kMaxBatch) return KAZE_ERR_INVALID_ARGUMENT;
     if (p->max_width < 32 || p->max_height < 32) return KAZE_ERR_IMAGE_TOO_SMALL;
     if (p->max_width > 8192 || p->max_height > 8192) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->scheme != KAZE_SCHEME_AOS && p->scheme != KAZE_SCHEME_FED) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->scheme == KAZE_SCHEME_FED && !(p->tau_max > 0 && p->tau_max <= 0.25)) return KAZE_ERR_INVALID_ARGUMENT;
     return KAZE_OK;
 }
 
@@ -266,6 +327,27 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
             launch_cond(prev, SL, c->cbuf, SP, g, n, c->g1, 1, c->p.diffusivity, c->kval, nullptr, s);
         }
         KZ_CHECK_LAUNCH(c, "cond");
+        if (c->p.scheme == KAZE_SCHEME_FED) {  // one FED cycle, K <= kFedMaxK steps per launch (A20, A21)
+            const std::vector<float>& taus = c->fed[i];
+            const int ns = (int)taus.size(), nl = (ns + kFedMaxK - 1) / kFedMaxK;
+            int done = 0;
+            for (int j = 0; j < nl; ++j) {
+                const int k = (ns - done + (nl - j) - 1) / (nl - j);
+                FedTaus ft{};
+                for (int q = 0; q < k; ++q) ft.t[q] = taus[done + q];
+                // ping-pong so that the last launch writes L_i: launch j writes cur iff nl-1-j is even
+                float* dst = ((nl - 1 - j) % 2 == 0) ? cur : c->ubuf;
+                const float* src = j == 0 ? prev : (((nl - j) % 2 == 0) ? cur : c->ubuf);
+                const size_t s_src = j == 0 ? SL : (src == cur ? SL : SP), s_dst = dst == cur ? SL : SP;
+                {
+                    Launch L(c, KC_FED, 12.0 * px, s);
+                    launch_fed_steps(src, s_src, c->cbuf, SP, dst, s_dst, g, n, ft, k, s);
+                }
+                KZ_CHECK_LAUNCH(c, "fed");
+                done += k;
+            }
+            continue;
+        }
         const float tau = (float)(c->t[i] - c->t[i - 1]);
         {   // U = column solves (ubuf holds U)
             Launch L(c, KC_AOS_COLS, 12.0 * px, s);
@@ -417,6 +499,8 @@ kaze_status kaze_default_params(kaze_params* p) {
     p->max_keypoints = 65536;
     p->ori_windows = 42;
     p->flags = 0;
+    p->scheme = KAZE_SCHEME_AOS;
+    p->tau_max = 0.25;
     return KAZE_OK;
 }
 
@@ -445,6 +529,10 @@ kaze_status kaze_create(const kaze_params* p, int device, kaze_ctx** out) {
             c->lt.step[i] = c->step[i];
             c->lt.sigma[i] = (float)c->sigma[i];
         }
+    if (p->scheme == KAZE_SCHEME_FED) {
+        c->fed.resize(c->N);
+        for (int i = 1; i < c->N; ++i) c->fed[i] = fed_cycle(c->t[i] - c->t[i - 1], p->tau_max);
+    }
     c->lt.n = c->N;
     c->lt.S = p->sublevels;
     c->g0 = make_taps(p->sigma0);
@@ -719,6 +807,13 @@ kaze_status kaze_get_profile(kaze_ctx* c, kaze_kernel_stat* out, int32_t cap, in
 }
 
 int64_t kaze_launch_count(const kaze_ctx* c) { return c ? c->launches : 0; }
+
+int32_t kaze_fed_cycle(double T, double tau_max, float* taus, int32_t cap) {
+    if (!(T > 0) || !(tau_max > 0 && tau_max <= 0.25) || cap < 0 || (cap > 0 && !taus)) return KAZE_ERR_INVALID_ARGUMENT;
+    const std::vector<float> t = fed_cycle(T, tau_max);
+    for (int32_t j = 0; j < cap && j < (int32_t)t.size(); ++j) taus[j] = t[j];
+    return (int32_t)t.size();
+}
 
 
 const char* kaze_status_string(kaze_status s) {

@@ -57,6 +57,15 @@ bool launch_aos_cols(const float* L, const float* c, float* U, Strides st, Geom 
 bool launch_aos_rows(const float* L, const float* c, const float* U, float* Lout, Strides st, Geom g, int nimg,
                      float tau, cudaStream_t s);
 
+// ---- fed.cu ----  (scheme KAZE_SCHEME_FED, A20/A21)
+constexpr int kFedMaxK = 8;  // explicit steps per temporally blocked launch
+struct FedTaus {
+    float t[kFedMaxK];
+};
+// Lout = nsteps (1..kFedMaxK) explicit steps L += τ_j div(c ∇L) applied to Lin in order t[0..nsteps). Lin != Lout.
+bool launch_fed_steps(const float* Lin, size_t s_in, const float* c, size_t s_c, float* Lout, size_t s_out, Geom g,
+                      int nimg, const FedTaus& t, int nsteps, cudaStream_t s);
+
 // ---- hessian.cu ----  (all N levels of nimg images in one launch; level stride = plane)
 // Lxy: interleaved (s·∂x L, s·∂y L) float2 planes, same element strides as the float pyramids.
 void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, int nimg, const LevelTable& lt,

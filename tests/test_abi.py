@@ -49,7 +49,8 @@ def test_struct_layouts_match_c(K, tmp_path):
         '#include <stdio.h>\n#include <stddef.h>\n#include "kaze.h"\n'
         "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(kaze_params), sizeof(kaze_keypoint),"
         " sizeof(kaze_kernel_stat), offsetof(kaze_params, sigma0), offsetof(kaze_params, max_keypoints),"
-        " offsetof(kaze_keypoint, level), offsetof(kaze_keypoint, flags)); return 0;}\n"
+        " offsetof(kaze_keypoint, level), offsetof(kaze_keypoint, flags)); printf(\"%zu\\n\", offsetof(kaze_params, tau_max));"
+        " return 0;}\n"
     )
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)], check=True)
@@ -57,7 +58,7 @@ def test_struct_layouts_match_c(K, tmp_path):
     assert vals == [
         C.sizeof(K.KazeParams), C.sizeof(K.KazeKeypoint), C.sizeof(K.KazeKernelStat),
         K.KazeParams.sigma0.offset, K.KazeParams.max_keypoints.offset,
-        K.KazeKeypoint.level.offset, K.KazeKeypoint.flags.offset,
+        K.KazeKeypoint.level.offset, K.KazeKeypoint.flags.offset, K.KazeParams.tau_max.offset,
     ]
     assert vals[1] == 32
 
@@ -69,7 +70,8 @@ def test_defaults_and_status_strings(K):
     lib = K.lib()
     for st in (0, -1, -2, -3, -4, -5, -6):
         assert lib.kaze_status_string(st)
-    assert K.kaze_abi_version() == 1
+    assert K.kaze_abi_version() == 2
+    assert (p.scheme, p.tau_max) == (K.SCHEME_AOS, 0.25)
 
 
 @pytest.mark.parametrize(
@@ -78,7 +80,8 @@ def test_defaults_and_status_strings(K):
         ({"octaves": 0}, -1), ({"sublevels": 0}, -1), ({"sigma0": 0.0}, -1), ({"sigma0": -1.0}, -1),
         ({"k_percentile": 0.0}, -1), ({"k_percentile": 1.0}, -1), ({"k_bins": 0}, -1), ({"diffusivity": 3}, -1),
         ({"threshold": -1.0}, -1), ({"max_keypoints": 0}, -1), ({"ori_windows": 65}, -1), ({"max_batch": 0}, -1),
-        ({"max_width": 31}, -2), ({"max_height": 16}, -2),
+        ({"max_width": 31}, -2), ({"max_height": 16}, -2), ({"scheme": 2}, -1),
+        ({"scheme": 1, "tau_max": 0.3}, -1), ({"scheme": 1, "tau_max": 0.0}, -1),
     ],
 )
 def test_create_rejects_invalid_parameters_before_touching_a_device(K, override, status):
@@ -113,3 +116,23 @@ def test_product_never_routes_through_the_oracle():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert "import paper_1706_06750_b200" not in txt and "from paper_1706_06750_b200" not in txt
             assert '#include "kaze.h"' not in txt and "include/kaze.h" not in txt and "libkaze_b200" not in txt
+
+
+def test_fed_cycle_host_schedule_matches_the_oracle(K, oracle_lib):
+    """The product's FED cycle (host code inside libkaze_b200.so) against the pinned oracle (P22, A20, A21): the
+    same n, the same step sizes (fp32 rounding) and the same κ execution order, for every level transition of the
+    KAZE schedule and a few other totals."""
+    import numpy as np
+
+    O = oracle_lib
+    _, t, _ = O.schedule(4, 4, 1.6)
+    totals = list(np.diff(t)) + [0.01, 0.25, 1.0, 3.3, 100.0]
+    for T in totals:
+        ref = O.fed_cycle(T)
+        order = O.fed_order(ref)
+        got = K.kaze_fed_cycle(T)
+        assert len(got) == len(ref)
+        np.testing.assert_allclose(got, ref[order], rtol=2e-7)
+        assert abs(float(np.sum(got.astype(np.float64))) / T - 1) < 1e-6
+    assert K.lib().kaze_fed_cycle(-1.0, 0.25, None, 0) == -1
+    assert K.lib().kaze_fed_cycle(1.0, 0.5, None, 0) == -1

@@ -372,3 +372,51 @@ def test_aos_step_4096_stage_isolated(O, level):
         K.kaze_get_level(kz.ctx, 0, 0, K.PLANE_COND, cg)
         assert np.max(np.abs(cg.cpu().numpy() - c)) < 2e-5
     kz.close()
+
+
+# ------------------------------------------------------------------------------------------- FED backend (§8 f1)
+@pytest.mark.parametrize("w,h,O_,S_", [(640, 480, 4, 4), (128, 128, 2, 2), (333, 257, 3, 4), (64, 48, 2, 3)])
+def test_fed_scale_space_levels_with_injected_k(O, w, h, O_, S_):
+    """scheme = FED (Eq. 5, A20/A21): every level within 1e-4 relative of the oracle's fp64 FED cycles (k injected);
+    each cycle conserves the image mean (Neumann faces)."""
+    img, ref = oracle_run(O, w, h, octaves=O_, sublevels=S_, scheme=1)
+    kz = make(w, h, octaves=O_, sublevels=S_, k_override=ref["k"], scheme=K.SCHEME_FED)
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    lv = gpu_levels(kz, O_ * S_)
+    for i in range(O_ * S_):
+        assert rel_err(lv[i], ref["levels"][i]) <= 1e-4, (i, rel_err(lv[i], ref["levels"][i]))
+    for i in range(1, O_ * S_):
+        assert abs(lv[i].mean() / lv[i - 1].mean() - 1) < 1e-5
+    kz.close()
+
+
+def test_fed_keypoints_and_descriptors_end_to_end(O):
+    img, ref = oracle_run(O, 640, 480, scheme=1)
+    kz = make(640, 480, scheme=K.SCHEME_FED)
+    kps, counts, desc = kz.extract(torch.from_numpy(img).cuda()[None])
+    got = K.Kaze.keypoints_numpy(kps, counts)[0]
+    assert ref["count"] > 0
+    f1, idx = match_keypoints(ref["kps"], got)
+    f2, _ = match_keypoints(got, ref["kps"])
+    assert f1 >= 0.99 and f2 >= 0.99, (f1, f2, ref["count"], int(counts[0]))
+    d = desc[0, : len(got)].cpu().numpy().astype(np.float64)
+    m = idx >= 0
+    a, b = ref["desc"][m], d[idx[m]]
+    cos = np.sum(a * b, 1) / (np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1) + 1e-30)
+    assert np.mean(cos >= 0.999) >= 0.99, np.mean(cos >= 0.999)
+    kz.close()
+
+
+def test_fed_constant_image_is_identity_and_batch_matches_single():
+    kz = make(96, 80, batch=2, scheme=K.SCHEME_FED, k_override=0.05)
+    img = torch.full((1, 80, 96), 0.25, device="cuda")
+    K.kaze_build_scale_space(kz.ctx, img)
+    assert np.allclose(gpu_levels(kz, 16), 0.25, atol=1e-6)
+    imgs = torch.from_numpy(np.stack([kaze_inputs.synth_image(96, 80, s) for s in (3, 4)])).cuda()
+    K.kaze_build_scale_space(kz.ctx, imgs)
+    both = [gpu_levels(kz, 16, img=i) for i in range(2)]
+    single = make(96, 80, batch=1, scheme=K.SCHEME_FED, k_override=0.05)
+    K.kaze_build_scale_space(single.ctx, imgs[1:2])
+    assert np.array_equal(gpu_levels(single, 16), both[1])
+    kz.close()
+    single.close()
