@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--distinct", type=int, default=8, help="distinct generated images (the rest are shifts/flips)")
+    ap.add_argument("--scheme", default="aos", choices=["aos", "fed"],
+                    help="scale-space solver: AOS (Eq. 4, the north star) or FED cycles (Eq. 5, SURVEY 8 f1)")
     return ap.parse_args()
 
 
@@ -190,7 +192,8 @@ def main():
     host = make_inputs(n_local, first, args.distinct)  # untimed staging
     imgs = torch.from_numpy(host).to(dev)
     B = min(args.batch, max(1, n_local))
-    kz = K.Kaze(W_IMG, H_IMG, batch=B, device=local_rank, max_keypoints=args.max_keypoints)
+    scheme = K.SCHEME_FED if args.scheme == "fed" else K.SCHEME_AOS
+    kz = K.Kaze(W_IMG, H_IMG, batch=B, device=local_rank, max_keypoints=args.max_keypoints, scheme=scheme)
     kps, counts, desc = kz.alloc_outputs(n_local)
     stream = torch.cuda.current_stream(dev)
 
@@ -291,7 +294,8 @@ def main():
             "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": "configs[4]: batch of 256 synthetic 1920x1200 images sharded over the GPUs, "
-                                   "full path (AOS scale space, Hessian detector, orientation, 64-D M-SURF)",
+                                   f"full path ({args.scheme.upper()} scale space, Hessian detector, orientation, "
+                                   "64-D M-SURF)", "scheme": args.scheme,
                        "images": args.images, "width": W_IMG, "height": H_IMG, "octaves": 4, "sublevels": 4,
                        "max_batch": B, "max_keypoints": args.max_keypoints, "parallelism": f"dp{ws}",
                        "l2": "inputs (%.2f GB) larger than L2; no flush" % (args.images * H_IMG * W_IMG * 4 / 1e9),
