@@ -6,7 +6,7 @@
 // which equals s⁴(LxxLyy − Lxy²) with per-pixel derivatives (the factor s per derivative order is absorbed in
 // N).  Second derivatives read the MATERIALISED first derivatives at clamped coordinates (A10), so they are two
 // passes: hess_first (L → Lx, Ly) and hess_det (Lx, Ly → Ldet).  One launch covers every level of every image
-// (blockIdx.y packs (level, row-tile)); the per-level step s_i comes from the LevelTable.  (A fused shared-memory
+// (blockIdx.y packs (level, chain block), see ChainTable); the per-level step s_i comes from the LevelTable.  (A fused shared-memory
 // tile form moving 16 instead of 24 B/px measured slower on B200 at every step: 80-87 µs vs 59 µs per level and
 // 4 images — the (T+4s)² halo recomputation costs more than the 8 B/px it saves.)
 #include "kaze_internal.cuh"
@@ -17,51 +17,6 @@ namespace {
 
 constexpr float kW0 = 0.1875f, kW1 = 0.625f;  // (3, 10, 3) / 16
 
-// Two-pass form, one launch per pass for ALL levels (blockIdx.y packs (level, 32-row tile)).  A thread computes
-// four outputs (rows ty, ty+8, ty+16, ty+24 of a 32x32 tile); the eight ring taps at distance s are fixed 32-bit
-// offsets from the output address, so interior tiles issue plain loads with no clamping or 64-bit index math.
-__global__ void __launch_bounds__(256) k_hess_first(const float* __restrict__ Lt, float2* __restrict__ Lxy,
-                                                    size_t img_stride, Geom g, LevelTable lt, int tiles_y) {
-    const int level = blockIdx.y / tiles_y, ty_t = blockIdx.y - level * tiles_y;
-    const int s = lt.step[level];
-    const int x = blockIdx.x * 32 + threadIdx.x, yb = ty_t * 32 + threadIdx.y;
-    const size_t base = blockIdx.z * img_stride + (size_t)level * g.plane;
-    const float* L = Lt + base;
-    float2* D = Lxy + base;
-    const bool interior = (blockIdx.x * 32 >= s) && (blockIdx.x * 32 + 32 + s <= g.W) && (ty_t * 32 >= s) &&
-                          (ty_t * 32 + 32 + s <= g.H);
-    if (interior) {
-        const int P = g.P, sp = s * P;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int y = yb + 8 * k;
-            const float* q = L + (size_t)y * P + x;
-            const float a = __ldg(q - sp - s), b = __ldg(q - sp), c = __ldg(q - sp + s);
-            const float d = __ldg(q - s), f = __ldg(q + s);
-            const float h = __ldg(q + sp - s), i = __ldg(q + sp), j = __ldg(q + sp + s);
-            D[(size_t)y * P + x] = make_float2(0.5f * (kW0 * (c - a) + kW1 * (f - d) + kW0 * (j - h)),
-                                               0.5f * (kW0 * (h - a) + kW1 * (i - b) + kW0 * (j - c)));
-        }
-        return;
-    }
-    if (x >= g.W) return;
-    const int xm = max(x - s, 0), xp = min(x + s, g.W - 1);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int y = yb + 8 * k;
-        if (y >= g.H) break;
-        const int ym = max(y - s, 0), yp = min(y + s, g.H - 1);
-        const float* rm = L + (size_t)ym * g.P;
-        const float* r0 = L + (size_t)y * g.P;
-        const float* rp = L + (size_t)yp * g.P;
-        const float a = __ldg(rm + xm), b = __ldg(rm + x), c = __ldg(rm + xp);
-        const float d = __ldg(r0 + xm), f = __ldg(r0 + xp);
-        const float h = __ldg(rp + xm), i = __ldg(rp + x), j = __ldg(rp + xp);
-        D[(size_t)y * g.P + x] = make_float2(0.5f * (kW0 * (c - a) + kW1 * (f - d) + kW0 * (j - h)),
-                                             0.5f * (kW0 * (h - a) + kW1 * (i - b) + kW0 * (j - c)));
-    }
-}
-
 __device__ __forceinline__ float det_from_ring(float2 a, float2 b, float2 c, float2 d, float2 f, float2 h, float2 i,
                                                float2 j) {
     const float lxx = 0.5f * (kW0 * (c.x - a.x) + kW1 * (f.x - d.x) + kW0 * (j.x - h.x));  // N_x(Lx)
@@ -70,38 +25,97 @@ __device__ __forceinline__ float det_from_ring(float2 a, float2 b, float2 c, flo
     return lxx * lyy - lxy * lxy;
 }
 
-__global__ void __launch_bounds__(256) k_hess_det(const float2* __restrict__ Lxy, float* __restrict__ Ldet,
-                                                  size_t img_stride, Geom g, LevelTable lt, int tiles_y) {
-    const int level = blockIdx.y / tiles_y, ty_t = blockIdx.y - level * tiles_y;
+// Chain form: a thread computes R outputs of one column at rows y_j = y_0 + j·s (j < R) — a "chain" in the row
+// residue class of y_0 mod s.  Output j reads rows y_j − s, y_j, y_j + s = chain rows j−1, j, j+1, so the R outputs
+// need (R + 2) rows × 3 taps instead of 8R taps: 44% fewer L1 wavefronts at R = 4, 61% at R = 8.  Chains tile the
+// rows band by band: band b = [b·R·s, (b+1)·R·s) holds the s chains y_0 = b·R·s + r, r < s.  Every tap is read at
+// clamped coordinates (A10/A16); the clamp of row y_j ± s equals the clamp of the neighbouring chain row.
+constexpr int kChainR = 8;  // measured at 1920x1200 (256-image step): R = 8 51.3 ms, 12 53.0, 4 61.1, 32x32 tiles 59.2
+
+struct ChainTable {
+    int blk0[kMaxLevels + 1];  // first blockIdx.y of each level
+    int nch[kMaxLevels];       // chains of each level
+};
+
+__device__ __forceinline__ int find_level(const ChainTable& ct, int n, int by) {
+    int l = 0;
+    while (l + 1 < n && by >= ct.blk0[l + 1]) ++l;
+    return l;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_hess_first_chain(const float* __restrict__ Lt, float2* __restrict__ Lxy,
+                                                          size_t img_stride, Geom g, LevelTable lt, ChainTable ct) {
+    const int level = find_level(ct, lt.n, blockIdx.y);
     const int s = lt.step[level];
-    const int x = blockIdx.x * 32 + threadIdx.x, yb = ty_t * 32 + threadIdx.y;
+    const int ch = (blockIdx.y - ct.blk0[level]) * 8 + threadIdx.y;
+    const int x = blockIdx.x * 32 + threadIdx.x;
+    if (ch >= ct.nch[level] || x >= g.W) return;
+    const int b = ch / s, y0 = b * R * s + (ch - b * s);
+    const size_t base = blockIdx.z * img_stride + (size_t)level * g.plane;
+    const float* L = Lt + base;
+    float2* D = Lxy + base;
+    const int xm = max(x - s, 0), xp = min(x + s, g.W - 1);
+    float a[R + 2], m[R + 2], c[R + 2];  // columns x−s, x, x+s of chain rows −1..R
+#pragma unroll
+    for (int k = 0; k < R + 2; ++k) {
+        const int ro = clampi(y0 + (k - 1) * s, 0, g.H - 1) * g.P;
+        a[k] = __ldg(L + ro + xm);
+        m[k] = __ldg(L + ro + x);
+        c[k] = __ldg(L + ro + xp);
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int y = y0 + j * s;
+        if (y < g.H)
+            D[y * g.P + x] = make_float2(0.5f * (kW0 * (c[j] - a[j]) + kW1 * (c[j + 1] - a[j + 1]) + kW0 * (c[j + 2] - a[j + 2])),
+                                         0.5f * (kW0 * (a[j + 2] - a[j]) + kW1 * (m[j + 2] - m[j]) + kW0 * (c[j + 2] - c[j])));
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict__ Lxy, float* __restrict__ Ldet,
+                                                        size_t img_stride, Geom g, LevelTable lt, ChainTable ct) {
+    const int level = find_level(ct, lt.n, blockIdx.y);
+    const int s = lt.step[level];
+    const int ch = (blockIdx.y - ct.blk0[level]) * 8 + threadIdx.y;
+    const int x = blockIdx.x * 32 + threadIdx.x;
+    if (ch >= ct.nch[level] || x >= g.W) return;
+    const int b = ch / s, y0 = b * R * s + (ch - b * s);
     const size_t base = blockIdx.z * img_stride + (size_t)level * g.plane;
     const float2* D = Lxy + base;
     float* O = Ldet + base;
-    const bool interior = (blockIdx.x * 32 >= s) && (blockIdx.x * 32 + 32 + s <= g.W) && (ty_t * 32 >= s) &&
-                          (ty_t * 32 + 32 + s <= g.H);
-    if (interior) {
-        const int P = g.P, sp = s * P;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int y = yb + 8 * k;
-            const float2* q = D + (size_t)y * P + x;
-            O[(size_t)y * P + x] = det_from_ring(__ldg(q - sp - s), __ldg(q - sp), __ldg(q - sp + s), __ldg(q - s),
-                                                 __ldg(q + s), __ldg(q + sp - s), __ldg(q + sp), __ldg(q + sp + s));
-        }
-        return;
-    }
-    if (x >= g.W) return;
     const int xm = max(x - s, 0), xp = min(x + s, g.W - 1);
+    float2 a[R + 2], m[R + 2], c[R + 2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int y = yb + 8 * k;
-        if (y >= g.H) break;
-        const int ym = max(y - s, 0), yp = min(y + s, g.H - 1);
-        const size_t om = (size_t)ym * g.P, o0 = (size_t)y * g.P, op = (size_t)yp * g.P;
-        O[o0 + x] = det_from_ring(__ldg(D + om + xm), __ldg(D + om + x), __ldg(D + om + xp), __ldg(D + o0 + xm),
-                                  __ldg(D + o0 + xp), __ldg(D + op + xm), __ldg(D + op + x), __ldg(D + op + xp));
+    for (int k = 0; k < R + 2; ++k) {
+        const int ro = clampi(y0 + (k - 1) * s, 0, g.H - 1) * g.P;
+        a[k] = __ldg(D + ro + xm);
+        m[k] = __ldg(D + ro + x);
+        c[k] = __ldg(D + ro + xp);
     }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int y = y0 + j * s;
+        if (y < g.H)
+            O[y * g.P + x] = det_from_ring(a[j], m[j], c[j], a[j + 1], c[j + 1], a[j + 2], m[j + 2], c[j + 2]);
+    }
+}
+
+template <int R>
+ChainTable make_chains(Geom g, const LevelTable& lt, int* total_blocks) {
+    ChainTable ct{};
+    int blk = 0;
+    for (int l = 0; l < lt.n; ++l) {
+        const int s = lt.step[l];
+        const int bands = (g.H + R * s - 1) / (R * s);
+        ct.nch[l] = bands * s;
+        ct.blk0[l] = blk;
+        blk += (ct.nch[l] + 7) / 8;
+    }
+    ct.blk0[lt.n] = blk;
+    *total_blocks = blk;
+    return ct;
 }
 
 __global__ void k_component_copy(float2* __restrict__ plane, int comp, float* __restrict__ tight, int to_tight,
@@ -117,16 +131,16 @@ __global__ void k_component_copy(float2* __restrict__ plane, int comp, float* __
 
 void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                        cudaStream_t s) {
-    int ty = (g.H + 31) / 32;
-    dim3 grid((g.W + 31) / 32, ty * lt.n, nimg);
-    k_hess_first<<<grid, dim3(32, 8), 0, s>>>(Lt, Lxy, img_stride, g, lt, ty);
+    int nb = 0;
+    const ChainTable ct = make_chains<kChainR>(g, lt, &nb);
+    k_hess_first_chain<kChainR><<<dim3((g.W + 31) / 32, nb, nimg), dim3(32, 8), 0, s>>>(Lt, Lxy, img_stride, g, lt, ct);
 }
 
 void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                      cudaStream_t s) {
-    int ty = (g.H + 31) / 32;
-    dim3 grid((g.W + 31) / 32, ty * lt.n, nimg);
-    k_hess_det<<<grid, dim3(32, 8), 0, s>>>(Lxy, Ldet, img_stride, g, lt, ty);
+    int nb = 0;
+    const ChainTable ct = make_chains<kChainR>(g, lt, &nb);
+    k_hess_det_chain<kChainR><<<dim3((g.W + 31) / 32, nb, nimg), dim3(32, 8), 0, s>>>(Lxy, Ldet, img_stride, g, lt, ct);
 }
 
 void launch_component_copy(float2* plane, int comp, float* tight, int to_tight, Geom g, cudaStream_t s) {
