@@ -62,99 +62,95 @@ __device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const 
     return refine(patch, er, ox, oy);
 }
 
-// nms_mark: one WARP per (32-column strip, NSEG-row segment, level, image), streaming down the rows.  Lane l owns
-// column x0+l and keeps, for each of the levels i-1, i, i+1, the last three rows of its column in registers (lanes 0
-// and 31 also keep the halo columns x0-1 / x0+32).  The 26-neighbour maximum is
-//   max(vmax_{i-1}, vmax_{i+1} over columns x-1..x+1;  vmax_i over x-1, x+1;  D_i(x, y±1))
-// with vmax = vertical 3-maximum, the column neighbours coming from shuffles: ~30 instructions per pixel, 3
-// coalesced loads per pixel, no shared memory, no barriers.  Only candidates run the edge test / sub-pixel fit.
-// The warp writes the row's 32-bit candidate word; row counts come from k_rowcount.
-constexpr int NSEG = 64;
+// nms_mark: one WARP per (strip, NSEG-row segment, block of LB centre levels, image), streaming down the rows.
+// A strip is 32 lanes over columns x0−1 .. x0+30 (x0 = 30·strip): lanes 1..30 decide columns x0 .. x0+29 and the
+// edge lanes only supply neighbours, so no halo logic is needed and the bitmap word of a strip holds 30 bits
+// (bit b ↔ column 30·strip + b).  The warp keeps the last three rows of its column for LB + 2 consecutive levels
+// in registers, so each Ldet value is loaded once per block of LB centres (1.29 loads per pixel-level at LB = 7,
+// not 3).  Per plane and row: vertical 3-max vm, two shuffles → the 3x3 max M; for a centre level also the
+// 8-neighbour max N8 = max(vm_left, vm_right, up, down).  Keep iff v > thr, v > N8_i, v > M_{i−1}, v > M_{i+1}
+// (strict, A11); only candidates run the edge test / sub-pixel fit.  The row loop is unrolled by three so the
+// row window rotates by renaming, not by moves.
+constexpr int NSEG = 63;   // rows per warp (multiple of 3)
+constexpr int NMS_LB = 7;  // centre levels per warp (16 levels → two blocks of 7)
+constexpr int STRIP = 30;  // output columns per strip
 
-__global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
-                                                  DetectParams dp, uint32_t* __restrict__ bitmap) {
-    const int lane = threadIdx.x & 31;
-    const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int words = (g.W + 31) / 32;
-    if (strip >= words) return;  // warp-uniform
-    const int x0 = strip * 32, x = x0 + lane;
-    const int y0 = blockIdx.y * NSEG;
-    const int li = blockIdx.z % (N - 2), img = blockIdx.z / (N - 2), level = li + 1;
-    const int W = g.W, H = g.H;
-    const float* D1 = Ldet + img * img_stride + (size_t)level * g.plane;
-    const float* D0 = D1 - g.plane;
-    const float* D2 = D1 + g.plane;
-    const int xc = min(x, W - 1);
-    const bool halo = lane == 0 || lane == 31;
-    const int xh = lane == 0 ? max(x0 - 1, 0) : min(x0 + 32, W - 1);
-    // windows: [0] = row y-1, [1] = y, [2] = y+1 (own column), h* = halo column
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
-    float ha0 = 0.f, ha1 = 0.f, ha2 = 0.f, hb0 = 0.f, hb1 = 0.f, hb2 = 0.f, hc0 = 0.f, hc1 = 0.f, hc2 = 0.f;
-    const int ylast = min(y0 + NSEG, H - 1);  // last row loaded (the row below the last output row)
-    uint32_t* bm = bitmap + (((size_t)img * (N - 2) + li) * H) * words + strip;
-    // software pipeline: the next row's loads are issued before the current row is consumed
-    size_t ro = (size_t)max(y0 - 1, 0) * g.P;
-    float na = __ldg(D0 + ro + xc), nb = __ldg(D1 + ro + xc), nc = __ldg(D2 + ro + xc);
-    float nha = 0.f, nhb = 0.f, nhc = 0.f;
-    if (halo) {
-        nha = __ldg(D0 + ro + xh);
-        nhb = __ldg(D1 + ro + xh);
-        nhc = __ldg(D2 + ro + xh);
+template <int LB, int PH>
+__device__ __forceinline__ void nms_row(float (&w)[LB + 2][3], const float* __restrict__ base, const int (&off)[LB + 2], int P,
+                                        int y, int H, int W, int x, int lane, int nc, const DetectParams& dp,
+                                        uint32_t* __restrict__ bm, size_t lvl_stride, int words) {
+    // load row y+1 (clamped) into slot (PH + 2) % 3; the window then holds rows y-1, y, y+1 in slots PH, PH+1, PH+2
+    const int ro = min(y + 1, H - 1) * P;
+#pragma unroll
+    for (int q = 0; q < LB + 2; ++q) w[q][(PH + 2) % 3] = __ldg(base + (unsigned)(off[q] + ro));
+    float M[LB + 2], N8[LB + 2];
+#pragma unroll
+    for (int q = 0; q < LB + 2; ++q) {
+        const float up = w[q][PH % 3], ce = w[q][(PH + 1) % 3], dn = w[q][(PH + 2) % 3];
+        const float vm = fmaxf(up, fmaxf(ce, dn));
+        const float vl = __shfl_up_sync(0xffffffffu, vm, 1), vr = __shfl_down_sync(0xffffffffu, vm, 1);
+        const float lr = fmaxf(vl, vr);
+        M[q] = fmaxf(vm, lr);
+        N8[q] = fmaxf(lr, fmaxf(up, dn));
     }
-    for (int r = y0 - 1; r <= ylast; ++r) {
-        a0 = a1; a1 = a2; a2 = na;
-        b0 = b1; b1 = b2; b2 = nb;
-        c0 = c1; c1 = c2; c2 = nc;
-        if (halo) {
-            ha0 = ha1; ha1 = ha2; ha2 = nha;
-            hb0 = hb1; hb1 = hb2; hb2 = nhb;
-            hc0 = hc1; hc1 = hc2; hc2 = nhc;
-        }
-        if (r < ylast) {
-            ro = (size_t)(r + 1) * g.P;
-            na = __ldg(D0 + ro + xc);
-            nb = __ldg(D1 + ro + xc);
-            nc = __ldg(D2 + ro + xc);
-            if (halo) {
-                nha = __ldg(D0 + ro + xh);
-                nhb = __ldg(D1 + ro + xh);
-                nhc = __ldg(D2 + ro + xh);
-            }
-        }
-        const int y = r - 1;  // the window now holds rows y-1, y, y+1
-        if (y < y0) continue;
-        const float va = fmaxf(a0, fmaxf(a1, a2)), vc = fmaxf(c0, fmaxf(c1, c2)), vb = fmaxf(b0, fmaxf(b1, b2));
-        float val = __shfl_up_sync(0xffffffffu, va, 1), var = __shfl_down_sync(0xffffffffu, va, 1);
-        float vcl = __shfl_up_sync(0xffffffffu, vc, 1), vcr = __shfl_down_sync(0xffffffffu, vc, 1);
-        float vbl = __shfl_up_sync(0xffffffffu, vb, 1), vbr = __shfl_down_sync(0xffffffffu, vb, 1);
-        if (halo) {
-            const float hva = fmaxf(ha0, fmaxf(ha1, ha2)), hvc = fmaxf(hc0, fmaxf(hc1, hc2));
-            const float hvb = fmaxf(hb0, fmaxf(hb1, hb2));
-            if (lane == 0) { val = hva; vcl = hvc; vbl = hvb; }
-            else { var = hva; vcr = hvc; vbr = hvb; }
-        }
-        float m = fmaxf(fmaxf(val, va), fmaxf(var, vc));
-        m = fmaxf(m, fmaxf(fmaxf(vcl, vcr), fmaxf(vbl, vbr)));
-        m = fmaxf(m, fmaxf(b0, b2));
-        bool k = (x >= 1 && x <= W - 2 && y >= 1 && y <= H - 2) && b1 > dp.threshold && b1 > m;
-        if (__any_sync(0xffffffffu, k)) {  // rare: gather the level-i 3x3 patch and fit
-            float l0 = __shfl_up_sync(0xffffffffu, b0, 1), l1 = __shfl_up_sync(0xffffffffu, b1, 1);
-            float l2 = __shfl_up_sync(0xffffffffu, b2, 1);
-            float q0 = __shfl_down_sync(0xffffffffu, b0, 1), q1 = __shfl_down_sync(0xffffffffu, b1, 1);
-            float q2 = __shfl_down_sync(0xffffffffu, b2, 1);
-            if (lane == 0) { l0 = hb0; l1 = hb1; l2 = hb2; }
-            if (lane == 31) { q0 = hb0; q1 = hb1; q2 = hb2; }
+    const bool inside = lane >= 1 && lane <= STRIP && x >= 1 && x <= W - 2 && y >= 1 && y <= H - 2;
+#pragma unroll
+    for (int c = 1; c <= LB; ++c) {
+        if (c > nc) break;  // warp-uniform
+        const float v = w[c][(PH + 1) % 3];
+        bool k = inside && v > dp.threshold && v > N8[c] && v > M[c - 1] && v > M[c + 1];
+        if (__any_sync(0xffffffffu, k)) {  // rare: the level's 3x3 patch by shuffles, then the fit
+            const float u0 = w[c][PH % 3], u2 = w[c][(PH + 2) % 3];
+            const float l0 = __shfl_up_sync(0xffffffffu, u0, 1), l1 = __shfl_up_sync(0xffffffffu, v, 1);
+            const float l2 = __shfl_up_sync(0xffffffffu, u2, 1);
+            const float r0 = __shfl_down_sync(0xffffffffu, u0, 1), r1 = __shfl_down_sync(0xffffffffu, v, 1);
+            const float r2 = __shfl_down_sync(0xffffffffu, u2, 1);
             if (k) {
-                const float patch[3][3] = {{l0, b0, q0}, {l1, b1, q1}, {l2, b2, q2}};
+                const float patch[3][3] = {{l0, u0, r0}, {l1, v, r1}, {l2, u2, r2}};
                 float ox, oy;
                 k = refine(patch, dp.edge_ratio, ox, oy);
             }
         }
         const uint32_t bits = __ballot_sync(0xffffffffu, k);
-        if (lane == 0 && y < H) bm[(size_t)y * words] = bits;
+        if (lane == 0) bm[(size_t)(c - 1) * lvl_stride + (size_t)y * words] = (bits >> 1) & ((1u << STRIP) - 1u);
     }
-    // the last image row is never a window centre above; it has no candidates (border)
-    if (lane == 0 && y0 + NSEG >= H && H - 1 >= y0) bm[(size_t)(H - 1) * words] = 0u;
+}
+
+template <int LB>
+__global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
+                                                  DetectParams dp, uint32_t* __restrict__ bitmap, int words) {
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (strip >= words) return;  // warp-uniform
+    const int nblk = (N - 2 + LB - 1) / LB;
+    const int blk = blockIdx.z % nblk, img = blockIdx.z / nblk;
+    const int l0 = 1 + blk * LB;             // first centre level
+    const int nc = min(LB, N - 1 - l0);      // centres in this block
+    const int W = g.W, H = g.H;
+    const int x = strip * STRIP - 1 + lane;
+    const int xc = clampi(x, 0, W - 1);
+    const int y0 = blockIdx.y * NSEG;
+    const int yend = min(y0 + NSEG, H);
+    // planes q = 0..LB+1 are levels l0-1+q (clamped to N-1 past the last level; never a used neighbour)
+    const float* base = opaque(Ldet + img * img_stride + (size_t)(l0 - 1) * g.plane + xc);
+    const int qmax = N - l0;  // last valid plane index; planes past it (short last block) re-read the last level
+    int off[LB + 2];
+#pragma unroll
+    for (int q = 0; q < LB + 2; ++q) off[q] = min(q, qmax) * (int)g.plane;
+    const size_t lvl_stride = (size_t)H * words;
+    uint32_t* bm = bitmap + ((size_t)img * (N - 2) + (l0 - 1)) * lvl_stride + strip;
+    float w[LB + 2][3];
+    const int rm = max(y0 - 1, 0) * g.P, r0 = y0 * g.P;
+#pragma unroll
+    for (int q = 0; q < LB + 2; ++q) {
+        w[q][0] = __ldg(base + (unsigned)(off[q] + rm));
+        w[q][1] = __ldg(base + (unsigned)(off[q] + r0));
+    }
+    for (int y = y0; y < yend; y += 3) {
+        nms_row<LB, 0>(w, base, off, g.P, y, H, W, x, lane, nc, dp, bm, lvl_stride, words);
+        if (y + 1 < yend) nms_row<LB, 1>(w, base, off, g.P, y + 1, H, W, x, lane, nc, dp, bm, lvl_stride, words);
+        if (y + 2 < yend) nms_row<LB, 2>(w, base, off, g.P, y + 2, H, W, x, lane, nc, dp, bm, lvl_stride, words);
+    }
 }
 
 // Row candidate counts from the bitmap: one warp per (image, level, row).
@@ -219,7 +215,7 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
     if (rowcnt[q] == 0) return;  // warp-uniform
     const int N = lt.n;
     const int y = q % g.H, rest = q / g.H, li = rest % (N - 2), img = rest / (N - 2), level = li + 1;
-    const int words = (g.W + 31) / 32;
+    const int words = (g.W + STRIP - 1) / STRIP;
     const uint32_t* bm = bitmap + (size_t)q * words;
     const float* D0 = Ldet + img * img_stride + (size_t)level * g.plane;
     int run = rowoff[q];
@@ -237,7 +233,7 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
             const int bit = __ffs(word) - 1;
             word &= word - 1;
             if (rank < dp.cap) {
-                const int x = (w0 + lane) * 32 + bit;
+                const int x = (w0 + lane) * STRIP + bit;
                 float ox = 0.f, oy = 0.f, v = 0.f;
                 is_keypoint(D0 - g.plane, D0, D0 + g.plane, g.P, x, y, dp.threshold, dp.edge_ratio, ox, oy, v);
                 kaze_keypoint kp;
@@ -259,11 +255,14 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
 
 }  // namespace
 
+int nms_words(int W) { return (W + STRIP - 1) / STRIP; }
+
 void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, int N, DetectParams dp, uint32_t* bitmap,
                      int* rowcnt, cudaStream_t s) {
-    const int words = (g.W + 31) / 32;
-    dim3 grid((words + 7) / 8, (g.H + NSEG - 1) / NSEG, nimg * (N - 2));
-    k_nms_mark<<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, bitmap);
+    const int words = nms_words(g.W);
+    const int nblk = (N - 2 + NMS_LB - 1) / NMS_LB;
+    dim3 grid((words + 7) / 8, (g.H + NSEG - 1) / NSEG, nimg * nblk);
+    k_nms_mark<NMS_LB><<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, bitmap, words);
     const int total = g.H * (N - 2) * nimg;
     k_rowcount<<<(total + 7) / 8, 256, 0, s>>>(bitmap, words, total, rowcnt);
 }

@@ -6,7 +6,7 @@
 // which equals s⁴(LxxLyy − Lxy²) with per-pixel derivatives (the factor s per derivative order is absorbed in
 // N).  Second derivatives read the MATERIALISED first derivatives at clamped coordinates (A10), so they are two
 // passes: hess_first (L → Lx, Ly) and hess_det (Lx, Ly → Ldet).  One launch covers every level of every image
-// (blockIdx.y packs (level, chain block), see ChainTable); the per-level step s_i comes from the LevelTable.  (A fused shared-memory
+// (blockIdx.z packs (image, level), blockIdx.y the chain block); the per-level step s_i comes from the LevelTable.  (A fused shared-memory
 // tile form moving 16 instead of 24 B/px measured slower on B200 at every step: 80-87 µs vs 59 µs per level and
 // 4 images — the (T+4s)² halo recomputation costs more than the 8 B/px it saves.)
 #include "kaze_internal.cuh"
@@ -32,90 +32,78 @@ __device__ __forceinline__ float det_from_ring(float2 a, float2 b, float2 c, flo
 // clamped coordinates (A10/A16); the clamp of row y_j ± s equals the clamp of the neighbouring chain row.
 constexpr int kChainR = 8;  // measured at 1920x1200 (256-image step): R = 8 51.3 ms, 12 53.0, 4 61.1, 32x32 tiles 59.2
 
-struct ChainTable {
-    int blk0[kMaxLevels + 1];  // first blockIdx.y of each level
-    int nch[kMaxLevels];       // chains of each level
-};
-
-__device__ __forceinline__ int find_level(const ChainTable& ct, int n, int by) {
-    int l = 0;
-    while (l + 1 < n && by >= ct.blk0[l + 1]) ++l;
-    return l;
-}
+// Chains of one level: s per band, ceil(H / (R·s)) bands.  grid.y covers the largest level; blocks past a level's
+// chain count exit at once.  b = ch / s via a float quotient: (ch + ½)/s stays >= 1/(2s) away from an integer, far
+// beyond the error of __fdividef at these sizes (ch < 2^16, s < 64).
+__device__ __forceinline__ int chain_band(int ch, int s) { return (int)__fdividef((float)ch + 0.5f, (float)s); }
 
 template <int R>
 __global__ void __launch_bounds__(256) k_hess_first_chain(const float* __restrict__ Lt, float2* __restrict__ Lxy,
-                                                          size_t img_stride, Geom g, LevelTable lt, ChainTable ct) {
-    const int level = find_level(ct, lt.n, blockIdx.y);
+                                                          size_t img_stride, Geom g, LevelTable lt) {
+    const int img = chain_band(blockIdx.z, lt.n), level = blockIdx.z - img * lt.n;
     const int s = lt.step[level];
-    const int ch = (blockIdx.y - ct.blk0[level]) * 8 + threadIdx.y;
+    const int ch = blockIdx.y * 8 + threadIdx.y;
     const int x = blockIdx.x * 32 + threadIdx.x;
-    if (ch >= ct.nch[level] || x >= g.W) return;
-    const int b = ch / s, y0 = b * R * s + (ch - b * s);
-    const size_t base = blockIdx.z * img_stride + (size_t)level * g.plane;
-    const float* L = Lt + base;
-    float2* D = Lxy + base;
+    if (ch >= s * ((g.H + R * s - 1) / (R * s)) || x >= g.W) return;
+    const int b = chain_band(ch, s), y0 = b * R * s + (ch - b * s);
+    const size_t base = img * img_stride + (size_t)level * g.plane;
+    const float* L = opaque(Lt + base);
+    float2* D = opaque(Lxy + base);
     const int xm = max(x - s, 0), xp = min(x + s, g.W - 1);
     float a[R + 2], m[R + 2], c[R + 2];  // columns x−s, x, x+s of chain rows −1..R
 #pragma unroll
     for (int k = 0; k < R + 2; ++k) {
         const int ro = clampi(y0 + (k - 1) * s, 0, g.H - 1) * g.P;
-        a[k] = __ldg(L + ro + xm);
-        m[k] = __ldg(L + ro + x);
-        c[k] = __ldg(L + ro + xp);
+        a[k] = __ldg(L + (unsigned)(ro + xm));  // unsigned 32-bit offsets: one IMAD.WIDE.U32 per address
+        m[k] = __ldg(L + (unsigned)(ro + x));
+        c[k] = __ldg(L + (unsigned)(ro + xp));
     }
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int y = y0 + j * s;
         if (y < g.H)
-            D[y * g.P + x] = make_float2(0.5f * (kW0 * (c[j] - a[j]) + kW1 * (c[j + 1] - a[j + 1]) + kW0 * (c[j + 2] - a[j + 2])),
+            D[(unsigned)(y * g.P + x)] = make_float2(0.5f * (kW0 * (c[j] - a[j]) + kW1 * (c[j + 1] - a[j + 1]) + kW0 * (c[j + 2] - a[j + 2])),
                                          0.5f * (kW0 * (a[j + 2] - a[j]) + kW1 * (m[j + 2] - m[j]) + kW0 * (c[j + 2] - c[j])));
     }
 }
 
 template <int R>
 __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict__ Lxy, float* __restrict__ Ldet,
-                                                        size_t img_stride, Geom g, LevelTable lt, ChainTable ct) {
-    const int level = find_level(ct, lt.n, blockIdx.y);
+                                                        size_t img_stride, Geom g, LevelTable lt) {
+    const int img = chain_band(blockIdx.z, lt.n), level = blockIdx.z - img * lt.n;
     const int s = lt.step[level];
-    const int ch = (blockIdx.y - ct.blk0[level]) * 8 + threadIdx.y;
+    const int ch = blockIdx.y * 8 + threadIdx.y;
     const int x = blockIdx.x * 32 + threadIdx.x;
-    if (ch >= ct.nch[level] || x >= g.W) return;
-    const int b = ch / s, y0 = b * R * s + (ch - b * s);
-    const size_t base = blockIdx.z * img_stride + (size_t)level * g.plane;
-    const float2* D = Lxy + base;
-    float* O = Ldet + base;
+    if (ch >= s * ((g.H + R * s - 1) / (R * s)) || x >= g.W) return;
+    const int b = chain_band(ch, s), y0 = b * R * s + (ch - b * s);
+    const size_t base = img * img_stride + (size_t)level * g.plane;
+    const float2* D = opaque(Lxy + base);
+    float* O = opaque(Ldet + base);
     const int xm = max(x - s, 0), xp = min(x + s, g.W - 1);
     float2 a[R + 2], m[R + 2], c[R + 2];
 #pragma unroll
     for (int k = 0; k < R + 2; ++k) {
         const int ro = clampi(y0 + (k - 1) * s, 0, g.H - 1) * g.P;
-        a[k] = __ldg(D + ro + xm);
-        m[k] = __ldg(D + ro + x);
-        c[k] = __ldg(D + ro + xp);
+        a[k] = __ldg(D + (unsigned)(ro + xm));
+        m[k] = __ldg(D + (unsigned)(ro + x));
+        c[k] = __ldg(D + (unsigned)(ro + xp));
     }
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int y = y0 + j * s;
         if (y < g.H)
-            O[y * g.P + x] = det_from_ring(a[j], m[j], c[j], a[j + 1], c[j + 1], a[j + 2], m[j + 2], c[j + 2]);
+            O[(unsigned)(y * g.P + x)] = det_from_ring(a[j], m[j], c[j], a[j + 1], c[j + 1], a[j + 2], m[j + 2], c[j + 2]);
     }
 }
 
 template <int R>
-ChainTable make_chains(Geom g, const LevelTable& lt, int* total_blocks) {
-    ChainTable ct{};
-    int blk = 0;
+int max_chain_blocks(Geom g, const LevelTable& lt) {
+    int m = 1;
     for (int l = 0; l < lt.n; ++l) {
         const int s = lt.step[l];
-        const int bands = (g.H + R * s - 1) / (R * s);
-        ct.nch[l] = bands * s;
-        ct.blk0[l] = blk;
-        blk += (ct.nch[l] + 7) / 8;
+        m = max(m, (s * ((g.H + R * s - 1) / (R * s)) + 7) / 8);
     }
-    ct.blk0[lt.n] = blk;
-    *total_blocks = blk;
-    return ct;
+    return m;
 }
 
 __global__ void k_component_copy(float2* __restrict__ plane, int comp, float* __restrict__ tight, int to_tight,
@@ -131,16 +119,14 @@ __global__ void k_component_copy(float2* __restrict__ plane, int comp, float* __
 
 void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                        cudaStream_t s) {
-    int nb = 0;
-    const ChainTable ct = make_chains<kChainR>(g, lt, &nb);
-    k_hess_first_chain<kChainR><<<dim3((g.W + 31) / 32, nb, nimg), dim3(32, 8), 0, s>>>(Lt, Lxy, img_stride, g, lt, ct);
+    const dim3 grid((g.W + 31) / 32, max_chain_blocks<kChainR>(g, lt), nimg * lt.n);
+    k_hess_first_chain<kChainR><<<grid, dim3(32, 8), 0, s>>>(Lt, Lxy, img_stride, g, lt);
 }
 
 void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                      cudaStream_t s) {
-    int nb = 0;
-    const ChainTable ct = make_chains<kChainR>(g, lt, &nb);
-    k_hess_det_chain<kChainR><<<dim3((g.W + 31) / 32, nb, nimg), dim3(32, 8), 0, s>>>(Lxy, Ldet, img_stride, g, lt, ct);
+    const dim3 grid((g.W + 31) / 32, max_chain_blocks<kChainR>(g, lt), nimg * lt.n);
+    k_hess_det_chain<kChainR><<<grid, dim3(32, 8), 0, s>>>(Lxy, Ldet, img_stride, g, lt);
 }
 
 void launch_component_copy(float2* plane, int comp, float* tight, int to_tight, Geom g, cudaStream_t s) {

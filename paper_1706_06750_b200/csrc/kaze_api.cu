@@ -541,7 +541,7 @@ kaze_status kaze_create(const kaze_params* p, int device, kaze_ctx** out) {
     c->plane_max = plane_of(p->max_width, p->max_height);  // >= every build's plane (see plane_of)
     const size_t B = p->max_batch, N = c->N;
     const size_t pyr = sizeof(float) * c->plane_max * N * B;
-    const int words = (p->max_width + 31) / 32;
+    const int words = nms_words(p->max_width);
     const size_t rows = (size_t)(N > 2 ? N - 2 : 1) * p->max_height * B;
     bool ok = cudaMalloc(&c->Lt, pyr) == cudaSuccess && cudaMalloc(&c->Lxy, 2 * pyr) == cudaSuccess &&
               cudaMalloc(&c->Ldet, pyr) == cudaSuccess &&

@@ -82,6 +82,8 @@ struct DetectParams {
     float edge_ratio;
     int cap;
 };
+// Candidate bitmap words per row: 30 columns per 32-bit word (bit b of word w ↔ column 30·w + b).
+int nms_words(int W);
 void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, int N, DetectParams dp,
                      uint32_t* bitmap, int* rowcnt, cudaStream_t s);
 void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, int* counts, cudaStream_t s);
@@ -97,5 +99,14 @@ void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t 
                      cudaStream_t s);
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Hides a base pointer from re-association, so `opaque(p) + (unsigned)i` compiles to ONE IMAD.WIDE.U32 per address
+// instead of a 64-bit index add + LEA/LEA.HI.X pair (the compiler otherwise folds the 64-bit plane offset into
+// every index).
+template <class T>
+__device__ __forceinline__ T* opaque(T* p) {
+    asm("" : "+l"(p));
+    return p;
+}
 
 }  // namespace kz
