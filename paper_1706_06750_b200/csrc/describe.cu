@@ -38,13 +38,15 @@ __device__ __forceinline__ float2 bilinear2(const float2* __restrict__ img, int 
 }
 
 constexpr int kWarps = 8;
+constexpr int kSP = 25;         // pitch of the staged 24 x 24 M-SURF samples
+constexpr int kMaxBinWin = 48;  // binned orientation path: nwin % 6 == 0 and nwin <= 48 (2·nwin <= 96 bins)
 
 __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy,
                                                   const cudaTextureObject_t* __restrict__ texs, size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
                                                   const int* __restrict__ counts, int cap, float* __restrict__ desc,
                                                   int nwin, int keep_angle, int N) {
     __shared__ int pre[kMaxBatch + 1];
-    __shared__ __align__(16) float sbuf[kWarps][2 * 576];
+    __shared__ __align__(16) float sbuf[kWarps][2 * kSP * 24];
     if (threadIdx.x == 0) {
         int r = 0;
         for (int i = 0; i < nimg; ++i) {
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
     const int total = pre[nimg];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sx = sbuf[warp];
-    float* sy = sx + 576;
+    float* sy = sx + kSP * 24;
     for (int f = blockIdx.x * kWarps + warp; f < total; f += gridDim.x * kWarps) {
         int img = 0;
         while (img + 1 < nimg && pre[img + 1] <= f) ++img;  // nimg is small
@@ -73,39 +75,137 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
             angle = kp->angle;
         } else {
             // ---- orientation ----
-            float4* so = reinterpret_cast<float4*>(sx);  // (phase, w·Lx, w·Ly, -) per sample
-#pragma unroll
-            for (int j = lane; j < kOriSamples; j += 32) {
-                const float px = x + sigma * c_ori_u[j], py = y + sigma * c_ori_v[j];
-                const float w = c_ori_w[j];
-                const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);  // exact: the window choice is an argmax
-                const float rx = w * gv.x, ry = w * gv.y;
-                float ph = atan2f(ry, rx);
-                if (ph < 0.f) ph += kTwoPi;
-                so[j] = make_float4(ph, rx, ry, 0.f);
-            }
-            __syncwarp();
             float best = 0.f, bx = 0.f, by = 0.f;
             int bk = 0x7fffffff;
-            for (int kw = lane; kw < nwin; kw += 32) {
-                const float th = kTwoPi * (float)kw / (float)nwin;
-                float ax = 0.f, ay = 0.f;
-#pragma unroll 4
-                for (int j = 0; j < kOriSamples; ++j) {
-                    const float4 e = so[j];  // broadcast read
-                    float d = e.x - th;
-                    if (d > kPi) d -= kTwoPi;
-                    else if (d <= -kPi) d += kTwoPi;
-                    const bool in = fabsf(d) < kPi / 6.f;
-                    ax += in ? e.y : 0.f;
-                    ay += in ? e.z : 0.f;
+            if (nwin % 6 == 0 && nwin <= kMaxBinWin) {
+                // Fine angular bins of width π/nwin: window k (centre 2πk/nwin, half-width π/6) is exactly the bins
+                // [2k − h, 2k + h), h = nwin/6, up to the measure-zero boundary points.  A stable counting sort
+                // (integer counts; ranks from __match_any_sync, so the order is deterministic) groups the samples by
+                // bin, each bin is summed in sample order, and each window sums its 2h bins in bin order: ~500
+                // instructions per keypoint instead of a 113 x nwin scan.
+                const int nb = 2 * nwin, h = nwin / 6;
+                int* cnt = reinterpret_cast<int*>(sx);           // [nb]
+                int* off = cnt + kMaxBinWin * 2;                 // [nb]
+                float2* srt = reinterpret_cast<float2*>(off + kMaxBinWin * 2);  // [113] samples sorted by bin
+                float2* bsum = srt + kOriSamples + 1;            // [nb]
+                for (int i = lane; i < nb; i += 32) cnt[i] = 0;
+                __syncwarp();
+                float2 val[4];
+                int bin[4], pos[4];
+                const float fb = (float)nb / kTwoPi;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int j = lane + 32 * r;
+                    const bool ok = j < kOriSamples;
+                    float rx = 0.f, ry = 0.f;
+                    int bb = -1 - lane;  // never matches another lane
+                    if (ok) {
+                        const float px = x + sigma * c_ori_u[j], py = y + sigma * c_ori_v[j];
+                        const float w = c_ori_w[j];
+                        const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);  // exact: the window is an argmax
+                        rx = w * gv.x;
+                        ry = w * gv.y;
+                        float ph = atan2f(ry, rx);
+                        if (ph < 0.f) ph += kTwoPi;
+                        bb = min((int)(ph * fb), nb - 1);
+                    }
+                    const unsigned peers = __match_any_sync(0xffffffffu, bb);
+                    const int base = ok ? cnt[bb] : 0;
+                    __syncwarp();
+                    const int rank = __popc(peers & ((1u << lane) - 1u));
+                    if (ok && rank == 0) cnt[bb] = base + __popc(peers);
+                    __syncwarp();
+                    val[r] = make_float2(rx, ry);
+                    bin[r] = bb;
+                    pos[r] = base + rank;
                 }
-                const float m = ax * ax + ay * ay;
-                if (m > best) {
-                    best = m;
-                    bx = ax;
-                    by = ay;
-                    bk = kw;
+                // exclusive scan of the counts (3 bins per lane, nb <= 96)
+                int c3[3], run = 0;
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    const int i = 3 * lane + t;
+                    c3[t] = i < nb ? cnt[i] : 0;
+                    run += c3[t];
+                }
+                int incl = run;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int tv = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += tv;
+                }
+                int ex = incl - run;
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    const int i = 3 * lane + t;
+                    if (i < nb) off[i] = ex;
+                    ex += c3[t];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (lane + 32 * r < kOriSamples) srt[off[bin[r]] + pos[r]] = val[r];
+                __syncwarp();
+                for (int i = lane; i < nb; i += 32) {
+                    float ax = 0.f, ay = 0.f;
+                    const int e = off[i] + cnt[i];
+                    for (int q = off[i]; q < e; ++q) {
+                        ax += srt[q].x;
+                        ay += srt[q].y;
+                    }
+                    bsum[i] = make_float2(ax, ay);
+                }
+                __syncwarp();
+                for (int kw = lane; kw < nwin; kw += 32) {
+                    float ax = 0.f, ay = 0.f;
+                    int i = 2 * kw - h;
+                    if (i < 0) i += nb;
+                    for (int q = 0; q < 2 * h; ++q) {
+                        const float2 v = bsum[i];
+                        ax += v.x;
+                        ay += v.y;
+                        if (++i == nb) i = 0;
+                    }
+                    const float m = ax * ax + ay * ay;
+                    if (m > best) {
+                        best = m;
+                        bx = ax;
+                        by = ay;
+                        bk = kw;
+                    }
+                }
+            } else {  // any other window count: direct scan of the samples for every window
+                float4* so = reinterpret_cast<float4*>(sx);  // (phase, w·Lx, w·Ly, -) per sample
+#pragma unroll
+                for (int j = lane; j < kOriSamples; j += 32) {
+                    const float px = x + sigma * c_ori_u[j], py = y + sigma * c_ori_v[j];
+                    const float w = c_ori_w[j];
+                    const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);
+                    const float rx = w * gv.x, ry = w * gv.y;
+                    float ph = atan2f(ry, rx);
+                    if (ph < 0.f) ph += kTwoPi;
+                    so[j] = make_float4(ph, rx, ry, 0.f);
+                }
+                __syncwarp();
+                for (int kw = lane; kw < nwin; kw += 32) {
+                    const float th = kTwoPi * (float)kw / (float)nwin;
+                    float ax = 0.f, ay = 0.f;
+#pragma unroll 4
+                    for (int j = 0; j < kOriSamples; ++j) {
+                        const float4 e = so[j];  // broadcast read
+                        float d = e.x - th;
+                        if (d > kPi) d -= kTwoPi;
+                        else if (d <= -kPi) d += kTwoPi;
+                        const bool in = fabsf(d) < kPi / 6.f;
+                        ax += in ? e.y : 0.f;
+                        ay += in ? e.z : 0.f;
+                    }
+                    const float m = ax * ax + ay * ay;
+                    if (m > best) {
+                        best = m;
+                        bx = ax;
+                        by = ay;
+                        bk = kw;
+                    }
                 }
             }
             // warp arg-max, ties → lowest window index
@@ -146,8 +246,8 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
             // hardware bilinear filtering (texel centres at +0.5; clamped addressing = clamped taps, A14/A16)
             const float2 gv = tex2D<float2>(tex, px + 0.5f, py + 0.5f);
             const float gx = gv.x, gy = gv.y;
-            sx[p * 24 + q] = gx * co + gy * si;
-            sy[p * 24 + q] = -gx * si + gy * co;
+            sx[p * kSP + q] = gx * co + gy * si;  // pitch 25: conflict-free for lanes along p or q
+            sy[p * kSP + q] = -gx * si + gy * co;
         }
         __syncwarp();
         const int sr = lane >> 1, half = lane & 1;
@@ -159,7 +259,7 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
             for (int j = 0; j < 9; ++j) {
                 const int q = 5 * b + j;
                 const float w = c_w1[i * 9 + j];
-                const float du = w * sx[p * 24 + q], dv = w * sy[p * 24 + q];
+                const float du = w * sx[p * kSP + q], dv = w * sy[p * kSP + q];
                 s0 += du;
                 s1 += dv;
                 s2 += fabsf(du);
