@@ -45,6 +45,8 @@ class Params(C.Structure):
         ("keep_angle", C.c_int32),
         ("scheme", C.c_int32),
         ("tau_max", C.c_double),
+        ("exact_window", C.c_int32),
+        ("refine3d", C.c_int32),
     ]
 
 
@@ -97,6 +99,11 @@ def lib():
         L.kazeref_extrema.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_double,
                                       C.c_double, C.POINTER(KP), C.c_int64]
         L.kazeref_extrema.restype = C.c_int64
+        L.kazeref_extrema2.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.POINTER(C.c_int32),
+                                       C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(KP), C.c_int64]
+        L.kazeref_extrema2.restype = C.c_int64
+        L.kazeref_refine3d.argtypes = [_dp, C.c_double, _dp, _dp, _dp]
+        L.kazeref_exact_radius.argtypes = [C.c_int]
         L.kazeref_bilinear.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double]
         L.kazeref_bilinear.restype = C.c_double
         L.kazeref_orientation.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double,
@@ -260,13 +267,27 @@ def refine(patch, edge_ratio: float = 10.0):
     return bool(keep), dx.value, dy.value
 
 
-def extrema(Ldet, S: int, sigma, threshold: float = 1e-3, edge_ratio: float = 10.0, cap: int = 1 << 20):
+def refine3d(block, edge_ratio: float = 10.0):
+    """Returns (keep, dx, dy, ds) for a 3x3x3 response block [level][row][col]."""
+    p = _f64(np.asarray(block).reshape(27))
+    dx, dy, ds = C.c_double(np.nan), C.c_double(np.nan), C.c_double(np.nan)
+    keep = lib().kazeref_refine3d(_d(p), edge_ratio, C.byref(dx), C.byref(dy), C.byref(ds))
+    return bool(keep), dx.value, dy.value, ds.value
+
+
+def exact_radius(step: int) -> int:
+    return int(lib().kazeref_exact_radius(step))
+
+
+def extrema(Ldet, S: int, sigma, threshold: float = 1e-3, edge_ratio: float = 10.0, cap: int = 1 << 20,
+            step=None, exact: bool = False, refine3d: bool = False):
     Ld = _f64(Ldet)
     N, H, W = Ld.shape
     sg = _f64(sigma)
+    st = np.ascontiguousarray(step if step is not None else np.ones(N), dtype=np.int32)
     buf = np.zeros(cap, KP_DTYPE)
-    n = lib().kazeref_extrema(_d(Ld), N, W, H, S, _d(sg), threshold, edge_ratio,
-                              buf.ctypes.data_as(C.POINTER(KP)), cap)
+    n = lib().kazeref_extrema2(_d(Ld), N, W, H, S, _d(sg), st.ctypes.data_as(C.POINTER(C.c_int32)), threshold,
+                               edge_ratio, int(exact), int(refine3d), buf.ctypes.data_as(C.POINTER(KP)), cap)
     _chk(n)
     return buf[: min(n, cap)].copy(), n
 

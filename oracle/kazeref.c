@@ -40,6 +40,8 @@ void kazeref_default_params(kazeref_params* p) {
     p->keep_angle = 0;
     p->scheme = 0;
     p->tau_max = 0.25;  /* S:L118 */
+    p->exact_window = 0;
+    p->refine3d = 0;
 }
 
 /* ---------------------------------------------------------------------------------------
@@ -185,7 +187,7 @@ int kazeref_contrast_k(const double* L0, int W, int H, double perc, int bins,
  * (P:L124-126); ∇I_σ = Scharr step 1 of G(σ=1) * L (reading A5; "L_smooth ... first order
  * ... derivatives ... Scharr"). */
 int kazeref_conductivity(const double* L, int W, int H, double k, int diffusivity, double* c) {
-    if (!(k > 0) || (diffusivity != 1 && diffusivity != 2)) return -1;
+    if (!(k > 0) || diffusivity < 1 || diffusivity > 3) return -1;
     size_t np = (size_t)W * H;
     double* Ls = (double*)malloc(sizeof(double) * np);
     double* gx = (double*)malloc(sizeof(double) * np);
@@ -195,7 +197,9 @@ int kazeref_conductivity(const double* L, int W, int H, double k, int diffusivit
     kazeref_scharr(Ls, W, H, 1, 1, gy);
     for (size_t i = 0; i < np; ++i) {
         double q = (gx[i] * gx[i] + gy[i] * gy[i]) / (k * k);
-        c[i] = (diffusivity == 2) ? 1.0 / (1.0 + q) : exp(-q);
+        if (diffusivity == 2) c[i] = 1.0 / (1.0 + q);
+        else if (diffusivity == 1) c[i] = exp(-q);
+        else c[i] = q > 0.0 ? 1.0 - exp(-3.315 / (q * q * q * q)) : 1.0;  /* (|∇|/k)^8 = q^4 (A24) */
     }
     free(Ls); free(gx); free(gy);
     return 0;
@@ -453,15 +457,55 @@ int kazeref_refine(const double* D, double edge_ratio, double* dx, double* dy) {
     return 1;
 }
 
-/* Scale-space extrema (approximate 3x3x3 procedure of P:L461) [A11]: for levels
- * i = 1..N−2 and pixels at least 1 from the border, keep (x, y) iff Ldet_i(x,y) > threshold and it
- * is strictly greater than all 26 neighbours in levels i−1, i, i+1; then kazeref_refine. */
-int64_t kazeref_extrema(const double* Ldet, int N, int W, int H, int S, const double* sigma,
-                        double threshold, double edge_ratio, kazeref_kp* kps, int64_t cap) {
+int kazeref_refine3d(const double* D27, double edge_ratio, double* dx, double* dy, double* ds) {
+    const double* Dm = D27;       /* level i-1 */
+    const double* D = D27 + 9;    /* level i   */
+    const double* Dp = D27 + 18;  /* level i+1 */
+    double c = D[4];
+    double Dxx = D[5] + D[3] - 2.0 * c;
+    double Dyy = D[7] + D[1] - 2.0 * c;
+    double Dss = Dp[4] + Dm[4] - 2.0 * c;
+    double Dxy = 0.25 * (D[8] + D[0] - D[2] - D[6]);
+    double Dxs = 0.25 * (Dp[5] - Dp[3] - Dm[5] + Dm[3]);
+    double Dys = 0.25 * (Dp[7] - Dp[1] - Dm[7] + Dm[1]);
+    double gx = 0.5 * (D[5] - D[3]), gy = 0.5 * (D[7] - D[1]), gs = 0.5 * (Dp[4] - Dm[4]);
+    if (edge_ratio > 0) {  /* the 2-D edge test of Eqs. 9-12 on the detection level (A12) */
+        double det2 = Dxx * Dyy - Dxy * Dxy, tr = Dxx + Dyy;
+        if (!(det2 > 0.0)) return 0;
+        if (!(tr * tr / det2 < (edge_ratio + 1.0) * (edge_ratio + 1.0) / edge_ratio)) return 0;
+    }
+    /* H = [[Dxx Dxy Dxs] [Dxy Dyy Dys] [Dxs Dys Dss]]; δ = −H⁻¹ g by the adjugate (H symmetric) */
+    double A00 = Dyy * Dss - Dys * Dys, A01 = Dxs * Dys - Dxy * Dss, A02 = Dxy * Dys - Dxs * Dyy;
+    double A11 = Dxx * Dss - Dxs * Dxs, A12 = Dxy * Dxs - Dxx * Dys, A22 = Dxx * Dyy - Dxy * Dxy;
+    double det = Dxx * A00 + Dxy * A01 + Dxs * A02;
+    if (fabs(det) < 1e-12) return 0;
+    double ox = -(A00 * gx + A01 * gy + A02 * gs) / det;
+    double oy = -(A01 * gx + A11 * gy + A12 * gs) / det;
+    double os = -(A02 * gx + A12 * gy + A22 * gs) / det;
+    if (fabs(ox) > 1.0 || fabs(oy) > 1.0 || fabs(os) > 1.0) return 0;
+    if (dx) *dx = ox;
+    if (dy) *dy = oy;
+    if (ds) *ds = os;
+    return 1;
+}
+
+int kazeref_exact_radius(int step) { return step / 2 > 1 ? step / 2 : 1; }
+
+/* Scale-space extrema [A11]: for levels i = 1..N−2 and pixels at least 1 from the border, keep
+ * (x, y) iff Ldet_i(x,y) > threshold and it is strictly greater than
+ *   approximate (exact = 0): all 26 neighbours in the 3x3 windows of levels i−1, i, i+1;
+ *   exact (exact = 1, A22): its 8 neighbours at level i and every in-image pixel of the
+ *     (2r_i+1)² window centred on it at levels i−1 and i+1;
+ * then the edge test and the 2-D fit (kazeref_refine, A13) or the 3-D fit (kazeref_refine3d, A23; σ becomes
+ * σ_i·2^{δs/S}, one level being 1/S octave). */
+int64_t kazeref_extrema2(const double* Ldet, int N, int W, int H, int S, const double* sigma, const int32_t* step,
+                         double threshold, double edge_ratio, int exact, int refine3d, kazeref_kp* kps, int64_t cap) {
     size_t np = (size_t)W * H;
     int64_t count = 0;
+    if (exact && !step) return -1;
     for (int i = 1; i < N - 1; ++i) {
         const double* D = Ldet + (size_t)i * np;
+        const int r = exact ? kazeref_exact_radius(step[i]) : 1;
         for (int y = 1; y < H - 1; ++y) {
             for (int x = 1; x < W - 1; ++x) {
                 double v = D[(size_t)y * W + x];
@@ -469,24 +513,37 @@ int64_t kazeref_extrema(const double* Ldet, int N, int W, int H, int S, const do
                 int ismax = 1;
                 for (int l = -1; l <= 1 && ismax; ++l) {
                     const double* Dl = Ldet + (size_t)(i + l) * np;
-                    for (int yy = -1; yy <= 1 && ismax; ++yy)
-                        for (int xx = -1; xx <= 1; ++xx) {
+                    const int rr = l == 0 ? 1 : r;
+                    for (int yy = -rr; yy <= rr && ismax; ++yy)
+                        for (int xx = -rr; xx <= rr; ++xx) {
                             if (l == 0 && yy == 0 && xx == 0) continue;
-                            if (!(v > Dl[(size_t)(y + yy) * W + (x + xx)])) { ismax = 0; break; }
+                            int qx = x + xx, qy = y + yy;
+                            if (qx < 0 || qx >= W || qy < 0 || qy >= H) continue;  /* in-image pixels only */
+                            if (!(v > Dl[(size_t)qy * W + qx])) { ismax = 0; break; }
                         }
                 }
                 if (!ismax) continue;
-                double patch[9];
-                for (int yy = -1; yy <= 1; ++yy)
-                    for (int xx = -1; xx <= 1; ++xx)
-                        patch[(yy + 1) * 3 + (xx + 1)] = D[(size_t)(y + yy) * W + (x + xx)];
-                double ox, oy;
-                if (!kazeref_refine(patch, edge_ratio, &ox, &oy)) continue;
+                double ox, oy, os = 0.0;
+                if (refine3d) {
+                    double blk[27];
+                    for (int l = -1; l <= 1; ++l)
+                        for (int yy = -1; yy <= 1; ++yy)
+                            for (int xx = -1; xx <= 1; ++xx)
+                                blk[(l + 1) * 9 + (yy + 1) * 3 + (xx + 1)] =
+                                    Ldet[(size_t)(i + l) * np + (size_t)(y + yy) * W + (x + xx)];
+                    if (!kazeref_refine3d(blk, edge_ratio, &ox, &oy, &os)) continue;
+                } else {
+                    double patch[9];
+                    for (int yy = -1; yy <= 1; ++yy)
+                        for (int xx = -1; xx <= 1; ++xx)
+                            patch[(yy + 1) * 3 + (xx + 1)] = D[(size_t)(y + yy) * W + (x + xx)];
+                    if (!kazeref_refine(patch, edge_ratio, &ox, &oy)) continue;
+                }
                 if (kps && count < cap) {
                     kazeref_kp* k = &kps[count];
                     k->x = x + ox;
                     k->y = y + oy;
-                    k->sigma = sigma[i];
+                    k->sigma = refine3d ? sigma[i] * pow(2.0, os / S) : sigma[i];
                     k->response = v;
                     k->angle = 0.0;
                     k->level = i;
@@ -499,6 +556,11 @@ int64_t kazeref_extrema(const double* Ldet, int N, int W, int H, int S, const do
         }
     }
     return count;
+}
+
+int64_t kazeref_extrema(const double* Ldet, int N, int W, int H, int S, const double* sigma,
+                        double threshold, double edge_ratio, kazeref_kp* kps, int64_t cap) {
+    return kazeref_extrema2(Ldet, N, W, H, S, sigma, NULL, threshold, edge_ratio, 0, 0, kps, cap);
 }
 
 /* Bilinear interpolation with clamped taps (reading A14: bilinear reads; A16 replicate). */
@@ -656,7 +718,8 @@ int64_t kazeref_run(const float* img, int W, int H, const kazeref_params* p,
         for (int i = 0; i < N; ++i)
             kazeref_hessian(lv + (size_t)i * np, W, H, st[i], lx + (size_t)i * np,
                             ly + (size_t)i * np, ld + (size_t)i * np);
-        count = kazeref_extrema(ld, N, W, H, p->sublevels, sg, p->threshold, p->edge_ratio, kps, cap);
+        count = kazeref_extrema2(ld, N, W, H, p->sublevels, sg, st, p->threshold, p->edge_ratio, p->exact_window,
+                                 p->refine3d, kps, cap);
         int64_t nd = count < cap ? count : cap;
         if (kps && nd > 0) kazeref_describe(lx, ly, N, W, H, kps, nd, p->ori_windows, 0, desc);
     }

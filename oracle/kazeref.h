@@ -36,6 +36,8 @@ typedef struct {
     int32_t keep_angle;     /* 1: describe with the angles already in kps (stage-isolated use) */
     int32_t scheme;         /* 0 = AOS (Eq. 4, BASELINE north_star, A1); 1 = FED cycles (Eq. 5, A20) */
     double  tau_max;        /* FED stability bound of one explicit step (A20), default 0.25 */
+    int32_t exact_window;   /* 0 = approximate 3x3x3 test (A11); 1 = exact σ window at levels i±1 (A22) */
+    int32_t refine3d;       /* 0 = 2-D sub-pixel fit (A13); 1 = 3-D (x, y, σ) fit */
 } kazeref_params;
 
 typedef struct {
@@ -67,7 +69,8 @@ int kazeref_scharr(const double* in, int W, int H, int s, int dir, double* out);
 int kazeref_contrast_k(const double* L0, int W, int H, double perc, int bins,
                        double* k, int64_t* hist, int32_t* fallback);
 
-/* Conductivity c = g(|∇(G_1 * L)|) (Eqs. 2-3, reading A5). */
+/* Conductivity c = g(|∇(G_1 * L)|) (Eqs. 2-3, reading A5); diffusivity 1 = g1, 2 = g2,
+ * 3 = Weickert's g3 = 1 − exp(−3.315 / (|∇|/k)^8) (1 at |∇| = 0, reading A24). */
 int kazeref_conductivity(const double* L, int W, int H, double k, int diffusivity, double* c);
 
 /* Thomas algorithm for a_j x_{j-1} + b_j x_j + c_j x_{j+1} = d_j (a_0, c_{n-1} ignored). */
@@ -112,6 +115,19 @@ int kazeref_refine(const double* D, double edge_ratio, double* dx, double* dy);
 
 /* 3x3x3 extrema over levels 1..N-2 (A11-A13), brute-force scan.
  * Ldet: N*H*W.  Writes up to cap keypoints in (level, y, x) order; returns the true count. */
+/* 3-D quadratic fit of the response in (x, y, level) from the 3x3x3 block D27[l][row][col] (l = level −1..+1)
+ * with central differences (reading A23): the 2-D edge test of kazeref_refine on the centre slice first, then
+ * δ = −H₃⁻¹∇D; keep iff |det H₃| >= 1e-12 and |δx|, |δy|, |δs| <= 1.  ds is in level units. */
+int kazeref_refine3d(const double* D27, double edge_ratio, double* dx, double* dy, double* ds);
+
+/* Window radius of the exact procedure at level i (reading A22): r_i = max(1, floor(s_i / 2)), s_i the
+ * integer derivative step (A9) — a (2r_i+1)² window, about σ_i pixels on a side. */
+int kazeref_exact_radius(int step);
+
+/* Extrema with the detector variants of SURVEY §8 f2: exact (0/1, A22) and refine3d (0/1, A23); step[N] is the
+ * per-level derivative step (used by the exact window).  kazeref_extrema = both off. */
+int64_t kazeref_extrema2(const double* Ldet, int N, int W, int H, int S, const double* sigma, const int32_t* step,
+                         double threshold, double edge_ratio, int exact, int refine3d, kazeref_kp* kps, int64_t cap);
 int64_t kazeref_extrema(const double* Ldet, int N, int W, int H, int S, const double* sigma,
                         double threshold, double edge_ratio, kazeref_kp* kps, int64_t cap);
 

@@ -420,3 +420,38 @@ def test_fed_constant_image_is_identity_and_batch_matches_single():
     assert np.array_equal(gpu_levels(single, 16), both[1])
     kz.close()
     single.close()
+
+
+@pytest.mark.parametrize("nwin", [48, 40, 12])
+def test_orientation_window_counts_stage_isolated(O, nwin):
+    """Orientation with pinned Lx/Ly and keypoints for other window counts: 48 and 12 take the binned path
+    (nwin % 6 == 0: window = 2·nwin/6 whole π/nwin bins), 40 the direct scan; >= 99% within 1e-3 rad of the oracle."""
+    img, ref = oracle_run(O, 333, 257, octaves=3, sublevels=4)
+    N = 12
+    kz = make(333, 257, octaves=3, sublevels=4, k_override=ref["k"], ori_windows=nwin)
+    K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
+    K.kaze_detect(kz.ctx, torch.zeros((1, kz.cap, 8), dtype=torch.int32, device="cuda"),
+                  torch.zeros(1, dtype=torch.int32, device="cuda"))
+    Lx32, Ly32 = ref["Lx"].astype(np.float32), ref["Ly"].astype(np.float32)
+    for i in range(N):
+        K.kaze_set_level(kz.ctx, 0, i, K.PLANE_LX, torch.from_numpy(Lx32[i]).cuda())
+        K.kaze_set_level(kz.ctx, 0, i, K.PLANE_LY, torch.from_numpy(Ly32[i]).cuda())
+    rk = ref["kps"]
+    n = len(rk)
+    assert n > 50
+    arr = np.zeros(kz.cap, K.KP_DTYPE)
+    for f in ("x", "y", "sigma", "response", "level", "octave", "sublevel"):
+        arr[f][:n] = rk[f]
+    kps = torch.from_numpy(arr.view(np.int32).reshape(1, kz.cap, 8).copy()).cuda()
+    counts = torch.tensor([n], dtype=torch.int32, device="cuda")
+    desc = torch.zeros((1, kz.cap, 64), device="cuda")
+    K.kaze_describe(kz.ctx, kps, counts, desc)
+    got = K.Kaze.keypoints_numpy(kps, counts)[0]
+    kref, dref = O.describe(Lx32.astype(np.float64), Ly32.astype(np.float64), rk, nwin=nwin, keep_angle=False)
+    dang = np.abs((got["angle"] - kref["angle"] + math.pi) % (2 * math.pi) - math.pi)
+    assert np.mean(dang < 1e-3) >= 0.99, np.mean(dang < 1e-3)
+    d = desc[0, :n].cpu().numpy().astype(np.float64)
+    ok = dang < 1e-3
+    cos = np.sum(d * dref, 1) / (np.linalg.norm(d, axis=1) * np.linalg.norm(dref, axis=1) + 1e-30)
+    assert np.all(cos[ok] >= 0.999), np.min(cos[ok])
+    kz.close()

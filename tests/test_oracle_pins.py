@@ -623,3 +623,124 @@ def test_fed_order_is_permutation_and_stable(O):
         return L
     np.testing.assert_allclose(cycle(O.fed_order(taus)), exact, atol=1e-12)
     assert np.abs(cycle(range(29)) - exact).max() > 1e-8  # the natural order is measurably worse
+
+
+# ----------------------------------------------------------------------------- P23 Weickert diffusivity (A24)
+def test_weickert_conductivity_closed_forms(O):
+    """g3 = 1 − exp(−3.315/(|∇|/k)^8): on a ramp of slope a the interior gradient is exactly a (G1 and the
+    Scharr operator both reproduce linear functions), so c = 1 − e^{−3.315} at k = a and 1 − e^{−3.315/256} at
+    k = a/2; a constant image gives c = 1 (the |∇| = 0 limit); g1 / g2 stay e^{−1} / ½ at k = a."""
+    a = 0.013
+    yy, xx = np.mgrid[0:40, 0:48].astype(float)
+    L = a * xx
+    inner = (slice(6, -6), slice(6, -6))
+    np.testing.assert_allclose(O.conductivity(L, a, 3)[inner], 1 - math.exp(-3.315), rtol=1e-12)
+    np.testing.assert_allclose(O.conductivity(L, a / 2, 3)[inner], 1 - math.exp(-3.315 / 256), rtol=1e-12)
+    np.testing.assert_allclose(O.conductivity(L, a, 1)[inner], math.exp(-1), rtol=1e-12)
+    np.testing.assert_allclose(O.conductivity(L, a, 2)[inner], 0.5, rtol=1e-12)
+    np.testing.assert_array_equal(O.conductivity(np.full((20, 30), 0.4), 0.05, 3), 1.0)
+    # monotone non-increasing in the slope, bounded in (0, 1]
+    cs = [O.conductivity(s * xx, 0.02, 3)[20, 24] for s in (0.001, 0.01, 0.02, 0.03, 0.1)]
+    assert all(b <= a_ for a_, b in zip(cs, cs[1:])) and 0 < cs[-1] <= cs[0] <= 1
+
+
+# ----------------------------------------------------------------------------- P24 exact σ window (A22)
+def test_exact_window_radius_and_subset(O):
+    assert [O.exact_radius(s) for s in (1, 2, 3, 4, 5, 8, 9, 22)] == [1, 1, 1, 2, 2, 4, 4, 11]
+    sg, _, st = O.schedule(4, 4, 1.6)
+    img = kaze_inputs.synth_image(160, 120, 1234)
+    res = O.run(img, want_levels=True)
+    D = res["Ldet"]
+    approx, na = O.extrema(D, 4, sg, step=st)
+    exact, ne = O.extrema(D, 4, sg, step=st, exact=True)
+    assert 0 < ne < na  # P:L461: "relatively less number of keypoints when using the exact procedure"
+    key = lambda k: (int(k["level"]), round(float(k["x"]), 9), round(float(k["y"]), 9))  # noqa: E731
+    assert {key(k) for k in exact} <= {key(k) for k in approx}
+
+
+def test_exact_window_vs_maximum_filter(O):
+    """A second statement of the exact rule through a library primitive: scipy's maximum_filter with −inf
+    outside the image gives the (2r+1)² window maxima at levels i±1, the 3x3 ring at level i."""
+    ndi = pytest.importorskip("scipy.ndimage")
+    sg, _, st = O.schedule(3, 3, 1.6)
+    for seed in range(2):
+        img = kaze_inputs.synth_image(72, 64, 300 + seed)
+        res = O.run(img, octaves=3, sublevels=3, want_levels=True, edge_ratio=0.0)
+        D = res["Ldet"]
+        N, H, W = D.shape
+        ring = np.ones((3, 3), bool)
+        ring[1, 1] = False
+        found = set()
+        for i in range(1, N - 1):
+            r = O.exact_radius(int(st[i]))
+            box = np.ones((2 * r + 1, 2 * r + 1), bool)
+            m = np.maximum(ndi.maximum_filter(D[i - 1], footprint=box, mode="constant", cval=-np.inf),
+                           ndi.maximum_filter(D[i + 1], footprint=box, mode="constant", cval=-np.inf))
+            m = np.maximum(m, ndi.maximum_filter(D[i], footprint=ring, mode="constant", cval=-np.inf))
+            ok = (D[i] > 1e-3) & (D[i] > m)
+            ok[0, :] = ok[-1, :] = ok[:, 0] = ok[:, -1] = False
+            for y, x in zip(*np.nonzero(ok)):
+                if O.refine(D[i, y - 1:y + 2, x - 1:x + 2], 0.0)[0]:
+                    found.add((i, float(D[i, y, x])))
+        got, n = O.extrema(D, 3, sg, step=st, exact=True, edge_ratio=0.0)
+        assert n == len(found) > 0
+        assert {(int(k["level"]), float(k["response"])) for k in got} == found
+
+
+def test_exact_window_rejects_a_larger_neighbour_two_pixels_away(O):
+    D = np.zeros((3, 24, 24))
+    D[1, 10, 10] = 1.0
+    D[1, 9:12, 9:12] += 0.5 * np.array([[0.2, 0.5, 0.2], [0.5, 0.0, 0.5], [0.2, 0.5, 0.2]])
+    D[2, 10, 12] = 1.5  # outside the 3x3 of level i, inside the 5x5 (r = 2 for step 4)
+    sg, st = np.array([1.0, 2.0, 4.0]), np.array([4, 4, 4], np.int32)
+    _, na = O.extrema(D, 1, sg, step=st, edge_ratio=0.0)
+    _, ne = O.extrema(D, 1, sg, step=st, edge_ratio=0.0, exact=True)
+    assert (na, ne) == (1, 0)
+
+
+# ----------------------------------------------------------------------------- P25 3-D refinement (A23)
+def _quad3(x0, y0, s0, A, v0=1.0):
+    l, yy, xx = np.mgrid[-1:2, -1:2, -1:2].astype(float)
+    d = np.stack([xx - x0, yy - y0, l - s0])
+    return v0 - 0.5 * np.einsum("i...,ij,j...->...", d, A, d)
+
+
+@pytest.mark.parametrize("off", [(0.3, -0.2, 0.25), (-0.45, 0.1, -0.6), (0.0, 0.0, 0.0)])
+def test_refine3d_recovers_a_quadratic_peak(O, off):
+    """Central differences are exact on quadratics, so the 3-D fit returns the peak of any concave quadratic in
+    (x, y, level), cross terms included."""
+    A = np.array([[2.0, 0.3, 0.2], [0.3, 1.5, -0.1], [0.2, -0.1, 1.2]])
+    keep, dx, dy, ds = O.refine3d(_quad3(*off, A), edge_ratio=0.0)
+    assert keep
+    np.testing.assert_allclose([dx, dy, ds], off, atol=1e-12)
+
+
+def test_refine3d_rejections_and_reduction_to_2d(O):
+    A = np.diag([2.0, 1.5, 1.2])
+    assert not O.refine3d(_quad3(0.2, 0.1, 1.7, A), 0.0)[0]  # |δs| > 1
+    assert not O.refine3d(_quad3(1.4, 0.1, 0.0, A), 0.0)[0]  # |δx| > 1
+    assert not O.refine3d(np.tile(_quad3(0.2, 0.1, 0.0, A)[1], (3, 1, 1)), 0.0)[0]  # flat in level: singular
+    ridge = _quad3(0.1, 0.0, 0.0, np.diag([2.0, 0.002, 1.0]))
+    assert not O.refine3d(ridge, 10.0)[0] and O.refine3d(ridge, 0.0)[0]  # the 2-D edge test (A12) still applies
+    # no cross terms with the level axis: (δx, δy) equal the 2-D fit of the centre slice
+    B = np.array([[2.0, 0.4, 0.0], [0.4, 1.0, 0.0], [0.0, 0.0, 0.9]])
+    blk = _quad3(0.35, -0.25, 0.4, B)
+    k3, dx, dy, _ = O.refine3d(blk, 10.0)
+    k2, ex, ey = O.refine(blk[1], 10.0)
+    assert k3 and k2 and abs(dx - ex) < 1e-12 and abs(dy - ey) < 1e-12
+
+
+def test_refine3d_pipeline_sigma_and_positions(O):
+    """With refine3d every keypoint's σ is σ_i·2^{δs/S}, |δs| <= 1, and its position is within 1 px of an
+    approximate-procedure extremum of the same level (same candidates, different fit)."""
+    sg, _, st = O.schedule(4, 4, 1.6)
+    img = kaze_inputs.synth_image(128, 96, 1240)
+    r2 = O.run(img)
+    r3 = O.run(img, refine3d=1)
+    assert r3["count"] > 0
+    k = r3["kps"]
+    ratio = np.log2(k["sigma"] / sg[k["level"]]) * 4
+    assert np.all(np.abs(ratio) <= 1 + 1e-12) and np.any(np.abs(ratio) > 1e-3)
+    cand = {(int(a["level"]), int(round(a["response"] * 1e12))) for a in r2["kps"]}
+    inter = [(int(a["level"]), int(round(a["response"] * 1e12))) in cand for a in k]
+    assert np.mean(inter) > 0.5  # most survive both fits (the candidate sets are identical)
