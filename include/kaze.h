@@ -58,7 +58,7 @@ typedef struct {
     double  sigma0;        /* σ0 > 0, default 1.6 (Eq. 6; prefilter P:L255)                       */
     double  k_percentile;  /* in (0, 1), default 0.7 (A7)                             */
     int32_t k_bins;        /* 1..4096, default 300 (A7)                                           */
-    int32_t diffusivity;   /* 2 = g2 (default), 1 = g1 (Eq. 3)                        */
+    int32_t diffusivity;   /* 2 = g2 (default), 1 = g1 (Eq. 3), 3 = Weickert (A24)    */
     double  k_override;    /* <= 0: estimate k per image; > 0: use this k for every image         */
     double  threshold;     /* >= 0, default 1e-3: keep Ldet > threshold (A11)         */
     double  edge_ratio;    /* r of Eq. 12, default 10; <= 0 disables the edge test   */
@@ -78,6 +78,12 @@ typedef struct {
 /* kaze_describe uses the angles already stored in d_kps instead of computing them (stage-isolated
  * parity tests with pinned angles). */
 #define KAZE_FLAG_KEEP_ANGLE 1
+/* Detector variants.  EXACT_WINDOW: the paper's exact procedure — besides its 3x3 ring at
+ * level i, a keypoint must exceed every in-image response of the (2r_i+1)² window at levels i−1 and i+1,
+ * r_i = max(1, floor(s_i/2)) (A22).  REFINE_3D: quadratic fit in (x, y, level) from the
+ * 3x3x3 block instead of the 2-D fit; σ = σ_i·2^{δs/S} (A23). */
+#define KAZE_FLAG_EXACT_WINDOW 2
+#define KAZE_FLAG_REFINE_3D 4
 
 /* 32-byte keypoint (P:L212-214 sub-pixel position; D4 of SURVEY). */
 typedef struct {

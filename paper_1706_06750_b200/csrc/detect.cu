@@ -38,19 +38,50 @@ __device__ __forceinline__ bool refine(const float (&D)[3][3], float edge_ratio,
     return fabsf(ox) <= 1.f && fabsf(oy) <= 1.f;
 }
 
+// 3-D fit in (x, y, level) on the block B[l][r][c] (l = level −1..+1), A23: the 2-D edge test on the centre slice,
+// then δ = −H₃⁻¹∇D by the adjugate; keep iff |det| >= 1e-12 and |δ| <= 1 per axis.  Not inlined, so the mark and
+// emit passes run the very same instructions on the same values and take the same decision.
+__device__ __noinline__ bool refine3d(const float (&B)[3][3][3], float edge_ratio, float& ox, float& oy, float& os) {
+    const float cv = B[1][1][1];
+    const float dxx = B[1][1][2] + B[1][1][0] - 2.f * cv;
+    const float dyy = B[1][2][1] + B[1][0][1] - 2.f * cv;
+    const float dss = B[2][1][1] + B[0][1][1] - 2.f * cv;
+    const float dxy = 0.25f * (B[1][2][2] + B[1][0][0] - B[1][0][2] - B[1][2][0]);
+    const float dxs = 0.25f * (B[2][1][2] - B[2][1][0] - B[0][1][2] + B[0][1][0]);
+    const float dys = 0.25f * (B[2][2][1] - B[2][0][1] - B[0][2][1] + B[0][0][1]);
+    const float gx = 0.5f * (B[1][1][2] - B[1][1][0]), gy = 0.5f * (B[1][2][1] - B[1][0][1]);
+    const float gs = 0.5f * (B[2][1][1] - B[0][1][1]);
+    if (edge_ratio > 0.f) {
+        const float det2 = dxx * dyy - dxy * dxy, tr = dxx + dyy;
+        if (!(det2 > 0.f)) return false;
+        if (!(tr * tr / det2 < (edge_ratio + 1.f) * (edge_ratio + 1.f) / edge_ratio)) return false;
+    }
+    const float a00 = dyy * dss - dys * dys, a01 = dxs * dys - dxy * dss, a02 = dxy * dys - dxs * dyy;
+    const float a11 = dxx * dss - dxs * dxs, a12 = dxy * dxs - dxx * dys, a22 = dxx * dyy - dxy * dxy;
+    const float det = dxx * a00 + dxy * a01 + dxs * a02;
+    if (fabsf(det) < 1e-12f) return false;
+    ox = -(a00 * gx + a01 * gy + a02 * gs) / det;
+    oy = -(a01 * gx + a11 * gy + a12 * gs) / det;
+    os = -(a02 * gx + a12 * gy + a22 * gs) / det;
+    return fabsf(ox) <= 1.f && fabsf(oy) <= 1.f && fabsf(os) <= 1.f;
+}
+
 __device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const float* __restrict__ D0,
                                             const float* __restrict__ Dp, int P, int x, int y, float thr, float er,
-                                            float& ox, float& oy, float& v) {
+                                            int use3d, float& ox, float& oy, float& os, float& v) {
     const size_t o = (size_t)y * P + x;
     v = __ldg(D0 + o);
     if (!(v > thr)) return false;
-    float patch[3][3];
+    float patch[3][3], blk[3][3][3];
 #pragma unroll
     for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
         for (int dx = -1; dx <= 1; ++dx) {
             const size_t q = o + (ptrdiff_t)dy * P + dx;
             float a = __ldg(Dm + q), c = __ldg(Dp + q);
+            blk[0][dy + 1][dx + 1] = a;
+            blk[2][dy + 1][dx + 1] = c;
+            blk[1][dy + 1][dx + 1] = __ldg(D0 + q);
             if (!(v > a) || !(v > c)) return false;
             if (dx != 0 || dy != 0) {
                 float b = __ldg(D0 + q);
@@ -59,6 +90,9 @@ __device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const 
             }
         }
     patch[1][1] = v;
+    blk[1][1][1] = v;
+    if (use3d) return refine3d(blk, er, ox, oy, os);
+    os = 0.f;
     return refine(patch, er, ox, oy);
 }
 
@@ -75,10 +109,11 @@ constexpr int NSEG = 63;   // rows per warp (multiple of 3)
 constexpr int NMS_LB = 7;  // centre levels per warp (16 levels → two blocks of 7)
 constexpr int STRIP = 30;  // output columns per strip
 
-template <int LB, int PH>
+template <int LB, int PH, bool EXT>
 __device__ __forceinline__ void nms_row(float (&w)[LB + 2][3], const float* __restrict__ base, const int (&off)[LB + 2], int P,
                                         int y, int H, int W, int x, int lane, int nc, const DetectParams& dp,
-                                        uint32_t* __restrict__ bm, size_t lvl_stride, int words) {
+                                        uint32_t* __restrict__ bm, size_t lvl_stride, int words,
+                                        const LevelTable& lt, int l0) {
     // load row y+1 (clamped) into slot (PH + 2) % 3; the window then holds rows y-1, y, y+1 in slots PH, PH+1, PH+2
     const int ro = min(y + 1, H - 1) * P;
 #pragma unroll
@@ -99,14 +134,51 @@ __device__ __forceinline__ void nms_row(float (&w)[LB + 2][3], const float* __re
         if (c > nc) break;  // warp-uniform
         const float v = w[c][(PH + 1) % 3];
         bool k = inside && v > dp.threshold && v > N8[c] && v > M[c - 1] && v > M[c + 1];
-        if (__any_sync(0xffffffffu, k)) {  // rare: the level's 3x3 patch by shuffles, then the fit
+        if (EXT && __any_sync(0xffffffffu, k)) {  // variants (A22/A23): 3x3x3 block by shuffles, window test, fit
+            float blk[3][3][3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+#pragma unroll
+                for (int rr = 0; rr < 3; ++rr) {
+                    const float m = w[c - 1 + q][(PH + rr) % 3];
+                    blk[q][rr][1] = m;
+                    blk[q][rr][0] = __shfl_up_sync(0xffffffffu, m, 1);
+                    blk[q][rr][2] = __shfl_down_sync(0xffffffffu, m, 1);
+                }
+            if (k && dp.exact) {  // A22: every in-image response of the (2r+1)² window at levels i±1
+                const int level = l0 - 1 + c, r = max(1, lt.step[level] / 2);
+                for (int q = -1; q <= 1 && k; q += 2) {
+                    const float* Dq = base + off[c + q];
+                    for (int dy = -r; dy <= r && k; ++dy) {
+                        const int yy = y + dy;
+                        if (yy < 0 || yy >= H) continue;
+                        for (int dx = -r; dx <= r; ++dx) {
+                            const int xx = x + dx;
+                            if (xx < 0 || xx >= W) continue;
+                            if (!(v > __ldg(Dq + (ptrdiff_t)yy * P + dx))) { k = false; break; }
+                        }
+                    }
+                }
+            }
+            if (k) {
+                float ox, oy, os;
+                if (dp.refine3d) {
+                    k = refine3d(blk, dp.edge_ratio, ox, oy, os);
+                } else {
+                    const float patch[3][3] = {{blk[1][0][0], blk[1][0][1], blk[1][0][2]},
+                                               {blk[1][1][0], blk[1][1][1], blk[1][1][2]},
+                                               {blk[1][2][0], blk[1][2][1], blk[1][2][2]}};
+                    k = refine(patch, dp.edge_ratio, ox, oy);
+                }
+            }
+        } else if (!EXT && __any_sync(0xffffffffu, k)) {  // rare: the level's 3x3 patch by shuffles, then the fit
             const float u0 = w[c][PH % 3], u2 = w[c][(PH + 2) % 3];
-            const float l0 = __shfl_up_sync(0xffffffffu, u0, 1), l1 = __shfl_up_sync(0xffffffffu, v, 1);
+            const float l0s = __shfl_up_sync(0xffffffffu, u0, 1), l1 = __shfl_up_sync(0xffffffffu, v, 1);
             const float l2 = __shfl_up_sync(0xffffffffu, u2, 1);
             const float r0 = __shfl_down_sync(0xffffffffu, u0, 1), r1 = __shfl_down_sync(0xffffffffu, v, 1);
             const float r2 = __shfl_down_sync(0xffffffffu, u2, 1);
             if (k) {
-                const float patch[3][3] = {{l0, u0, r0}, {l1, v, r1}, {l2, u2, r2}};
+                const float patch[3][3] = {{l0s, u0, r0}, {l1, v, r1}, {l2, u2, r2}};
                 float ox, oy;
                 k = refine(patch, dp.edge_ratio, ox, oy);
             }
@@ -116,9 +188,10 @@ __device__ __forceinline__ void nms_row(float (&w)[LB + 2][3], const float* __re
     }
 }
 
-template <int LB>
+template <int LB, bool EXT>
 __global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
-                                                  DetectParams dp, uint32_t* __restrict__ bitmap, int words) {
+                                                  DetectParams dp, LevelTable lt, uint32_t* __restrict__ bitmap,
+                                                  int words) {
     const int lane = threadIdx.x & 31;
     const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (strip >= words) return;  // warp-uniform
@@ -147,9 +220,11 @@ __global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet
         w[q][1] = __ldg(base + (unsigned)(off[q] + r0));
     }
     for (int y = y0; y < yend; y += 3) {
-        nms_row<LB, 0>(w, base, off, g.P, y, H, W, x, lane, nc, dp, bm, lvl_stride, words);
-        if (y + 1 < yend) nms_row<LB, 1>(w, base, off, g.P, y + 1, H, W, x, lane, nc, dp, bm, lvl_stride, words);
-        if (y + 2 < yend) nms_row<LB, 2>(w, base, off, g.P, y + 2, H, W, x, lane, nc, dp, bm, lvl_stride, words);
+        nms_row<LB, 0, EXT>(w, base, off, g.P, y, H, W, x, lane, nc, dp, bm, lvl_stride, words, lt, l0);
+        if (y + 1 < yend)
+            nms_row<LB, 1, EXT>(w, base, off, g.P, y + 1, H, W, x, lane, nc, dp, bm, lvl_stride, words, lt, l0);
+        if (y + 2 < yend)
+            nms_row<LB, 2, EXT>(w, base, off, g.P, y + 2, H, W, x, lane, nc, dp, bm, lvl_stride, words, lt, l0);
     }
 }
 
@@ -234,12 +309,13 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
             word &= word - 1;
             if (rank < dp.cap) {
                 const int x = (w0 + lane) * STRIP + bit;
-                float ox = 0.f, oy = 0.f, v = 0.f;
-                is_keypoint(D0 - g.plane, D0, D0 + g.plane, g.P, x, y, dp.threshold, dp.edge_ratio, ox, oy, v);
+                float ox = 0.f, oy = 0.f, os = 0.f, v = 0.f;
+                is_keypoint(D0 - g.plane, D0, D0 + g.plane, g.P, x, y, dp.threshold, dp.edge_ratio, dp.refine3d, ox,
+                            oy, os, v);
                 kaze_keypoint kp;
                 kp.x = (float)x + ox;
                 kp.y = (float)y + oy;
-                kp.sigma = lt.sigma[level];
+                kp.sigma = dp.refine3d ? lt.sigma[level] * exp2f(os / (float)lt.S) : lt.sigma[level];
                 kp.response = v;
                 kp.angle = 0.f;
                 kp.level = level;
@@ -257,12 +333,16 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
 
 int nms_words(int W) { return (W + STRIP - 1) / STRIP; }
 
-void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, int N, DetectParams dp, uint32_t* bitmap,
-                     int* rowcnt, cudaStream_t s) {
+void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
+                     uint32_t* bitmap, int* rowcnt, cudaStream_t s) {
+    const int N = lt.n;
     const int words = nms_words(g.W);
     const int nblk = (N - 2 + NMS_LB - 1) / NMS_LB;
     dim3 grid((words + 7) / 8, (g.H + NSEG - 1) / NSEG, nimg * nblk);
-    k_nms_mark<NMS_LB><<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, bitmap, words);
+    if (dp.exact || dp.refine3d)  // detector variants (§8 f2) in their own instantiation: the default stays lean
+        k_nms_mark<NMS_LB, true><<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, lt, bitmap, words);
+    else
+        k_nms_mark<NMS_LB, false><<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, lt, bitmap, words);
     const int total = g.H * (N - 2) * nimg;
     k_rowcount<<<(total + 7) / 8, 256, 0, s>>>(bitmap, words, total, rowcnt);
 }

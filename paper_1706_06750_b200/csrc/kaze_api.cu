@@ -242,7 +242,7 @@ kaze_status validate_params(const kaze_params* p) {
     if (!(p->sigma0 > 0) || p->sigma0 > kMaxGaussR / 3.0) return KAZE_ERR_INVALID_ARGUMENT;
     if (!(p->k_percentile > 0 && p->k_percentile < 1)) return KAZE_ERR_INVALID_ARGUMENT;
     if (p->k_bins < 1 || p->k_bins > kMaxBins) return KAZE_ERR_INVALID_ARGUMENT;
-    if (p->diffusivity != 1 && p->diffusivity != 2) return KAZE_ERR_INVALID_ARGUMENT;
+    if (p->diffusivity < 1 || p->diffusivity > 3) return KAZE_ERR_INVALID_ARGUMENT;
     if (!(p->threshold >= 0)) return KAZE_ERR_INVALID_ARGUMENT;
     if (std::isnan(p->edge_ratio) || std::isnan(p->k_override)) return KAZE_ERR_INVALID_ARGUMENT;
     if (p->max_keypoints < 1 || p->ori_windows < 1 || p->ori_windows > 64) return KAZE_ERR_INVALID_ARGUMENT;
@@ -381,10 +381,11 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     if (N < 3) {
         KZ_CUDA(c, cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * n, s));
     } else {
-        DetectParams dp{(float)c->p.threshold, (float)c->p.edge_ratio, c->p.max_keypoints};
+        DetectParams dp{(float)c->p.threshold, (float)c->p.edge_ratio, c->p.max_keypoints,
+                        (c->p.flags & KAZE_FLAG_EXACT_WINDOW) ? 1 : 0, (c->p.flags & KAZE_FLAG_REFINE_3D) ? 1 : 0};
         {
             Launch L(c, KC_NMS_MARK, 4.0 * px * N, s, 2);  // nms_mark + rowcount
-            launch_nms_mark(c->Ldet, c->img_stride, g, n, N, dp, c->bitmap, c->rowcnt, s);
+            launch_nms_mark(c->Ldet, c->img_stride, g, n, c->lt, dp, c->bitmap, c->rowcnt, s);
         }
         KZ_CHECK_LAUNCH(c, "nms_mark");
         const int R = (N - 2) * g.H;

@@ -81,10 +81,12 @@ struct DetectParams {
     float threshold;
     float edge_ratio;
     int cap;
+    int exact;     // exact σ window at levels i±1 (A22)
+    int refine3d;  // 3-D (x, y, level) fit (A23)
 };
 // Candidate bitmap words per row: 30 columns per 32-bit word (bit b of word w ↔ column 30·w + b).
 int nms_words(int W);
-void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, int N, DetectParams dp,
+void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
                      uint32_t* bitmap, int* rowcnt, cudaStream_t s);
 void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, int* counts, cudaStream_t s);
 void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
@@ -99,6 +101,19 @@ void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t 
                      cudaStream_t s);
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Conductivity g(q), q = |∇|²/k² (Eq. 3): 2 = g2, 1 = g1, 3 = Weickert's 1 − exp(−3.315/q⁴) (A24;
+// expm1 keeps it accurate where 3.315/q⁴ is tiny, and q⁴ → 0 gives exactly 1).
+__device__ __forceinline__ float diffusivity_g(float q, int kind) {
+    if (kind == 2) {
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + q));
+        return r;
+    }
+    if (kind == 1) return __expf(-q);
+    const float q2 = q * q;
+    return -expm1f(-3.315f / (q2 * q2));
+}
 
 // Hides a base pointer from re-association, so `opaque(p) + (unsigned)i` compiles to ONE IMAD.WIDE.U32 per address
 // instead of a 64-bit index add + LEA/LEA.HI.X pair (the compiler otherwise folds the 64-bit plane offset into

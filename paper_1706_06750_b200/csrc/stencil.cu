@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
                 if (x >= 1 && x <= g.W - 2 && y >= 1 && y <= g.H - 2) lmax = fmaxf(lmax, sqrtf(g2));
             } else {
                 const float qv = g2 * ik2;
-                dst[(size_t)y * g.P + x] = diffusivity == 2 ? frcp(1.f + qv) : __expf(-qv);
+                dst[(size_t)y * g.P + x] = diffusivity_g(qv, diffusivity);
             }
         }
     }
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(256) k_c_from_g2(float* __restrict__ buf, size
     float k = kval[img];
     float* p = buf + img * img_stride + (size_t)y * g.P + x;
     const float q = *p * frcp(k * k);
-    *p = diffusivity == 2 ? frcp(1.f + q) : __expf(-q);
+    *p = diffusivity_g(q, diffusivity);
 }
 
 }  // namespace
