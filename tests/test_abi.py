@@ -78,7 +78,7 @@ def test_defaults_and_status_strings(K):
     "override,status",
     [
         ({"octaves": 0}, -1), ({"sublevels": 0}, -1), ({"sigma0": 0.0}, -1), ({"sigma0": -1.0}, -1),
-        ({"k_percentile": 0.0}, -1), ({"k_percentile": 1.0}, -1), ({"k_bins": 0}, -1), ({"diffusivity": 3}, -1),
+        ({"k_percentile": 0.0}, -1), ({"k_percentile": 1.0}, -1), ({"k_bins": 0}, -1), ({"diffusivity": 4}, -1), ({"diffusivity": 0}, -1),
         ({"threshold": -1.0}, -1), ({"max_keypoints": 0}, -1), ({"ori_windows": 65}, -1), ({"max_batch": 0}, -1),
         ({"max_width": 31}, -2), ({"max_height": 16}, -2), ({"scheme": 2}, -1),
         ({"scheme": 1, "tau_max": 0.3}, -1), ({"scheme": 1, "tau_max": 0.0}, -1),
