@@ -103,6 +103,8 @@ def lib():
                                        C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(KP), C.c_int64]
         L.kazeref_extrema2.restype = C.c_int64
         L.kazeref_refine3d.argtypes = [_dp, C.c_double, _dp, _dp, _dp]
+        L.kazeref_match.argtypes = [_dp, C.c_int, _dp, C.c_int, C.c_double, C.POINTER(C.c_int32), _dp, _dp]
+        L.kazeref_match.restype = C.c_int64
         L.kazeref_exact_radius.argtypes = [C.c_int]
         L.kazeref_bilinear.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double]
         L.kazeref_bilinear.restype = C.c_double
@@ -290,6 +292,18 @@ def extrema(Ldet, S: int, sigma, threshold: float = 1e-3, edge_ratio: float = 10
                                edge_ratio, int(exact), int(refine3d), buf.ctypes.data_as(C.POINTER(KP)), cap)
     _chk(n)
     return buf[: min(n, cap)].copy(), n
+
+
+def match(A, B, ratio: float = 0.8):
+    """Brute-force matcher (A25) → (match[na] (b or -1), d1[na], d2[na], count)."""
+    a = _f64(np.asarray(A).reshape(-1, 64))
+    b = _f64(np.asarray(B).reshape(-1, 64))
+    na, nb = len(a), len(b)
+    m = np.zeros(na, np.int32)
+    d1, d2 = np.zeros(na), np.zeros(na)
+    n = lib().kazeref_match(_d(a), na, _d(b), nb, ratio, m.ctypes.data_as(C.POINTER(C.c_int32)), _d(d1), _d(d2))
+    _chk(n)
+    return m, d1, d2, int(n)
 
 
 def bilinear(img, x: float, y: float) -> float:

@@ -731,6 +731,73 @@ int64_t kazeref_run(const float* img, int W, int H, const kazeref_params* p,
     return count;
 }
 
+/* A25: the matcher S:L399-440 defines (the paper cites matching as the application, but defines no
+ * matcher).  Distances are computed from the descriptor difference, in fp64, in the plain double loop. */
+static double kr_dist(const double* a, const double* b) {
+    double s = 0.0;
+    for (int i = 0; i < 64; ++i) {
+        double d = a[i] - b[i];
+        s += d * d;
+    }
+    return sqrt(s);
+}
+
+static int kr_degenerate(const double* a) {
+    for (int i = 0; i < 64; ++i)
+        if (a[i] != 0.0) return 0;
+    return 1;
+}
+
+/* nearest (and second) non-degenerate row of Y for x; ties → lower index. */
+static void kr_nearest(const double* x, const double* Y, int ny, const int* ydeg, int* i1, double* d1, double* d2) {
+    *i1 = -1;
+    *d1 = INFINITY;
+    *d2 = INFINITY;
+    for (int j = 0; j < ny; ++j) {
+        if (ydeg[j]) continue;
+        double d = kr_dist(x, Y + (size_t)j * 64);
+        if (d < *d1) {
+            *d2 = *d1;
+            *d1 = d;
+            *i1 = j;
+        } else if (d < *d2) {
+            *d2 = d;
+        }
+    }
+}
+
+int64_t kazeref_match(const double* A, int na, const double* B, int nb, double ratio,
+                      int32_t* match, double* dist, double* second) {
+    if (na < 0 || nb < 0 || !(ratio > 0 && ratio <= 1) || (na > 0 && (!A || !match)) || (nb > 0 && !B)) return -1;
+    int* adeg = (int*)malloc(sizeof(int) * (na > 0 ? na : 1));
+    int* bdeg = (int*)malloc(sizeof(int) * (nb > 0 ? nb : 1));
+    for (int i = 0; i < na; ++i) adeg[i] = kr_degenerate(A + (size_t)i * 64);
+    for (int j = 0; j < nb; ++j) bdeg[j] = kr_degenerate(B + (size_t)j * 64);
+    int64_t count = 0;
+    for (int i = 0; i < na; ++i) {
+        match[i] = -1;
+        if (dist) dist[i] = -1.0;
+        if (second) second[i] = -1.0;
+        if (adeg[i]) continue;
+        int j;
+        double d1, d2;
+        kr_nearest(A + (size_t)i * 64, B, nb, bdeg, &j, &d1, &d2);
+        if (j < 0) continue;
+        if (dist) dist[i] = d1;
+        if (second) second[i] = isinf(d2) ? -1.0 : d2;
+        if (!(d1 < ratio * d2)) continue;  /* d2 = ∞ passes */
+        int back;
+        double e1, e2;
+        kr_nearest(B + (size_t)j * 64, A, na, adeg, &back, &e1, &e2);
+        if (back != i) continue;
+        match[i] = j;
+        count += 1;
+    }
+    free(adeg);
+    free(bdeg);
+    return count;
+}
+
 int kazeref_run_batch(const float* imgs, int n, int W, int H, const kazeref_params* p,
                       int64_t cap, int nthreads, int64_t* counts) {
     if (n < 0 || !imgs || !counts) return -1;

@@ -155,6 +155,14 @@ int64_t kazeref_run(const float* img, int W, int H, const kazeref_params* p,
 int kazeref_describe(const double* Lx, const double* Ly, int N, int W, int H,
                      kazeref_kp* kps, int64_t n, int nwin, int keep_angle, double* desc);
 
+/* Brute-force descriptor matching (reading A25): for every a, the nearest and
+ * second-nearest b by L2 distance among the non-degenerate (nonzero) b (ties → lower index); keep iff
+ * d1 < ratio·d2 (d2 = ∞ with fewer than two candidates) and the symmetric cross-check holds (a is the nearest
+ * non-degenerate a of b, same tie rule).  match[a] = b or −1; dist[a] = d1 (or −1); second[a] = d2 (∞ → −1).
+ * Degenerate a never match.  A: na x 64, B: nb x 64, row-major.  Returns the number of matches. */
+int64_t kazeref_match(const double* A, int na, const double* B, int nb, double ratio,
+                      int32_t* match, double* dist, double* second);
+
 /* Batch of n images, OpenMP over images only (cpu_baseline timing).  counts[n]. */
 int kazeref_run_batch(const float* imgs, int n, int W, int H, const kazeref_params* p,
                       int64_t cap, int nthreads, int64_t* counts);

@@ -744,3 +744,73 @@ def test_refine3d_pipeline_sigma_and_positions(O):
     cand = {(int(a["level"]), int(round(a["response"] * 1e12))) for a in r2["kps"]}
     inter = [(int(a["level"]), int(round(a["response"] * 1e12))) in cand for a in k]
     assert np.mean(inter) > 0.5  # most survive both fits (the candidate sets are identical)
+
+
+# ----------------------------------------------------------------------------- P26 matcher (A25)
+def _units(rng, n, d=64):
+    x = rng.normal(size=(n, d))
+    return x / np.linalg.norm(x, axis=1, keepdims=True)
+
+
+def test_match_spec_examples(O):
+    assert "S:L413" in GOLD["match"]["cite"]
+    rng = np.random.default_rng(26)
+    A = _units(rng, 15)
+    m, d1, _, n = O.match(A, A, 0.8)  # identity, distances 0
+    assert n == 15 and np.array_equal(m, np.arange(15)) and np.all(d1 == 0)
+    E = np.eye(64)[:2]
+    m, _, _, n = O.match(E, E, 1.0)  # orthogonal pair, ratio 1: d1 = 0 < d2 = sqrt(2)
+    assert n == 2 and np.array_equal(m, [0, 1])
+    A = _units(rng, 20)
+    p = rng.permutation(20)
+    m, _, _, n = O.match(A, A[p], 0.8)
+    assert n == 20 and np.array_equal(p[m], np.arange(20))
+
+
+def test_match_properties_vs_cdist(O):
+    """Distances equal scipy's cdist (a library routine, not the oracle's loop); the mapping is injective;
+    shrinking the ratio never adds matches; the first/second distances are the row minima of cdist over the
+    non-degenerate columns; degenerate rows never match and are never candidates."""
+    sd = pytest.importorskip("scipy.spatial.distance")
+    rng = np.random.default_rng(27)
+    A = _units(rng, 60)
+    B = np.concatenate([A[rng.permutation(60)[:40]] + 0.15 * rng.normal(size=(40, 64)), _units(rng, 30)])
+    B /= np.linalg.norm(B, axis=1, keepdims=True)
+    B[5] = 0.0  # degenerate
+    A[7] = 0.0
+    D = sd.cdist(A, B)
+    D[:, 5] = np.inf
+    prev = None
+    for ratio in (1.0, 0.9, 0.8, 0.6, 0.3):
+        m, d1, d2, n = O.match(A, B, ratio)
+        ok = m >= 0
+        assert len(set(m[ok])) == ok.sum() == n  # injective
+        assert m[7] == -1 and 5 not in m
+        rows = [i for i in range(60) if i != 7]
+        srt = np.sort(D[rows], axis=1)
+        np.testing.assert_allclose(d1[rows], srt[:, 0], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(d2[rows], srt[:, 1], rtol=0, atol=1e-12)
+        for i in np.nonzero(ok)[0]:
+            j = m[i]
+            assert D[i, j] == D[i].min() and d1[i] < ratio * d2[i]
+            col = D[:, j].copy()
+            col[7] = np.inf
+            assert np.argmin(col) == i  # cross-check
+        if prev is not None:
+            assert set(np.nonzero(ok)[0]) <= prev
+        prev = set(np.nonzero(ok)[0])
+
+
+def test_match_ties_and_edge_cases(O):
+    rng = np.random.default_rng(28)
+    A = _units(rng, 4)
+    B = np.stack([A[1], A[1], A[2], A[3]])  # duplicate nearest: d1 == d2 → the ratio test rejects
+    m, d1, d2, _ = O.match(A, B, 1.0)
+    assert m[1] == -1 and d1[1] == d2[1] == 0.0
+    assert m[2] == 2 and m[3] == 3
+    m, d1, d2, n = O.match(A[:1], A[:1], 0.5)  # a single candidate: d2 = ∞ passes any ratio
+    assert n == 1 and d2[0] == -1.0
+    m, _, _, n = O.match(np.zeros((3, 64)), A, 0.8)
+    assert n == 0 and np.all(m == -1)
+    m, _, _, n = O.match(A, np.zeros((0, 64)), 0.8)
+    assert n == 0 and np.all(m == -1)
