@@ -178,6 +178,21 @@ kaze_status kaze_reset_profile(kaze_ctx* ctx);
 /* Number of kernels this context has launched since creation (or the last reset). */
 int64_t kaze_launch_count(const kaze_ctx* ctx);
 
+/* ---- descriptor matching (reading A25) — context-free ----
+ * Brute-force L2 matching of d_a[na][64] against d_b[nb][64] (fp32, row-major, 16-byte aligned, device):
+ * for each a its nearest and second-nearest non-degenerate (nonzero) b, ties → lower index; kept iff
+ * d1 < ratio·d2 (d2 = ∞ with fewer than two candidates) and a is b's nearest non-degenerate a (cross-check).
+ * d_match[na] ← b or −1; d_dist[na] (may be NULL) ← d1 (−1 if no candidate); d_stats (may be NULL, device
+ * int32[2]) ← [number of matches, rows that needed the exact fallback scan].  The dot products run on the
+ * tensor cores (fp16 operands, fp32 accumulation); candidates are re-ranked with exact fp32 distances and the
+ * result is certified against the fp16 error bound, else the row is rescanned exactly, so the decisions are
+ * the exact fp32 ones.  d_scratch: kaze_match_scratch_bytes(na, nb) bytes of device memory owned by the
+ * caller.  Asynchronous on `stream`.  Errors: INVALID_ARGUMENT (counts < 0, ratio outside (0, 1], null or
+ * misaligned pointers, scratch too small), CUDA. */
+size_t kaze_match_scratch_bytes(int32_t na, int32_t nb);
+kaze_status kaze_match(const float* d_a, int32_t na, const float* d_b, int32_t nb, float ratio, int32_t* d_match,
+                       float* d_dist, void* d_scratch, size_t scratch_bytes, int32_t* d_stats, void* stream);
+
 /* Host-only: the FED cycle the context runs for a level transition of total time T (Eq. 5, A20) —
  * step sizes in execution order (A21) written to taus[0 .. min(n, cap)); returns n (> 0), or
  * KAZE_ERR_INVALID_ARGUMENT for T <= 0, tau_max outside (0, 0.25], or taus == NULL with cap > 0. */

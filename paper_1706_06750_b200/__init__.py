@@ -20,7 +20,7 @@ __all__ = [
     "kaze_default_params", "kaze_create", "kaze_destroy", "kaze_build_scale_space", "kaze_detect",
     "kaze_describe", "kaze_extract", "kaze_extract_host", "kaze_get_k", "kaze_get_level", "kaze_set_level",
     "kaze_set_profiling", "kaze_get_profile", "kaze_reset_profile", "kaze_launch_count", "kaze_abi_version",
-    "kaze_fed_cycle", "Kaze", "PLANE_LT", "PLANE_LX", "PLANE_LY", "PLANE_LDET", "PLANE_COND", "FLAG_KEEP_ANGLE", "FLAG_EXACT_WINDOW", "FLAG_REFINE_3D", "SCHEME_AOS", "SCHEME_FED",
+    "kaze_fed_cycle", "kaze_match_scratch_bytes", "kaze_match", "Kaze", "PLANE_LT", "PLANE_LX", "PLANE_LY", "PLANE_LDET", "PLANE_COND", "FLAG_KEEP_ANGLE", "FLAG_EXACT_WINDOW", "FLAG_REFINE_3D", "SCHEME_AOS", "SCHEME_FED",
     "EXPORTED_SYMBOLS",
 ]
 
@@ -42,7 +42,8 @@ EXPORTED_SYMBOLS = [
     "kaze_default_params", "kaze_create", "kaze_destroy", "kaze_build_scale_space", "kaze_detect",
     "kaze_describe", "kaze_extract", "kaze_extract_host", "kaze_get_k", "kaze_get_level", "kaze_set_level",
     "kaze_set_profiling", "kaze_get_profile", "kaze_reset_profile", "kaze_launch_count",
-    "kaze_status_string", "kaze_last_error", "kaze_abi_version", "kaze_fed_cycle",
+    "kaze_status_string", "kaze_last_error", "kaze_abi_version", "kaze_fed_cycle", "kaze_match_scratch_bytes",
+    "kaze_match",
 ]
 
 
@@ -122,9 +123,12 @@ def lib():
     L.kaze_abi_version.restype = C.c_int32
     L.kaze_fed_cycle.argtypes = [C.c_double, C.c_double, _vp, C.c_int32]
     L.kaze_fed_cycle.restype = C.c_int32
+    L.kaze_match_scratch_bytes.argtypes = [C.c_int32, C.c_int32]
+    L.kaze_match_scratch_bytes.restype = C.c_size_t
+    L.kaze_match.argtypes = [_vp, C.c_int32, _vp, C.c_int32, C.c_float, _vp, _vp, _vp, C.c_size_t, _vp, _vp]
     for name in EXPORTED_SYMBOLS:
         if name not in ("kaze_launch_count", "kaze_status_string", "kaze_last_error", "kaze_abi_version",
-                        "kaze_fed_cycle"):
+                        "kaze_fed_cycle", "kaze_match_scratch_bytes"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -244,6 +248,30 @@ def kaze_launch_count(ctx: int) -> int:
 
 def kaze_abi_version() -> int:
     return int(lib().kaze_abi_version())
+
+
+def kaze_match_scratch_bytes(na: int, nb: int) -> int:
+    return int(lib().kaze_match_scratch_bytes(na, nb))
+
+
+def kaze_match(desc_a, desc_b, ratio: float = 0.8, scratch=None, stream=None):
+    """desc_a [na, 64], desc_b [nb, 64]: float32 CUDA tensors → (match [na] int32, dist [na] float32,
+    stats [2] int32 = [matches, rows rescanned exactly]).  All on the device; nothing is synchronised."""
+    import torch
+
+    na, nb = int(desc_a.shape[0]), int(desc_b.shape[0])
+    a = desc_a.contiguous()
+    b = desc_b.contiguous()
+    dev = a.device
+    match = torch.empty(na, dtype=torch.int32, device=dev)
+    dist = torch.empty(na, dtype=torch.float32, device=dev)
+    stats = torch.zeros(2, dtype=torch.int32, device=dev)
+    need = kaze_match_scratch_bytes(na, nb)
+    if scratch is None or scratch.numel() < need:
+        scratch = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+    _check(lib().kaze_match(_ptr(a) if na else None, na, _ptr(b) if nb else None, nb, ratio, _ptr(match),
+                            _ptr(dist), _ptr(scratch), scratch.numel(), _ptr(stats), _stream(stream)), "kaze_match")
+    return match, dist, stats
 
 
 def kaze_fed_cycle(T: float, tau_max: float = 0.25) -> np.ndarray:

@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libkaze_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["stencil.cu", "aos.cu", "fed.cu", "hessian.cu", "detect.cu", "describe.cu", "kaze_api.cu"]
+SOURCES = ["stencil.cu", "aos.cu", "fed.cu", "hessian.cu", "detect.cu", "describe.cu", "match.cu", "kaze_api.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -809,6 +809,25 @@ kaze_status kaze_get_profile(kaze_ctx* c, kaze_kernel_stat* out, int32_t cap, in
 
 int64_t kaze_launch_count(const kaze_ctx* c) { return c ? c->launches : 0; }
 
+size_t kaze_match_scratch_bytes(int32_t na, int32_t nb) {
+    if (na < 0 || nb < 0) return 0;
+    return match_scratch_bytes(na, nb);
+}
+
+kaze_status kaze_match(const float* d_a, int32_t na, const float* d_b, int32_t nb, float ratio, int32_t* d_match,
+                       float* d_dist, void* d_scratch, size_t scratch_bytes, int32_t* d_stats, void* stream) {
+    if (na < 0 || nb < 0 || !(ratio > 0.f && ratio <= 1.f)) return KAZE_ERR_INVALID_ARGUMENT;
+    if ((na > 0 && (!d_a || !d_match)) || (nb > 0 && !d_b)) return KAZE_ERR_INVALID_ARGUMENT;
+    if (na == 0) return KAZE_OK;
+    if (!d_scratch || scratch_bytes < match_scratch_bytes(na, nb)) return KAZE_ERR_INVALID_ARGUMENT;
+    if ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_b) |
+         reinterpret_cast<uintptr_t>(d_scratch)) & 15u)
+        return KAZE_ERR_INVALID_ARGUMENT;
+    const int rc = match_run(d_a, na, d_b, nb, ratio, d_match, d_dist, d_scratch, scratch_bytes, d_stats,
+                             (cudaStream_t)stream);
+    return rc == 0 ? KAZE_OK : KAZE_ERR_CUDA;
+}
+
 int32_t kaze_fed_cycle(double T, double tau_max, float* taus, int32_t cap) {
     if (!(T > 0) || !(tau_max > 0 && tau_max <= 0.25) || cap < 0 || (cap > 0 && !taus)) return KAZE_ERR_INVALID_ARGUMENT;
     const std::vector<float> t = fed_cycle(T, tau_max);

@@ -66,6 +66,12 @@ struct FedTaus {
 bool launch_fed_steps(const float* Lin, size_t s_in, const float* c, size_t s_c, float* Lout, size_t s_out, Geom g,
                       int nimg, const FedTaus& t, int nsteps, cudaStream_t s);
 
+// ---- match.cu ----  
+size_t match_scratch_bytes(int na, int nb);
+// returns 0 or a cudaError_t / −1 (scratch too small); stats (device, optional): [matches, uncertified rows]
+int match_run(const float* A, int na, const float* B, int nb, float ratio, int32_t* match, float* dist,
+              void* scratch, size_t bytes, int* stats, cudaStream_t s);
+
 // ---- hessian.cu ----  (all N levels of nimg images in one launch; level stride = plane)
 // Lxy: interleaved (s·∂x L, s·∂y L) float2 planes, same element strides as the float pyramids.
 void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, int nimg, const LevelTable& lt,

@@ -506,3 +506,84 @@ def test_detector_variants_end_to_end(O, flags, kw):
 def kz_sigma(kps):
     sg = 1.6 * 2.0 ** (kps["octave"].astype(np.float64) + kps["sublevel"].astype(np.float64) / 4)
     return sg
+
+
+# ------------------------------------------------------------------------------------------- matching (§8 f3)
+def _units(rng, n, d=64):
+    x = rng.normal(size=(n, d))
+    return (x / np.linalg.norm(x, axis=1, keepdims=True)).astype(np.float32)
+
+
+def _gpu_match(A, B, ratio):
+    m, d, st = K.kaze_match(torch.from_numpy(np.ascontiguousarray(A, np.float32)).cuda(),
+                            torch.from_numpy(np.ascontiguousarray(B, np.float32)).cuda(), ratio)
+    torch.cuda.synchronize()
+    return m.cpu().numpy(), d.cpu().numpy(), st.cpu().numpy()
+
+
+def test_match_spec_examples_gpu(O):
+    rng = np.random.default_rng(31)
+    A = _units(rng, 300)
+    m, d, st = _gpu_match(A, A, 0.8)
+    assert np.array_equal(m, np.arange(300)) and np.allclose(d, 0, atol=1e-6) and st[0] == 300
+    p = rng.permutation(300)
+    m, _, _ = _gpu_match(A, A[p], 0.8)
+    assert np.array_equal(p[m], np.arange(300))
+    E = np.eye(64, dtype=np.float32)[:2]
+    m, _, _ = _gpu_match(E, E, 1.0)
+    assert np.array_equal(m, [0, 1])
+
+
+@pytest.mark.parametrize("na,nb,ratio", [(3000, 2700, 0.8), (129, 257, 0.9), (1, 1, 0.5), (700, 1, 1.0)])
+def test_match_vs_oracle_synthetic(O, na, nb, ratio):
+    """Perturbed copies + distractors + degenerate rows, ragged sizes: the GPU matcher (tensor-core candidates,
+    exact fp32 re-rank) equals the fp64 oracle on >= 99.9% of rows; every matched distance within 1e-5."""
+    rng = np.random.default_rng(na + nb)
+    A = _units(rng, na)
+    k = min(na, nb) * 2 // 3
+    B = np.concatenate([A[rng.permutation(na)[:k]] + 0.2 * rng.normal(size=(k, 64)).astype(np.float32),
+                        _units(rng, nb - k)]) if nb > 1 else A[:1].copy()
+    B /= np.maximum(np.linalg.norm(B, axis=1, keepdims=True), 1e-30)
+    if na > 10:
+        A[3] = 0.0
+    if nb > 10:
+        B[7] = 0.0
+    mg, dg, st = _gpu_match(A, B, ratio)
+    mo, do, _, no = O.match(A.astype(np.float64), B.astype(np.float64), ratio)
+    assert np.mean(mg == mo) >= 0.999, (np.mean(mg == mo), st)
+    both = (mg >= 0) & (mg == mo)
+    assert np.all(np.abs(dg[both] - do[both]) <= 1e-5)
+    assert len(set(mg[mg >= 0])) == int((mg >= 0).sum())  # injective
+    if na > 10:
+        assert mg[3] == -1
+    if nb > 10:
+        assert 7 not in mg
+
+
+def test_match_kaze_descriptors_vs_oracle(O):
+    """Real M-SURF descriptors (the oracle's, of an image and its translated copy): identical matching."""
+    img = kaze_inputs.synth_image(480, 360, 1234)
+    shifted = np.full_like(img, 0.5)
+    shifted[:, 9:] = img[:, :-9]
+    ra = O.run(img, octaves=3, sublevels=3)
+    rb = O.run(shifted, octaves=3, sublevels=3)
+    A, B = ra["desc"].astype(np.float32), rb["desc"].astype(np.float32)
+    mg, dg, st = _gpu_match(A, B, 0.8)
+    mo, do, _, no = O.match(A.astype(np.float64), B.astype(np.float64), 0.8)
+    assert no > 100
+    assert np.mean(mg == mo) >= 0.999, np.mean(mg == mo)
+    ok = mg >= 0
+    np.testing.assert_allclose(dg[ok], do[ok], atol=1e-5)
+
+
+def test_match_bench_size_vs_oracle(O):
+    """configs[2]-sized sets (~15.6k descriptors each) in the bench's launch configuration."""
+    rng = np.random.default_rng(77)
+    n = 15600
+    A = _units(rng, n)
+    B = A[rng.permutation(n)] + 0.25 * rng.normal(size=(n, 64)).astype(np.float32)
+    B /= np.linalg.norm(B, axis=1, keepdims=True)
+    mg, dg, st = _gpu_match(A, B, 0.8)
+    mo, do, _, no = O.match(A.astype(np.float64), B.astype(np.float64), 0.8)
+    assert np.mean(mg == mo) >= 0.999, np.mean(mg == mo)
+    assert st[1] <= 0.01 * n  # the exact fallback stays rare
