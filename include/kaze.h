@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define KAZE_ABI_VERSION 2
+#define KAZE_ABI_VERSION 3
 
 typedef struct kaze_ctx kaze_ctx;
 
@@ -177,6 +177,24 @@ kaze_status kaze_get_profile(kaze_ctx* ctx, kaze_kernel_stat* out, int32_t cap, 
 kaze_status kaze_reset_profile(kaze_ctx* ctx);
 /* Number of kernels this context has launched since creation (or the last reset). */
 int64_t kaze_launch_count(const kaze_ctx* ctx);
+
+/* Device memory the context holds, by role (the paper's memory-footprint study, P:L424-437,
+ * Fig. "Memory foot print").  Byte counts are exactly the sizes the context passed to cudaMalloc; they depend
+ * only on kaze_params (max_width, max_height, max_batch, octaves, sublevels, k_bins, max_keypoints), not on
+ * the images built since.  The paper's "scratch images L_step" are `scratch` here.  Errors:
+ * INVALID_ARGUMENT if ctx or out is NULL. */
+typedef struct {
+    uint64_t evolution;   /* L_i pyramid: max_batch x N planes (pitch x height fp32, 512 B aligned)   */
+    uint64_t derivatives; /* interleaved (Lx, Ly) pyramid, float2                                      */
+    uint64_t response;    /* Ldet pyramid                                                               */
+    uint64_t scratch;     /* conductivity c and the AOS column result U (or FED ping-pong), per image */
+    uint64_t detector;    /* contrast k, hmax, histograms, fallback flags, candidate bitmap, row scans */
+    uint64_t textures;    /* descriptor texture-object table (allocated at the first kaze_describe)     */
+    uint64_t host_path;   /* kaze_extract_host staging (device side, 2 buffers; 0 until first used)    */
+    uint64_t pinned_host; /* pinned host bytes of kaze_extract_host (0 until first used)               */
+    uint64_t total;       /* sum of the device fields                                                   */
+} kaze_memory;
+kaze_status kaze_memory_footprint(const kaze_ctx* ctx, kaze_memory* out);
 
 /* ---- descriptor matching (reading A25) — context-free ----
  * Brute-force L2 matching of d_a[na][64] against d_b[nb][64] (fp32, row-major, 16-byte aligned, device):

@@ -16,11 +16,15 @@ import numpy as np
 BASE_SEED = 1234
 
 
-def synth_image(width: int, height: int, seed: int = BASE_SEED) -> np.ndarray:
-    """One synthetic image as float32 (height, width) in [0, 1]."""
+def synth_image(width: int, height: int, seed: int = BASE_SEED, complexity: float = 1.0) -> np.ndarray:
+    """One synthetic image as float32 (height, width) in [0, 1].
+
+    ``complexity`` scales the number of shapes and blobs per area (1.0 = the recipe above); the stage-timing
+    sweep uses several values per size, like the paper's "6 images of varying complexity in each
+    dimension" (PAPER.md:L413-415)."""
     W, H = int(width), int(height)
     rng = np.random.default_rng(seed)
-    scale = (W * H) / (640.0 * 480.0)
+    scale = (W * H) / (640.0 * 480.0) * float(complexity)
     n_shapes = max(1, int(round(200 * scale)))
     n_blobs = max(1, int(round(4000 * scale)))
     img = np.full((H, W), 0.5, dtype=np.float64)

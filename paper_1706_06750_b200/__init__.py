@@ -20,7 +20,7 @@ __all__ = [
     "kaze_default_params", "kaze_create", "kaze_destroy", "kaze_build_scale_space", "kaze_detect",
     "kaze_describe", "kaze_extract", "kaze_extract_host", "kaze_get_k", "kaze_get_level", "kaze_set_level",
     "kaze_set_profiling", "kaze_get_profile", "kaze_reset_profile", "kaze_launch_count", "kaze_abi_version",
-    "kaze_fed_cycle", "kaze_match_scratch_bytes", "kaze_match", "Kaze", "PLANE_LT", "PLANE_LX", "PLANE_LY", "PLANE_LDET", "PLANE_COND", "FLAG_KEEP_ANGLE", "FLAG_EXACT_WINDOW", "FLAG_REFINE_3D", "SCHEME_AOS", "SCHEME_FED",
+    "kaze_fed_cycle", "kaze_match_scratch_bytes", "kaze_match", "kaze_memory_footprint", "KazeMemory", "Kaze", "PLANE_LT", "PLANE_LX", "PLANE_LY", "PLANE_LDET", "PLANE_COND", "FLAG_KEEP_ANGLE", "FLAG_EXACT_WINDOW", "FLAG_REFINE_3D", "SCHEME_AOS", "SCHEME_FED",
     "EXPORTED_SYMBOLS",
 ]
 
@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = [
     "kaze_describe", "kaze_extract", "kaze_extract_host", "kaze_get_k", "kaze_get_level", "kaze_set_level",
     "kaze_set_profiling", "kaze_get_profile", "kaze_reset_profile", "kaze_launch_count",
     "kaze_status_string", "kaze_last_error", "kaze_abi_version", "kaze_fed_cycle", "kaze_match_scratch_bytes",
-    "kaze_match",
+    "kaze_match", "kaze_memory_footprint",
 ]
 
 
@@ -85,6 +85,11 @@ class KazeKernelStat(C.Structure):
                 ("algo_bytes", C.c_double)]
 
 
+class KazeMemory(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("evolution", "derivatives", "response", "scratch", "detector", "textures",
+                                          "host_path", "pinned_host", "total")]
+
+
 _lib = None
 _vp = C.c_void_p
 
@@ -115,6 +120,7 @@ def lib():
     L.kaze_get_profile.argtypes = [_vp, P(KazeKernelStat), C.c_int32, P(C.c_int32)]
     L.kaze_reset_profile.argtypes = [_vp]
     L.kaze_launch_count.argtypes = [_vp]
+    L.kaze_memory_footprint.argtypes = [_vp, P(KazeMemory)]
     L.kaze_launch_count.restype = C.c_int64
     L.kaze_status_string.argtypes = [C.c_int]
     L.kaze_status_string.restype = C.c_char_p
@@ -244,6 +250,13 @@ def kaze_get_profile(ctx: int) -> dict:
 
 def kaze_launch_count(ctx: int) -> int:
     return int(lib().kaze_launch_count(ctx))
+
+
+def kaze_memory_footprint(ctx: int) -> dict:
+    """Device bytes the context holds, by role (include/kaze.h kaze_memory)."""
+    m = KazeMemory()
+    _check(lib().kaze_memory_footprint(ctx, C.byref(m)), "kaze_memory_footprint", ctx)
+    return {n: int(getattr(m, n)) for n, _ in KazeMemory._fields_}
 
 
 def kaze_abi_version() -> int:

@@ -218,10 +218,11 @@ __device__ __forceinline__ void chunk_reduce(const float (&dv)[M], const float (
     e.D = fmaf(tq[1], P, dv[0]) * rB;
 }
 
-// Interior of the chunk with x_0 = x0 and x_{M-1} = xl known; writes the samples j0+i < n (stride P floats).
-template <int M>
+// Interior of the chunk with x_0 = x0 and x_{M-1} = xl known; writes the samples j0+i < n at out + o0 + i·P (32-bit
+// element offsets from an opaque base: one IMAD.WIDE per address).  FULL: every sample is inside the line.
+template <int M, bool FULL>
 __device__ __forceinline__ void chunk_finish(float (&dv)[M], float (&tq)[M + 1], float x0, float xl,
-                                             float* __restrict__ out, int P, int nvalid) {
+                                             float* __restrict__ out, unsigned o0, unsigned P, int nvalid) {
     float Fp = x0, G = 0.f;
 #pragma unroll
     for (int i = 1; i < M - 1; ++i) {
@@ -231,13 +232,13 @@ __device__ __forceinline__ void chunk_finish(float (&dv)[M], float (&tq)[M + 1],
         dv[i] = Fp;  // F'_i
         tq[i] = G;   // G_i
     }
-    out[0] = x0;
-    if (M - 1 < nvalid) out[(size_t)(M - 1) * P] = xl;
+    __stwb(out + o0, x0);  // st.global (the opaque base hides the address space)
+    if (FULL || M - 1 < nvalid) __stwb(out + (o0 + (M - 1) * P), xl);
     float xn = xl;
 #pragma unroll
     for (int i = M - 2; i >= 1; --i) {
         xn = fmaf(-tq[i], xn, dv[i]);
-        if (i < nvalid) out[(size_t)i * P] = xn;
+        if (FULL || i < nvalid) __stwb(out + (o0 + i * P), xn);
     }
 }
 
@@ -262,23 +263,41 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_u(const float* __restrict
     const int nvalid = n - j0;  // samples of this chunk inside the line (>= 1 for p < T)
     float dv[M], tq[M + 1];
     ChunkEq e{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    // 32-bit element offsets from opaque per-image bases (the plane is < 2^32 elements)
+    const float* Lb = opaque(L + blockIdx.z * st.L);
+    const float* cb = opaque(c + blockIdx.z * st.c);
+    const unsigned P = (unsigned)g.P, o0 = (unsigned)j0 * P + (unsigned)x;
+    const bool full = nvalid > M;  // all M samples and the next chunk's first sample exist
     if (active) {
-        const float* Lc = L + blockIdx.z * st.L + (size_t)j0 * g.P + x;
-        const float* cc = c + blockIdx.z * st.c + (size_t)j0 * g.P + x;
         float cv[M];
+        float cprev = 0.f, cnext = 0.f;
+        if (full) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) {
-            const bool in = i < nvalid;
-            dv[i] = in ? __ldg(Lc + (size_t)i * g.P) : 0.f;
-            cv[i] = in ? __ldg(cc + (size_t)i * g.P) : 0.f;
+            for (int i = 0; i < M; ++i) {
+                dv[i] = __ldg(Lb + (o0 + i * P));
+                cv[i] = __ldg(cb + (o0 + i * P));
+            }
+            cnext = __ldg(cb + (o0 + M * P));
+        } else {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const bool in = i < nvalid;
+                dv[i] = in ? __ldg(Lb + (o0 + i * P)) : 0.f;
+                cv[i] = in ? __ldg(cb + (o0 + i * P)) : 0.f;
+            }
         }
-        const float cprev = j0 > 0 ? __ldg(cc - g.P) : 0.f;
-        const float cnext = M < nvalid ? __ldg(cc + (size_t)M * g.P) : 0.f;
+        if (j0 > 0) cprev = __ldg(cb + (o0 - P));
         // edge i joins samples j0+i-1 and j0+i; it exists iff 1 <= j0+i <= n-1 (Neumann ends, padding decoupled)
         tq[0] = j0 > 0 ? tau * (cprev + cv[0]) : 0.f;
+        if (full) {
 #pragma unroll
-        for (int i = 1; i < M; ++i) tq[i] = i < nvalid ? tau * (cv[i - 1] + cv[i]) : 0.f;
-        tq[M] = M < nvalid ? tau * (cv[M - 1] + cnext) : 0.f;
+            for (int i = 1; i < M; ++i) tq[i] = tau * (cv[i - 1] + cv[i]);
+            tq[M] = tau * (cv[M - 1] + cnext);
+        } else {
+#pragma unroll
+            for (int i = 1; i < M; ++i) tq[i] = i < nvalid ? tau * (cv[i - 1] + cv[i]) : 0.f;
+            tq[M] = 0.f;
+        }
         chunk_reduce<M>(dv, tq, e);
     }
     const int idx = p * CW + cx;
@@ -306,7 +325,9 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_u(const float* __restrict
     if (!active) return;
     const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
     const float xl = e.lF - e.lG * xnext - e.lH * xf;
-    chunk_finish<M>(dv, tq, xf, xl, U + blockIdx.z * st.out + (size_t)j0 * g.P + x, g.P, nvalid);
+    float* Ub = opaque(U + blockIdx.z * st.out);
+    if (full) chunk_finish<M, true>(dv, tq, xf, xl, Ub, o0, P, nvalid);
+    else chunk_finish<M, false>(dv, tq, xf, xl, Ub, o0, P, nvalid);
 }
 
 // -------------------------------------------------------------------------------------------------------------

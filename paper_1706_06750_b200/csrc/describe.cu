@@ -1,7 +1,7 @@
 // describe.cu — dominant orientation (A14) and 64-D M-SURF (A15).
 //
 // One warp per keypoint over the FLAT list of all keypoints of all levels and images (the paper's load-balancing
-// remedy: "all the image scales are computed at the same time"), persistent grid of 148·k CTAs.
+// remedy: "all the image scales are computed at the same time"), persistent grid of one full wave (occupancy-sized).
 //   orientation: 113 samples at kp + σ(u, v), u² + v² <= 36, spread over the lanes; Gaussian weight
 //                exp(−(u²+v²)/12.5) (std 2.5σ); the weighted (Lx, Ly) vectors go to shared memory; lanes own the
 //                window centres θ_k = 2πk/nwin and sum the vectors within ±π/6; a warp arg-max (first k on
@@ -318,7 +318,18 @@ void init_describe_tables() {
 void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t img_stride, Geom g, int nimg, int N,
                      kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
                      cudaStream_t s) {
-    k_describe<<<148 * 5, 256, 0, s>>>(Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N);
+    // Persistent grid of exactly one wave: the CTAs that fit on every SM at once (registers limit it to 4 of 256
+    // threads).  A grid larger than one wave leaves the surplus CTAs' share of the static keypoint stride to a
+    // second, mostly idle wave (measured: 148·5 CTAs = 1.25 waves).
+    static int grid = 0;
+    if (grid == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_describe, 256, 0);
+        grid = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    k_describe<<<grid, 256, 0, s>>>(Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N);
 }
 
 }  // namespace kz

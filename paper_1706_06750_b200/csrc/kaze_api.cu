@@ -809,6 +809,28 @@ kaze_status kaze_get_profile(kaze_ctx* c, kaze_kernel_stat* out, int32_t cap, in
 
 int64_t kaze_launch_count(const kaze_ctx* c) { return c ? c->launches : 0; }
 
+kaze_status kaze_memory_footprint(const kaze_ctx* c, kaze_memory* out) {
+    if (!c || !out) return KAZE_ERR_INVALID_ARGUMENT;
+    memset(out, 0, sizeof(*out));
+    const uint64_t B = c->p.max_batch, N = c->N, plane = sizeof(float) * c->plane_max;
+    const uint64_t rows = (uint64_t)(N > 2 ? N - 2 : 1) * c->p.max_height * B;
+    const uint64_t cap = (uint64_t)c->p.max_keypoints;
+    out->evolution = plane * N * B;
+    out->derivatives = 2 * plane * N * B;
+    out->response = plane * N * B;
+    out->scratch = 2 * plane * B;
+    out->detector = sizeof(float) * B + sizeof(unsigned) * B + sizeof(int) * B * c->p.k_bins + sizeof(int) * B +
+                    sizeof(uint32_t) * rows * nms_words(c->p.max_width) + 2 * sizeof(int) * rows;
+    out->textures = c->d_texs ? sizeof(cudaTextureObject_t) * B * N : 0;
+    if (c->s_h2d) {
+        out->host_path = 2 * (plane * B + sizeof(kaze_keypoint) * cap * B + sizeof(int) * B + sizeof(float) * 64 * cap * B);
+        out->pinned_host = sizeof(int) * 2 * B;
+    }
+    out->total = out->evolution + out->derivatives + out->response + out->scratch + out->detector + out->textures +
+                 out->host_path;
+    return KAZE_OK;
+}
+
 size_t kaze_match_scratch_bytes(int32_t na, int32_t nb) {
     if (na < 0 || nb < 0) return 0;
     return match_scratch_bytes(na, nb);

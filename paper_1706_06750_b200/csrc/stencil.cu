@@ -85,18 +85,66 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ in,
 // exactly with the vertical G1 pass (they act on different axes and both clamp per axis):
 //   gx = ½ Σ_dy w(dy) Va(clamp(y+dy)),  Va = G1_y * A,  A(x) = Hl(clamp(x+1)) − Hl(clamp(x−1))
 //   gy = ½ [Vb(clamp(y+1)) − Vb(clamp(y−1))],  Vb = G1_y * B,  B(x) = Σ_dx w(dx) Hl(clamp(x+dx))
-// with w = (3, 10, 3)/16.  Phase 1 (one 4-column row segment per item, registers only): three 16-byte loads give
-// L over 12 columns, six Hl values, and A, B for the four columns, stored to shared memory.  Phase 2 (one column
-// × a 14-row chain per thread): vertical G1 of A and B in registers, the vertical Scharr taps, the conductivity,
-// and one coalesced store per row.  Tile 64 x 56 outputs; the 64 shared-memory rows hold image rows
-// clamp(y0 − 4 + r), so every vertical tap reads the clamped row of its virtual coordinate.  (Measured on B200,
-// 256-image 1920x1200 step: 29.8 ms vs 39.3 ms for the earlier 32x32 Ls-tile kernel with three shared passes.)
+// with w = (3, 10, 3)/16.  Phase 1 (one 8-column row segment per item, two items per thread, all eight 16-byte
+// loads issued before any arithmetic): L over 16 columns, ten Hl values, and A, B for the eight columns, stored to
+// shared memory.  Phase 2 (one column × a 14-row chain per thread): vertical G1 of A and B in registers, the
+// vertical Scharr taps, the conductivity, and one coalesced store per row.  Tile 64 x 56 outputs; the 64
+// shared-memory rows hold image rows clamp(y0 − 4 + r), so every vertical tap reads the clamped row of its virtual
+// coordinate.  The diffusivity is a template parameter and interior tiles skip every clamp and store predicate.
+// (Measured on B200, 256-image 1920x1200 step: 4-column segments with per-row loads and a runtime diffusivity
+// switch 30.5 ms — issue-bound at 88 instructions per pixel; the 32x32 Ls-tile kernel with three shared passes
+// 39.3 ms.)
 constexpr int CW2 = 64, CH2 = 56, CR2 = CH2 + 8, CQ2 = 14;
-template <int MODE>
+
+// Phase-1 item: row r of the tile (image row clamp(y0 − 4 + r)), columns xb .. xb+7.
+__device__ __forceinline__ void cond_load16(const float* __restrict__ row, int xb, int W, bool fast, float (&v)[16]) {
+    if (fast) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(row + xb - 4) + q);
+            v[4 * q] = t.x;
+            v[4 * q + 1] = t.y;
+            v[4 * q + 2] = t.z;
+            v[4 * q + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = __ldg(row + clampi(xb - 4 + q, 0, W - 1));
+    }
+}
+
+__device__ __forceinline__ void cond_hpass(const float (&v)[16], const float (&w)[7], int xb, int W, bool fast,
+                                           float* __restrict__ dA, float* __restrict__ dB) {
+    float h[10];  // Hl at columns xb-1 .. xb+8
+#pragma unroll
+    for (int q = 0; q < 10; ++q) {
+        float acc = w[0] * v[q];
+#pragma unroll
+        for (int d = 1; d < 7; ++d) acc = fmaf(w[d], v[q + d], acc);
+        h[q] = acc;
+    }
+    if (!fast) {  // Hl is read at clamped columns: column -1 → 0, columns >= W → W-1
+        if (xb - 1 < 0) h[0] = h[1];
+#pragma unroll
+        for (int q = 1; q < 10; ++q)
+            if (xb - 1 + q > W - 1) h[q] = h[q - 1];
+    }
+    float A[8], B[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        A[i] = h[i + 2] - h[i];
+        B[i] = fmaf(kW0c, h[i] + h[i + 2], kW1c * h[i + 1]);
+    }
+    reinterpret_cast<float4*>(dA)[0] = make_float4(A[0], A[1], A[2], A[3]);
+    reinterpret_cast<float4*>(dA)[1] = make_float4(A[4], A[5], A[6], A[7]);
+    reinterpret_cast<float4*>(dB)[0] = make_float4(B[0], B[1], B[2], B[3]);
+    reinterpret_cast<float4*>(dB)[1] = make_float4(B[4], B[5], B[6], B[7]);
+}
+
+template <int MODE, int DIFF>
 __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size_t in_img_stride,
                                                float* __restrict__ out, size_t out_img_stride, Geom g, GaussTaps t,
-                                               int diffusivity, const float* __restrict__ kval,
-                                               unsigned* __restrict__ hmax_bits) {
+                                               const float* __restrict__ kval, unsigned* __restrict__ hmax_bits) {
     __shared__ __align__(16) float sA[CR2][CW2];
     __shared__ __align__(16) float sB[CR2][CW2];
     __shared__ float red[8];
@@ -107,47 +155,15 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
 #pragma unroll
     for (int d = 0; d < 7; ++d) w[d] = t.w[d];
     {
-        const int sg = tid & 15, xb = x0 + 4 * sg;
-        const bool fast = (xb >= 4) && (xb + 8 <= g.W);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int r = (tid >> 4) + 16 * k;
-            const float* row = src + (size_t)clampi(y0 - 4 + r, 0, g.H - 1) * g.P;
-            float v[12];
-            if (fast) {
-                const float4 a = __ldg(reinterpret_cast<const float4*>(row + xb - 4));
-                const float4 b = __ldg(reinterpret_cast<const float4*>(row + xb));
-                const float4 c = __ldg(reinterpret_cast<const float4*>(row + xb + 4));
-                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-                v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-                v[8] = c.x; v[9] = c.y; v[10] = c.z; v[11] = c.w;
-            } else {
-#pragma unroll
-                for (int q = 0; q < 12; ++q) v[q] = __ldg(row + clampi(xb - 4 + q, 0, g.W - 1));
-            }
-            float h[6];  // Hl at columns xb-1 .. xb+4
-#pragma unroll
-            for (int q = 0; q < 6; ++q) {
-                float acc = 0.f;
-#pragma unroll
-                for (int d = 0; d < 7; ++d) acc = fmaf(w[d], v[q + d], acc);
-                h[q] = acc;
-            }
-            if (!fast) {  // Hl is read at clamped columns: column -1 → 0, columns >= W → W-1
-                if (xb - 1 < 0) h[0] = h[1];
-#pragma unroll
-                for (int q = 1; q < 6; ++q)
-                    if (xb - 1 + q > g.W - 1) h[q] = h[q - 1];
-            }
-            float4 A, B;
-            A.x = h[2] - h[0]; A.y = h[3] - h[1]; A.z = h[4] - h[2]; A.w = h[5] - h[3];
-            B.x = kW0c * (h[0] + h[2]) + kW1c * h[1];
-            B.y = kW0c * (h[1] + h[3]) + kW1c * h[2];
-            B.z = kW0c * (h[2] + h[4]) + kW1c * h[3];
-            B.w = kW0c * (h[3] + h[5]) + kW1c * h[4];
-            *reinterpret_cast<float4*>(&sA[r][4 * sg]) = A;
-            *reinterpret_cast<float4*>(&sB[r][4 * sg]) = B;
-        }
+        const int sg = tid & 7, r0 = tid >> 3, xb = x0 + 8 * sg;
+        const bool fast = (xb >= 4) && (xb + 12 <= g.W);
+        const float* row0 = src + (size_t)clampi(y0 - 4 + r0, 0, g.H - 1) * g.P;
+        const float* row1 = src + (size_t)clampi(y0 - 4 + r0 + 32, 0, g.H - 1) * g.P;
+        float v0[16], v1[16];
+        cond_load16(row0, xb, g.W, fast, v0);
+        cond_load16(row1, xb, g.W, fast, v1);
+        cond_hpass(v0, w, xb, g.W, fast, &sA[r0][8 * sg], &sB[r0][8 * sg]);
+        cond_hpass(v1, w, xb, g.W, fast, &sA[r0 + 32][8 * sg], &sB[r0 + 32][8 * sg]);
     }
     __syncthreads();
     const int cl = tid & 63, q0 = (tid >> 6) * CQ2;  // column, first chain row (tile-relative)
@@ -155,9 +171,9 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
     float va[CQ2 + 2], vb[CQ2 + 2];  // rows q0-1 .. q0+CQ2
 #pragma unroll
     for (int j = 0; j < CQ2 + 2; ++j) {
-        float aa = 0.f, bb = 0.f;
+        float aa = w[0] * sA[q0 + j][cl], bb = w[0] * sB[q0 + j][cl];
 #pragma unroll
-        for (int d = 0; d < 7; ++d) {
+        for (int d = 1; d < 7; ++d) {
             aa = fmaf(w[d], sA[q0 + j + d][cl], aa);
             bb = fmaf(w[d], sB[q0 + j + d][cl], bb);
         }
@@ -170,23 +186,32 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
         ik2 = frcp(k * k);
     }
     float lmax = 0.f;
-    float* dst = out + img * out_img_stride;
+    float* dst = out + img * out_img_stride + (size_t)(y0 + q0) * g.P + x;
+    const bool interior = (y0 > 0) && (y0 + CH2 < g.H) && (x0 + CW2 <= g.W);  // CTA-uniform
+    if (MODE == 1 && interior) {
+#pragma unroll
+        for (int j = 0; j < CQ2; ++j) {
+            const float gx = 0.5f * fmaf(kW0c, va[j] + va[j + 2], kW1c * va[j + 1]);
+            const float gy = 0.5f * (vb[j + 2] - vb[j]);
+            dst[(size_t)j * g.P] = diffusivity_g(fmaf(gx, gx, gy * gy) * ik2, DIFF);
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < CQ2; ++j) {
         const int y = y0 + q0 + j;
         const bool top = (y == 0), bot = (y >= g.H - 1);
         const float aup = top ? va[j + 1] : va[j], adn = bot ? va[j + 1] : va[j + 2];
         const float bup = top ? vb[j + 1] : vb[j], bdn = bot ? vb[j + 1] : vb[j + 2];
-        const float gx = 0.5f * (kW0c * (aup + adn) + kW1c * va[j + 1]);
+        const float gx = 0.5f * fmaf(kW0c, aup + adn, kW1c * va[j + 1]);
         const float gy = 0.5f * (bdn - bup);
-        const float g2 = gx * gx + gy * gy;
+        const float g2 = fmaf(gx, gx, gy * gy);
         if (x < g.W && y < g.H) {
             if (MODE == 0) {
-                dst[(size_t)y * g.P + x] = g2;
+                dst[(size_t)j * g.P] = g2;
                 if (x >= 1 && x <= g.W - 2 && y >= 1 && y <= g.H - 2) lmax = fmaxf(lmax, sqrtf(g2));
             } else {
-                const float qv = g2 * ik2;
-                dst[(size_t)y * g.P + x] = diffusivity_g(qv, diffusivity);
+                dst[(size_t)j * g.P] = diffusivity_g(g2 * ik2, DIFF);
             }
         }
     }
@@ -296,10 +321,15 @@ void launch_cond(const float* L, size_t in_img_stride, float* out, size_t out_im
                  cudaStream_t s) {
     // G(σ=1) always has radius 3 (A6), which k_cond2's 7-tap loops and 4-row halo assume
     dim3 grid((g.W + CW2 - 1) / CW2, (g.H + CH2 - 1) / CH2, nimg);
-    if (mode == 0)
-        k_cond2<0><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval, hmax_bits);
-    else
-        k_cond2<1><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, diffusivity, kval, hmax_bits);
+    if (mode == 0) {
+        k_cond2<0, 2><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits);
+        return;
+    }
+    switch (diffusivity) {
+        case 1: k_cond2<1, 1><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
+        case 3: k_cond2<1, 3><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
+        default: k_cond2<1, 2><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
+    }
 }
 
 void launch_khist(const float* g2, size_t img_stride, Geom g, int nimg, int bins, const unsigned* hmax_bits, int* hist,

@@ -70,7 +70,7 @@ def test_defaults_and_status_strings(K):
     lib = K.lib()
     for st in (0, -1, -2, -3, -4, -5, -6):
         assert lib.kaze_status_string(st)
-    assert K.kaze_abi_version() == 2
+    assert K.kaze_abi_version() == 3
     assert (p.scheme, p.tau_max) == (K.SCHEME_AOS, 0.25)
 
 

@@ -322,6 +322,32 @@ def test_profile_counts_launches():
     kz.close()
 
 
+def test_memory_footprint_accounts_for_the_arena():
+    """kaze_memory_footprint's device total is what kaze_create + the first describe / host
+    extract allocate (cudaMemGetInfo drop, up to the allocator's 2 MiB granularity per buffer), and the pyramid
+    terms scale with max_batch x N planes."""
+    W, H = 640, 480
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    kz = make(W, H, batch=2, max_keypoints=4096)
+    img = torch.from_numpy(kaze_inputs.synth_image(W, H)).cuda()[None]
+    kz.extract(img)
+    kps = np.zeros((1, 4096, 8), np.int32)
+    cnt = np.zeros(1, np.int32)
+    K.kaze_extract_host(kz.ctx, np.ascontiguousarray(img.cpu().numpy()), kps, cnt)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    m = K.kaze_memory_footprint(kz.ctx)
+    plane = 4 * ((((W + 31) // 32 * 32) * H + 127) // 128 * 128)
+    assert m["evolution"] == m["response"] == plane * 16 * 2 and m["derivatives"] == 2 * m["evolution"]
+    assert m["scratch"] == 2 * plane * 2 and m["textures"] > 0 and m["host_path"] > 0
+    assert m["total"] == sum(m[k] for k in ("evolution", "derivatives", "response", "scratch", "detector",
+                                             "textures", "host_path"))
+    drop = free0 - free1  # torch's own tensors above are small next to the arena
+    assert m["total"] <= drop + (8 << 20) and drop <= m["total"] + 64 * (2 << 20) + (16 << 20), (m, drop)
+    kz.close()
+
+
 # ------------------------------------------------------------------------------------------- full sizes
 @pytest.mark.slow
 def test_full_size_1920x1200_in_bench_launch_configuration(O):
