@@ -129,6 +129,43 @@ __device__ __forceinline__ void nms_row(float (&w)[LB + 2][3], const float* __re
         N8[q] = fmaxf(lr, fmaxf(up, dn));
     }
     const bool inside = lane >= 1 && lane <= STRIP && x >= 1 && x <= W - 2 && y >= 1 && y <= H - 2;
+    if constexpr (!EXT) {
+        // Default detector: per centre one FMNMX3 + FMNMX + compare + ballot; the rare candidates of every centre
+        // are refined in one branch after all ballots, and lane c−1 stores centre c's bitmap word.
+        uint32_t bits[LB], anyb = 0u;
+#pragma unroll
+        for (int c = 1; c <= LB; ++c) {
+            const float v = w[c][(PH + 1) % 3];
+            const float nb = fmaxf(fmaxf(N8[c], M[c - 1]), fmaxf(M[c + 1], dp.threshold));
+            bits[c - 1] = c <= nc ? __ballot_sync(0xffffffffu, inside && v > nb) : 0u;
+            anyb |= bits[c - 1];
+        }
+        if (anyb) {  // warp-uniform and rare: the level's 3x3 patch by shuffles, edge test and 2-D fit
+#pragma unroll
+            for (int c = 1; c <= LB; ++c) {
+                if (!bits[c - 1]) continue;  // warp-uniform
+                const float v = w[c][(PH + 1) % 3];
+                const float u0 = w[c][PH % 3], u2 = w[c][(PH + 2) % 3];
+                const float l0s = __shfl_up_sync(0xffffffffu, u0, 1), l1 = __shfl_up_sync(0xffffffffu, v, 1);
+                const float l2 = __shfl_up_sync(0xffffffffu, u2, 1);
+                const float r0 = __shfl_down_sync(0xffffffffu, u0, 1), r1 = __shfl_down_sync(0xffffffffu, v, 1);
+                const float r2 = __shfl_down_sync(0xffffffffu, u2, 1);
+                bool k = (bits[c - 1] >> lane) & 1u;
+                if (k) {
+                    const float patch[3][3] = {{l0s, u0, r0}, {l1, v, r1}, {l2, u2, r2}};
+                    float ox, oy;
+                    k = refine(patch, dp.edge_ratio, ox, oy);
+                }
+                bits[c - 1] = __ballot_sync(0xffffffffu, k);
+            }
+        }
+        uint32_t mine = 0u;
+#pragma unroll
+        for (int c = 1; c <= LB; ++c)
+            if (lane == c - 1) mine = bits[c - 1];
+        if (lane < nc) bm[(size_t)lane * lvl_stride + (size_t)y * words] = (mine >> 1) & ((1u << STRIP) - 1u);
+        return;
+    }
 #pragma unroll
     for (int c = 1; c <= LB; ++c) {
         if (c > nc) break;  // warp-uniform
@@ -171,17 +208,6 @@ __device__ __forceinline__ void nms_row(float (&w)[LB + 2][3], const float* __re
                     k = refine(patch, dp.edge_ratio, ox, oy);
                 }
             }
-        } else if (!EXT && __any_sync(0xffffffffu, k)) {  // rare: the level's 3x3 patch by shuffles, then the fit
-            const float u0 = w[c][PH % 3], u2 = w[c][(PH + 2) % 3];
-            const float l0s = __shfl_up_sync(0xffffffffu, u0, 1), l1 = __shfl_up_sync(0xffffffffu, v, 1);
-            const float l2 = __shfl_up_sync(0xffffffffu, u2, 1);
-            const float r0 = __shfl_down_sync(0xffffffffu, u0, 1), r1 = __shfl_down_sync(0xffffffffu, v, 1);
-            const float r2 = __shfl_down_sync(0xffffffffu, u2, 1);
-            if (k) {
-                const float patch[3][3] = {{l0s, u0, r0}, {l1, v, r1}, {l2, u2, r2}};
-                float ox, oy;
-                k = refine(patch, dp.edge_ratio, ox, oy);
-            }
         }
         const uint32_t bits = __ballot_sync(0xffffffffu, k);
         if (lane == 0) bm[(size_t)(c - 1) * lvl_stride + (size_t)y * words] = (bits >> 1) & ((1u << STRIP) - 1u);
@@ -189,7 +215,7 @@ __device__ __forceinline__ void nms_row(float (&w)[LB + 2][3], const float* __re
 }
 
 template <int LB, bool EXT>
-__global__ void __launch_bounds__(256) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
+__global__ void __launch_bounds__(256, EXT ? 1 : 4) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
                                                   DetectParams dp, LevelTable lt, uint32_t* __restrict__ bitmap,
                                                   int words) {
     const int lane = threadIdx.x & 31;
