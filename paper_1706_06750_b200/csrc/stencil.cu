@@ -6,6 +6,8 @@
 //               Mode 0 (level 1) writes |∇|² and the image maximum of |∇| for the k histogram.
 //  * khist / kfinal: 300-bin histogram of |∇| over the interior, percentile → k on the device
 //               (A7), no host round trip.
+#include <algorithm>
+
 #include "kaze_internal.cuh"
 
 namespace kz {
@@ -228,34 +230,36 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
 }
 
 // -------------------------------------------------------------------------------------------------
-// Histogram of |∇| over the interior (A7): warp-aggregated shared-memory atomics, one global add per bin.
+// Histogram of |∇| over the interior (A7): rows are dealt to the CTAs, each warp counts into its own shared-memory
+// sub-histogram with plain shared atomics (bins <= 1024; one shared histogram above), one global add per bin.
+// bin = min(floor(bins·|∇| / hmax), bins − 1) for |∇| > 0, IEEE sqrt and division (the same decision as before).
+// (Measured on B200, 256-image 1920x1200 step: a flattened interior index with an integer division per pixel and
+// __match_any_sync aggregation took 4.1 ms.)
 __global__ void __launch_bounds__(256) k_khist(const float* __restrict__ g2buf, size_t img_stride, Geom g, int bins,
                                                const unsigned* __restrict__ hmax_bits, int* __restrict__ hist) {
     extern __shared__ int sh[];
     const int img = blockIdx.y;
-    for (int i = threadIdx.x; i < bins; i += blockDim.x) sh[i] = 0;
+    const bool per_warp = bins <= 1024;
+    const int nsub = per_warp ? 8 : 1;
+    for (int i = threadIdx.x; i < bins * nsub; i += blockDim.x) sh[i] = 0;
     __syncthreads();
+    int* mine = sh + (per_warp ? (threadIdx.x >> 5) * bins : 0);
     const float hmax = __uint_as_float(hmax_bits[img]);
     const float fb = (float)bins;
     const float* src = g2buf + img * img_stride;
-    const int iw = g.W - 2, ih = g.H - 2;
-    const long long total = (long long)iw * ih;
-    const unsigned lane = threadIdx.x & 31;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < total; base += (long long)gridDim.x * blockDim.x) {
-        long long i = base + threadIdx.x;
-        int b = -1;
-        if (i < total) {
-            int y = 1 + (int)(i / iw), x = 1 + (int)(i % iw);
-            float gm = sqrtf(src[(size_t)y * g.P + x]);
-            if (gm > 0.f) b = min((int)floorf(fb * gm / hmax), bins - 1);
+    for (int y = 1 + blockIdx.x; y <= g.H - 2; y += gridDim.x) {
+        const float* row = src + (size_t)y * g.P;
+        for (int x = 1 + threadIdx.x; x <= g.W - 2; x += blockDim.x) {
+            const float gm = sqrtf(__ldg(row + x));
+            if (gm > 0.f) atomicAdd(mine + min((int)floorf(fb * gm / hmax), bins - 1), 1);
         }
-        unsigned peers = __match_any_sync(0xffffffffu, b);
-        int leader = __ffs(peers) - 1;
-        if (b >= 0 && (int)lane == leader) atomicAdd(&sh[b], __popc(peers));
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < bins; i += blockDim.x)
-        if (sh[i]) atomicAdd(&hist[img * bins + i], sh[i]);
+    for (int i = threadIdx.x; i < bins; i += blockDim.x) {
+        int v = 0;
+        for (int w = 0; w < nsub; ++w) v += sh[w * bins + i];
+        if (v) atomicAdd(&hist[img * bins + i], v);
+    }
 }
 
 // Percentile → k = hmax·(b+1)/bins with b the first bin whose cumulative count reaches floor(perc·n).
@@ -334,10 +338,10 @@ void launch_cond(const float* L, size_t in_img_stride, float* out, size_t out_im
 
 void launch_khist(const float* g2, size_t img_stride, Geom g, int nimg, int bins, const unsigned* hmax_bits, int* hist,
                   cudaStream_t s) {
-    long long total = (long long)(g.W - 2) * (g.H - 2);
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > 148) blocks = 148;
-    k_khist<<<dim3(blocks, nimg), 256, sizeof(int) * bins, s>>>(g2, img_stride, g, bins, hmax_bits, hist);
+    int blocks = std::min(g.H - 2, 296);  // two CTAs per SM per image batch is plenty for a 4 B/px read
+    if (blocks < 1) blocks = 1;
+    const size_t smem = sizeof(int) * bins * (bins <= 1024 ? 8 : 1);
+    k_khist<<<dim3(blocks, nimg), 256, smem, s>>>(g2, img_stride, g, bins, hmax_bits, hist);
 }
 
 void launch_kfinal(const int* hist, int bins, const unsigned* hmax_bits, int nimg, double perc, double k_override,
