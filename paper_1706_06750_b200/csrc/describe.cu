@@ -7,9 +7,12 @@
 //                window centres θ_k = 2πk/nwin and sum the vectors within ±π/6; a warp arg-max (first k on
 //                ties) picks the longest sum; angle = atan2 of it in [0, 2π).
 //   M-SURF:      24 x 24 samples at step σ rotated by the angle, bilinear (Lx, Ly) rotated into the keypoint
-//                frame (du, dv) and staged in shared memory; lane pair (2·sr, 2·sr+1) accumulates subregion sr's 9 x 9
-//                window (Gaussian std 2.5 about its centre), the 4x4 mask (std 1.5) weights it, the warp
-//                normalises the 64-vector and writes it with 16-byte stores.
+//                frame (du, dv); lane t < 24 walks grid line t in registers and keeps, per subregion along the walk,
+//                the line sums weighted by the separable Gaussian (std 2.5 about the subregion centre); a cross-line
+//                pass over shared memory sums 9 lines per subregion, the 4x4 mask (std 1.5) weights it, the warp
+//                normalises the 64-vector and writes it with coalesced stores.  (Measured on B200: staging all 576
+//                samples in shared memory and summing 9 x 9 windows per lane pair cost 2-way bank conflicts on
+//                every access — 47% of the kernel's shared wavefronts — and 26.4 ms per 256-image step.)
 #include "kaze_internal.cuh"
 
 namespace kz {
@@ -18,7 +21,7 @@ namespace {
 
 constexpr int kOriSamples = 113;
 __constant__ float c_ori_u[kOriSamples], c_ori_v[kOriSamples], c_ori_w[kOriSamples];
-__constant__ float c_w1[81];  // exp(-((i-4)^2 + (j-4)^2) / (2 * 2.5^2)), i, j = 0..8
+__constant__ float c_g1[9];   // exp(-(i-4)^2 / (2 * 2.5^2)), i = 0..8: w1(i, j) = g1(i)·g1(j) (separable, A15)
 __constant__ float c_w2[16];  // exp(-((a-1.5)^2 + (b-1.5)^2) / (2 * 1.5^2)), index 4b + a
 
 constexpr float kTwoPi = 6.283185307179586f;
@@ -38,7 +41,8 @@ __device__ __forceinline__ float2 bilinear2(const float2* __restrict__ img, int 
 }
 
 constexpr int kWarps = 8;
-constexpr int kSP = 25;         // pitch of the staged 24 x 24 M-SURF samples
+constexpr int kLP = 17;         // pitch of the staged per-line subregion sums (24 lines x 16)
+constexpr int kWarpBuf = 640;   // floats of shared scratch per warp (orientation sort: 612)
 constexpr int kMaxBinWin = 48;  // binned orientation path: nwin % 6 == 0 and nwin <= 48 (2·nwin <= 96 bins)
 
 __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy,
@@ -46,7 +50,7 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
                                                   const int* __restrict__ counts, int cap, float* __restrict__ desc,
                                                   int nwin, int keep_angle, int N) {
     __shared__ int pre[kMaxBatch + 1];
-    __shared__ __align__(16) float sbuf[kWarps][2 * kSP * 24];
+    __shared__ __align__(16) float sbuf[kWarps][kWarpBuf];
     if (threadIdx.x == 0) {
         int r = 0;
         for (int i = 0; i < nimg; ++i) {
@@ -59,7 +63,6 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
     const int total = pre[nimg];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sx = sbuf[warp];
-    float* sy = sx + kSP * 24;
     for (int f = blockIdx.x * kWarps + warp; f < total; f += gridDim.x * kWarps) {
         int img = 0;
         while (img + 1 < nimg && pre[img + 1] <= f) ++img;  // nimg is small
@@ -234,54 +237,61 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
         // ---- M-SURF ----
         float si, co;
         sincosf(angle, &si, &co);
-        // lanes walk the rotated axis that runs closest to image x, so a warp's gathers share cache lines
+        // Grid sample (p, q) sits at u = p − 11.5, v = q − 11.5 (steps of σ, keypoint frame).  Lane t < 24 owns one
+        // grid line across the rotated axis that runs closest to image x (lanes along u when |cos| >= |sin|), so the
+        // warp's 24 gathers of a step lie on one line and share cache lines; it walks the line's 24 samples and, as
+        // the subregion weight is separable (w1(i, j) = g(i)·g(j), g(i) = exp(−(i−4)²/12.5)), accumulates g-weighted
+        // line sums of the four subregions along the walk.  The cross-line pass then sums 9 lines per subregion.
         const bool u_fast = fabsf(co) >= fabsf(si);
-#pragma unroll 6
-        for (int s = lane; s < 576; s += 32) {
-            const int hi = s / 24, lo = s - hi * 24;
-            const int p = u_fast ? lo : hi, q = u_fast ? hi : lo;
-            const float u = (float)p - 11.5f, v = (float)q - 11.5f;
-            const float px = x + sigma * (u * co - v * si);
-            const float py = y + sigma * (u * si + v * co);
-            // hardware bilinear filtering (texel centres at +0.5; clamped addressing = clamped taps, A14/A16)
-            const float2 gv = tex2D<float2>(tex, px + 0.5f, py + 0.5f);
-            const float gx = gv.x, gy = gv.y;
-            sx[p * kSP + q] = gx * co + gy * si;  // pitch 25: conflict-free for lanes along p or q
-            sy[p * kSP + q] = -gx * si + gy * co;
+        float acc[4][4];  // [subregion along the walk][Σdu, Σdv, Σ|du|, Σ|dv|]
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) acc[r][q4] = 0.f;
+        if (lane < 24) {
+#pragma unroll
+            for (int t = 0; t < 24; ++t) {
+                const int p = u_fast ? lane : t, q = u_fast ? t : lane;
+                const float u = (float)p - 11.5f, v = (float)q - 11.5f;
+                const float px = x + sigma * (u * co - v * si);
+                const float py = y + sigma * (u * si + v * co);
+                // hardware bilinear filtering (texel centres at +0.5; clamped addressing = clamped taps, A14/A16)
+                const float2 gv = tex2D<float2>(tex, px + 0.5f, py + 0.5f);
+                const float du = gv.x * co + gv.y * si, dv = -gv.x * si + gv.y * co;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int i = t - 5 * r;  // compile-time: sample t is row i of subregion r iff 0 <= i <= 8
+                    if (i < 0 || i > 8) continue;
+                    const float wg = c_g1[i];
+                    acc[r][0] = fmaf(wg, du, acc[r][0]);
+                    acc[r][1] = fmaf(wg, dv, acc[r][1]);
+                    acc[r][2] = fmaf(wg, fabsf(du), acc[r][2]);
+                    acc[r][3] = fmaf(wg, fabsf(dv), acc[r][3]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) sx[lane * kLP + 4 * r + q4] = acc[r][q4];
         }
         __syncwarp();
-        const int sr = lane >> 1, half = lane & 1;
-        const int a = sr & 3, b = sr >> 2;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        for (int i = half; i < 9; i += 2) {
-            const int p = 5 * a + i;
+        // output o = 4(4b + a) + j (A15): lane L computes o = L and o = L + 32
+        float ov[2];
 #pragma unroll
-            for (int j = 0; j < 9; ++j) {
-                const int q = 5 * b + j;
-                const float w = c_w1[i * 9 + j];
-                const float du = w * sx[p * kSP + q], dv = w * sy[p * kSP + q];
-                s0 += du;
-                s1 += dv;
-                s2 += fabsf(du);
-                s3 += fabsf(dv);
-            }
+        for (int h = 0; h < 2; ++h) {
+            const int o = lane + 32 * h, sr = o >> 2, j = o & 3, a = sr & 3, b = sr >> 2;
+            const int l = u_fast ? a : b, r = u_fast ? b : a;  // subregion index across lines / along the walk
+            float sum = 0.f;
+#pragma unroll
+            for (int i = 0; i < 9; ++i) sum = fmaf(c_g1[i], sx[(5 * l + i) * kLP + 4 * r + j], sum);
+            ov[h] = sum * c_w2[sr];
         }
-        s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
-        s3 += __shfl_xor_sync(0xffffffffu, s3, 1);
-        const float w2 = c_w2[sr];
-        s0 *= w2;
-        s1 *= w2;
-        s2 *= w2;
-        s3 *= w2;
-        float n2 = half == 0 ? s0 * s0 + s1 * s1 + s2 * s2 + s3 * s3 : 0.f;
+        float n2 = ov[0] * ov[0] + ov[1] * ov[1];
         for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
         const float inv = n2 > 0.f ? rsqrtf(n2) : 0.f;
-        if (half == 0) {
-            float4 out = make_float4(s0 * inv, s1 * inv, s2 * inv, s3 * inv);
-            reinterpret_cast<float4*>(desc + ((size_t)img * cap + k) * 64)[sr] = out;
-        }
+        float* dk = desc + ((size_t)img * cap + k) * 64;
+        dk[lane] = ov[0] * inv;
+        dk[lane + 32] = ov[1] * inv;
         if (lane == 0 && !keep_angle) {
             kp->angle = angle;
             kp->flags = flags;
@@ -303,15 +313,14 @@ void init_describe_tables() {
             w[n] = (float)exp(-(double)(uu * uu + vv * vv) / 12.5);
             ++n;
         }
-    float w1[81], w2[16];
-    for (int i = 0; i < 9; ++i)
-        for (int j = 0; j < 9; ++j) w1[i * 9 + j] = (float)exp(-(double)((i - 4) * (i - 4) + (j - 4) * (j - 4)) / 12.5);
+    float g1[9], w2[16];
+    for (int i = 0; i < 9; ++i) g1[i] = (float)exp(-(double)((i - 4) * (i - 4)) / 12.5);
     for (int b = 0; b < 4; ++b)
         for (int a = 0; a < 4; ++a) w2[4 * b + a] = (float)exp(-((a - 1.5) * (a - 1.5) + (b - 1.5) * (b - 1.5)) / 4.5);
     cudaMemcpyToSymbol(c_ori_u, u, sizeof(u));
     cudaMemcpyToSymbol(c_ori_v, v, sizeof(v));
     cudaMemcpyToSymbol(c_ori_w, w, sizeof(w));
-    cudaMemcpyToSymbol(c_w1, w1, sizeof(w1));
+    cudaMemcpyToSymbol(c_g1, g1, sizeof(g1));
     cudaMemcpyToSymbol(c_w2, w2, sizeof(w2));
 }
 
