@@ -19,7 +19,9 @@
 //            stream L, c and U, and it writes L_i = ½(U + V) with 16-byte stores.  (Measured on B200, 256-image
 //            1920x1200 step: this order and kernel 34.7 + 25.0 ms vs 58.3 + 22.9 ms for rows-first with a
 //            three-value column kernel; earlier column variants — TMA-pipelined persistent strips, three
-//            register-light passes, re-mapped warp SPIKE — were slower still.)
+//            register-light passes, re-mapped warp SPIKE — were slower still.  Two columns per thread in packed
+//            fp32x2 (FFMA2/FMUL2, M = 10 to fit 64 registers) issued 35 instead of 55 instructions per pixel but
+//            ran 42.0 vs 32.2 ms: twice the chunks make the shared-memory PCR (7 steps, float2) the bottleneck.)
 //   rows:    one CTA (4 or 8 warps) per row.  The TMA engine streams the row's L, c and U into shared memory (1-D
 //            bulk copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is
 //            solved by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve).

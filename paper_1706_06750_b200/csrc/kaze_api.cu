@@ -5,6 +5,7 @@
 // oracle/ (DESIGN.md §2).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -808,6 +809,17 @@ kaze_status kaze_get_profile(kaze_ctx* c, kaze_kernel_stat* out, int32_t cap, in
 }
 
 int64_t kaze_launch_count(const kaze_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"
+
+namespace kz {
+int tune_knob(const char* name, int def) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : def;
+}
+}  // namespace kz
+
+extern "C" {
 
 kaze_status kaze_memory_footprint(const kaze_ctx* c, kaze_memory* out) {
     if (!c || !out) return KAZE_ERR_INVALID_ARGUMENT;

@@ -31,6 +31,9 @@ struct LevelTable {          // per-level scalars passed by value to whole-pyram
     float sigma[kMaxLevels]; // σ_i
 };
 
+// Debug/tuning knob read once from the environment (A/B runs only; the defaults are the measured best).
+int tune_knob(const char* name, int def);
+
 // ---- stencil.cu ----
 void launch_prefilter(const float* img, int64_t in_pitch, size_t in_img_stride, float* L0,
                       size_t out_img_stride, Geom g, int nimg, const GaussTaps& t, cudaStream_t s);
