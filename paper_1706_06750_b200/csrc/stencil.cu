@@ -143,6 +143,61 @@ __device__ __forceinline__ void cond_hpass(const float (&v)[16], const float (&w
     reinterpret_cast<float4*>(dB)[1] = make_float4(B[4], B[5], B[6], B[7]);
 }
 
+// Phase 2 of the conductivity pass in packed fp32x2 (FFMA2/FMUL2 on sm_100a): thread = (column pair cp, 7-row
+// group); the vertical G1 of A and B slides down a 7-row register window of the pair's shared-memory columns (one
+// 8-byte load per array and row), so each output row costs 2 loads + 14 FFMA2 + the epilogue for two pixels.
+// Operation order per component is the scalar order (same rounding).
+__device__ __forceinline__ float2 c2(float a) { return make_float2(a, a); }
+
+template <int DIFF>
+__device__ __forceinline__ void cond_vpass_x2(const float (*sA)[CW2], const float (*sB)[CW2], const float (&w)[7],
+                                              float* __restrict__ dst, Geom g, int x0, int y0, int tid, float ik2) {
+    constexpr int RG = 7;  // output rows per thread (8 groups x 7 = CH2)
+    const int cp = tid & 31, q0 = (tid >> 5) * RG;
+    const int x = x0 + 2 * cp;
+    float2 wa[7], wb[7];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        wa[d] = *reinterpret_cast<const float2*>(&sA[q0 + d][2 * cp]);
+        wb[d] = *reinterpret_cast<const float2*>(&sB[q0 + d][2 * cp]);
+    }
+    const bool interior = (y0 > 0) && (y0 + CH2 < g.H) && (x0 + CW2 <= g.W);  // CTA-uniform
+    const float2 ik = c2(ik2);
+    float2 va0 = c2(0.f), va1 = c2(0.f), vb0 = c2(0.f), vb1 = c2(0.f);  // va/vb at window rows j-2, j-1
+#pragma unroll
+    for (int j = 0; j < RG + 2; ++j) {  // va_j, vb_j at tile row q0 - 1 + j
+        wa[(j + 6) % 7] = *reinterpret_cast<const float2*>(&sA[q0 + j + 6][2 * cp]);
+        wb[(j + 6) % 7] = *reinterpret_cast<const float2*>(&sB[q0 + j + 6][2 * cp]);
+        float2 a = __fmul2_rn(c2(w[0]), wa[j % 7]), b = __fmul2_rn(c2(w[0]), wb[j % 7]);
+#pragma unroll
+        for (int d = 1; d < 7; ++d) {
+            a = __ffma2_rn(c2(w[d]), wa[(j + d) % 7], a);
+            b = __ffma2_rn(c2(w[d]), wb[(j + d) % 7], b);
+        }
+        if (j >= 2) {  // output row r = j - 2 (tile row q0 + r): va at rows r-1, r, r+1 = va0, va1, a
+            const int r = j - 2, y = y0 + q0 + r;
+            float2 aup = va0, adn = a, bup = vb0, bdn = b;
+            if (!interior) {
+                if (y == 0) { aup = va1; bup = vb1; }
+                if (y >= g.H - 1) { adn = va1; bdn = vb1; }
+            }
+            const float2 gx = __fmul2_rn(c2(0.5f), __ffma2_rn(c2(kW0c), __fadd2_rn(aup, adn), __fmul2_rn(c2(kW1c), va1)));
+            const float2 gy = __fmul2_rn(c2(0.5f), __fadd2_rn(bdn, make_float2(-bup.x, -bup.y)));
+            const float2 q = __fmul2_rn(__ffma2_rn(gx, gx, __fmul2_rn(gy, gy)), ik);
+            const float2 cv = make_float2(diffusivity_g(q.x, DIFF), diffusivity_g(q.y, DIFF));
+            float* o = dst + (unsigned)(y * g.P + x);  // dst is opaque: one IMAD.WIDE per row
+            if (interior) {
+                __stwb(reinterpret_cast<float2*>(o), cv);
+            } else if (y < g.H) {
+                if (x + 1 < g.W) __stwb(reinterpret_cast<float2*>(o), cv);
+                else if (x < g.W) __stwb(o, cv.x);
+            }
+        }
+        va0 = va1; va1 = a;
+        vb0 = vb1; vb1 = b;
+    }
+}
+
 template <int MODE, int DIFF>
 __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size_t in_img_stride,
                                                float* __restrict__ out, size_t out_img_stride, Geom g, GaussTaps t,
@@ -168,6 +223,10 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
         cond_hpass(v1, w, xb, g.W, fast, &sA[r0 + 32][8 * sg], &sB[r0 + 32][8 * sg]);
     }
     __syncthreads();
+    if constexpr (MODE == 1) {
+        cond_vpass_x2<DIFF>(sA, sB, w, opaque(out + img * out_img_stride), g, x0, y0, tid, frcp(kval[img] * kval[img]));
+        return;
+    }
     const int cl = tid & 63, q0 = (tid >> 6) * CQ2;  // column, first chain row (tile-relative)
     const int x = x0 + cl;
     float va[CQ2 + 2], vb[CQ2 + 2];  // rows q0-1 .. q0+CQ2
