@@ -84,6 +84,10 @@ typedef struct {
  * 3x3x3 block instead of the 2-D fit; σ = σ_i·2^{δs/S} (A23). */
 #define KAZE_FLAG_EXACT_WINDOW 2
 #define KAZE_FLAG_REFINE_3D 4
+/* kaze_extract / kaze_extract_host replay each (inputs, outputs, sizes, stream) chunk they have seen twice as one
+ * CUDA graph (captured on a private stream, launched on the caller's); this flag disables that (every kernel is
+ * launched directly).  Profiling (kaze_set_profiling) also launches directly. */
+#define KAZE_FLAG_NO_GRAPHS 8
 
 /* 32-byte keypoint (P:L212-214 sub-pixel position; D4 of SURVEY). */
 typedef struct {

@@ -89,6 +89,27 @@ struct kaze_ctx {
     int tex_W = 0, tex_H = 0;
     // profiling
     bool prof = false;
+    // CUDA graphs of whole chunks (build + detect + describe), keyed by everything a replay bakes in
+    struct GraphKey {
+        const void *img, *kps, *cnt, *desc;
+        int n, w, h;
+        int64_t pitch;
+        cudaStream_t s;
+        bool operator==(const GraphKey& o) const {
+            return img == o.img && kps == o.kps && cnt == o.cnt && desc == o.desc && n == o.n && w == o.w &&
+                   h == o.h && pitch == o.pitch && s == o.s;
+        }
+    };
+    struct GraphEntry {
+        GraphKey key;
+        cudaGraphExec_t exec;
+        int64_t nk;
+        uint64_t used;
+    };
+    std::vector<GraphEntry> graphs;
+    std::vector<GraphKey> seen;
+    uint64_t tick = 0;
+    cudaStream_t s_cap = nullptr;
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> pool;
     int64_t launches = 0;
@@ -451,6 +472,84 @@ kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_coun
     return KAZE_OK;
 }
 
+// One chunk of m <= max_batch images through the three steps, directly or as a CUDA graph: a chunk key seen for
+// the first time runs directly (which also settles every lazily initialised kernel attribute and the texture
+// objects), the second time it is captured on the context's private stream, and from then on its graph is
+// replayed on the caller's stream.  Graphs are per key (pointers, sizes, stream); at most kMaxGraphs are kept.
+constexpr size_t kMaxGraphs = 96;
+
+kaze_status run_chunk_direct(kaze_ctx* c, const float* img, int m, int w, int h, int64_t pitch, kaze_keypoint* kps,
+                             int32_t* cnt, float* desc, cudaStream_t s) {
+    kaze_status st = do_build(c, img, m, w, h, pitch, s);
+    if (st != KAZE_OK) return st;
+    st = do_detect(c, kps, cnt, s);
+    if (st != KAZE_OK) return st;
+    return do_describe(c, kps, cnt, desc, s);
+}
+
+kaze_status run_chunk(kaze_ctx* c, const float* img, int m, int w, int h, int64_t pitch, kaze_keypoint* kps,
+                      int32_t* cnt, float* desc, cudaStream_t s) {
+    if (c->prof || (c->p.flags & KAZE_FLAG_NO_GRAPHS)) return run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, s);
+    const kaze_ctx::GraphKey key{img, kps, cnt, desc, m, w, h, pitch, s};
+    for (auto& ge : c->graphs)
+        if (ge.key == key) {
+            set_geometry(c, m, w, h);
+            KZ_CUDA(c, cudaGraphLaunch(ge.exec, s));
+            c->launches += ge.nk;
+            ge.used = ++c->tick;
+            c->built = c->detected = true;
+            c->last_stream = s;
+            return KAZE_OK;
+        }
+    bool again = false;
+    for (auto& k : c->seen) again |= (k == key);
+    if (!again) {
+        if (c->seen.size() >= 4 * kMaxGraphs) c->seen.erase(c->seen.begin());
+        c->seen.push_back(key);
+        return run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, s);
+    }
+    if (!c->s_cap) KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking));
+    set_geometry(c, m, w, h);
+    kaze_status st = ensure_textures(c);  // host-side setup (synchronous copies) must precede the capture
+    if (st != KAZE_OK) return st;
+    // the capture stream must not start before the caller's prior work when the graph is launched; a graph
+    // launched on s is ordered after s's prior work by the launch itself, so the capture needs no dependency
+    const int64_t l0 = c->launches;
+    KZ_CUDA(c, cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal));
+    st = run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, c->s_cap);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->s_cap, &graph);
+    if (st != KAZE_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (ec != cudaSuccess) {
+        c->err = std::string("graph capture: ") + cudaGetErrorString(ec);
+        return KAZE_ERR_CUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        c->err = std::string("graph instantiate: ") + cudaGetErrorString(ei);
+        return KAZE_ERR_CUDA;
+    }
+    const int64_t nk = c->launches - l0;
+    c->launches = l0;  // the capture launched nothing
+    if (c->graphs.size() >= kMaxGraphs) {
+        auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                    [](const auto& a, const auto& b) { return a.used < b.used; });
+        cudaGraphExecDestroy(lru->exec);
+        c->graphs.erase(lru);
+    }
+    c->graphs.push_back({key, exec, nk, ++c->tick});
+    KZ_CUDA(c, cudaGraphLaunch(exec, s));
+    c->launches += nk;
+    c->built = c->detected = true;
+    c->last_stream = s;
+    return KAZE_OK;
+}
+
 kaze_status check_dims(const kaze_ctx* c, int n, int w, int h, int64_t pitch) {
     if (n < 1 || n > c->p.max_batch) return KAZE_ERR_INVALID_ARGUMENT;
     if (w < 32 || h < 32 || w > c->p.max_width || h > c->p.max_height) return KAZE_ERR_IMAGE_TOO_SMALL;
@@ -590,6 +689,8 @@ kaze_status kaze_destroy(kaze_ctx* c) {
         if (c->ev_cnt[b]) cudaEventDestroy(c->ev_cnt[b]);
         if (c->ev_d2h[b]) cudaEventDestroy(c->ev_d2h[b]);
     }
+    for (auto& ge : c->graphs) cudaGraphExecDestroy(ge.exec);
+    if (c->s_cap) cudaStreamDestroy(c->s_cap);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     free_arena(c);
@@ -631,11 +732,8 @@ kaze_status kaze_extract(kaze_ctx* c, const float* d_imgs, int32_t n, int32_t w,
     const size_t cap = (size_t)c->p.max_keypoints;
     for (int i0 = 0; i0 < n; i0 += c->p.max_batch) {
         const int m = n - i0 < c->p.max_batch ? n - i0 : c->p.max_batch;
-        st = do_build(c, d_imgs + (size_t)i0 * pitch * h, m, w, h, pitch, s);
-        if (st != KAZE_OK) return st;
-        st = do_detect(c, d_kps + i0 * cap, d_counts + i0, s);
-        if (st != KAZE_OK) return st;
-        st = do_describe(c, d_kps + i0 * cap, d_counts + i0, d_desc + i0 * cap * 64, s);
+        st = run_chunk(c, d_imgs + (size_t)i0 * pitch * h, m, w, h, pitch, d_kps + i0 * cap, d_counts + i0,
+                       d_desc + i0 * cap * 64, s);
         if (st != KAZE_OK) return st;
     }
     return KAZE_OK;
@@ -685,13 +783,9 @@ kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32
         KZ_CUDA(c, cudaEventRecord(c->ev_h2d[b], c->s_h2d));
         KZ_CUDA(c, cudaStreamWaitEvent(s, c->ev_h2d[b], 0));
         if (j >= 2) KZ_CUDA(c, cudaStreamWaitEvent(s, c->ev_d2h[b], 0));
-        st = do_build(c, c->hin[b], m, w, h, P, s);
+        st = run_chunk(c, c->hin[b], m, w, h, P, c->hkps[b], c->hcnt[b], c->hdesc[b], s);
         if (st != KAZE_OK) return st;
-        KZ_CUDA(c, cudaEventRecord(c->ev_comp[b], s));  // input buffer b free after the build... conservatively here
-        st = do_detect(c, c->hkps[b], c->hcnt[b], s);
-        if (st != KAZE_OK) return st;
-        st = do_describe(c, c->hkps[b], c->hcnt[b], c->hdesc[b], s);
-        if (st != KAZE_OK) return st;
+        KZ_CUDA(c, cudaEventRecord(c->ev_comp[b], s));  // input buffer b is free once the chunk is done
         KZ_CUDA(c, cudaMemcpyAsync(c->pinned_counts + b * B, c->hcnt[b], sizeof(int) * m, cudaMemcpyDeviceToHost, s));
         KZ_CUDA(c, cudaEventRecord(c->ev_cnt[b], s));
         KZ_CUDA(c, cudaStreamWaitEvent(c->s_d2h, c->ev_cnt[b], 0));

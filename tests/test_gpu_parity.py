@@ -322,6 +322,36 @@ def test_profile_counts_launches():
     kz.close()
 
 
+def test_graph_replay_equals_direct_launches():
+    """kaze_extract replays a chunk as a CUDA graph from its third call on (first direct, second captured): the
+    outputs are bit-identical to a context that launches every kernel directly, the launch count matches, and a
+    new pointer set (another key) or another size is captured separately."""
+    W, H = 333, 257
+    imgs = torch.from_numpy(kaze_inputs.synth_batch(3, W, H)).cuda()
+    g = make(W, H, batch=2, octaves=3, sublevels=3, max_keypoints=4096)
+    d = make(W, H, batch=2, octaves=3, sublevels=3, max_keypoints=4096, flags=K.FLAG_NO_GRAPHS)
+    ref = d.extract(imgs)
+    nd = K.kaze_launch_count(d.ctx)
+    outs = [g.alloc_outputs(3) for _ in range(2)]
+    for it in range(4):
+        o = outs[it % 2]  # two pointer sets: each is seen, captured, replayed
+        K.kaze_extract(g.ctx, imgs, *o)
+        torch.cuda.synchronize()
+        for a, b in zip(o, ref):
+            assert torch.equal(a, b), it
+    assert K.kaze_launch_count(g.ctx) == 4 * nd
+    small = imgs[:, :200, :300].contiguous()
+    r2 = d.extract(small)
+    o2 = g.alloc_outputs(3)
+    for _ in range(3):
+        K.kaze_extract(g.ctx, small, *o2)
+    torch.cuda.synchronize()
+    for a, b in zip(o2, r2):
+        assert torch.equal(a, b)
+    g.close()
+    d.close()
+
+
 def test_memory_footprint_accounts_for_the_arena():
     """kaze_memory_footprint's device total is what kaze_create + the first describe / host
     extract allocate (cudaMemGetInfo drop, up to the allocator's 2 MiB granularity per buffer), and the pyramid
