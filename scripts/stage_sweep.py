@@ -62,6 +62,16 @@ def _time_stages(kz: K.Kaze, imgs: torch.Tensor, reps: int, warmup: int) -> dict
     med = {st: statistics.median(v) for st, v in out.items()}
     med["total"] = sum(med[st] for st in STAGES)
     med["keypoints"] = counts.cpu().numpy().astype(int).tolist()
+    # the whole path through kaze_extract (one CUDA-graph replay per chunk once the chunk has been seen twice)
+    g = []
+    for r in range(warmup + reps):
+        ev[0].record(s)
+        K.kaze_extract(kz.ctx, imgs, kps, counts, desc)
+        ev[1].record(s)
+        torch.cuda.synchronize()
+        if r >= max(warmup, 2):
+            g.append(ev[0].elapsed_time(ev[1]))
+    med["extract_graph"] = statistics.median(g)
     return med
 
 
@@ -92,10 +102,10 @@ def sweep(sizes, complexity, reps: int, warmup: int, batch: int) -> dict:
         kb.close()
         row = {
             "width": W, "height": H, "pixels": W * H,
-            "latency_ms": {st: statistics.mean(t[st] for t in per_img) for st in (*STAGES, "total")},
+            "latency_ms": {st: statistics.mean(t[st] for t in per_img) for st in (*STAGES, "total", "extract_graph")},
             "latency_ms_per_image": [{k: t[k] for k in (*STAGES, "total", "complexity", "keypoints")} for t in per_img],
             "keypoints_mean": statistics.mean(t["keypoints"] for t in per_img),
-            "batched_ms_per_image": {st: tb[st] / batch for st in (*STAGES, "total")},
+            "batched_ms_per_image": {st: tb[st] / batch for st in (*STAGES, "total", "extract_graph")},
             "batch": batch,
             "memory_bytes": mem,
             "memory_bytes_batch": mem_b,
@@ -105,7 +115,8 @@ def sweep(sizes, complexity, reps: int, warmup: int, batch: int) -> dict:
         row["ratio_ss_det_desc"] = [lat[st] / lat["describe"] if lat["describe"] > 0 else None for st in STAGES]
         rows.append(row)
         print(f"{W}x{H}: latency {lat['total']:.3f} ms (ss {lat['scale_space']:.3f}, det {lat['detect']:.3f}, "
-              f"desc {lat['describe']:.3f}), batched {row['batched_ms_per_image']['total']:.3f} ms/img, "
+              f"desc {lat['describe']:.3f}), graph {lat['extract_graph']:.3f} ms, "
+              f"batched {row['batched_ms_per_image']['extract_graph']:.3f} ms/img, "
               f"kps {row['keypoints_mean']:.0f}, mem {mem['total'] / 2**20:.1f} MiB", flush=True)
     return {
         "device": torch.cuda.get_device_name(0),
@@ -116,17 +127,21 @@ def sweep(sizes, complexity, reps: int, warmup: int, batch: int) -> dict:
 
 def to_markdown(res: dict) -> str:
     L = [f"# Stage-timing sweep (SURVEY §8 f4) — {res['device']}", "",
-         "Single-image latency through the C ABI (kaze_build_scale_space / kaze_detect / kaze_describe, CUDA events, "
-         f"median of {res['reps']} per image, mean over the 6 complexity levels), per-image time in batched mode, "
-         "keypoints, and the context's device memory (kaze_memory_footprint, max_batch = 1).", "",
+         "Single-image latency through the C ABI (kaze_build_scale_space / kaze_detect / kaze_describe timed apart, "
+         "direct launches, CUDA events, "
+         f"median of {res['reps']} per image, mean over the 6 complexity levels); the whole path through kaze_extract "
+         "(CUDA-graph replay) for one image and per image in batches of 8; keypoints; the context's device memory "
+         "(kaze_memory_footprint, max_batch = 1).", "",
          "| size (WxH) | keypoints | scale space ms | detect ms | describe ms | total ms | ratio ss:det:desc | "
-         "batched ms/img | memory MiB (L_step scratch MiB) |", "|---|---|---|---|---|---|---|---|---|"]
+         "kaze_extract (graph) ms | batched ms/img (graph) | memory MiB (L_step scratch MiB) |",
+         "|---|---|---|---|---|---|---|---|---|---|"]
     for r in res["rows"]:
         lat, m = r["latency_ms"], r["memory_bytes"]
         rat = ":".join(f"{x:.1f}" for x in r["ratio_ss_det_desc"])
         L.append(f"| {r['width']}x{r['height']} | {r['keypoints_mean']:.0f} | {lat['scale_space']:.3f} | "
                  f"{lat['detect']:.3f} | {lat['describe']:.3f} | {lat['total']:.3f} | {rat} | "
-                 f"{r['batched_ms_per_image']['total']:.3f} | {m['total'] / 2**20:.1f} ({m['scratch'] / 2**20:.1f}) |")
+                 f"{lat['extract_graph']:.3f} | {r['batched_ms_per_image']['extract_graph']:.3f} | "
+                 f"{m['total'] / 2**20:.1f} ({m['scratch'] / 2**20:.1f}) |")
     return "\n".join(L) + "\n"
 
 
