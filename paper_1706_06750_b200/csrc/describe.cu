@@ -63,6 +63,9 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
     const int total = pre[nimg];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* sx = sbuf[warp];
+    // CTA b's warps take 8 consecutive keypoints, then jump by the grid: the whole grid works on one narrow window
+    // of the (image, level, y, x)-ordered list, so the planes it samples stay in L2.  (A contiguous range per CTA —
+    // more L1 sharing, but the grid spread over every image and level at once — measured 48.8 vs 24.7 ms.)
     for (int f = blockIdx.x * kWarps + warp; f < total; f += gridDim.x * kWarps) {
         int img = 0;
         while (img + 1 < nimg && pre[img + 1] <= f) ++img;  // nimg is small
