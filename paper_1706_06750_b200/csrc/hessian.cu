@@ -5,10 +5,12 @@
 //     Lx = N_x L,  Ly = N_y L,  Ldet = N_x(Lx)·N_y(Ly) − N_y(Lx)²
 // which equals s⁴(LxxLyy − Lxy²) with per-pixel derivatives (the factor s per derivative order is absorbed in
 // N).  Second derivatives read the MATERIALISED first derivatives at clamped coordinates (A10), so they are two
-// passes: hess_first (L → Lx, Ly) and hess_det (Lx, Ly → Ldet).  One launch covers every level of every image
-// (blockIdx.z packs (image, level), blockIdx.y the chain block); the per-level step s_i comes from the LevelTable.  (A fused shared-memory
-// tile form moving 16 instead of 24 B/px measured slower on B200 at every step: 80-87 µs vs 59 µs per level and
-// 4 images — the (T+4s)² halo recomputation costs more than the 8 B/px it saves.)
+// passes in principle: hess_first (L → Lx, Ly) and hess_det (Lx, Ly → Ldet).  The default is ONE fused pass
+// (k_hess_fused, 16 instead of 24 B/px): a CTA owns one chain of rows y0 + j·s and a block of columns, keeps the
+// chain's (Lx, Ly) with an s-column halo in shared memory and forms Ldet from it (256-image 1920x1200 step: 39.8
+// vs 45.8 ms for the two chain passes).  One launch covers every level of every image (blockIdx.z packs (image,
+// level)); the per-level step s_i comes from the LevelTable.  (An earlier fused form on square tiles recomputed a
+// (T+4s)² halo and lost to the two passes: 80-87 µs vs 59 µs per level and 4 images.)
 #include "kaze_internal.cuh"
 
 namespace kz {
@@ -153,6 +155,110 @@ __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict
     }
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// Fused form (one pass, 16 instead of 24 B/px): a CTA owns ONE chain (rows y0 + j·s, j < R, of one residue class)
+// and CW output columns [x0, x0 + CW).  Phase A: thread t computes (Lx, Ly) of virtual column x0 − s + t at the
+// chain rows −1..R — at clamped coordinates, exactly what the second pass of the two-pass form reads (A10) — into
+// shared memory, and stores the rows 0..R−1 of the output columns to the Lxy pyramid (the descriptor samples it).
+// Phase B: thread t < CW forms Ldet of column x0 + t from the ring at columns ±s, rows ±1 in shared memory.  Only
+// the s-column halo of (Lx, Ly) is recomputed (CW + 2s ≤ 256 columns per 256 threads), and the L taps of the
+// column halo and of the two extra chain rows come from L1/L2.  Same arithmetic, same order as the two passes:
+// bit-identical results.
+constexpr int kFusedR = 8;
+
+__device__ __forceinline__ int fused_cw(int s) { return s <= 16 ? 224 : 192; }  // CW + 2s <= 256
+__host__ inline int fused_cw_host(int s) { return s <= 16 ? 224 : 192; }
+
+template <int R, int SC>
+__device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, float2* __restrict__ D, float* __restrict__ O,
+                                                Geom g, int s_rt, int ch, int xb, float2 (*sm)[256]) {
+    const int s = SC > 0 ? SC : s_rt;
+    const int cw = fused_cw(s);
+    const int nch = s * ((g.H + R * s - 1) / (R * s));
+    const int x0 = xb * cw;
+    if (ch >= nch || x0 >= g.W) return;  // CTA-uniform
+    const int b = SC > 0 ? ch / SC : chain_band(ch, s);
+    const int y0 = b * R * s + (ch - b * s);
+    const int t = threadIdx.x;
+    const int vc = x0 - s + t;  // virtual column of this thread in phase A
+    const bool in_a = t < cw + 2 * s;
+    const bool fast = SC > 0 && y0 >= 2 * s && y0 + (R + 1) * s <= g.H - 1 && x0 >= 2 * s && x0 + cw + 2 * s <= g.W;
+    if (in_a) {
+        const int cc = clampi(vc, 0, g.W - 1);
+        const bool store_col = vc >= x0 && vc < x0 + cw && vc < g.W;
+        if (fast) {
+            // chain rows k = -2..R+1 of columns cc - s, cc, cc + s (no clamps anywhere)
+            float a[R + 4], m[R + 4], c[R + 4];
+#pragma unroll
+            for (int k = 0; k < R + 4; ++k) {
+                const float* p = L + (unsigned)((y0 + (k - 2) * SC) * g.P + cc);
+                a[k] = __ldg(p - SC);
+                m[k] = __ldg(p);
+                c[k] = __ldg(p + SC);
+            }
+#pragma unroll
+            for (int k = 0; k < R + 2; ++k) {  // chain row k - 1 uses rows k, k+1, k+2 of the arrays
+                const float2 v = make_float2(
+                    0.5f * (kW0 * (c[k] - a[k]) + kW1 * (c[k + 1] - a[k + 1]) + kW0 * (c[k + 2] - a[k + 2])),
+                    0.5f * (kW0 * (a[k + 2] - a[k]) + kW1 * (m[k + 2] - m[k]) + kW0 * (c[k + 2] - c[k])));
+                sm[k][t] = v;
+                if (k >= 1 && k <= R && store_col) __stwb(D + (unsigned)((y0 + (k - 1) * SC) * g.P + vc), v);
+            }
+        } else {
+            const int xm = max(cc - s, 0), xp = min(cc + s, g.W - 1);
+#pragma unroll
+            for (int k = 0; k < R + 2; ++k) {
+                const int yv = y0 + (k - 1) * s;  // chain row k - 1 (virtual)
+                const int yc = clampi(yv, 0, g.H - 1);
+                const int ro[3] = {max(yc - s, 0) * g.P, yc * g.P, min(yc + s, g.H - 1) * g.P};
+                float a3[3], m3[3], c3[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    a3[q] = __ldg(L + (unsigned)(ro[q] + xm));
+                    m3[q] = __ldg(L + (unsigned)(ro[q] + cc));
+                    c3[q] = __ldg(L + (unsigned)(ro[q] + xp));
+                }
+                const float2 v = make_float2(
+                    0.5f * (kW0 * (c3[0] - a3[0]) + kW1 * (c3[1] - a3[1]) + kW0 * (c3[2] - a3[2])),
+                    0.5f * (kW0 * (a3[2] - a3[0]) + kW1 * (m3[2] - m3[0]) + kW0 * (c3[2] - c3[0])));
+                sm[k][t] = v;
+                if (k >= 1 && k <= R && store_col && yv < g.H) __stwb(D + (unsigned)(yv * g.P + vc), v);
+            }
+        }
+    }
+    __syncthreads();
+    if (t < cw && x0 + t < g.W) {
+        // ring: columns x − s, x, x + s ↔ shared columns t, t + s, t + 2s; chain rows −1..R ↔ shared rows 0..R+1
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int y = y0 + j * s;
+            if (!fast && y >= g.H) break;
+            const float v = det_from_ring(sm[j][t], sm[j][t + s], sm[j][t + 2 * s], sm[j + 1][t], sm[j + 1][t + 2 * s],
+                                          sm[j + 2][t], sm[j + 2][t + s], sm[j + 2][t + 2 * s]);
+            __stwb(O + (unsigned)(y * g.P + x0 + t), v);
+        }
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_hess_fused(const float* __restrict__ Lt, float2* __restrict__ Lxy,
+                                                    float* __restrict__ Ldet, size_t img_stride, Geom g, LevelTable lt) {
+    __shared__ float2 sm[R + 2][256];
+    const int img = chain_band(blockIdx.z, lt.n), level = blockIdx.z - img * lt.n;
+    const int s = lt.step[level];
+    const size_t base = img * img_stride + (size_t)level * g.plane;
+    const float* L = opaque(Lt + base);
+    float2* D = opaque(Lxy + base);
+    float* O = opaque(Ldet + base);
+    switch (s) {
+#define KZ_CASE(S) \
+    case S: hess_fused_body<R, S>(L, D, O, g, s, blockIdx.y, blockIdx.x, sm); break;
+        KZ_STEP_CASES(KZ_CASE)
+#undef KZ_CASE
+        default: hess_fused_body<R, 0>(L, D, O, g, s, blockIdx.y, blockIdx.x, sm); break;
+    }
+}
+
 template <int R>
 int max_chain_blocks(Geom g, const LevelTable& lt) {
     int m = 1;
@@ -184,6 +290,19 @@ void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, 
                      cudaStream_t s) {
     const dim3 grid((g.W + 31) / 32, max_chain_blocks<kChainR>(g, lt), nimg * lt.n);
     k_hess_det_chain<kChainR><<<grid, dim3(32, 8), 0, s>>>(Lxy, Ldet, img_stride, g, lt);
+}
+
+bool launch_hess_fused(const float* Lt, float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg,
+                       const LevelTable& lt, cudaStream_t s) {
+    int gx = 1, gy = 1;
+    for (int l = 0; l < lt.n; ++l) {
+        const int st = lt.step[l];
+        if (st > 32) return false;  // CW + 2s > 256: the two-pass form handles it
+        gx = max(gx, (g.W + fused_cw_host(st) - 1) / fused_cw_host(st));
+        gy = max(gy, st * ((g.H + kFusedR * st - 1) / (kFusedR * st)));
+    }
+    k_hess_fused<kFusedR><<<dim3(gx, gy, nimg * lt.n), 256, 0, s>>>(Lt, Lxy, Ldet, img_stride, g, lt);
+    return true;
 }
 
 void launch_component_copy(float2* plane, int comp, float* tight, int to_tight, Geom g, cudaStream_t s) {

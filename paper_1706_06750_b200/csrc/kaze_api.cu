@@ -395,9 +395,20 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     const Geom g = c->geom;
     const double px = (double)g.W * g.H * n;
     {   // Hessian (Eq. 8), all levels in two launches: L → (Lx, Ly) → Ldet
-        Launch L(c, KC_HESSIAN, 24.0 * px * N, s, 2);
-        launch_hess_first(c->Lt, c->Lxy, c->img_stride, g, n, c->lt, s);
-        launch_hess_det(c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s);
+        static const int fused = tune_knob("KAZE_HESS_FUSED", 1);
+        if (fused) {
+            Launch L(c, KC_HESSIAN, 16.0 * px * N, s, 1);
+            if (!launch_hess_fused(c->Lt, c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s)) {
+                launch_hess_first(c->Lt, c->Lxy, c->img_stride, g, n, c->lt, s);
+                launch_hess_det(c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s);
+                L.bytes = 24.0 * px * N;
+                L.nk = 2;
+            }
+        } else {
+            Launch L(c, KC_HESSIAN, 24.0 * px * N, s, 2);
+            launch_hess_first(c->Lt, c->Lxy, c->img_stride, g, n, c->lt, s);
+            launch_hess_det(c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s);
+        }
     }
     KZ_CHECK_LAUNCH(c, "hessian");
     if (N < 3) {

@@ -79,6 +79,9 @@ int match_run(const float* A, int na, const float* B, int nb, float ratio, int32
 // Lxy: interleaved (s·∂x L, s·∂y L) float2 planes, same element strides as the float pyramids.
 void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                        cudaStream_t s);
+// One pass (16 B/px): Lxy and Ldet of every level of nimg images; false if some step exceeds the fused form's 32.
+bool launch_hess_fused(const float* Lt, float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg,
+                       const LevelTable& lt, cudaStream_t s);
 void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                      cudaStream_t s);
 // Diagnostic copy of one component of an interleaved plane to/from a tightly packed w x h buffer
