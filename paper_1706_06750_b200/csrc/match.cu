@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
         }
     } else {  // ===== epilogue warps: TMEM → registers → running top-4 per query row =====
         const int g = warp & 3, h = warp >> 2;  // TMEM lane group (query rows 32g..), column half
+        float* sv = reinterpret_cast<float*>(sB + 2 * kTileBytes) + warp * 32 * 32;  // 4 KB per epilogue warp
         TopK tk;
 #pragma unroll
         for (int q = 0; q < kCand; ++q) {
@@ -229,9 +230,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
                 tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(a * kTileR + col), v);
                 const int j0 = t * kTileR + col;
                 const uint32_t vm = __ldg(rvalid + (j0 >> 5));  // 32 columns = one validity word
+                // candidate mask of this lane's row: columns scoring above its current 8th best
+                const float thr = tk.s[kCand - 1];
+                uint32_t cand = 0u;
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if ((vm >> i) & 1u) topk_insert(tk, v[i], j0 + i);
+                for (int i = 0; i < 32; ++i) cand |= (v[i] > thr ? 1u : 0u) << i;
+                cand &= vm;
+                if (__any_sync(0xffffffffu, cand != 0u)) {
+                    // Insert each lane's candidates in column order; the warp iterates max-over-lanes times, not
+                    // once per column any lane needs (the values go through shared memory for indexed access).
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) sv[i * 32 + lane] = v[i];
+                    __syncwarp();
+                    while (__any_sync(0xffffffffu, cand != 0u)) {
+                        if (cand) {
+                            const int i = __ffs(cand) - 1;
+                            cand &= cand - 1u;
+                            topk_insert(tk, sv[i * 32 + lane], j0 + i);
+                        }
+                    }
+                    __syncwarp();
+                }
             }
             tc_fence_before();
             mbar_arrive(&bar_acc_empty[a]);
@@ -294,6 +313,7 @@ __global__ void __launch_bounds__(256) k_match_rerank(const float* __restrict__ 
                                                       const float* __restrict__ cand_s, const int* __restrict__ cand_j,
                                                       int* __restrict__ best, float* __restrict__ d1o,
                                                       float* __restrict__ d2o, int* __restrict__ uncertified) {
+    __shared__ __align__(16) float qsh[8][64];  // the query, for the lane-parallel exact scan
     const int lane = threadIdx.x & 31;
     const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (q >= nq) return;
@@ -336,20 +356,48 @@ __global__ void __launch_bounds__(256) k_match_rerank(const float* __restrict__ 
         const float bound = na2 + bmin * bmin - 2.f * (s4 + eps);
         cert = bd2 < bound * (1.f - 4e-7f) - 1e-7f;
     }
-    if (!cert) {  // exact scan of every valid reference (rare)
+    if (!cert) {  // exact scan of every valid reference (rare): lane-parallel over the references
         if (lane == 0) atomicAdd(uncertified, 1);
+        float* qa = qsh[threadIdx.x >> 5];
+        qa[2 * lane] = a.x;
+        qa[2 * lane + 1] = a.y;
+        __syncwarp();
         bd1 = INFINITY;
         bd2 = INFINITY;
         bj1 = -1;
-        for (int j = 0; j < nr; ++j) {
+        for (int j = lane; j < nr; j += 32) {  // each lane: its references in increasing j
             if (!((__ldg(rvalid + (j >> 5)) >> (j & 31)) & 1u)) continue;
-            const float d = exact_d2(a, R, j, lane);
+            const float4* b4 = reinterpret_cast<const float4*>(R + (size_t)j * 64);
+            float d = 0.f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const float4 b = __ldg(b4 + k);
+                const float4 q = reinterpret_cast<const float4*>(qa)[k];
+                const float dx = q.x - b.x, dy = q.y - b.y, dz = q.z - b.z, dw = q.w - b.w;
+                d = fmaf(dx, dx, d);
+                d = fmaf(dy, dy, d);
+                d = fmaf(dz, dz, d);
+                d = fmaf(dw, dw, d);
+            }
             if (before(d, j, bd1, bj1)) {
                 bd2 = bd1;
                 bd1 = d;
                 bj1 = j;
             } else if (d < bd2) {
                 bd2 = d;
+            }
+        }
+        // merge the lanes' (first, second) lists: first by (distance, index), second = next distance
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float od1 = __shfl_xor_sync(0xffffffffu, bd1, o), od2 = __shfl_xor_sync(0xffffffffu, bd2, o);
+            const int oj1 = __shfl_xor_sync(0xffffffffu, bj1, o);
+            if (oj1 >= 0 && (bj1 < 0 || before(od1, oj1, bd1, bj1))) {
+                bd2 = fminf(bd1, od2);
+                bd1 = od1;
+                bj1 = oj1;
+            } else {
+                bd2 = fminf(bd2, od1);
             }
         }
     }
@@ -421,7 +469,7 @@ static cudaError_t run_direction(const float* Q, int nq, const uint8_t* Qt, cons
                                  const uint32_t* rvalid, const unsigned* rnorm, float* cs, int* cj, int* best,
                                  float* d1, float* d2, int* unc, cudaStream_t s) {
     static bool attr = false;
-    const int smem = kTileQ * 128 + 2 * kTileBytes + 1024;
+    const int smem = kTileQ * 128 + 2 * kTileBytes + kEpiWarps * 32 * 32 * 4 + 1024;
     if (!attr) {
         cudaFuncSetAttribute(k_match_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;

@@ -5,7 +5,7 @@ set -u
 export KAZE_BENCH_ALLOW_SHORT=1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --images 8 --batch 8 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-for kv in cols:k_aos_cols:4 rows:k_aos_rows_cta:4 cond:k_cond2:3 hfirst:k_hess_first_chain:0 hdet:k_hess_det_chain:0 \
+for kv in cols:k_aos_cols:4 rows:k_aos_rows_cta:4 cond:k_cond2:3 hfused:k_hess_fused:0 \
           nms:k_nms_mark:0 desc:k_describe:0 emit:k_kp_emit:0 pre:k_prefilter:0 khist:k_khist:0 ${KAZE_PROFILE_EXTRA:-}; do
   IFS=: read t r sk <<< "$kv"
   scripts/ncu_full.sh "$t" "$r" "$sk"
