@@ -230,12 +230,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
                 tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(a * kTileR + col), v);
                 const int j0 = t * kTileR + col;
                 const uint32_t vm = __ldg(rvalid + (j0 >> 5));  // 32 columns = one validity word
-                // candidate mask of this lane's row: columns scoring above its current 8th best
+                if (vm != 0xffffffffu) {  // warp-uniform and rare: padding / degenerate references never compete
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = ((vm >> i) & 1u) ? v[i] : -INFINITY;
+                }
+                // Chunk maximum first: once the lists have settled, most chunks beat no row's 8th best and cost
+                // ~16 FMNMX3 instead of a per-column candidate mask.
                 const float thr = tk.s[kCand - 1];
+                float mx = v[0];
+#pragma unroll
+                for (int i = 1; i < 31; i += 2) mx = fmaxf(mx, fmaxf(v[i], v[i + 1]));
+                mx = fmaxf(mx, v[31]);
+                if (!__any_sync(0xffffffffu, mx > thr)) continue;
+                // candidate mask of this lane's row: columns scoring above its current 8th best
                 uint32_t cand = 0u;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) cand |= (v[i] > thr ? 1u : 0u) << i;
-                cand &= vm;
                 if (__any_sync(0xffffffffu, cand != 0u)) {
                     // Insert each lane's candidates in column order; the warp iterates max-over-lanes times, not
                     // once per column any lane needs (the values go through shared memory for indexed access).
