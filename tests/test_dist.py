@@ -1,4 +1,4 @@
-"""Host-side multi-GPU logic on CPU: sharding and the C1 count gather over gloo with world_size 2."""
+"""Host-side multi-GPU logic on CPU: sharding, the C1 count gather and the C2 result gather over gloo, world size 2."""
 import os
 import socket
 
@@ -56,3 +56,44 @@ def test_gather_counts_gloo_world2(n):
     for rank, allc, mx in res:
         assert allc == want
         assert mx == 2.0
+
+
+def _worker_results(rank, ws, port, n, cap, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    first, cnt = D.shard(n, rank, ws)
+    g = torch.Generator().manual_seed(1000 + rank)
+    counts = torch.tensor([(7 * (first + i)) % (cap + 3) for i in range(cnt)], dtype=torch.int32)  # some > cap
+    kps = torch.randint(-1000, 1000, (cnt, cap, 8), dtype=torch.int32, generator=g)
+    desc = torch.randn((cnt, cap, 64), generator=g)
+    kl, dl, allc = D.gather_results(kps, counts, desc)
+    q.put((rank, [t.tolist() for t in kl], [t.tolist() for t in dl], allc.tolist(),
+           {first + i: (kps[i, : min(int(counts[i]), cap)].tolist(), desc[i, : min(int(counts[i]), cap)].tolist())
+            for i in range(cnt)}))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [6, 3])
+def test_gather_results_gloo_world2(n):
+    """C2: every rank ends with every image's count-truncated keypoints and descriptors, bit for bit, in global
+    image order, whatever the shard sizes (including a rank with fewer images) and counts above capacity."""
+    cap = 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_results, args=(r, 2, port, n, cap, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    truth = {}
+    for r in res:
+        truth.update(r[4])
+    want_counts = [min((7 * i) % (cap + 3), cap) for i in range(n)]
+    for rank, kl, dl, allc, _ in res:
+        assert allc == want_counts
+        assert len(kl) == n
+        for i in range(n):
+            assert kl[i] == truth[i][0] and dl[i] == truth[i][1]
