@@ -26,7 +26,8 @@ KEYS = [
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma_pct"),
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lsu_pct"),
 ]
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+        "ns": 1e-3, "us": 1, "ms": 1e3, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
 def summarise(rep):
