@@ -248,6 +248,7 @@ template <int CW, int M, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_aos_cols_u(const float* __restrict__ L, const float* __restrict__ c,
                                                          float* __restrict__ U, Strides st, Geom g, float tau, int T,
                                                          int TP) {
+    KZ_PDL_PROLOGUE();
     extern __shared__ float sm[];
     const int NTOT = CW * TP;
     float* sa = sm;
@@ -342,6 +343,7 @@ template <int M, int NW>
 __global__ void __launch_bounds__(32 * NW) k_aos_rows_cta(const float* __restrict__ L, const float* __restrict__ c,
                                                           const float* __restrict__ U, float* __restrict__ Lout,
                                                           Strides st, Geom g, float tau, int T) {
+    KZ_PDL_PROLOGUE();
     constexpr int MC = M + 1, TP = 32 * NW;
     extern __shared__ __align__(16) float rs[];
     __shared__ __align__(8) uint64_t bar;
@@ -488,7 +490,7 @@ void run_rows_cta(const float* L, const float* c, const float* U, float* Lout, S
         cudaFuncSetAttribute(k_aos_rows_cta<M, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    k_aos_rows_cta<M, NW><<<g.H * nimg, 32 * NW, smem, s>>>(L, c, U, Lout, st, g, tau, T);
+    kz_launch(k_aos_rows_cta<M, NW>, dim3(g.H * nimg), dim3(32 * NW), smem, s, L, c, U, Lout, st, g, tau, T);
 }
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -504,7 +506,7 @@ void run_cols(const float* L, const float* c, float* U, Strides st, Geom g, int 
         attr = true;
     }
     dim3 grid((g.W + CW - 1) / CW, 1, nimg);
-    k_aos_cols_u<CW, M, NT, MINB><<<grid, CW * TP, smem, s>>>(L, c, U, st, g, tau, T, TP);
+    kz_launch(k_aos_cols_u<CW, M, NT, MINB>, dim3(grid), dim3(CW * TP), smem, s, L, c, U, st, g, tau, T, TP);
 }
 
 }  // namespace

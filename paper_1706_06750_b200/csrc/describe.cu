@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(256) k_describe(const float2* __restrict__ Lxy
                                                   const cudaTextureObject_t* __restrict__ texs, size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
                                                   const int* __restrict__ counts, int cap, float* __restrict__ desc,
                                                   int nwin, int keep_angle, int N) {
+    KZ_PDL_PROLOGUE();
     __shared__ int pre[kMaxBatch + 1];
     __shared__ __align__(16) float sbuf[kWarps][kWarpBuf];
     if (threadIdx.x == 0) {
@@ -341,7 +342,7 @@ void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_describe, 256, 0);
         grid = sms * (per_sm > 0 ? per_sm : 1);
     }
-    k_describe<<<grid, 256, 0, s>>>(Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N);
+    kz_launch(k_describe, dim3(grid), dim3(256), 0, s, Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N);
 }
 
 }  // namespace kz

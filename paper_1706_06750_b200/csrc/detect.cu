@@ -218,6 +218,7 @@ template <int LB, bool EXT>
 __global__ void __launch_bounds__(256, EXT ? 1 : 4) k_nms_mark(const float* __restrict__ Ldet, size_t img_stride, Geom g, int N,
                                                   DetectParams dp, LevelTable lt, uint32_t* __restrict__ bitmap,
                                                   int words) {
+    KZ_PDL_PROLOGUE();
     const int lane = threadIdx.x & 31;
     const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (strip >= words) return;  // warp-uniform
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(256, EXT ? 1 : 4) k_nms_mark(const float* __re
 // Row candidate counts from the bitmap: one warp per (image, level, row).
 __global__ void __launch_bounds__(256) k_rowcount(const uint32_t* __restrict__ bitmap, int words, int total_rows,
                                                   int* __restrict__ rowcnt) {
+    KZ_PDL_PROLOGUE();
     const int lane = threadIdx.x & 31;
     const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (q >= total_rows) return;
@@ -270,6 +272,7 @@ __global__ void __launch_bounds__(256) k_rowcount(const uint32_t* __restrict__ b
 // One CTA per image: exclusive scan of R row counts.
 __global__ void __launch_bounds__(1024) k_kp_scan(const int* __restrict__ rowcnt, int R, int* __restrict__ rowoff,
                                                   int* __restrict__ counts) {
+    KZ_PDL_PROLOGUE();
     __shared__ int wsum[32];
     const int img = blockIdx.x;
     const int* rc = rowcnt + (size_t)img * R;
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
                                                  LevelTable lt, DetectParams dp, const uint32_t* __restrict__ bitmap,
                                                  const int* __restrict__ rowcnt, const int* __restrict__ rowoff,
                                                  kaze_keypoint* __restrict__ kps, int total_rows) {
+    KZ_PDL_PROLOGUE();
     const int lane = threadIdx.x & 31;
     const int q = blockIdx.x * 8 + (threadIdx.x >> 5);  // flat row id over (img, level-1, y)
     if (q >= total_rows) return;
@@ -366,21 +370,21 @@ void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, con
     const int nblk = (N - 2 + NMS_LB - 1) / NMS_LB;
     dim3 grid((words + 7) / 8, (g.H + NSEG - 1) / NSEG, nimg * nblk);
     if (dp.exact || dp.refine3d)  // detector variants (§8 f2) in their own instantiation: the default stays lean
-        k_nms_mark<NMS_LB, true><<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, lt, bitmap, words);
+        kz_launch(k_nms_mark<NMS_LB, true>, dim3(grid), dim3(256), 0, s, Ldet, img_stride, g, N, dp, lt, bitmap, words);
     else
-        k_nms_mark<NMS_LB, false><<<grid, 256, 0, s>>>(Ldet, img_stride, g, N, dp, lt, bitmap, words);
+        kz_launch(k_nms_mark<NMS_LB, false>, dim3(grid), dim3(256), 0, s, Ldet, img_stride, g, N, dp, lt, bitmap, words);
     const int total = g.H * (N - 2) * nimg;
-    k_rowcount<<<(total + 7) / 8, 256, 0, s>>>(bitmap, words, total, rowcnt);
+    kz_launch(k_rowcount, dim3((total + 7) / 8), dim3(256), 0, s, bitmap, words, total, rowcnt);
 }
 
 void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, int* counts, cudaStream_t s) {
-    k_kp_scan<<<nimg, 1024, 0, s>>>(rowcnt, rows_per_img, rowoff, counts);
+    kz_launch(k_kp_scan, dim3(nimg), dim3(1024), 0, s, rowcnt, rows_per_img, rowoff, counts);
 }
 
 void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
                     const uint32_t* bitmap, const int* rowcnt, const int* rowoff, kaze_keypoint* kps, cudaStream_t s) {
     const int total = g.H * (lt.n - 2) * nimg;
-    k_kp_emit<<<(total + 7) / 8, 256, 0, s>>>(Ldet, img_stride, g, lt, dp, bitmap, rowcnt, rowoff, kps, total);
+    kz_launch(k_kp_emit, dim3((total + 7) / 8), dim3(256), 0, s, Ldet, img_stride, g, lt, dp, bitmap, rowcnt, rowoff, kps, total);
 }
 
 }  // namespace kz

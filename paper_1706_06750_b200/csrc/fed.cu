@@ -22,6 +22,7 @@ template <int K>
 __global__ void __launch_bounds__(256) k_fed(const float* __restrict__ Lin, size_t s_in, const float* __restrict__ c,
                                              size_t s_c, float* __restrict__ Lout, size_t s_out, Geom g,
                                              FedTaus taus) {
+    KZ_PDL_PROLOGUE();
     constexpr int EW = FTW + 2 * K, EH = FTH + 2 * K, SP = EW + 1;
     extern __shared__ float sm[];
     float* A = sm;
@@ -88,7 +89,7 @@ void run_fed(const float* Lin, size_t s_in, const float* c, size_t s_c, float* L
         attr = true;
     }
     dim3 grid((g.W + FTW - 1) / FTW, (g.H + FTH - 1) / FTH, nimg);
-    k_fed<K><<<grid, dim3(32, 8), smem, s>>>(Lin, s_in, c, s_c, Lout, s_out, g, t);
+    kz_launch(k_fed<K>, dim3(grid), dim3(dim3(32, 8)), smem, s, Lin, s_in, c, s_c, Lout, s_out, g, t);
 }
 
 }  // namespace

@@ -120,6 +120,7 @@ __device__ __forceinline__ void hess_det_body(const float2* __restrict__ D, floa
 template <int R>
 __global__ void __launch_bounds__(256) k_hess_first_chain(const float* __restrict__ Lt, float2* __restrict__ Lxy,
                                                           size_t img_stride, Geom g, LevelTable lt) {
+    KZ_PDL_PROLOGUE();
     const int img = chain_band(blockIdx.z, lt.n), level = blockIdx.z - img * lt.n;
     const int s = lt.step[level];
     const int ch = blockIdx.y * 8 + threadIdx.y;
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(256) k_hess_first_chain(const float* __restric
 template <int R>
 __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict__ Lxy, float* __restrict__ Ldet,
                                                         size_t img_stride, Geom g, LevelTable lt) {
+    KZ_PDL_PROLOGUE();
     const int img = chain_band(blockIdx.z, lt.n), level = blockIdx.z - img * lt.n;
     const int s = lt.step[level];
     const int ch = blockIdx.y * 8 + threadIdx.y;
@@ -243,6 +245,7 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
 template <int R>
 __global__ void __launch_bounds__(256) k_hess_fused(const float* __restrict__ Lt, float2* __restrict__ Lxy,
                                                     float* __restrict__ Ldet, size_t img_stride, Geom g, LevelTable lt) {
+    KZ_PDL_PROLOGUE();
     __shared__ float2 sm[R + 2][256];  // 36 KB at R = 16.  (Staging the L taps in shared memory as well — each
                                        // loaded once instead of three times through L1 — measured slower: 76.7 ms.)
     const int img = chain_band(blockIdx.z, lt.n), level = blockIdx.z - img * lt.n;
@@ -272,6 +275,7 @@ int max_chain_blocks(Geom g, const LevelTable& lt) {
 
 __global__ void k_component_copy(float2* __restrict__ plane, int comp, float* __restrict__ tight, int to_tight,
                                  Geom g) {
+    KZ_PDL_PROLOGUE();
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
     if (x >= g.W) return;
     float* e = reinterpret_cast<float*>(plane + (size_t)y * g.P + x) + comp;
@@ -284,13 +288,13 @@ __global__ void k_component_copy(float2* __restrict__ plane, int comp, float* __
 void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                        cudaStream_t s) {
     const dim3 grid((g.W + 31) / 32, max_chain_blocks<kChainR>(g, lt), nimg * lt.n);
-    k_hess_first_chain<kChainR><<<grid, dim3(32, 8), 0, s>>>(Lt, Lxy, img_stride, g, lt);
+    kz_launch(k_hess_first_chain<kChainR>, dim3(grid), dim3(dim3(32, 8)), 0, s, Lt, Lxy, img_stride, g, lt);
 }
 
 void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                      cudaStream_t s) {
     const dim3 grid((g.W + 31) / 32, max_chain_blocks<kChainR>(g, lt), nimg * lt.n);
-    k_hess_det_chain<kChainR><<<grid, dim3(32, 8), 0, s>>>(Lxy, Ldet, img_stride, g, lt);
+    kz_launch(k_hess_det_chain<kChainR>, dim3(grid), dim3(dim3(32, 8)), 0, s, Lxy, Ldet, img_stride, g, lt);
 }
 
 bool launch_hess_fused(const float* Lt, float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg,
@@ -302,12 +306,12 @@ bool launch_hess_fused(const float* Lt, float2* Lxy, float* Ldet, size_t img_str
         gx = max(gx, (g.W + fused_cw_host(st) - 1) / fused_cw_host(st));
         gy = max(gy, st * ((g.H + kFusedR * st - 1) / (kFusedR * st)));
     }
-    k_hess_fused<kFusedR><<<dim3(gx, gy, nimg * lt.n), 256, 0, s>>>(Lt, Lxy, Ldet, img_stride, g, lt);
+    kz_launch(k_hess_fused<kFusedR>, dim3(dim3(gx, gy, nimg * lt.n)), dim3(256), 0, s, Lt, Lxy, Ldet, img_stride, g, lt);
     return true;
 }
 
 void launch_component_copy(float2* plane, int comp, float* tight, int to_tight, Geom g, cudaStream_t s) {
-    k_component_copy<<<dim3((g.W + 255) / 256, g.H), 256, 0, s>>>(plane, comp, tight, to_tight, g);
+    kz_launch(k_component_copy, dim3(dim3((g.W + 255) / 256, g.H)), dim3(256), 0, s, plane, comp, tight, to_tight, g);
 }
 
 }  // namespace kz

@@ -31,6 +31,39 @@ struct LevelTable {          // per-level scalars passed by value to whole-pyram
     float sigma[kMaxLevels]; // σ_i
 };
 
+// ---- programmatic dependent launch (PDL) ----
+// Every kernel of the path starts with KZ_PDL_PROLOGUE(): griddepcontrol.wait blocks until the preceding kernel in
+// the stream has completed and its writes are visible (a no-op without a programmatic dependency), then
+// launch_dependents lets the NEXT kernel's CTAs be scheduled as this grid's CTAs retire, so launch latency and
+// ramp-up overlap this kernel's tail.  kz_launch sets the programmatic-serialization attribute (knob KAZE_PDL=0
+// turns it off).  Because every kernel waits before touching memory, dependencies stay transitive.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#define KZ_PDL_PROLOGUE() \
+    do {                  \
+        kz::pdl_wait();   \
+        kz::pdl_trigger(); \
+    } while (0)
+
+// PDL mode (knob KAZE_PDL): 0 off; 1 for direct launches only (not inside captured CUDA graphs); 2 always.
+bool pdl_enabled();
+void pdl_set_capturing(bool on);
+
+template <typename... KArgs, typename... Args>
+inline void kz_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Debug/tuning knob read once from the environment (A/B runs only; the defaults are the measured best).
 int tune_knob(const char* name, int def);
 

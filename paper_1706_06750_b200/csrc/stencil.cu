@@ -31,6 +31,7 @@ template <int R>
 __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ in, int64_t in_pitch,
                                                    size_t in_img_stride, float* __restrict__ out,
                                                    size_t out_img_stride, Geom g, GaussTaps t) {
+    KZ_PDL_PROLOGUE();
     constexpr int LW = TW + 2 * R, LH = TH + 2 * R;
     __shared__ float tin[LH][LW];
     __shared__ float tmid[LH][TW];
@@ -202,6 +203,7 @@ template <int MODE, int DIFF>
 __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size_t in_img_stride,
                                                float* __restrict__ out, size_t out_img_stride, Geom g, GaussTaps t,
                                                const float* __restrict__ kval, unsigned* __restrict__ hmax_bits) {
+    KZ_PDL_PROLOGUE();
     __shared__ __align__(16) float sA[CR2][CW2];
     __shared__ __align__(16) float sB[CR2][CW2];
     __shared__ float red[8];
@@ -296,6 +298,7 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
 // __match_any_sync aggregation took 4.1 ms.)
 __global__ void __launch_bounds__(256) k_khist(const float* __restrict__ g2buf, size_t img_stride, Geom g, int bins,
                                                const unsigned* __restrict__ hmax_bits, int* __restrict__ hist) {
+    KZ_PDL_PROLOGUE();
     extern __shared__ int sh[];
     const int img = blockIdx.y;
     const bool per_warp = bins <= 1024;
@@ -324,6 +327,7 @@ __global__ void __launch_bounds__(256) k_khist(const float* __restrict__ g2buf, 
 // Percentile → k = hmax·(b+1)/bins with b the first bin whose cumulative count reaches floor(perc·n).
 __global__ void k_kfinal(const int* __restrict__ hist, int bins, const unsigned* __restrict__ hmax_bits,
                          double perc, double k_override, float* __restrict__ kval, int* __restrict__ fallback) {
+    KZ_PDL_PROLOGUE();
     const int img = blockIdx.x;
     if (threadIdx.x != 0) return;
     if (k_override > 0) {
@@ -353,6 +357,7 @@ __global__ void k_kfinal(const int* __restrict__ hist, int bins, const unsigned*
 
 __global__ void __launch_bounds__(256) k_c_from_g2(float* __restrict__ buf, size_t img_stride, Geom g,
                                                    int diffusivity, const float* __restrict__ kval) {
+    KZ_PDL_PROLOGUE();
     const int img = blockIdx.z;
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
     if (x >= g.W) return;
@@ -370,7 +375,7 @@ void launch_prefilter(const float* img, int64_t in_pitch, size_t in_img_stride, 
     dim3 block(32, 8);
     switch (t.r) {
 #define KZ_PF(R) \
-    case R: k_prefilter<R><<<grid, block, 0, s>>>(img, in_pitch, in_img_stride, L0, out_img_stride, g, t); break;
+    case R: kz_launch(k_prefilter<R>, dim3(grid), dim3(block), 0, s, img, in_pitch, in_img_stride, L0, out_img_stride, g, t); break;
         KZ_PF(1) KZ_PF(2) KZ_PF(3) KZ_PF(4) KZ_PF(5) KZ_PF(6) KZ_PF(7) KZ_PF(8) KZ_PF(9) KZ_PF(10) KZ_PF(11)
         KZ_PF(12) KZ_PF(13) KZ_PF(14) KZ_PF(15) KZ_PF(16) KZ_PF(17) KZ_PF(18) KZ_PF(19) KZ_PF(20) KZ_PF(21)
         KZ_PF(22) KZ_PF(23) KZ_PF(24)
@@ -385,13 +390,13 @@ void launch_cond(const float* L, size_t in_img_stride, float* out, size_t out_im
     // G(σ=1) always has radius 3 (A6), which k_cond2's 7-tap loops and 4-row halo assume
     dim3 grid((g.W + CW2 - 1) / CW2, (g.H + CH2 - 1) / CH2, nimg);
     if (mode == 0) {
-        k_cond2<0, 2><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits);
+        kz_launch(k_cond2<0, 2>, dim3(grid), dim3(256), 0, s, L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits);
         return;
     }
     switch (diffusivity) {
-        case 1: k_cond2<1, 1><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
-        case 3: k_cond2<1, 3><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
-        default: k_cond2<1, 2><<<grid, 256, 0, s>>>(L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
+        case 1: kz_launch(k_cond2<1, 1>, dim3(grid), dim3(256), 0, s, L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
+        case 3: kz_launch(k_cond2<1, 3>, dim3(grid), dim3(256), 0, s, L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
+        default: kz_launch(k_cond2<1, 2>, dim3(grid), dim3(256), 0, s, L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
     }
 }
 
@@ -400,18 +405,18 @@ void launch_khist(const float* g2, size_t img_stride, Geom g, int nimg, int bins
     int blocks = std::min(g.H - 2, 296);  // two CTAs per SM per image batch is plenty for a 4 B/px read
     if (blocks < 1) blocks = 1;
     const size_t smem = sizeof(int) * bins * (bins <= 1024 ? 8 : 1);
-    k_khist<<<dim3(blocks, nimg), 256, smem, s>>>(g2, img_stride, g, bins, hmax_bits, hist);
+    kz_launch(k_khist, dim3(dim3(blocks, nimg)), dim3(256), smem, s, g2, img_stride, g, bins, hmax_bits, hist);
 }
 
 void launch_kfinal(const int* hist, int bins, const unsigned* hmax_bits, int nimg, double perc, double k_override,
                    float* kval, int* fallback, cudaStream_t s) {
-    k_kfinal<<<nimg, 32, 0, s>>>(hist, bins, hmax_bits, perc, k_override, kval, fallback);
+    kz_launch(k_kfinal, dim3(nimg), dim3(32), 0, s, hist, bins, hmax_bits, perc, k_override, kval, fallback);
 }
 
 void launch_c_from_g2(float* buf, size_t img_stride, Geom g, int nimg, int diffusivity, const float* kval,
                       cudaStream_t s) {
     dim3 grid((g.W + 255) / 256, g.H, nimg);
-    k_c_from_g2<<<grid, 256, 0, s>>>(buf, img_stride, g, diffusivity, kval);
+    kz_launch(k_c_from_g2, dim3(grid), dim3(256), 0, s, buf, img_stride, g, diffusivity, kval);
 }
 
 }  // namespace kz
