@@ -79,8 +79,7 @@ void launch_khist(const float* g2, size_t img_stride, Geom g, int nimg, int bins
                   int* hist, cudaStream_t s);
 void launch_kfinal(const int* hist, int bins, const unsigned* hmax_bits, int nimg, double perc, double k_override,
                    float* kval, int* fallback, cudaStream_t s);
-void launch_c_from_g2(float* buf, size_t img_stride, Geom g, int nimg, int diffusivity, const float* kval,
-                      cudaStream_t s);
+
 
 // ---- aos.cu ----
 struct Strides {  // per-image strides (floats) of the four buffers an AOS pass touches

@@ -355,18 +355,6 @@ __global__ void k_kfinal(const int* __restrict__ hist, int bins, const unsigned*
     fallback[img] = 0;
 }
 
-__global__ void __launch_bounds__(256) k_c_from_g2(float* __restrict__ buf, size_t img_stride, Geom g,
-                                                   int diffusivity, const float* __restrict__ kval) {
-    KZ_PDL_PROLOGUE();
-    const int img = blockIdx.z;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-    if (x >= g.W) return;
-    float k = kval[img];
-    float* p = buf + img * img_stride + (size_t)y * g.P + x;
-    const float q = *p * frcp(k * k);
-    *p = diffusivity_g(q, diffusivity);
-}
-
 }  // namespace
 
 void launch_prefilter(const float* img, int64_t in_pitch, size_t in_img_stride, float* L0, size_t out_img_stride,
@@ -413,10 +401,5 @@ void launch_kfinal(const int* hist, int bins, const unsigned* hmax_bits, int nim
     kz_launch(k_kfinal, dim3(nimg), dim3(32), 0, s, hist, bins, hmax_bits, perc, k_override, kval, fallback);
 }
 
-void launch_c_from_g2(float* buf, size_t img_stride, Geom g, int nimg, int diffusivity, const float* kval,
-                      cudaStream_t s) {
-    dim3 grid((g.W + 255) / 256, g.H, nimg);
-    kz_launch(k_c_from_g2, dim3(grid), dim3(256), 0, s, buf, img_stride, g, diffusivity, kval);
-}
 
 }  // namespace kz
