@@ -54,14 +54,24 @@ __global__ void __launch_bounds__(256) k_fed(const float* __restrict__ Lin, size
 #pragma unroll 1
     for (int s = 1; s <= K; ++s) {
         const float tau = taus.t[s - 1];
-        for (int ly = s + ty; ly < EH - s; ly += 8)
-            for (int lx = s + tx; lx < EW - s; lx += 32) {
-                const int o = ly * SP + lx;
-                const float v = src[o];
-                const float f = WX[o] * (src[o + 1] - v) - WX[o - 1] * (v - src[o - 1]) + WY[o] * (src[o + SP] - v) -
-                                WY[o - SP] * (v - src[o - SP]);
+        // thread (tx, ty): columns s + tx + 32k, and a contiguous eighth of the rows [s, EH - s), walked downwards
+        // with the cell above and its face weight kept in registers (6 shared loads per cell instead of 9)
+        const int nrow = EH - 2 * s, per = (nrow + 7) / 8;
+        const int r0 = s + ty * per, r1 = min(r0 + per, EH - s);
+        for (int lx = s + tx; lx < EW - s; lx += 32) {
+            if (r0 >= r1) break;
+            int o = r0 * SP + lx;
+            float up = src[o - SP], wyu = WY[o - SP], v = src[o];
+            for (int ly = r0; ly < r1; ++ly, o += SP) {
+                const float dn = src[o + SP], wy = WY[o];
+                const float f = WX[o] * (src[o + 1] - v) - WX[o - 1] * (v - src[o - 1]) + wy * (dn - v) -
+                                wyu * (v - up);
                 dst[o] = fmaf(tau, f, v);
+                up = v;
+                v = dn;
+                wyu = wy;
             }
+        }
         __syncthreads();
         float* t = src;
         src = dst;
