@@ -153,7 +153,8 @@ __device__ __forceinline__ float2 c2(float a) { return make_float2(a, a); }
 template <int DIFF>
 __device__ __forceinline__ void cond_vpass_x2(const float (*sA)[CW2], const float (*sB)[CW2], const float (&w)[7],
                                               float* __restrict__ dst, Geom g, int x0, int y0, int tid, float ik2) {
-    constexpr int RG = 7;  // output rows per thread (8 groups x 7 = CH2)
+    constexpr int RG = 7;  // output rows per thread (8 groups x 7 = CH2); 4 groups x 14 rows on half the threads
+                           // (fewer window re-reads) measured 22.3 vs 21.8 ms
     const int cp = tid & 31, q0 = (tid >> 5) * RG;
     const int x = x0 + 2 * cp;
     float2 wa[7], wb[7];
