@@ -147,8 +147,22 @@ __device__ __forceinline__ void topk_push(TopK& t, float v, int j) {
         j = sw ? tj : j;
     }
 }
+// Scan-time insertion: columns arrive in increasing j, so "higher score first" alone already keeps the earlier of
+// equal scores; no index comparisons (5 instead of 8 instructions per stage).
+__device__ __forceinline__ void topk_push_scan(TopK& t, float v, int j) {
+#pragma unroll
+    for (int q = 0; q < kCand; ++q) {
+        const bool sw = v > t.s[q];
+        const float ts = t.s[q];
+        const int tj = t.j[q];
+        t.s[q] = sw ? v : ts;
+        t.j[q] = sw ? j : tj;
+        v = sw ? ts : v;
+        j = sw ? tj : j;
+    }
+}
 __device__ __forceinline__ void topk_insert(TopK& t, float v, int j) {
-    if (v > t.s[kCand - 1]) topk_push(t, v, j);  // columns arrive in increasing j: equal scores keep the earlier
+    if (v > t.s[kCand - 1]) topk_push_scan(t, v, j);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __restrict__ Qt, int nq,
