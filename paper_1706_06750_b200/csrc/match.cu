@@ -31,7 +31,8 @@ constexpr int kTileR = 256;                 // reference rows per tile (UMMA N)
 constexpr int kTileQ = 128;                 // query rows per CTA (UMMA M)
 constexpr int kTileBytes = kTileR * 128;    // 64 bf16 = 128 B per row
 constexpr int kCand = 8;                    // approximate candidates kept per query
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 4.06 vs 3.98 ms at 65536^2)
+constexpr int kColGroups = kEpiWarps / 4;
 constexpr int kThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
 constexpr float kEps = 1.0f / 1024.0f + 2e-5f;  // fp16 rounding of both operands (2·2^-11) + fp32 sum slack
 
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
             }
         }
     } else {  // ===== epilogue warps: TMEM → registers → running top-4 per query row =====
-        const int g = warp & 3, h = warp >> 2;  // TMEM lane group (query rows 32g..), column half
+        const int g = warp & 3, h = warp >> 2;  // TMEM lane group (query rows 32g..), column group
         float* sv = reinterpret_cast<float*>(sB + 2 * kTileBytes) + warp * 32 * 32;  // 4 KB per epilogue warp
         TopK tk;
 #pragma unroll
@@ -238,8 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
             mbar_wait(&bar_acc_full[a], (t >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int ch = 0; ch < 4; ++ch) {
-                const int col = h * 128 + ch * 32;
+            for (int ch = 0; ch < kTileR / kColGroups / 32; ++ch) {
+                const int col = h * (kTileR / kColGroups) + ch * 32;
                 float v[32];
                 tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(a * kTileR + col), v);
                 const int j0 = t * kTileR + col;
@@ -279,26 +280,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
             tc_fence_before();
             mbar_arrive(&bar_acc_empty[a]);
         }
-        // merge the two column halves of each row through shared memory (the B ring is free by now)
+        // merge the column groups of each row through shared memory (the B ring is free by now)
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32));
         float* ms = reinterpret_cast<float*>(sB);
-        int* mj = reinterpret_cast<int*>(sB + kTileQ * kCand * 2 * sizeof(float));
+        int* mj = reinterpret_cast<int*>(sB + (kColGroups - 1) * kTileQ * kCand * sizeof(float));
         const int row = 32 * g + lane;
-        if (h == 1) {
+        if (h > 0) {
 #pragma unroll
             for (int q = 0; q < kCand; ++q) {
-                ms[row * kCand + q] = tk.s[q];
-                mj[row * kCand + q] = tk.j[q];
+                ms[((h - 1) * kTileQ + row) * kCand + q] = tk.s[q];
+                mj[((h - 1) * kTileQ + row) * kCand + q] = tk.j[q];
             }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32));
         if (h == 0) {
-            // half 1's columns all come after half 0's within a tile but not across tiles: merge by (score, index)
+            // the other groups' columns interleave with group 0's across tiles: merge by (score, index)
+            for (int h2 = 1; h2 < kColGroups; ++h2)
 #pragma unroll
-            for (int q = 0; q < kCand; ++q) {
-                const int j = mj[row * kCand + q];
-                if (j >= 0) topk_push(tk, ms[row * kCand + q], j);
-            }
+                for (int q = 0; q < kCand; ++q) {
+                    const int j = mj[((h2 - 1) * kTileQ + row) * kCand + q];
+                    if (j >= 0) topk_push(tk, ms[((h2 - 1) * kTileQ + row) * kCand + q], j);
+                }
             const int qg = q0 + row;
             if (qg < nq) {
 #pragma unroll
