@@ -105,7 +105,8 @@ __device__ __forceinline__ bool is_keypoint(const float* __restrict__ Dm, const 
 // 8-neighbour max N8 = max(vm_left, vm_right, up, down).  Keep iff v > thr, v > N8_i, v > M_{i−1}, v > M_{i+1}
 // (strict, A11); only candidates run the edge test / sub-pixel fit.  The row loop is unrolled by three so the
 // row window rotates by renaming, not by moves.
-constexpr int NSEG = 63;   // rows per warp (multiple of 3)
+constexpr int NSEG = 63;   // rows per warp (multiple of 3).  (Streaming rows through a per-warp cp.async ring three
+                           // rows ahead measured 12.3 vs 11.5 ms; a fourth register slot for the next row 19.6 vs 18.9.)
 constexpr int NMS_LB = 7;  // centre levels per warp (16 levels → two blocks of 7)
 constexpr int STRIP = 30;  // output columns per strip
 
