@@ -6,7 +6,7 @@
  * Style: scalar loops in the paper's order and notation; 2-D clamped convolutions instead
  * of separable passes; a textbook Thomas solve per line; brute-force 26-neighbour scans.
  * No blocking, fusion or reordering.  Each function cites the passage it follows; the
- * readings A1..A19 are listed in DESIGN.md §3.
+ * readings A1..A26 are listed in DESIGN.md §3.
  */
 #include "kazeref.h"
 

@@ -410,6 +410,33 @@ def test_full_size_1920x1200_in_bench_launch_configuration(O):
 
 
 @pytest.mark.slow
+def test_full_size_4096x4096_end_to_end(O):
+    """BASELINE configs[3]: one 4096x4096 image through the whole path (column systems of 4096 rows, row systems of
+    4096 columns, 114k keypoints) against the full fp64 oracle: k in the same bin, >= 99% of keypoints matched both
+    ways, >= 99% of matched descriptors with cos >= 0.999."""
+    psutil = pytest.importorskip("psutil")
+    if psutil.virtual_memory().available < 24 << 30:  # the oracle keeps four fp64 pyramids (8.6 GB)
+        pytest.skip("not enough host memory for the 4096^2 oracle")
+    img = kaze_inputs.synth_image(4096, 4096)
+    ref = O.run(img, cap=1 << 19)
+    kz = make(4096, 4096, max_keypoints=1 << 18)
+    kps, counts, desc = kz.extract(torch.from_numpy(img).cuda()[None])
+    k, _ = K.kaze_get_k(kz.ctx, 1)
+    assert abs(k[0] / ref["k"] - 1) < 1e-5
+    got = K.Kaze.keypoints_numpy(kps, counts)[0]
+    assert ref["count"] > 50000
+    f1, idx = match_keypoints(ref["kps"], got)
+    f2, _ = match_keypoints(got, ref["kps"])
+    assert f1 >= 0.99 and f2 >= 0.99, (f1, f2, ref["count"], int(counts[0]))
+    d = desc[0, : len(got)].cpu().numpy().astype(np.float64)
+    m = idx >= 0
+    a, b = ref["desc"][m], d[idx[m]]
+    cos = np.sum(a * b, 1) / (np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1) + 1e-30)
+    assert np.mean(cos >= 0.999) >= 0.99, np.mean(cos >= 0.999)
+    kz.close()
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("level", [1, 15])
 def test_aos_step_4096_stage_isolated(O, level):
     """configs[3] (4096x4096, long AOS lines): one AOS step from the GPU's own L_{i-1}, against the oracle's
