@@ -321,6 +321,13 @@ def main():
                         for k, v in prof.items()},
             "clocks": clocks.summary(),
         }
+        if "describe" in prof and prof["describe"]["ms"] > 0:
+            # gather roofline of the descriptor pass: 113 + 576 bilinear samples x 4 taps x 8 B
+            # (float2 texels) = 22 KB per keypoint, served mostly by L1/L2 (each plane is read ~once from HBM)
+            per_kp = (113 + 576) * 4 * 8
+            kp_local = int(torch.clamp(counts, max=args.max_keypoints).sum())  # this rank's keypoints per step
+            out["kernels"]["describe"]["gather_gbs"] = kp_local * per_kp * args.steps / (prof["describe"]["ms"] * 1e-3) / 1e9
+            out["kernels"]["describe"]["gather_bytes_per_keypoint"] = per_kp
         print(json.dumps(out), flush=True)
     kz.close()
     if ws > 1:
