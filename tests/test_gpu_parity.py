@@ -352,6 +352,41 @@ def test_graph_replay_equals_direct_launches():
     d.close()
 
 
+def test_graph_replay_on_a_side_stream_and_host_path_keys():
+    """Graphs are keyed by stream: replays on a non-default torch stream give the direct result, interleaved with
+    default-stream calls on the same buffers; the host path (two staging buffers -> two keys) replays too."""
+    W, H = 200, 150
+    imgs = torch.from_numpy(kaze_inputs.synth_batch(4, W, H)).cuda()
+    g = make(W, H, batch=2, octaves=3, sublevels=3, max_keypoints=2048)
+    d = make(W, H, batch=2, octaves=3, sublevels=3, max_keypoints=2048, flags=K.FLAG_NO_GRAPHS)
+    ref = d.extract(imgs)
+    out = g.alloc_outputs(4)
+    side = torch.cuda.Stream()
+    for it in range(4):
+        if it % 2:
+            with torch.cuda.stream(side):
+                K.kaze_extract(g.ctx, imgs, *out, stream=side.cuda_stream)
+            side.synchronize()
+        else:
+            K.kaze_extract(g.ctx, imgs, *out)
+            torch.cuda.synchronize()
+        for a, b in zip(out, ref):
+            assert torch.equal(a, b), it
+    hi = np.ascontiguousarray(imgs.cpu().numpy())
+    for it in range(3):
+        hk = np.zeros((4, 2048, 8), np.int32)
+        hc = np.zeros(4, np.int32)
+        hd = np.zeros((4, 2048, 64), np.float32)
+        K.kaze_extract_host(g.ctx, hi, hk, hc, hd)
+        assert np.array_equal(hc, ref[1].cpu().numpy())
+        for i in range(4):
+            n = int(hc[i])
+            assert np.array_equal(hk[i, :n], ref[0][i, :n].cpu().numpy())
+            assert np.array_equal(hd[i, :n], ref[2][i, :n].cpu().numpy())
+    g.close()
+    d.close()
+
+
 def test_memory_footprint_accounts_for_the_arena():
     """kaze_memory_footprint's device total is what kaze_create + the first describe / host
     extract allocate (cudaMemGetInfo drop, up to the allocator's 2 MiB granularity per buffer), and the pyramid
