@@ -22,7 +22,6 @@ enum KernelClass {
     KC_GRAD_L1,
     KC_KHIST,
     KC_KFINAL,
-    KC_C_FROM_G2,
     KC_COND,
     KC_AOS_COLS,
     KC_AOS_ROWS,
@@ -34,7 +33,7 @@ enum KernelClass {
     KC_FED,
     KC_COUNT
 };
-const char* kKernelNames[KC_COUNT] = {"prefilter", "grad_l1",  "k_hist",   "k_final",  "c_from_g2",
+const char* kKernelNames[KC_COUNT] = {"prefilter", "grad_l1",  "k_hist",   "k_final",
                                       "cond",      "aos_cols", "aos_rows", "hessian",
                                       "nms_mark",  "kp_scan",  "kp_emit",  "describe", "fed"};
 
