@@ -21,7 +21,8 @@
 //            three-value column kernel; earlier column variants — TMA-pipelined persistent strips, three
 //            register-light passes, re-mapped warp SPIKE — were slower still.  Two columns per thread in packed
 //            fp32x2 (FFMA2/FMUL2, M = 10 to fit 64 registers) issued 35 instead of 55 instructions per pixel but
-//            ran 42.0 vs 32.2 ms: twice the chunks make the shared-memory PCR (7 steps, float2) the bottleneck.)
+//            ran 42.0 vs 32.2 ms: twice the chunks make the shared-memory PCR (7 steps, float2) the bottleneck.
+//            CTA shape at M = 20: 4 columns x 4 CTAs/SM 39.3 ms, 16 columns x 1 CTA/SM 34.1, 8 x 2 (kept) 29.5.)
 //   rows:    one CTA (4 or 8 warps) per row.  The TMA engine streams the row's L, c and U into shared memory (1-D
 //            bulk copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is
 //            solved by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve).
