@@ -16,7 +16,7 @@ namespace kz {
 
 namespace {
 
-constexpr int FTW = 64, FTH = 32;  // output tile
+constexpr int FTW = 64, FTH = 32;  // output tile (64 x 64 measured 255 vs 252 ms per 256-image step)
 
 template <int K>
 __global__ void __launch_bounds__(256) k_fed(const float* __restrict__ Lin, size_t s_in, const float* __restrict__ c,
