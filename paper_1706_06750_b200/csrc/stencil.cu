@@ -83,6 +83,90 @@ __global__ void __launch_bounds__(256) k_prefilter(const float* __restrict__ in,
 }
 
 // -------------------------------------------------------------------------------------------------
+// Prefilter for radius 5 (σ0 = 1.6, the default) in the conductivity kernel's two-phase form: tile 64 x 56; phase 1
+// one 8-column row segment per item (the 18 input columns from six 16-byte loads, all issued before the arithmetic,
+// when the input rows are 16-byte aligned; clamped scalar loads otherwise) → horizontal 11-tap pass in registers
+// → shared memory; phase 2 column pairs in fp32x2 (FFMA2) sliding an 11-row register window, one 8-byte store per
+// row.  The 66 shared rows hold image rows clamp(y0 − 5 + r), so the vertical pass reads clamped rows exactly as
+// the separable clamped convolution does.  (The generic 32x32 k_prefilter: 2.96 ms per 256-image step,
+// shared-load bound at ~25 shared loads per pixel.)
+constexpr int PW = 64, PH5 = 56, PR5 = 5, PRows = PH5 + 2 * PR5, PRG = 7;
+__global__ void __launch_bounds__(256) k_prefilter5(const float* __restrict__ in, int64_t in_pitch,
+                                                    size_t in_img_stride, float* __restrict__ out,
+                                                    size_t out_img_stride, Geom g, GaussTaps t, int aligned) {
+    KZ_PDL_PROLOGUE();
+    __shared__ __align__(16) float sH[PRows][PW];
+    const int x0 = blockIdx.x * PW, y0 = blockIdx.y * PH5, img = blockIdx.z;
+    const float* src = in + img * in_img_stride;
+    const int tid = threadIdx.x;
+    float w[11];
+#pragma unroll
+    for (int d = 0; d < 11; ++d) w[d] = t.w[d];
+    {
+        const int sg = tid & 7, xb = x0 + 8 * sg;
+        const bool fast = aligned && (xb >= 8) && (xb + 16 <= g.W);
+        constexpr int NI = (PRows * 8 + 255) / 256;  // items per thread (3, the last partial)
+        float v[NI][24];
+#pragma unroll
+        for (int it = 0; it < NI; ++it) {
+            const int r = (tid >> 3) + 32 * it;
+            if (r < PRows) {
+                const float* row = src + (int64_t)clampi(y0 - PR5 + r, 0, g.H - 1) * in_pitch;
+                if (fast) {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) {
+                        const float4 a = __ldg(reinterpret_cast<const float4*>(row + xb - 8) + q);
+                        v[it][4 * q] = a.x;
+                        v[it][4 * q + 1] = a.y;
+                        v[it][4 * q + 2] = a.z;
+                        v[it][4 * q + 3] = a.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 3; q < 21; ++q) v[it][q] = __ldg(row + clampi(xb - 8 + q, 0, g.W - 1));
+                }
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < NI; ++it) {
+            const int r = (tid >> 3) + 32 * it;
+            if (r < PRows) {
+                float h[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {  // output column xb + i uses inputs xb + i − 5 .. xb + i + 5 = v[i + 3 ..]
+                    float acc = w[0] * v[it][i + 3];
+#pragma unroll
+                    for (int d = 1; d < 11; ++d) acc = fmaf(w[d], v[it][i + 3 + d], acc);
+                    h[i] = acc;
+                }
+                reinterpret_cast<float4*>(&sH[r][8 * sg])[0] = make_float4(h[0], h[1], h[2], h[3]);
+                reinterpret_cast<float4*>(&sH[r][8 * sg])[1] = make_float4(h[4], h[5], h[6], h[7]);
+            }
+        }
+    }
+    __syncthreads();
+    const int cp = tid & 31, q0 = (tid >> 5) * PRG;
+    const int x = x0 + 2 * cp;
+    float2 wv[11];
+#pragma unroll
+    for (int d = 0; d < 10; ++d) wv[d] = *reinterpret_cast<const float2*>(&sH[q0 + d][2 * cp]);
+    float* dst = opaque(out + img * out_img_stride);
+#pragma unroll
+    for (int j = 0; j < PRG; ++j) {  // output row q0 + j uses shared rows q0 + j .. q0 + j + 10
+        wv[(j + 10) % 11] = *reinterpret_cast<const float2*>(&sH[q0 + j + 10][2 * cp]);
+        float2 acc = __fmul2_rn(make_float2(w[0], w[0]), wv[j % 11]);
+#pragma unroll
+        for (int d = 1; d < 11; ++d) acc = __ffma2_rn(make_float2(w[d], w[d]), wv[(j + d) % 11], acc);
+        const int y = y0 + q0 + j;
+        if (y < g.H) {
+            float* o = dst + (unsigned)(y * g.P + x);
+            if (x + 1 < g.W) __stwb(reinterpret_cast<float2*>(o), acc);
+            else if (x < g.W) __stwb(o, acc.x);
+        }
+    }
+}
+
+// -------------------------------------------------------------------------------------------------
 // -------------------------------------------------------------------------------------------------
 // |∇(G1 * L)|² → c (mode 1) or |∇|² + max|∇| (mode 0); G(σ=1) has radius 3 (A6).  Horizontal-first form: with Hl = G1_x * L (clamped columns), the Scharr step commutes
 // exactly with the vertical G1 pass (they act on different axes and both clamp per axis):
@@ -360,6 +444,13 @@ __global__ void k_kfinal(const int* __restrict__ hist, int bins, const unsigned*
 
 void launch_prefilter(const float* img, int64_t in_pitch, size_t in_img_stride, float* L0, size_t out_img_stride,
                       Geom g, int nimg, const GaussTaps& t, cudaStream_t s) {
+    static const int v5 = tune_knob("KAZE_PREFILTER5", 1);
+    if (t.r == PR5 && v5) {
+        const int aligned = ((reinterpret_cast<uintptr_t>(img) & 15) == 0) && (in_pitch % 4 == 0) && (in_img_stride % 4 == 0);
+        kz_launch(k_prefilter5, dim3((g.W + PW - 1) / PW, (g.H + PH5 - 1) / PH5, nimg), dim3(256), 0, s, img, in_pitch,
+                  in_img_stride, L0, out_img_stride, g, t, aligned);
+        return;
+    }
     dim3 grid((g.W + TW - 1) / TW, (g.H + TH - 1) / TH, nimg);
     dim3 block(32, 8);
     switch (t.r) {
