@@ -174,14 +174,15 @@ __global__ void __launch_bounds__(256) k_prefilter5(const float* __restrict__ in
 //   gy = ½ [Vb(clamp(y+1)) − Vb(clamp(y−1))],  Vb = G1_y * B,  B(x) = Σ_dx w(dx) Hl(clamp(x+dx))
 // with w = (3, 10, 3)/16.  Phase 1 (one 8-column row segment per item, two items per thread, all eight 16-byte
 // loads issued before any arithmetic): L over 16 columns, ten Hl values, and A, B for the eight columns, stored to
-// shared memory.  Phase 2 (one column × a 14-row chain per thread): vertical G1 of A and B in registers, the
-// vertical Scharr taps, the conductivity, and one coalesced store per row.  Tile 64 x 56 outputs; the 64
+// shared memory.  Phase 2 (cond_vpass_x2: a column pair × 7 rows per thread in fp32x2): vertical G1 of A and B
+// sliding a 7-row register window, the vertical Scharr taps, the conductivity (or |∇|² and the interior max for the
+// k histogram), and one 8-byte store per row.  Tile 64 x 56 outputs; the 64
 // shared-memory rows hold image rows clamp(y0 − 4 + r), so every vertical tap reads the clamped row of its virtual
 // coordinate.  The diffusivity is a template parameter and interior tiles skip every clamp and store predicate.
 // (Measured on B200, 256-image 1920x1200 step: 4-column segments with per-row loads and a runtime diffusivity
 // switch 30.5 ms — issue-bound at 88 instructions per pixel; the 32x32 Ls-tile kernel with three shared passes
 // 39.3 ms.)
-constexpr int CW2 = 64, CH2 = 56, CR2 = CH2 + 8, CQ2 = 14;
+constexpr int CW2 = 64, CH2 = 56, CR2 = CH2 + 8;
 
 // Phase-1 item: row r of the tile (image row clamp(y0 − 4 + r)), columns xb .. xb+7.
 __device__ __forceinline__ void cond_load16(const float* __restrict__ row, int xb, int W, bool fast, float (&v)[16]) {
@@ -234,9 +235,11 @@ __device__ __forceinline__ void cond_hpass(const float (&v)[16], const float (&w
 // Operation order per component is the scalar order (same rounding).
 __device__ __forceinline__ float2 c2(float a) { return make_float2(a, a); }
 
-template <int DIFF>
-__device__ __forceinline__ void cond_vpass_x2(const float (*sA)[CW2], const float (*sB)[CW2], const float (&w)[7],
-                                              float* __restrict__ dst, Geom g, int x0, int y0, int tid, float ik2) {
+// MODE 1 stores the conductivity; MODE 0 stores |∇|² and returns this thread's max |∇| over the image interior.
+template <int MODE, int DIFF>
+__device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const float (*sB)[CW2], const float (&w)[7],
+                                               float* __restrict__ dst, Geom g, int x0, int y0, int tid, float ik2) {
+    float lmax = 0.f;
     constexpr int RG = 7;  // output rows per thread (8 groups x 7 = CH2); 4 groups x 14 rows on half the threads
                            // (fewer window re-reads) measured 22.3 vs 21.8 ms
     const int cp = tid & 31, q0 = (tid >> 5) * RG;
@@ -269,8 +272,18 @@ __device__ __forceinline__ void cond_vpass_x2(const float (*sA)[CW2], const floa
             }
             const float2 gx = __fmul2_rn(c2(0.5f), __ffma2_rn(c2(kW0c), __fadd2_rn(aup, adn), __fmul2_rn(c2(kW1c), va1)));
             const float2 gy = __fmul2_rn(c2(0.5f), __fadd2_rn(bdn, make_float2(-bup.x, -bup.y)));
-            const float2 q = __fmul2_rn(__ffma2_rn(gx, gx, __fmul2_rn(gy, gy)), ik);
-            const float2 cv = make_float2(diffusivity_g(q.x, DIFF), diffusivity_g(q.y, DIFF));
+            const float2 g2 = __ffma2_rn(gx, gx, __fmul2_rn(gy, gy));
+            float2 cv;
+            if constexpr (MODE == 1) {
+                const float2 q = __fmul2_rn(g2, ik);
+                cv = make_float2(diffusivity_g(q.x, DIFF), diffusivity_g(q.y, DIFF));
+            } else {
+                cv = g2;
+                if (y >= 1 && y <= g.H - 2) {
+                    if (x >= 1 && x <= g.W - 2) lmax = fmaxf(lmax, sqrtf(g2.x));
+                    if (x + 1 >= 1 && x + 1 <= g.W - 2) lmax = fmaxf(lmax, sqrtf(g2.y));
+                }
+            }
             float* o = dst + (unsigned)(y * g.P + x);  // dst is opaque: one IMAD.WIDE per row
             if (interior) {
                 __stwb(reinterpret_cast<float2*>(o), cv);
@@ -282,6 +295,7 @@ __device__ __forceinline__ void cond_vpass_x2(const float (*sA)[CW2], const floa
         va0 = va1; va1 = a;
         vb0 = vb1; vb1 = b;
     }
+    return lmax;
 }
 
 template <int MODE, int DIFF>
@@ -311,59 +325,10 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
     }
     __syncthreads();
     if constexpr (MODE == 1) {
-        cond_vpass_x2<DIFF>(sA, sB, w, opaque(out + img * out_img_stride), g, x0, y0, tid, frcp(kval[img] * kval[img]));
+        cond_vpass_x2<1, DIFF>(sA, sB, w, opaque(out + img * out_img_stride), g, x0, y0, tid, frcp(kval[img] * kval[img]));
         return;
-    }
-    const int cl = tid & 63, q0 = (tid >> 6) * CQ2;  // column, first chain row (tile-relative)
-    const int x = x0 + cl;
-    float va[CQ2 + 2], vb[CQ2 + 2];  // rows q0-1 .. q0+CQ2
-#pragma unroll
-    for (int j = 0; j < CQ2 + 2; ++j) {
-        float aa = w[0] * sA[q0 + j][cl], bb = w[0] * sB[q0 + j][cl];
-#pragma unroll
-        for (int d = 1; d < 7; ++d) {
-            aa = fmaf(w[d], sA[q0 + j + d][cl], aa);
-            bb = fmaf(w[d], sB[q0 + j + d][cl], bb);
-        }
-        va[j] = aa;
-        vb[j] = bb;
-    }
-    float ik2 = 1.f;
-    if (MODE == 1) {
-        const float k = kval[img];
-        ik2 = frcp(k * k);
-    }
-    float lmax = 0.f;
-    float* dst = out + img * out_img_stride + (size_t)(y0 + q0) * g.P + x;
-    const bool interior = (y0 > 0) && (y0 + CH2 < g.H) && (x0 + CW2 <= g.W);  // CTA-uniform
-    if (MODE == 1 && interior) {
-#pragma unroll
-        for (int j = 0; j < CQ2; ++j) {
-            const float gx = 0.5f * fmaf(kW0c, va[j] + va[j + 2], kW1c * va[j + 1]);
-            const float gy = 0.5f * (vb[j + 2] - vb[j]);
-            dst[(size_t)j * g.P] = diffusivity_g(fmaf(gx, gx, gy * gy) * ik2, DIFF);
-        }
-        return;
-    }
-#pragma unroll
-    for (int j = 0; j < CQ2; ++j) {
-        const int y = y0 + q0 + j;
-        const bool top = (y == 0), bot = (y >= g.H - 1);
-        const float aup = top ? va[j + 1] : va[j], adn = bot ? va[j + 1] : va[j + 2];
-        const float bup = top ? vb[j + 1] : vb[j], bdn = bot ? vb[j + 1] : vb[j + 2];
-        const float gx = 0.5f * fmaf(kW0c, aup + adn, kW1c * va[j + 1]);
-        const float gy = 0.5f * (bdn - bup);
-        const float g2 = fmaf(gx, gx, gy * gy);
-        if (x < g.W && y < g.H) {
-            if (MODE == 0) {
-                dst[(size_t)j * g.P] = g2;
-                if (x >= 1 && x <= g.W - 2 && y >= 1 && y <= g.H - 2) lmax = fmaxf(lmax, sqrtf(g2));
-            } else {
-                dst[(size_t)j * g.P] = diffusivity_g(g2 * ik2, DIFF);
-            }
-        }
-    }
-    if (MODE == 0) {
+    } else {
+        float lmax = cond_vpass_x2<0, DIFF>(sA, sB, w, opaque(out + img * out_img_stride), g, x0, y0, tid, 1.f);
         for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
         if ((tid & 31) == 0) red[tid >> 5] = lmax;
         __syncthreads();
@@ -372,6 +337,7 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
             for (int wv = 0; wv < 8; ++wv) m = fmaxf(m, red[wv]);
             atomicMax(hmax_bits + img, __float_as_uint(m));
         }
+        return;
     }
 }
 
