@@ -142,7 +142,13 @@ kaze_status kaze_describe(kaze_ctx* ctx, kaze_keypoint* d_kps, const int32_t* d_
                           void* stream);
 
 /* Convenience: build + detect + describe for n images (any n >= 0; processed in chunks of
- * max_batch).  Outputs are indexed by image as in kaze_detect / kaze_describe. */
+ * max_batch).  Outputs are indexed by image as in kaze_detect / kaze_describe.  Unless
+ * KAZE_FLAG_NO_GRAPHS is set (or profiling is on), a chunk whose (d_imgs, d_kps, d_counts, d_desc
+ * offsets, n, w, h, pitch, stream) key has been seen twice is replayed as one CUDA graph captured on
+ * a context-private stream (the graph bakes in those pointers; up to 96 keys are cached, least
+ * recently used evicted); results are bit-identical to direct launches.  The call is asynchronous on
+ * `stream` like the stage entry points.  Errors: as the stage entry points, plus CUDA for a failed
+ * capture or instantiation. */
 kaze_status kaze_extract(kaze_ctx* ctx, const float* d_imgs, int32_t n, int32_t w, int32_t h,
                          int64_t pitch_elems, kaze_keypoint* d_kps, int32_t* d_counts, float* d_desc,
                          void* stream);
