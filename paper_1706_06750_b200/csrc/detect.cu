@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(1024) k_kp_scan(const int* __restrict__ rowcnt
     if (threadIdx.x == blockDim.x - 1) counts[img] = run;
 }
 
-// One WARP per (image, level, row); 8 rows per CTA.  Lane w of a 32-word step owns bitmap word w: an inclusive warp
+// One WARP per (image, level, row); 8 rows per CTA.  (Four rows per warp, their counts and offsets in one load each:
+// 3.2 vs 2.8 ms per 256-image step — the rows then run serially in the warp.)  Lane w of a 32-word step owns bitmap word w: an inclusive warp
 // scan of the word popcounts gives each word's rank base, and the lane walks its set bits in x order.
 __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet, size_t img_stride, Geom g,
                                                  LevelTable lt, DetectParams dp, const uint32_t* __restrict__ bitmap,
