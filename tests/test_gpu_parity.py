@@ -291,6 +291,13 @@ def test_pitched_input_equals_packed_input():
     kb, cb, db = a.alloc_outputs(1)
     K.kaze_extract(a.ctx, padded[:, :, :130], kb, cb, db)
     assert torch.equal(ca, cb) and torch.equal(ka, kb) and torch.equal(da, db)
+    # odd pitch and a base pointer off the 16-byte grid: the prefilter's scalar-load path, same result
+    buf = torch.zeros(1 + 100 * 131, device="cuda")
+    odd = buf[1:].view(1, 100, 131)
+    odd[:, :, :130] = img
+    kc, cc, dc = a.alloc_outputs(1)
+    K.kaze_extract(a.ctx, odd[:, :, :130], kc, cc, dc)
+    assert torch.equal(ca, cc) and torch.equal(ka, kc) and torch.equal(da, dc)
     a.close()
 
 
