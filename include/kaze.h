@@ -88,6 +88,10 @@ typedef struct {
  * CUDA graph (captured on a private stream, launched on the caller's); this flag disables that (every kernel is
  * launched directly).  Profiling (kaze_set_profiling) also launches directly. */
 #define KAZE_FLAG_NO_GRAPHS 8
+/* Materialise (Lx, Ly) of the first and last level too.  Those two levels carry no keypoints (A11), so their first
+ * derivatives feed only their own Ldet, which the fused Hessian pass forms on chip; by default they are not stored
+ * and kaze_get_level(KAZE_PLANE_LX / LY) of level 0 or N−1 returns KAZE_ERR_STATE. */
+#define KAZE_FLAG_ALL_DERIVATIVES 16
 
 /* 32-byte keypoint (P:L212-214 sub-pixel position; D4 of SURVEY). */
 typedef struct {
@@ -169,7 +173,8 @@ kaze_status kaze_extract_host(kaze_ctx* ctx, const float* h_imgs, int32_t n, int
 kaze_status kaze_get_k(kaze_ctx* ctx, float* h_k, int32_t* h_fallback);
 
 /* Copies plane `which` of level `level` of image `img` (h x w, tightly packed) to/from d_buf.
- * Errors: INVALID_ARGUMENT (range), STATE (nothing built), CUDA. */
+ * Errors: INVALID_ARGUMENT (range), STATE (nothing built; or LX / LY of level 0 or N−1 without
+ * KAZE_FLAG_ALL_DERIVATIVES), CUDA. */
 kaze_status kaze_get_level(kaze_ctx* ctx, int32_t img, int32_t level, int32_t which, float* d_out, void* stream);
 kaze_status kaze_set_level(kaze_ctx* ctx, int32_t img, int32_t level, int32_t which, const float* d_in, void* stream);
 

@@ -20,7 +20,7 @@ __all__ = [
     "kaze_default_params", "kaze_create", "kaze_destroy", "kaze_build_scale_space", "kaze_detect",
     "kaze_describe", "kaze_extract", "kaze_extract_host", "kaze_get_k", "kaze_get_level", "kaze_set_level",
     "kaze_set_profiling", "kaze_get_profile", "kaze_reset_profile", "kaze_launch_count", "kaze_abi_version",
-    "kaze_fed_cycle", "kaze_match_scratch_bytes", "kaze_match", "kaze_memory_footprint", "KazeMemory", "Kaze", "PLANE_LT", "PLANE_LX", "PLANE_LY", "PLANE_LDET", "PLANE_COND", "FLAG_KEEP_ANGLE", "FLAG_EXACT_WINDOW", "FLAG_REFINE_3D", "FLAG_NO_GRAPHS", "SCHEME_AOS", "SCHEME_FED",
+    "kaze_fed_cycle", "kaze_match_scratch_bytes", "kaze_match", "kaze_memory_footprint", "KazeMemory", "Kaze", "PLANE_LT", "PLANE_LX", "PLANE_LY", "PLANE_LDET", "PLANE_COND", "FLAG_KEEP_ANGLE", "FLAG_EXACT_WINDOW", "FLAG_REFINE_3D", "FLAG_NO_GRAPHS", "FLAG_ALL_DERIVATIVES", "SCHEME_AOS", "SCHEME_FED",
     "EXPORTED_SYMBOLS",
 ]
 
@@ -31,6 +31,7 @@ PLANE_LT, PLANE_LX, PLANE_LY, PLANE_LDET, PLANE_COND = 0, 1, 2, 3, 4
 FLAG_KEEP_ANGLE = 1
 FLAG_EXACT_WINDOW, FLAG_REFINE_3D = 2, 4
 FLAG_NO_GRAPHS = 8  # kaze_extract launches every kernel directly instead of replaying CUDA graphs
+FLAG_ALL_DERIVATIVES = 16  # also store (Lx, Ly) of the first and last level (otherwise only their Ldet exists)
 SCHEME_AOS, SCHEME_FED = 0, 1
 
 STATUS = {

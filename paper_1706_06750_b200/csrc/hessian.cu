@@ -176,7 +176,7 @@ __host__ inline int fused_cw_host(int s) { return s <= 16 ? 224 : 192; }
 
 template <int R, int SC>
 __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, float2* __restrict__ D, float* __restrict__ O,
-                                                Geom g, int s_rt, int ch, int xb, float2 (*sm)[256]) {
+                                                Geom g, int s_rt, int ch, int xb, float2 (*sm)[256], bool keep_d) {
     const int s = SC > 0 ? SC : s_rt;
     const int cw = fused_cw(s);
     const int nch = s * ((g.H + R * s - 1) / (R * s));
@@ -190,7 +190,7 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
     const bool fast = SC > 0 && y0 >= 2 * s && y0 + (R + 1) * s <= g.H - 1 && x0 >= 2 * s && x0 + cw + 2 * s <= g.W;
     if (in_a) {
         const int cc = clampi(vc, 0, g.W - 1);
-        const bool store_col = vc >= x0 && vc < x0 + cw && vc < g.W;
+        const bool store_col = keep_d && vc >= x0 && vc < x0 + cw && vc < g.W;
         if (fast) {
             // chain rows k = -2..R+1 of columns cc - s, cc, cc + s (no clamps anywhere)
             float a[R + 4], m[R + 4], c[R + 4];
@@ -247,7 +247,8 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
 
 template <int R>
 __global__ void __launch_bounds__(256) k_hess_fused(const float* __restrict__ Lt, float2* __restrict__ Lxy,
-                                                    float* __restrict__ Ldet, size_t img_stride, Geom g, LevelTable lt) {
+                                                    float* __restrict__ Ldet, size_t img_stride, Geom g, LevelTable lt,
+                                                    int keep_edges) {
     KZ_PDL_PROLOGUE();
     __shared__ float2 sm[R + 2][256];  // 36 KB at R = 16.  (Staging the L taps in shared memory as well — each
                                        // loaded once instead of three times through L1 — measured slower: 76.7 ms.)
@@ -257,12 +258,14 @@ __global__ void __launch_bounds__(256) k_hess_fused(const float* __restrict__ Lt
     const float* L = opaque(Lt + base);
     float2* D = opaque(Lxy + base);
     float* O = opaque(Ldet + base);
+    // (Lx, Ly) of the first and last level only feed their own Ldet (no keypoints there): not stored by default
+    const bool keep_d = keep_edges || (level > 0 && level < lt.n - 1);
     switch (s) {
 #define KZ_CASE(S) \
-    case S: hess_fused_body<R, S>(L, D, O, g, s, blockIdx.y, blockIdx.x, sm); break;
+    case S: hess_fused_body<R, S>(L, D, O, g, s, blockIdx.y, blockIdx.x, sm, keep_d); break;
         KZ_STEP_CASES(KZ_CASE)
 #undef KZ_CASE
-        default: hess_fused_body<R, 0>(L, D, O, g, s, blockIdx.y, blockIdx.x, sm); break;
+        default: hess_fused_body<R, 0>(L, D, O, g, s, blockIdx.y, blockIdx.x, sm, keep_d); break;
     }
 }
 
@@ -301,7 +304,7 @@ void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, 
 }
 
 bool launch_hess_fused(const float* Lt, float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg,
-                       const LevelTable& lt, cudaStream_t s) {
+                       const LevelTable& lt, int keep_edges, cudaStream_t s) {
     int gx = 1, gy = 1;
     for (int l = 0; l < lt.n; ++l) {
         const int st = lt.step[l];
@@ -309,7 +312,7 @@ bool launch_hess_fused(const float* Lt, float2* Lxy, float* Ldet, size_t img_str
         gx = max(gx, (g.W + fused_cw_host(st) - 1) / fused_cw_host(st));
         gy = max(gy, st * ((g.H + kFusedR * st - 1) / (kFusedR * st)));
     }
-    kz_launch(k_hess_fused<kFusedR>, dim3(dim3(gx, gy, nimg * lt.n)), dim3(256), 0, s, Lt, Lxy, Ldet, img_stride, g, lt);
+    kz_launch(k_hess_fused<kFusedR>, dim3(dim3(gx, gy, nimg * lt.n)), dim3(256), 0, s, Lt, Lxy, Ldet, img_stride, g, lt, keep_edges);
     return true;
 }
 

@@ -73,6 +73,7 @@ struct kaze_ctx {
     Geom geom{};
     size_t img_stride = 0;  // N * plane
     bool built = false, detected = false;
+    bool edge_derivs = true;  // (Lx, Ly) of levels 0 and N−1 materialised by the last detect
     cudaStream_t last_stream = nullptr;
     // host path
     float* hin[2] = {nullptr, nullptr};
@@ -394,14 +395,19 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     {   // Hessian (Eq. 8), all levels in two launches: L → (Lx, Ly) → Ldet
         static const int fused = tune_knob("KAZE_HESS_FUSED", 1);
         if (fused) {
-            Launch L(c, KC_HESSIAN, 16.0 * px * N, s, 1);
-            if (!launch_hess_fused(c->Lt, c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s)) {
+            const int keep = (c->p.flags & KAZE_FLAG_ALL_DERIVATIVES) ? 1 : 0;
+            // 16 B/px per level; the first and last level store no (Lx, Ly) unless asked: 8 B/px there
+            Launch L(c, KC_HESSIAN, (keep ? 16.0 * N : 16.0 * N - 16.0) * px, s, 1);
+            c->edge_derivs = keep != 0;
+            if (!launch_hess_fused(c->Lt, c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, keep, s)) {
                 launch_hess_first(c->Lt, c->Lxy, c->img_stride, g, n, c->lt, s);
                 launch_hess_det(c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s);
                 L.bytes = 24.0 * px * N;
                 L.nk = 2;
+                c->edge_derivs = true;
             }
         } else {
+            c->edge_derivs = true;
             Launch L(c, KC_HESSIAN, 24.0 * px * N, s, 2);
             launch_hess_first(c->Lt, c->Lxy, c->img_stride, g, n, c->lt, s);
             launch_hess_det(c->Lxy, c->Ldet, c->img_stride, g, n, c->lt, s);
@@ -874,6 +880,8 @@ static kaze_status plane_ptr(kaze_ctx* c, int32_t img, int32_t level, int32_t wh
 
 kaze_status kaze_get_level(kaze_ctx* c, int32_t img, int32_t level, int32_t which, float* d_out, void* stream) {
     if (!c || !d_out) return KAZE_ERR_INVALID_ARGUMENT;
+    if ((which == KAZE_PLANE_LX || which == KAZE_PLANE_LY) && (level == 0 || level == c->N - 1) && !c->edge_derivs)
+        return KAZE_ERR_STATE;
     float* src = nullptr;
     kaze_status st = plane_ptr(c, img, level, which, &src);
     if (st != KAZE_OK) return st;

@@ -113,7 +113,7 @@ void launch_hess_first(const float* Lt, float2* Lxy, size_t img_stride, Geom g, 
                        cudaStream_t s);
 // One pass (16 B/px): Lxy and Ldet of every level of nimg images; false if some step exceeds the fused form's 32.
 bool launch_hess_fused(const float* Lt, float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg,
-                       const LevelTable& lt, cudaStream_t s);
+                       const LevelTable& lt, int keep_edges, cudaStream_t s);
 void launch_hess_det(const float2* Lxy, float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                      cudaStream_t s);
 // Diagnostic copy of one component of an interleaved plane to/from a tightly packed w x h buffer

@@ -141,7 +141,7 @@ def test_batch_in_grid_equals_single_images(O):
 def test_hessian_stage_isolated(O):
     """Oracle levels (as fp32) injected through kaze_set_level; Lx, Ly, Ldet vs the oracle Hessian of the same."""
     img, ref = oracle_run(O, 333, 257, octaves=3, sublevels=4)
-    kz = make(333, 257, octaves=3, sublevels=4, k_override=ref["k"])
+    kz = make(333, 257, octaves=3, sublevels=4, k_override=ref["k"], flags=K.FLAG_ALL_DERIVATIVES)
     K.kaze_build_scale_space(kz.ctx, torch.from_numpy(img).cuda()[None])
     lv32 = ref["levels"].astype(np.float32)
     for i in range(12):
@@ -161,6 +161,26 @@ def test_hessian_stage_isolated(O):
     frac, _ = match_keypoints(kref, got, tol=1e-3)
     assert abs(int(counts[0]) - nref) <= max(2, 0.002 * nref) and frac >= 0.995
     kz.close()
+
+
+def test_edge_level_derivatives_are_not_materialised_by_default():
+    """Levels 0 and N-1 carry no keypoints: by default their (Lx, Ly) are not stored (get_level -> STATE), every
+    other plane is, and the keypoints/descriptors are identical with and without KAZE_FLAG_ALL_DERIVATIVES."""
+    img = torch.from_numpy(kaze_inputs.synth_image(200, 150)).cuda()[None]
+    a = make(200, 150, octaves=3, sublevels=3)
+    b = make(200, 150, octaves=3, sublevels=3, flags=K.FLAG_ALL_DERIVATIVES)
+    ra, rb = a.extract(img), b.extract(img)
+    for x, y in zip(ra, rb):
+        assert torch.equal(x, y)
+    out = torch.empty((150, 200), device="cuda")
+    for lvl in (0, 8):
+        with pytest.raises(K.KazeError):
+            K.kaze_get_level(a.ctx, 0, lvl, K.PLANE_LX, out)
+        K.kaze_get_level(b.ctx, 0, lvl, K.PLANE_LX, out)
+    K.kaze_get_level(a.ctx, 0, 4, K.PLANE_LY, out)
+    K.kaze_get_level(a.ctx, 0, 0, K.PLANE_LDET, out)
+    a.close()
+    b.close()
 
 
 @pytest.mark.parametrize("w,h,O_,S_", [(640, 480, 4, 4), (128, 128, 2, 2), (333, 257, 3, 4)])
