@@ -558,6 +558,35 @@ def test_fed_keypoints_and_descriptors_end_to_end(O):
     kz.close()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("mode", ["fed", "exact", "refine3d"])
+def test_f_rows_at_full_size_in_bench_launch_configuration(O, mode):
+    """SURVEY §8 f1/f2 at BASELINE configs[2] size in the bench's launch configuration (16 images per launch, graph
+    replay): the FED backend and the two detector variants, image 0 of the batch against the full fp64 oracle
+    (>= 99% of keypoints both ways, >= 99% of matched descriptors with cos >= 0.999)."""
+    kw, gk = {"fed": ({"scheme": 1}, {"scheme": K.SCHEME_FED}),
+              "exact": ({"exact_window": 1}, {"flags": K.FLAG_EXACT_WINDOW}),
+              "refine3d": ({"refine3d": 1}, {"flags": K.FLAG_REFINE_3D})}[mode]
+    imgs = kaze_inputs.synth_batch(16, 1920, 1200, distinct=2)
+    ref = O.run(imgs[0], cap=1 << 17, **kw)
+    kz = make(1920, 1200, batch=16, max_keypoints=32768, **gk)
+    dimg = torch.from_numpy(imgs).cuda()
+    out = kz.alloc_outputs(16)
+    for _ in range(3):
+        K.kaze_extract(kz.ctx, dimg, *out)
+    kps, counts, desc = out
+    got = K.Kaze.keypoints_numpy(kps, counts)[0]
+    f1, idx = match_keypoints(ref["kps"], got)
+    f2, _ = match_keypoints(got, ref["kps"])
+    assert f1 >= 0.99 and f2 >= 0.99, (mode, f1, f2, ref["count"], int(counts[0]))
+    d = desc[0, : len(got)].cpu().numpy().astype(np.float64)
+    m = idx >= 0
+    a, b = ref["desc"][m], d[idx[m]]
+    cos = np.sum(a * b, 1) / (np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1) + 1e-30)
+    assert np.mean(cos >= 0.999) >= 0.99, (mode, np.mean(cos >= 0.999))
+    kz.close()
+
+
 def test_fed_constant_image_is_identity_and_batch_matches_single():
     kz = make(96, 80, batch=2, scheme=K.SCHEME_FED, k_override=0.05)
     img = torch.full((1, 80, 96), 0.25, device="cuda")
