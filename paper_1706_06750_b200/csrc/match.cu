@@ -30,6 +30,7 @@ namespace {
 constexpr int kTileR = 256;                 // reference rows per tile (UMMA N)
 constexpr int kTileQ = 128;                 // query rows per CTA (UMMA M)
 constexpr int kTileBytes = kTileR * 128;    // 64 bf16 = 128 B per row
+constexpr int kStages = 4;  // reference-tile ring depth (TMA → MMA)
 constexpr int kCand = 8;  // approximate candidates kept per query (4: 1400 of 15.8k KAZE rows uncertified, 3.4 ms)
 constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 4.06 vs 3.98 ms at 65536^2)
 constexpr int kColGroups = kEpiWarps / 4;
@@ -174,16 +175,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
     // 1024-byte alignment for the swizzle atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;                    // 16 KB
-    uint8_t* sB = smem + kTileQ * 128;     // 2 x 32 KB
-    __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2], bar_acc_full[2], bar_acc_empty[2], bar_a;
+    uint8_t* sB = smem + kTileQ * 128;     // kStages x 32 KB
+    __shared__ __align__(8) uint64_t bar_full[kStages], bar_empty[kStages], bar_acc_full[2], bar_acc_empty[2], bar_a;
     __shared__ uint32_t tmem_base_slot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (nr + kTileR - 1) / kTileR;
     const int q0 = blockIdx.x * kTileQ;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kStages; ++i) {
             mbar_init(&bar_full[i], 1);
             mbar_init(&bar_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_acc_full[i], 1);
             mbar_init(&bar_acc_empty[i], kEpiWarps * 32);
         }
@@ -201,8 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
             mbar_arrive_expect_tx(&bar_a, kTileQ * 128);
             bulk_g2s(sA, Qt + (size_t)q0 * 128, kTileQ * 128, &bar_a);
             for (int t = 0; t < ntiles; ++t) {
-                const int s = t & 1;
-                if (t >= 2) mbar_wait(&bar_empty[s], ((t >> 1) - 1) & 1);
+                const int s = t % kStages;
+                if (t >= kStages) mbar_wait(&bar_empty[s], ((t / kStages) - 1) & 1);
                 mbar_arrive_expect_tx(&bar_full[s], kTileBytes);
                 bulk_g2s(sB + s * kTileBytes, Rt + (size_t)t * kTileBytes, kTileBytes, &bar_full[s]);
             }
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
             mbar_wait(&bar_a, 0);
             const uint32_t a_addr = smem_u32(sA);
             for (int t = 0; t < ntiles; ++t) {
-                const int s = t & 1, a = t & 1;
-                mbar_wait(&bar_full[s], (t >> 1) & 1);
+                const int s = t % kStages, a = t & 1;
+                mbar_wait(&bar_full[s], (t / kStages) & 1);
                 if (t >= 2) mbar_wait(&bar_acc_empty[a], ((t >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t b_addr = smem_u32(sB + s * kTileBytes);
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
         }
     } else {  // ===== epilogue warps: TMEM → registers → running top-4 per query row =====
         const int g = warp & 3, h = warp >> 2;  // TMEM lane group (query rows 32g..), column group
-        float* sv = reinterpret_cast<float*>(sB + 2 * kTileBytes) + warp * 32 * 32;  // 4 KB per epilogue warp
+        float* sv = reinterpret_cast<float*>(sB + kStages * kTileBytes) + warp * 32 * 32;  // 4 KB per epilogue warp
         TopK tk;
 #pragma unroll
         for (int q = 0; q < kCand; ++q) {
@@ -495,7 +498,7 @@ static cudaError_t run_direction(const float* Q, int nq, const uint8_t* Qt, cons
                                  const uint32_t* rvalid, const unsigned* rnorm, float* cs, int* cj, int* best,
                                  float* d1, float* d2, int* unc, cudaStream_t s) {
     static bool attr = false;
-    const int smem = kTileQ * 128 + 2 * kTileBytes + kEpiWarps * 32 * 32 * 4 + 1024;
+    const int smem = kTileQ * 128 + kStages * kTileBytes + kEpiWarps * 32 * 32 * 4 + 1024;
     if (!attr) {
         cudaFuncSetAttribute(k_match_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
