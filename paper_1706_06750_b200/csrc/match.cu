@@ -63,6 +63,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // 32 lanes x 32 columns of 32-bit accumulators → 32 registers per thread (thread i ↔ lane base+i).
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
     asm volatile(
@@ -241,11 +252,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
             const int a = t & 1;
             mbar_wait(&bar_acc_full[a], (t >> 1) & 1);
             tc_fence_after();
-#pragma unroll 1
-            for (int ch = 0; ch < kTileR / kColGroups / 32; ++ch) {
+            // all of this warp's chunks of the tile leave TMEM behind one wait (several loads in flight, not one)
+            constexpr int kChunks = kTileR / kColGroups / 32;
+            uint32_t vr[kChunks][32];
+#pragma unroll
+            for (int ch = 0; ch < kChunks; ++ch)
+                tmem_ld32_nowait(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(a * kTileR + h * (kTileR / kColGroups) + ch * 32),
+                                 vr[ch]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int ch = 0; ch < kChunks; ++ch) {
                 const int col = h * (kTileR / kColGroups) + ch * 32;
                 float v[32];
-                tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(a * kTileR + col), v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(vr[ch][i]);
                 const int j0 = t * kTileR + col;
                 const uint32_t vm = __ldg(rvalid + (j0 >> 5));  // 32 columns = one validity word
                 if (vm != 0xffffffffu) {  // warp-uniform and rare: padding / degenerate references never compete
