@@ -260,6 +260,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
                 tmem_ld32_nowait(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(a * kTileR + h * (kTileR / kColGroups) + ch * 32),
                                  vr[ch]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            // the accumulator is in registers now: hand it back to the MMA issuer before scanning it
+            tc_fence_before();
+            mbar_arrive(&bar_acc_empty[a]);
 #pragma unroll
             for (int ch = 0; ch < kChunks; ++ch) {
                 const int col = h * (kTileR / kColGroups) + ch * 32;
@@ -300,8 +303,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
                     __syncwarp();
                 }
             }
-            tc_fence_before();
-            mbar_arrive(&bar_acc_empty[a]);
         }
         // merge the column groups of each row through shared memory (the B ring is free by now)
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32));
