@@ -32,7 +32,7 @@ constexpr int kTileQ = 128;                 // query rows per CTA (UMMA M)
 constexpr int kTileBytes = kTileR * 128;    // 64 bf16 = 128 B per row
 constexpr int kStages = 4;  // reference-tile ring depth (TMA → MMA)
 constexpr int kCand = 8;  // approximate candidates kept per query (4: 1400 of 15.8k KAZE rows uncertified, 3.4 ms)
-constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 4.06 vs 3.98 ms at 65536^2)
+constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 3.64 vs 3.59 ms at 65536^2)
 constexpr int kColGroups = kEpiWarps / 4;
 constexpr int kThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
 constexpr float kEps = 1.0f / 1024.0f + 2e-5f;  // fp16 rounding of both operands (2·2^-11) + fp32 sum slack
