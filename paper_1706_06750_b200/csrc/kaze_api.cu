@@ -1,5 +1,6 @@
 // kaze_api.cu — the C ABI of include/kaze.h: context, arena, level schedule, orchestration of the sm_100a
-// kernels on the caller's stream, the pipelined host-buffer path, and per-kernel event profiling.
+// kernels on the caller's stream, CUDA-graph capture/replay of whole chunks (run_chunk), the pipelined
+// host-buffer path, per-kernel event profiling, and the host side of programmatic dependent launch.
 //
 // Host-side arithmetic kept here (schedule, Gaussian taps, τ_i) is this product's own; it shares nothing with
 // oracle/ (DESIGN.md §2).
@@ -392,7 +393,7 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
     const int N = c->N, n = c->n;
     const Geom g = c->geom;
     const double px = (double)g.W * g.H * n;
-    {   // Hessian (Eq. 8), all levels in two launches: L → (Lx, Ly) → Ldet
+    {   // Hessian (Eq. 8), all levels of all images in one fused launch (two chain passes for steps > 32)
         static const int fused = tune_knob("KAZE_HESS_FUSED", 1);
         if (fused) {
             const int keep = (c->p.flags & KAZE_FLAG_ALL_DERIVATIVES) ? 1 : 0;
