@@ -6,7 +6,7 @@
 //      mask per tile (degenerate = all-zero descriptors and padding rows are never candidates) and the norm
 //      range of the valid rows.
 //   2. k_match_topk: one CTA per 128 query rows.  A TMA warp streams the reference tiles (double-buffered
-//      mbarrier ring), one thread issues tcgen05.mma kind::f16 (M = 128, N = 256, K = 4 x 16) into a
+//      mbarrier ring), one thread issues tcgen05.mma kind::f16 (M = 128, N = 128, K = 4 x 16) into a
 //      double-buffered TMEM accumulator (2 x 256 columns), and 8 epilogue warps drain it with tcgen05.ld
 //      (warp w reads TMEM lanes 32·(w%4).. = its 32 query rows, column half w/4), keeping each row's eight best
 //      approximate scores.  fp16 operands (descriptor components lie in [−1, 1]; fp16 has bf16's tensor rate and
@@ -27,10 +27,10 @@ namespace kz {
 
 namespace {
 
-constexpr int kTileR = 256;                 // reference rows per tile (UMMA N)
+constexpr int kTileR = 128;                 // reference rows per tile (UMMA N); 128 lets two CTAs share an SM's TMEM
 constexpr int kTileQ = 128;                 // query rows per CTA (UMMA M)
 constexpr int kTileBytes = kTileR * 128;    // 64 bf16 = 128 B per row
-constexpr int kStages = 4;  // reference-tile ring depth (TMA → MMA)
+constexpr int kStages = 3;  // reference-tile ring depth (TMA → MMA)
 constexpr int kCand = 8;  // approximate candidates kept per query (4: 1400 of 15.8k KAZE rows uncertified, 3.4 ms)
 constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 3.64 vs 3.59 ms at 65536^2)
 constexpr int kColGroups = kEpiWarps / 4;
@@ -95,7 +95,7 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 // Instruction descriptor kind::f16: D f32 (bits 4-5 = 1), A/B f16 (format 0 at bits 7-9 / 10-12), both K-major,
-// N = 256 (bits 17-22 = N/8), M = 128 (bits 24-28 = M/16).
+// N = kTileR (bits 17-22 = N/8), M = 128 (bits 24-28 = M/16).
 constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kTileR >> 3) << 17) | ((uint32_t)(kTileQ >> 4) << 24);
 
 __global__ void __launch_bounds__(256) k_match_prep(const float* __restrict__ D, int n, int ntiles,
@@ -178,7 +178,7 @@ __device__ __forceinline__ void topk_insert(TopK& t, float v, int j) {
     if (v > t.s[kCand - 1]) topk_push_scan(t, v, j);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __restrict__ Qt, int nq,
+__global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __restrict__ Qt, int nq,
                                                             const uint8_t* __restrict__ Rt, int nr,
                                                             const uint32_t* __restrict__ rvalid,
                                                             float* __restrict__ cand_s, int* __restrict__ cand_j) {
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
         mbar_init(&bar_a, 1);
         fence_mbar_init();
     }
-    if (warp == kEpiWarps + 1) tmem_alloc(&tmem_base_slot, 512);
+    if (warp == kEpiWarps + 1) tmem_alloc(&tmem_base_slot, 2 * kTileR);  // double-buffered accumulator
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_match_topk(const uint8_t* __res
     __syncthreads();
     if (warp == kEpiWarps + 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, 2 * kTileR);
     }
 }
 
