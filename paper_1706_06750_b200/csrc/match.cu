@@ -31,6 +31,7 @@ constexpr int kTileR = 128;                 // reference rows per tile (UMMA N);
 constexpr int kTileQ = 128;                 // query rows per CTA (UMMA M)
 constexpr int kTileBytes = kTileR * 128;    // 64 bf16 = 128 B per row
 constexpr int kStages = 3;  // reference-tile ring depth (TMA → MMA)
+constexpr int kMaxSplit = 4;  // reference-range parts per query block when the query blocks alone cannot fill the GPU
 constexpr int kCand = 8;  // approximate candidates kept per query (4: 1400 of 15.8k KAZE rows uncertified, 3.4 ms)
 constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 3.64 vs 3.59 ms at 65536^2)
 constexpr int kColGroups = kEpiWarps / 4;
@@ -190,7 +191,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
     __shared__ __align__(8) uint64_t bar_full[kStages], bar_empty[kStages], bar_acc_full[2], bar_acc_empty[2], bar_a;
     __shared__ uint32_t tmem_base_slot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = (nr + kTileR - 1) / kTileR;
+    // this CTA scans reference tiles [tb, tb + ntiles) — part blockIdx.y of gridDim.y — and writes its own top-8
+    const int ntiles_all = (nr + kTileR - 1) / kTileR;
+    const int tb = (int)((long long)ntiles_all * blockIdx.y / gridDim.y);
+    const int ntiles = (int)((long long)ntiles_all * (blockIdx.y + 1) / gridDim.y) - tb;
+    Rt += (size_t)tb * kTileBytes;
+    rvalid += (size_t)tb * (kTileR / 32);
+    cand_s += (size_t)blockIdx.y * nq * kCand;
+    cand_j += (size_t)blockIdx.y * nq * kCand;
     const int q0 = blockIdx.x * kTileQ;
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) {
@@ -269,8 +277,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(vr[ch][i]);
-                const int j0 = t * kTileR + col;
-                const uint32_t vm = __ldg(rvalid + (j0 >> 5));  // 32 columns = one validity word
+                const int j0 = (tb + t) * kTileR + col;
+                const uint32_t vm = __ldg(rvalid + ((t * kTileR + col) >> 5));  // 32 columns = one validity word
                 if (vm != 0xffffffffu) {  // warp-uniform and rare: padding / degenerate references never compete
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = ((vm >> i) & 1u) ? v[i] : -INFINITY;
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(256) k_match_rerank(const float* __restrict__ 
                                                       int nr, const uint32_t* __restrict__ rvalid,
                                                       const unsigned* __restrict__ rnorm,
                                                       const float* __restrict__ cand_s, const int* __restrict__ cand_j,
-                                                      int* __restrict__ best, float* __restrict__ d1o,
+                                                      int nsplit, int* __restrict__ best, float* __restrict__ d1o,
                                                       float* __restrict__ d2o, int* __restrict__ uncertified) {
     __shared__ __align__(16) float qsh[8][64];  // the query, for the lane-parallel exact scan
     const int lane = threadIdx.x & 31;
@@ -381,29 +389,39 @@ __global__ void __launch_bounds__(256) k_match_rerank(const float* __restrict__ 
     }
     float bd1 = INFINITY, bd2 = INFINITY;
     int bj1 = -1;
-    int ncand = 0;
+    // the largest kept-last score over the parts whose list is full: every non-candidate scores at most that
+    float s8 = -INFINITY;
+    bool any_full = false;
+    for (int p = 0; p < nsplit; ++p) {  // parts cover disjoint reference ranges: no duplicates
+        const float* ps = cand_s + ((size_t)p * nq + q) * kCand;
+        const int* pj = cand_j + ((size_t)p * nq + q) * kCand;
+        int ncand = 0;
 #pragma unroll
-    for (int c = 0; c < kCand; ++c) {
-        const int j = __ldg(cand_j + (size_t)q * kCand + c);
-        if (j < 0) continue;
-        ++ncand;
-        const float d = exact_d2(a, R, j, lane);
-        if (before(d, j, bd1, bj1)) {
-            bd2 = bd1;
-            bd1 = d;
-            bj1 = j;
-        } else if (d < bd2) {
-            bd2 = d;
+        for (int c = 0; c < kCand; ++c) {
+            const int j = __ldg(pj + c);
+            if (j < 0) continue;
+            ++ncand;
+            const float d = exact_d2(a, R, j, lane);
+            if (before(d, j, bd1, bj1)) {
+                bd2 = bd1;
+                bd1 = d;
+                bj1 = j;
+            } else if (d < bd2) {
+                bd2 = d;
+            }
+        }
+        if (ncand == kCand) {  // a part with fewer kept than kCand kept all its valid references
+            any_full = true;
+            s8 = fmaxf(s8, __ldg(ps + kCand - 1));
         }
     }
-    // certification: a non-candidate has true score <= s_4 + ε|a|max|b|, hence distance² >= the bound below
+    // certification: a non-candidate has true score <= s8 + ε|a|max|b|, hence distance² >= the bound below
     bool cert = true;
-    if (ncand == kCand) {
+    if (any_full) {
         const float bmin = __uint_as_float(rnorm[0]), bmax = __uint_as_float(rnorm[1]);
         const float na = sqrtf(na2);
-        const float s4 = __ldg(cand_s + (size_t)q * kCand + kCand - 1);
         const float eps = kEps * na * bmax + 1e-5f;
-        const float bound = na2 + bmin * bmin - 2.f * (s4 + eps);
+        const float bound = na2 + bmin * bmin - 2.f * (s8 + eps);
         cert = bd2 < bound * (1.f - 4e-7f) - 1e-7f;
     }
     if (!cert) {  // exact scan of every valid reference (rare): lane-parallel over the references
@@ -500,8 +518,8 @@ static MatchScratch match_layout(int na, int nb) {
     m.validB = o; o += al(tb * kTileR / 8);
     m.normA = o; o += al(8);
     m.normB = o; o += al(8);
-    m.candS = o; o += al(nmax * kCand * sizeof(float));
-    m.candJ = o; o += al(nmax * kCand * sizeof(int));
+    m.candS = o; o += al(nmax * kCand * kMaxSplit * sizeof(float));
+    m.candJ = o; o += al(nmax * kCand * kMaxSplit * sizeof(int));
     m.bestAB = o; o += al((size_t)na * sizeof(int));
     m.bestBA = o; o += al((size_t)nb * sizeof(int));
     m.d1 = o; o += al((size_t)na * sizeof(float));
@@ -524,8 +542,13 @@ static cudaError_t run_direction(const float* Q, int nq, const uint8_t* Qt, cons
         cudaFuncSetAttribute(k_match_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_match_topk<<<(nq + kTileQ - 1) / kTileQ, kThreads, smem, s>>>(Qt, nq, Rt, nr, rvalid, cs, cj);
-    k_match_rerank<<<(nq + 7) / 8, 256, 0, s>>>(Q, nq, R, nr, rvalid, rnorm, cs, cj, best, d1, d2, unc);
+    // split the reference range when the query blocks alone would leave SMs idle (two CTAs fit per SM)
+    const int qblocks = (nq + kTileQ - 1) / kTileQ, rtiles = (nr + kTileR - 1) / kTileR;
+    int nsplit = (2 * 148 + qblocks - 1) / qblocks;
+    nsplit = nsplit < 1 ? 1 : (nsplit > kMaxSplit ? kMaxSplit : nsplit);
+    if (nsplit > rtiles) nsplit = rtiles > 0 ? rtiles : 1;
+    k_match_topk<<<dim3(qblocks, nsplit), kThreads, smem, s>>>(Qt, nq, Rt, nr, rvalid, cs, cj);
+    k_match_rerank<<<(nq + 7) / 8, 256, 0, s>>>(Q, nq, R, nr, rvalid, rnorm, cs, cj, nsplit, best, d1, d2, unc);
     return cudaGetLastError();
 }
 
