@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(256) k_fed(const float* __restrict__ Lin, size
     for (int s = 1; s <= K; ++s) {
         const float tau = taus.t[s - 1];
         // thread (tx, ty): columns s + tx + 32k, and a contiguous eighth of the rows [s, EH - s), walked downwards
-        // with the cell above and its face weight kept in registers (6 shared loads per cell instead of 9)
+        // with the cell above and its face weight kept in registers (6 shared loads per cell instead of 9).
+        // (Column pairs in fp32x2 from 8-byte shared loads — 6 loads per two cells — measured 264.6 vs 252 ms.)
         const int nrow = EH - 2 * s, per = (nrow + 7) / 8;
         const int r0 = s + ty * per, r1 = min(r0 + per, EH - s);
         for (int lx = s + tx; lx < EW - s; lx += 32) {
