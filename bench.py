@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--distinct", type=int, default=8, help="distinct generated images (the rest are shifts/flips)")
     ap.add_argument("--scheme", default="aos", choices=["aos", "fed"],
                     help="scale-space solver: AOS (Eq. 4, the north star) or FED cycles (Eq. 5, SURVEY 8 f1)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: a dry run of the multi-rank path, e.g. two ranks "
+                         "sharing one GPU)")
     return ap.parse_args()
 
 
@@ -126,7 +129,7 @@ def run_reference(args):
 
     oracle.build()
     cores = len(os.sched_getaffinity(0))
-    threads = max(1, min(cores, 8))
+    threads = max(1, cores)  # every host core the process may use (OpenMP over images, one image per thread)
     imgs = np.stack([kaze_inputs.synth_image(W_IMG, H_IMG, kaze_inputs.BASE_SEED + i) for i in range(threads)])
     times = []
     for i in range(args.warmup + args.steps):
@@ -135,7 +138,7 @@ def run_reference(args):
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
-    sec = statistics.mean(times)
+    sec = statistics.median(times)
     value = threads / sec
     cpu = next((l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")), "?")
     out = {
@@ -147,26 +150,35 @@ def run_reference(args):
         "ms_per_image": sec * 1e3 / threads,
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "oracle",
                          "sample": f"{threads} images (seeds 1234..{1233 + threads}) per step, one per thread, "
-                                   f"of the 1920x1200 full path; host '{cpu}', {cores} cores visible",
+                                   f"of the 1920x1200 full path; value from the median step of {len(times)}; "
+                                   f"host '{cpu}', {cores} cores usable",
                          "keypoints": [int(c) for c in counts]},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline_sample():
-    """Oracle timed on one image of the workload (1 thread) — ~10-20 s of CPU work."""
-    import kaze_inputs
+def cpu_baseline_sample(host_imgs, runs: int = 3):
+    """The oracle as it stands (OpenMP over images, one image per thread) on every usable host core: one image per
+    core of the workload's own first images, median of `runs` runs — ~20-30 s of CPU work."""
+    import numpy as np
+
     import oracle
 
     oracle.build()
-    img = kaze_inputs.synth_image(W_IMG, H_IMG, kaze_inputs.BASE_SEED)
-    t0 = time.perf_counter()
-    r = oracle.run(img, cap=1 << 17)
-    dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": "images/s", "cores": 1, "kind": "oracle",
-            "sample": f"1 image (seed 1234) of 1920x1200, full path, single thread: {dt:.2f} s, "
-                      f"{r['count']} keypoints"}
+    cores = max(1, len(os.sched_getaffinity(0)))
+    k = min(cores, len(host_imgs))
+    imgs = np.ascontiguousarray(host_imgs[:k])
+    times = []
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        counts = oracle.run_batch(imgs, cap=1 << 17, nthreads=k)
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    return {"value": k / dt, "unit": "images/s", "cores": k, "kind": "oracle",
+            "sample": f"{k} images of the workload (1920x1200, full path), one per thread on {k} of {cores} usable "
+                      f"cores; median of {runs} runs: {dt:.2f} s per run ({', '.join(f'{t:.2f}' for t in times)}); "
+                      f"{int(sum(counts))} keypoints"}
 
 
 def main():
@@ -182,10 +194,15 @@ def main():
     from paper_1706_06750_b200 import dist as D
 
     rank, local_rank, ws = D.world()
+    # a gloo dry run may put several ranks on one visible GPU; NCCL runs one rank per GPU
+    dev_index = local_rank % max(1, torch.cuda.device_count()) if args.dist_backend == "gloo" else local_rank
+    dev = torch.device("cuda", dev_index)
+    torch.cuda.set_device(dev)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     first, n_local = D.shard(args.images, rank, ws)
     assert args.warmup >= 3 or os.environ.get("KAZE_BENCH_ALLOW_SHORT"), "timing rules: W >= 3"
 
@@ -193,34 +210,34 @@ def main():
     imgs = torch.from_numpy(host).to(dev)
     B = min(args.batch, max(1, n_local))
     scheme = K.SCHEME_FED if args.scheme == "fed" else K.SCHEME_AOS
-    kz = K.Kaze(W_IMG, H_IMG, batch=B, device=local_rank, max_keypoints=args.max_keypoints, scheme=scheme)
+    kz = K.Kaze(W_IMG, H_IMG, batch=B, device=dev_index, max_keypoints=args.max_keypoints, scheme=scheme)
     kps, counts, desc = kz.alloc_outputs(n_local)
     stream = torch.cuda.current_stream(dev)
+    # C1's shard sizes are exchanged once here, outside the timed loop: a step's gather is then one collective
+    # with no host sync
+    cg = D.CountGather(n_local, device=dev) if ws > 1 else None
 
     def step():
         K.kaze_extract(kz.ctx, imgs, kps, counts, desc)
-        if ws > 1:
-            D.gather_counts(counts)
+        if cg is not None:
+            cg.gather(counts)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    if ws > 1:
-        dist.barrier()
+    D.barrier(dev)
     # Timed region: the production path (kaze_extract replays each chunk as a CUDA graph; profiling off).
     K.kaze_reset_profile(kz.ctx)  # also zeroes the launch counter
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
         torch.cuda.synchronize(dev)
-        if ws > 1:
-            dist.barrier()
+        D.barrier(dev)
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        if ws > 1:
-            dist.barrier()
+        D.barrier(dev)
     ms_local = e0.elapsed_time(e1) / args.steps
     launches = K.kaze_launch_count(kz.ctx)
     # Per-kernel device times: the same K steps again with the context's CUDA events around every launch on its
@@ -237,8 +254,20 @@ def main():
     prof = K.kaze_get_profile(kz.ctx)
     K.kaze_set_profiling(kz.ctx, False)
     ms = D.max_over_ranks(ms_local, device=dev)
-    total_counts = D.gather_counts(counts) if ws > 1 else counts
+    total_counts = cg.result() if cg is not None else counts
     kp_total = int(torch.clamp(total_counts, max=args.max_keypoints).sum())
+    c2 = None
+    if ws > 1:  # C2 once, untimed: every rank receives every image's records; check it against C1 and the local shard
+        t0 = time.perf_counter()
+        kl, dl, allc = D.gather_results(kps, counts, desc, cap=args.max_keypoints)
+        torch.cuda.synchronize(dev)
+        c2_ms = (time.perf_counter() - t0) * 1e3
+        ok = len(kl) == args.images and bool(torch.equal(allc.cpu(), total_counts.cpu().clamp(0, args.max_keypoints)))
+        for i in range(n_local):  # this rank's own images come back bit for bit
+            c = min(int(counts[i]), args.max_keypoints)
+            ok = ok and bool(torch.equal(kl[first + i].to(dev), kps[i, :c])) and bool(torch.equal(dl[first + i].to(dev), desc[i, :c]))
+        ok = D.max_over_ranks(0.0 if ok else 1.0, device=dev) == 0.0
+        c2 = {"ok": ok, "records": int(sum(t.shape[0] for t in kl)), "ms": c2_ms, "backend": args.dist_backend}
 
     # ---- roofline of the dominant kernel (largest device time in the step) ----
     peak, peak_kind = peaks()
@@ -270,8 +299,7 @@ def main():
         h_desc = torch.zeros((n_local, args.max_keypoints, 64), dtype=torch.float32).pin_memory()
         K.kaze_extract_host(kz.ctx, h_imgs, h_kps, h_cnt, h_desc)  # warm-up
         torch.cuda.synchronize(dev)
-        if ws > 1:
-            dist.barrier()
+        D.barrier(dev)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             K.kaze_extract_host(kz.ctx, h_imgs, h_kps, h_cnt, h_desc)
@@ -286,8 +314,8 @@ def main():
 
     if rank == 0:
         cpu = None
-        if ws == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline_sample()
+        if not args.no_cpu_baseline:
+            cpu = cpu_baseline_sample(host)
         out = {
             "metric": METRIC,
             "value": args.images / (ms * 1e-3),
@@ -321,6 +349,10 @@ def main():
                         for k, v in prof.items()},
             "clocks": clocks.summary(),
         }
+        if c2 is not None:
+            out["c2_gather_results"] = c2
+            out["config"]["dist_backend"] = args.dist_backend
+            out["config"]["devices_visible"] = torch.cuda.device_count()
         if "describe" in prof and prof["describe"]["ms"] > 0:
             # gather roofline of the descriptor pass: 113 + 576 bilinear samples x 4 taps x 8 B
             # (float2 texels) = 22 KB per keypoint, served mostly by L1/L2 (each plane is read ~once from HBM)

@@ -43,7 +43,7 @@ typedef struct kaze_ctx kaze_ctx;
 typedef enum {
     KAZE_OK = 0,
     KAZE_ERR_INVALID_ARGUMENT = -1, /* bad parameter value, null pointer, n > max_batch, ...      */
-    KAZE_ERR_IMAGE_TOO_SMALL = -2,  /* min(w, h) < 32, or w/h above the context's maxima          */
+    KAZE_ERR_IMAGE_TOO_SMALL = -2,  /* min(w, h) < 32, σ_{N−1} > min(w, h)/2, or w/h above maxima */
     KAZE_ERR_CAPACITY = -3,         /* reserved: capacity overflow is reported through d_counts    */
     KAZE_ERR_STATE = -4,            /* detect before build, describe before detect                 */
     KAZE_ERR_CUDA = -5,             /* CUDA runtime error (see kaze_last_error)                    */
@@ -127,6 +127,9 @@ kaze_status kaze_destroy(kaze_ctx* ctx);
 
 /* Step 1: nonlinear scale space for n images d_imgs[n][h][pitch] (n <= max_batch, 32 <= w <=
  * max_width, 32 <= h <= max_height, pitch >= w).  Levels stay in the context until the next build.
+ * The largest scale must fit the image: σ_{N−1} = σ0·2^{O−1+(S−1)/S} <= min(w, h)/2 (SPEC's "levels whose σ_i
+ * exceeds min(W,H)/2 are dropped", read as validation), else IMAGE_TOO_SMALL — e.g. the
+ * default O = S = 4 (σ_15 ≈ 21.5) needs min(w, h) >= 43.
  * Errors: INVALID_ARGUMENT, IMAGE_TOO_SMALL, CUDA. */
 kaze_status kaze_build_scale_space(kaze_ctx* ctx, const float* d_imgs, int32_t n, int32_t w, int32_t h,
                                    int64_t pitch_elems, void* stream);
@@ -140,7 +143,9 @@ kaze_status kaze_detect(kaze_ctx* ctx, kaze_keypoint* d_kps, int32_t* d_counts, 
 /* Step 3: orientation (unless KAZE_FLAG_KEEP_ANGLE; angle and flags written into d_kps) and 64-D
  * descriptors d_desc[j * max_keypoints + k][64] for k < min(d_counts[j], max_keypoints), over the flat
  * list of all keypoints of all levels and images.  Degenerate descriptors are zero.
- * d_counts may be the array kaze_detect wrote, or caller-supplied (stage-isolated use).
+ * d_counts may be the array kaze_detect wrote, or caller-supplied (stage-isolated use).  A keypoint whose
+ * level is outside 0..N−1, or is 0 or N−1 while those levels' (Lx, Ly) are not materialised (no detector output
+ * lies there; KAZE_FLAG_ALL_DERIVATIVES stores them), gets a zero descriptor, angle 0 and flags bit 0 set.
  * Errors: INVALID_ARGUMENT, STATE (no build), CUDA. */
 kaze_status kaze_describe(kaze_ctx* ctx, kaze_keypoint* d_kps, const int32_t* d_counts, float* d_desc,
                           void* stream);

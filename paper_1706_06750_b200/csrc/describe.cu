@@ -49,7 +49,7 @@ constexpr int kMaxBinWin = 48;  // binned orientation path: nwin % 6 == 0 and nw
 __global__ void __launch_bounds__(256, 5) k_describe(const float2* __restrict__ Lxy,
                                                   const cudaTextureObject_t* __restrict__ texs, size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
                                                   const int* __restrict__ counts, int cap, float* __restrict__ desc,
-                                                  int nwin, int keep_angle, int N) {
+                                                  int nwin, int keep_angle, int N, int lvl_lo, int lvl_hi) {
     KZ_PDL_PROLOGUE();
     __shared__ int pre[kMaxBatch + 1];
     __shared__ __align__(16) float sbuf[kWarps][kWarpBuf];
@@ -76,6 +76,17 @@ __global__ void __launch_bounds__(256, 5) k_describe(const float2* __restrict__ 
         kaze_keypoint* kp = kps + (size_t)img * cap + k;
         const float x = kp->x, y = kp->y, sigma = kp->sigma;
         const int level = kp->level;
+        if (level < lvl_lo || level > lvl_hi) {  // warp-uniform: no sampleable (Lx, Ly) planes at this level
+            float* dk = desc + ((size_t)img * cap + k) * 64;
+            dk[lane] = 0.f;
+            dk[lane + 32] = 0.f;
+            if (lane == 0) {
+                if (!keep_angle) kp->angle = 0.f;
+                kp->flags = 1;
+            }
+            __syncwarp();
+            continue;
+        }
         const float2* lxy = Lxy + img * img_stride + (size_t)level * g.plane;
         const cudaTextureObject_t tex = texs[img * N + level];
         float angle;
@@ -331,20 +342,15 @@ void init_describe_tables() {
 }
 
 void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t img_stride, Geom g, int nimg, int N,
-                     kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
+                     int lvl_lo, int lvl_hi, kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
                      cudaStream_t s) {
     // Persistent grid of exactly one wave: the CTAs that fit on every SM at once (registers limit it to 4 of 256
     // threads).  A grid larger than one wave leaves the surplus CTAs' share of the static keypoint stride to a
     // second, mostly idle wave (measured: 148·5 CTAs = 1.25 waves).
-    static int grid = 0;
-    if (grid == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_describe, 256, 0);
-        grid = sms * (per_sm > 0 ? per_sm : 1);
-    }
-    kz_launch(k_describe, dim3(grid), dim3(256), 0, s, Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N);
+    int per_sm = 0;  // (a per-device figure: cheap, and correct when contexts on other devices share the process)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_describe, 256, 0);
+    const int grid = device_sm_count() * (per_sm > 0 ? per_sm : 1);
+    kz_launch(k_describe, dim3(grid), dim3(256), 0, s, Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N, lvl_lo, lvl_hi);
 }
 
 }  // namespace kz

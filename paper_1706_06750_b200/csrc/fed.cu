@@ -112,11 +112,7 @@ void run_fed(const float* Lin, size_t s_in, const float* c, size_t s_c, float* L
              const FedTaus& t, cudaStream_t s) {
     constexpr int EW = FTW + 2 * K, EH = FTH + 2 * K, SP = EW + 1;
     const size_t smem = sizeof(float) * 4 * EH * SP;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_fed<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    ensure_smem_optin(reinterpret_cast<const void*>(k_fed<K>), (int)smem);
     dim3 grid((g.W + FTW - 1) / FTW, (g.H + FTH - 1) / FTH, nimg);
     kz_launch(k_fed<K>, dim3(grid), dim3(dim3(32, 8)), smem, s, Lin, s_in, c, s_c, Lout, s_out, g, t);
 }

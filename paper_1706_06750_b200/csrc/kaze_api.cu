@@ -9,7 +9,10 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "kaze_internal.cuh"
@@ -84,10 +87,16 @@ struct kaze_ctx {
     int* pinned_counts = nullptr;  // 2 * max_batch
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_cnt[2] = {}, ev_d2h[2] = {};
-    // descriptor texture objects over the Lxy planes, [max_batch][N], rebuilt when the geometry changes
-    std::vector<cudaTextureObject_t> texs;
-    cudaTextureObject_t* d_texs = nullptr;
-    int tex_W = 0, tex_H = 0;
+    // descriptor texture objects over the Lxy planes, [max_batch][N], one immutable table per image size: a
+    // captured graph bakes the device pointer of its size's table, so a table is never rewritten; it is destroyed
+    // only together with every graph of its size (LRU beyond kMaxTexTables sizes)
+    struct TexTable {
+        int W, H;
+        std::vector<cudaTextureObject_t> texs;
+        cudaTextureObject_t* d = nullptr;
+        uint64_t used = 0;
+    };
+    std::vector<TexTable> tex_tables;
     // profiling
     bool prof = false;
     // CUDA graphs of whole chunks (build + detect + describe), keyed by everything a replay bakes in
@@ -284,9 +293,11 @@ void free_arena(kaze_ctx* c) {
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (c->pinned_counts) cudaFreeHost(c->pinned_counts);
-    for (auto t : c->texs) cudaDestroyTextureObject(t);
-    c->texs.clear();
-    if (c->d_texs) cudaFree(c->d_texs);
+    for (auto& tt : c->tex_tables) {
+        for (auto t : tt.texs) cudaDestroyTextureObject(t);
+        if (tt.d) cudaFree(tt.d);
+    }
+    c->tex_tables.clear();
 }
 
 // Plane size in floats: pitch x H rounded to 128 floats, so every (image, level) plane of the interleaved float2
@@ -443,14 +454,44 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
 }
 
 // Texture objects (bilinear filtering, clamped addressing, unnormalised coordinates) over every (image, level)
-// Lxy plane of the current geometry, for the descriptor's 576 filtered samples per keypoint.
-kaze_status ensure_textures(kaze_ctx* c) {
-    if (c->tex_W == c->W && c->tex_H == c->H && !c->texs.empty()) return KAZE_OK;
-    for (auto t : c->texs) cudaDestroyTextureObject(t);
-    c->texs.clear();
+// Lxy plane of the current geometry, for the descriptor's 576 filtered samples per keypoint.  One table per image
+// size, built once (synchronous upload, before any capture) and immutable afterwards.
+constexpr size_t kMaxTexTables = 16;
+
+void drop_graphs_of_size(kaze_ctx* c, int w, int h);
+
+kaze_status ensure_textures(kaze_ctx* c, const cudaTextureObject_t** out) {
+    for (auto& tt : c->tex_tables)
+        if (tt.W == c->W && tt.H == c->H) {
+            tt.used = ++c->tick;
+            *out = tt.d;
+            return KAZE_OK;
+        }
+    if (c->tex_tables.size() >= kMaxTexTables) {  // evict the least recently used size and its graphs
+        auto lru = std::min_element(c->tex_tables.begin(), c->tex_tables.end(),
+                                    [](const auto& a, const auto& b) { return a.used < b.used; });
+        KZ_CUDA(c, cudaDeviceSynchronize());  // a launched graph or kernel may still sample it
+        drop_graphs_of_size(c, lru->W, lru->H);
+        for (auto t : lru->texs) cudaDestroyTextureObject(t);
+        if (lru->d) cudaFree(lru->d);
+        c->tex_tables.erase(lru);
+    }
     const int B = c->p.max_batch, N = c->N;
-    if (!c->d_texs && cudaMalloc(&c->d_texs, sizeof(cudaTextureObject_t) * B * N) != cudaSuccess) return KAZE_ERR_OOM;
-    c->texs.resize((size_t)B * N);
+    kaze_ctx::TexTable tt;
+    tt.W = c->W;
+    tt.H = c->H;
+    tt.texs.assign((size_t)B * N, 0);
+    auto cleanup = [&]() {
+        for (auto t : tt.texs)
+            if (t) cudaDestroyTextureObject(t);
+        if (tt.d) cudaFree(tt.d);
+    };
+    if (cudaMalloc(&tt.d, sizeof(cudaTextureObject_t) * B * N) != cudaSuccess) {
+        cudaGetLastError();
+        tt.d = nullptr;
+        cleanup();
+        return KAZE_ERR_OOM;
+    }
     for (int b = 0; b < B; ++b)
         for (int l = 0; l < N; ++l) {
             cudaResourceDesc rd{};
@@ -465,21 +506,32 @@ kaze_status ensure_textures(kaze_ctx* c) {
             td.filterMode = cudaFilterModeLinear;
             td.readMode = cudaReadModeElementType;
             td.normalizedCoords = 0;
-            KZ_CUDA(c, cudaCreateTextureObject(&c->texs[(size_t)b * N + l], &rd, &td, nullptr));
+            const cudaError_t e = cudaCreateTextureObject(&tt.texs[(size_t)b * N + l], &rd, &td, nullptr);
+            if (e != cudaSuccess) {
+                cleanup();
+                return cuda_fail(c, e, "cudaCreateTextureObject");
+            }
         }
-    KZ_CUDA(c, cudaMemcpy(c->d_texs, c->texs.data(), sizeof(cudaTextureObject_t) * B * N, cudaMemcpyHostToDevice));
-    c->tex_W = c->W;
-    c->tex_H = c->H;
+    const cudaError_t e = cudaMemcpy(tt.d, tt.texs.data(), sizeof(cudaTextureObject_t) * B * N, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cleanup();
+        return cuda_fail(c, e, "texture table upload");
+    }
+    tt.used = ++c->tick;
+    c->tex_tables.push_back(std::move(tt));
+    *out = c->tex_tables.back().d;
     return KAZE_OK;
 }
 
 // Step 3.
 kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_counts, float* d_desc, cudaStream_t s) {
-    kaze_status st = ensure_textures(c);
+    const cudaTextureObject_t* texs = nullptr;
+    kaze_status st = ensure_textures(c, &texs);
     if (st != KAZE_OK) return st;
     {
         Launch L(c, KC_DESCRIBE, 0.0, s);
-        launch_describe(c->Lxy, c->d_texs, c->img_stride, c->geom, c->n, c->N, d_kps, d_counts, c->p.max_keypoints,
+        const int lo = c->edge_derivs ? 0 : 1, hi = c->edge_derivs ? c->N - 1 : c->N - 2;  // sampleable levels
+        launch_describe(c->Lxy, texs, c->img_stride, c->geom, c->n, c->N, lo, hi, d_kps, d_counts, c->p.max_keypoints,
                         d_desc, c->p.ori_windows, (c->p.flags & KAZE_FLAG_KEEP_ANGLE) ? 1 : 0, s);
     }
     KZ_CHECK_LAUNCH(c, "describe");
@@ -525,7 +577,8 @@ kaze_status run_chunk(kaze_ctx* c, const float* img, int m, int w, int h, int64_
     }
     if (!c->s_cap) KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking));
     set_geometry(c, m, w, h);
-    kaze_status st = ensure_textures(c);  // host-side setup (synchronous copies) must precede the capture
+    const cudaTextureObject_t* texs = nullptr;
+    kaze_status st = ensure_textures(c, &texs);  // host-side setup (synchronous copies) must precede the capture
     if (st != KAZE_OK) return st;
     // the capture stream must not start before the caller's prior work when the graph is launched; a graph
     // launched on s is ordered after s's prior work by the launch itself, so the capture needs no dependency
@@ -567,10 +620,26 @@ kaze_status run_chunk(kaze_ctx* c, const float* img, int m, int w, int h, int64_
     return KAZE_OK;
 }
 
+void drop_graphs_of_size(kaze_ctx* c, int w, int h) {
+    for (size_t i = 0; i < c->graphs.size();) {
+        if (c->graphs[i].key.w == w && c->graphs[i].key.h == h) {
+            cudaGraphExecDestroy(c->graphs[i].exec);
+            c->graphs.erase(c->graphs.begin() + (long)i);
+        } else {
+            ++i;
+        }
+    }
+    for (size_t i = 0; i < c->seen.size();) {
+        if (c->seen[i].w == w && c->seen[i].h == h) c->seen.erase(c->seen.begin() + (long)i);
+        else ++i;
+    }
+}
+
 kaze_status check_dims(const kaze_ctx* c, int n, int w, int h, int64_t pitch) {
     if (n < 1 || n > c->p.max_batch) return KAZE_ERR_INVALID_ARGUMENT;
     if (w < 32 || h < 32 || w > c->p.max_width || h > c->p.max_height) return KAZE_ERR_IMAGE_TOO_SMALL;
     if (pitch < w) return KAZE_ERR_INVALID_ARGUMENT;
+    if (c->sigma[c->N - 1] > 0.5 * std::min(w, h)) return KAZE_ERR_IMAGE_TOO_SMALL;  // S:L222 as validation (A4)
     return KAZE_OK;
 }
 
@@ -966,6 +1035,35 @@ int tune_knob(const char* name, int def) {
     const char* v = getenv(name);
     return (v && *v) ? atoi(v) : def;
 }
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_smem_optin;  // (function, device) -> bytes set
+std::map<int, int> g_sm_count;                              // device -> multiprocessor count
+}  // namespace
+bool ensure_smem_optin(const void* func, int bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int& have = g_smem_optin[{func, dev}];
+    if (have >= bytes) return true;
+    if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    have = bytes;
+    return true;
+}
+int device_sm_count() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_sm_count.find(dev);
+    if (it != g_sm_count.end()) return it->second;
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 1;
+    g_sm_count[dev] = n;
+    return n;
+}
 static thread_local bool g_capturing = false;
 void pdl_set_capturing(bool on) { g_capturing = on; }
 bool pdl_enabled() {
@@ -990,7 +1088,7 @@ kaze_status kaze_memory_footprint(const kaze_ctx* c, kaze_memory* out) {
     out->scratch = 2 * plane * B;
     out->detector = sizeof(float) * B + sizeof(unsigned) * B + sizeof(int) * B * c->p.k_bins + sizeof(int) * B +
                     sizeof(uint32_t) * rows * nms_words(c->p.max_width) + 2 * sizeof(int) * rows;
-    out->textures = c->d_texs ? sizeof(cudaTextureObject_t) * B * N : 0;
+    out->textures = sizeof(cudaTextureObject_t) * B * N * (uint64_t)c->tex_tables.size();
     if (c->s_h2d) {
         out->host_path = 2 * (plane * B + sizeof(kaze_keypoint) * cap * B + sizeof(int) * B + sizeof(float) * 64 * cap * B);
         out->pinned_host = sizeof(int) * 2 * B;

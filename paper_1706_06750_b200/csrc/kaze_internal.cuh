@@ -67,6 +67,13 @@ inline void kz_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 // Debug/tuning knob read once from the environment (A/B runs only; the defaults are the measured best).
 int tune_knob(const char* name, int def);
 
+// Function attributes are per device and kaze.h lets contexts on different devices run concurrently: opt `func`
+// into `bytes` of dynamic shared memory on the CURRENT device (once per (function, device), thread safe; a larger
+// request raises it).  Returns false if the driver refuses.
+bool ensure_smem_optin(const void* func, int bytes);
+// Multiprocessor count of the current device (cached per device).
+int device_sm_count();
+
 // ---- stencil.cu ----
 void launch_prefilter(const float* img, int64_t in_pitch, size_t in_img_stride, float* L0,
                       size_t out_img_stride, Geom g, int nimg, const GaussTaps& t, cudaStream_t s);
@@ -140,8 +147,9 @@ void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, cons
 // ---- describe.cu ----
 void init_describe_tables();
 // texs: [nimg][N] texture objects over the Lxy planes (linear filtering, clamp) for the M-SURF samples.
+// Keypoints whose level lies outside [lvl_lo, lvl_hi] get a zero descriptor, angle 0 and flags = 1.
 void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t img_stride, Geom g, int nimg, int N,
-                     kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
+                     int lvl_lo, int lvl_hi, kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
                      cudaStream_t s);
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

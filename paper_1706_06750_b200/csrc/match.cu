@@ -536,15 +536,11 @@ size_t match_scratch_bytes(int na, int nb) { return match_layout(na, nb).total; 
 static cudaError_t run_direction(const float* Q, int nq, const uint8_t* Qt, const float* R, int nr, const uint8_t* Rt,
                                  const uint32_t* rvalid, const unsigned* rnorm, float* cs, int* cj, int* best,
                                  float* d1, float* d2, int* unc, cudaStream_t s) {
-    static bool attr = false;
     const int smem = kTileQ * 128 + kStages * kTileBytes + kEpiWarps * 32 * 32 * 4 + 1024;
-    if (!attr) {
-        cudaFuncSetAttribute(k_match_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    if (!ensure_smem_optin(reinterpret_cast<const void*>(k_match_topk), smem)) return cudaErrorInvalidValue;
     // split the reference range when the query blocks alone would leave SMs idle (two CTAs fit per SM)
     const int qblocks = (nq + kTileQ - 1) / kTileQ, rtiles = (nr + kTileR - 1) / kTileR;
-    int nsplit = (2 * 148 + qblocks - 1) / qblocks;
+    int nsplit = (2 * device_sm_count() + qblocks - 1) / qblocks;
     nsplit = nsplit < 1 ? 1 : (nsplit > kMaxSplit ? kMaxSplit : nsplit);
     if (nsplit > rtiles) nsplit = rtiles > 0 ? rtiles : 1;
     k_match_topk<<<dim3(qblocks, nsplit), kThreads, smem, s>>>(Qt, nq, Rt, nr, rvalid, cs, cj);

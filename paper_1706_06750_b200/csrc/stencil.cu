@@ -139,8 +139,11 @@ __global__ void __launch_bounds__(256) k_prefilter5(const float* __restrict__ in
                     for (int d = 1; d < 11; ++d) acc = fmaf(w[d], v[it][i + 3 + d], acc);
                     h[i] = acc;
                 }
-                reinterpret_cast<float4*>(&sH[r][8 * sg])[0] = make_float4(h[0], h[1], h[2], h[3]);
-                reinterpret_cast<float4*>(&sH[r][8 * sg])[1] = make_float4(h[4], h[5], h[6], h[7]);
+                // segments 4..7 store their upper half first: conflict-free 128-bit phases (see cond_hpass)
+                const int sw = sg >> 2;
+                const float4 h0 = make_float4(h[0], h[1], h[2], h[3]), h1 = make_float4(h[4], h[5], h[6], h[7]);
+                reinterpret_cast<float4*>(&sH[r][8 * sg])[sw] = sw ? h1 : h0;
+                reinterpret_cast<float4*>(&sH[r][8 * sg])[sw ^ 1] = sw ? h0 : h1;
             }
         }
     }
@@ -223,10 +226,16 @@ __device__ __forceinline__ void cond_hpass(const float (&v)[16], const float (&w
         A[i] = h[i + 2] - h[i];
         B[i] = fmaf(kW0c, h[i] + h[i + 2], kW1c * h[i + 1]);
     }
-    reinterpret_cast<float4*>(dA)[0] = make_float4(A[0], A[1], A[2], A[3]);
-    reinterpret_cast<float4*>(dA)[1] = make_float4(A[4], A[5], A[6], A[7]);
-    reinterpret_cast<float4*>(dB)[0] = make_float4(B[0], B[1], B[2], B[3]);
-    reinterpret_cast<float4*>(dB)[1] = make_float4(B[4], B[5], B[6], B[7]);
+    // The 8 lanes of a 128-bit store phase hold segments sg = 0..7 of one 64-float row: segment halves 8sg and
+    // 8(sg+4) fall in the same 4-bank group, so segments 4..7 store their upper half first (a 2-way conflict on
+    // every STS.128 otherwise: 26% of the kernel's shared wavefronts in the round-1 capture).
+    const bool sw = (xb >> 5) & 1;  // sg >= 4 ⇔ bit 5 of xb = x0 + 8sg (x0 is a multiple of 64)
+    const float4 a0 = make_float4(A[0], A[1], A[2], A[3]), a1 = make_float4(A[4], A[5], A[6], A[7]);
+    const float4 b0 = make_float4(B[0], B[1], B[2], B[3]), b1 = make_float4(B[4], B[5], B[6], B[7]);
+    reinterpret_cast<float4*>(dA)[sw] = sw ? a1 : a0;
+    reinterpret_cast<float4*>(dB)[sw] = sw ? b1 : b0;
+    reinterpret_cast<float4*>(dA)[!sw] = sw ? a0 : a1;
+    reinterpret_cast<float4*>(dB)[!sw] = sw ? b0 : b1;
 }
 
 // Phase 2 of the conductivity pass in packed fp32x2 (FFMA2/FMUL2 on sm_100a): thread = (column pair cp, 7-row

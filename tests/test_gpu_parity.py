@@ -269,9 +269,15 @@ def test_constant_image_degenerate_k_and_no_keypoints():
 
 
 def test_minimum_size_and_argument_errors():
+    small = make(64, 64, octaves=2, sublevels=2)  # σ_3 = 1.6·2^1.5 ≈ 4.5 fits a 32x32 image
+    small.extract(torch.rand((1, 32, 32), device="cuda"))  # 32x32 is the smallest accepted size
+    small.close()
     kz = make(64, 64, batch=2)
-    img = torch.rand((1, 32, 32), device="cuda")
-    kps, counts, desc = kz.extract(img)  # 32x32 is the smallest accepted size
+    # the default pyramid (σ_15 = 1.6·2^3.75 ≈ 21.53) needs σ_{N-1} <= min(w, h)/2 (S:L222 as validation, A4)
+    with pytest.raises(K.KazeError) as e:
+        K.kaze_build_scale_space(kz.ctx, torch.rand((1, 43, 60), device="cuda"))
+    assert e.value.status == -2
+    kps, counts, desc = kz.extract(torch.rand((1, 44, 60), device="cuda"))
     with pytest.raises(K.KazeError) as e:
         K.kaze_build_scale_space(kz.ctx, torch.rand((1, 31, 40), device="cuda"))
     assert e.value.status == -2

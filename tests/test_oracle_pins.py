@@ -416,6 +416,64 @@ def test_rot90_scale_space_equivariance(O):
         np.testing.assert_allclose(lb[i], np.rot90(la[i]), atol=1e-12)
 
 
+def _match_by_position(ka, kb, xa, ya):
+    """Index into kb of the keypoint at the same level nearest to each mapped position (xa, ya)."""
+    return np.array([int(np.argmin(np.hypot(kb["x"] - xa[j], kb["y"] - ya[j]) + 1e6 * (kb["level"] != ka["level"][j])))
+                     for j in range(len(ka))])
+
+
+def test_rot90_orientation_and_descriptor_equivariance(O):
+    """P13: under a 90° rotation the first derivatives rotate exactly ((Lx, Ly) ->
+    (Ly, -Lx) with clamped borders), the 113-sample disc and the 24x24 grid map onto themselves, and with 48 windows
+    (a multiple of 4) the window set is rotation invariant.  So every keypoint maps to x' = y, y' = W-1-x, its angle
+    drops by exactly π/2 and its descriptor is unchanged.  (Ldet itself is equivariant only away from the border:
+    N_y(N_x L) = N_x(N_y L) holds in the interior but not on the clamped intermediate, so keypoints within 2s_i + 1
+    px of the border are excluded.)"""
+    img = kaze_inputs.synth_image(150, 110, 31)
+    H, W = img.shape
+    kw = dict(octaves=3, sublevels=3, ori_windows=48)
+    ra, rb = O.run(img, **kw), O.run(np.ascontiguousarray(np.rot90(img)), **kw)
+    _, _, st = O.schedule(3, 3, 1.6)
+    ka, kb = ra["kps"], rb["kps"]
+    s = st[ka["level"]]
+    inner = np.minimum(np.minimum(ka["x"], ka["y"]), np.minimum(W - 1 - ka["x"], H - 1 - ka["y"])) >= 2 * s + 1
+    assert inner.sum() >= 50 and abs(ra["count"] - rb["count"]) <= (~inner).sum()
+    ka, da = ka[inner], ra["desc"][inner]
+    xa, ya = ka["y"], W - 1 - ka["x"]
+    idx = _match_by_position(ka, kb, xa, ya)
+    np.testing.assert_allclose(kb["x"][idx], xa, atol=1e-9)
+    np.testing.assert_allclose(kb["y"][idx], ya, atol=1e-9)
+    dang = (kb["angle"][idx] - (ka["angle"] - math.pi / 2) + math.pi) % (2 * math.pi) - math.pi
+    assert np.max(np.abs(dang)) < 1e-9
+    np.testing.assert_allclose(rb["desc"][idx], da, atol=1e-9)
+
+
+def test_flip_orientation_and_descriptor_signed_permutation(O):
+    """P16: a horizontal flip maps (Lx, Ly) -> (-Lx, Ly) exactly (every operator is symmetric and the
+    borders clamp), so x' = W-1-x, θ' = π - θ (42 windows: even, so the window set is flip invariant), and the
+    sample grid (u, v) of the flipped keypoint lands on (u, -v) of the original with du' = du, dv' = -dv: the
+    descriptor is the signed permutation d'[4(4(3-b)+a)+j] = ±d[4(4b+a)+j], minus sign for j = 1 (Σdv)."""
+    img = kaze_inputs.synth_image(150, 110, 31)
+    W = img.shape[1]
+    ra = O.run(img, octaves=3, sublevels=3)
+    rc = O.run(np.ascontiguousarray(img[:, ::-1]), octaves=3, sublevels=3)
+    assert ra["count"] == rc["count"] > 50
+    ka, kc = ra["kps"], rc["kps"]
+    idx = _match_by_position(ka, kc, W - 1 - ka["x"], ka["y"])
+    assert len(set(idx.tolist())) == len(idx)
+    np.testing.assert_allclose(kc["x"][idx], W - 1 - ka["x"], atol=1e-9)
+    np.testing.assert_allclose(kc["y"][idx], ka["y"], atol=1e-9)
+    dang = (kc["angle"][idx] - (math.pi - ka["angle"]) + math.pi) % (2 * math.pi) - math.pi
+    assert np.max(np.abs(dang)) < 1e-9
+    perm, sgn = np.zeros(64, int), np.ones(64)
+    for b in range(4):
+        for a in range(4):
+            for j in range(4):
+                perm[4 * (4 * b + a) + j] = 4 * (4 * (3 - b) + a) + j
+                sgn[4 * (4 * b + a) + j] = -1.0 if j == 1 else 1.0
+    np.testing.assert_allclose(rc["desc"][idx][:, perm] * sgn, ra["desc"], atol=1e-9)
+
+
 # ----------------------------------------------------------------------------- P20 orientation
 @pytest.mark.parametrize("theta", [0.0, 0.3, math.pi / 6, 2.0, 4.4, 6.0])
 def test_orientation_uniform_gradient(O, theta):
@@ -436,6 +494,37 @@ def test_orientation_degenerate_and_windows(O):
     Ly = np.where(xx >= 32, 0.3, 0.0)
     ang, _ = O.orientation(Lx, Ly, 32.0, 32.0, 1.0)
     assert abs(ang) < 1e-12 or abs(ang - 2 * math.pi) < 1e-12
+
+
+@pytest.mark.parametrize("r1,r2", [((5, 0), (1, 0)), ((3, 4), (0, 2)), ((6, 0), (2, 3)), ((0, -6), (4, 4))])
+def test_orientation_gaussian_weight_by_two_impulses(O, r1, r2):
+    """P20b (A14): σ = 2 at an integer keypoint puts the 113 samples on pixels 2 px apart, so a field
+    that is zero except at two sample pixels is read exactly (bilinear at integer points) by one sample each.  With
+    the two gradient directions more than π/3 apart no window holds both, and the longest window sum is the larger
+    of w(u, v)·|m|, w = exp(−(u² + v²)/12.5) in σ units (std 2.5σ).  Scaling the second impulse to 0.95 / 1.05 of
+    the tie w1·m1 / w2 must flip the winner — this fixes the weight's width and its σ units at these radii."""
+    w = lambda u, v: math.exp(-(u * u + v * v) / 12.5)  # noqa: E731
+    kx, ky, sigma = 40.0, 41.0, 2.0
+    phi1, phi2 = 0.4, 0.4 + 2.2
+    for f, want in ((0.95, phi1), (1.05, phi2)):
+        Lx, Ly = np.zeros((96, 96)), np.zeros((96, 96))
+        m2 = f * w(*r1) / w(*r2)
+        for (u, v), m, ph in ((r1, 1.0, phi1), (r2, m2, phi2)):
+            Lx[int(ky + sigma * v), int(kx + sigma * u)] = m * math.cos(ph)
+            Ly[int(ky + sigma * v), int(kx + sigma * u)] = m * math.sin(ph)
+        ang, deg = O.orientation(Lx, Ly, kx, ky, sigma)
+        assert not deg and abs(ang - want) < 1e-12, (r1, r2, f, ang, want)
+
+
+def test_orientation_sample_disc_is_radius_6(O):
+    """P20c (A14): the samples are the integer (u, v) with u² + v² <= 36 (113 of them): an impulse at (6, 0) or (0, −6)
+    (r² = 36) is seen, one at (1, 6), (4, 5) or (5, 4) (r² = 37, 41, 41) is not — the keypoint is then degenerate."""
+    assert sum(1 for u in range(-6, 7) for v in range(-6, 7) if u * u + v * v <= 36) == 113
+    for (u, v), seen in (((6, 0), True), ((0, -6), True), ((1, 6), False), ((4, 5), False), ((-5, 4), False)):
+        Lx, Ly = np.zeros((96, 96)), np.zeros((96, 96))
+        Lx[41 + 2 * v, 40 + 2 * u] = 1.0
+        ang, deg = O.orientation(Lx, Ly, 40.0, 41.0, 2.0)
+        assert deg == (not seen) and ang == 0.0
 
 
 # ----------------------------------------------------------------------------- P21 descriptor
@@ -593,6 +682,102 @@ def test_fed_scale_space_mass_and_agreement_with_aos(O):
         rms = np.sqrt(np.mean((lf[i] - la[i]) ** 2))
         assert rms < 0.25 * np.sqrt(np.mean((lf[i] - lf[0]) ** 2))
     assert lf.min() >= lf[0].min() - 1e-12 and lf.max() <= lf[0].max() + 1e-12
+
+
+def test_scale_space_schedule_is_gaussian_at_unit_conductivity(O):
+    """P27 (Eqs. 6-7: "filtering for time t = σ²/2 is equivalent to a Gaussian of σ"): with k huge,
+    c ≡ 1 and the FED scale space is linear diffusion, so level i must be G(sqrt(σ_i² − σ_0²)) * L_0 — the level has
+    evolved for t_i − t_0 in total, i.e. the per-level steps are τ_i = t_i − t_{i−1}.  Each level fits its own
+    time clearly better than the neighbouring levels' times (a wrong τ composition, e.g. τ_i = t_i, or an
+    off-by-one level misses by far more: checked below for τ_i = t_i)."""
+    H = W = 160
+    yy, xx = np.mgrid[0:H, 0:W].astype(float)
+    img = np.full((H, W), 0.3)
+    for (cx, cy, s, a) in [(80, 80, 7, 0.5), (62, 95, 4, -0.3), (100, 70, 3, 0.25), (75, 60, 9, 0.2)]:
+        img += a * np.exp(-((xx - cx) ** 2 + (yy - cy) ** 2) / (2 * s * s))
+    lv, _, _ = O.scale_space(img.astype(np.float32), octaves=3, sublevels=3, k_override=1e6, scheme=1)
+    sg, t, _ = O.schedule(3, 3, 1.6)
+    rms = lambda a, b: float(np.sqrt(np.mean((a - b) ** 2)))  # noqa: E731
+    G = [O.gaussian_blur(lv[0], math.sqrt(sg[i] ** 2 - sg[0] ** 2)) if i else lv[0] for i in range(9)]
+    for i in range(1, 9):
+        own = rms(lv[i], G[i])
+        assert own < 1e-3
+        assert own < 0.25 * rms(lv[i], G[i - 1])
+        if i + 1 < 9:
+            assert own < 0.25 * rms(lv[i], G[i + 1])
+        wrong = O.gaussian_blur(lv[0], math.sqrt(2 * t[1:i + 1].sum()))  # τ_i = t_i composition
+        assert rms(lv[i], wrong) > 2 * own
+
+
+def _conv_matrix(H, W, ky, kx):
+    """Dense (HW x HW) matrix of the 2-D correlation with taps ky (rows) ⊗ kx (columns), clamped reads (A16)."""
+    M = np.zeros((H * W, H * W))
+    ry, rx = len(ky) // 2, len(kx) // 2
+    for y in range(H):
+        for x in range(W):
+            for dy in range(-ry, ry + 1):
+                for dx in range(-rx, rx + 1):
+                    M[y * W + x, min(max(y + dy, 0), H - 1) * W + min(max(x + dx, 0), W - 1)] += ky[dy + ry] * kx[dx + rx]
+    return M
+
+
+def _gauss_taps(sigma):
+    r = max(1, math.ceil(3 * sigma))  # A6
+    g = np.exp(-np.arange(-r, r + 1) ** 2 / (2 * sigma * sigma))
+    return g / g.sum()
+
+
+def _edge_laplacian(H, W, c, axis):
+    """Graph Laplacian of the horizontal (axis 'x') or vertical edges, weight (c_p + c_q)/2 (A2), no border flux."""
+    A = np.zeros((H * W, H * W))
+    for y in range(H):
+        for x in range(W):
+            yy, xx = (y, x + 1) if axis == "x" else (y + 1, x)
+            if yy < H and xx < W:
+                p, q = y * W + x, yy * W + xx
+                w = 0.5 * (c[p] + c[q])
+                A[p, q] += w
+                A[q, p] += w
+                A[p, p] -= w
+                A[q, q] -= w
+    return A
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_scale_space_composition_vs_dense_brute_force(O, scheme):
+    """P28 (A1-A8, A20): brute force on a 12x10 image, whole-image dense
+    operators instead of per-line solves and separable passes.  L_0 = G(σ0) L (2-D clamped matrix); for i >= 1
+    c_i = g2(|Scharr(G(1) L_{i−1})|) from the PREVIOUS level, τ_i = t_i − t_{i−1} with t = σ²/2, σ_i = σ0·2^{o+s/S};
+    AOS: L_i = ½[(I − 2τA_y)⁻¹ + (I − 2τA_x)⁻¹] L_{i−1} by dense solves; FED: L_i = Π_j (I + τ_j (A_x + A_y)) L_{i−1}
+    with the cycle's step sizes (pinned by P22).  k is the oracle's histogram value (pinned by P6).  Computing c
+    from L_0, or τ_i = t_i, changes the levels by ~1e-2 here; the oracle agrees to ~1e-15."""
+    img = kaze_inputs.synth_image(12, 10, 8)
+    O_, S_, s0 = 2, 3, 1.6
+    lv, k, _ = O.scale_space(img, octaves=O_, sublevels=S_, scheme=scheme)
+    H, W = img.shape
+    n = H * W
+    sg = np.array([s0 * 2.0 ** (o + s / S_) for o in range(O_) for s in range(S_)])
+    t = sg ** 2 / 2
+    L = [_conv_matrix(H, W, _gauss_taps(s0), _gauss_taps(s0)) @ img.astype(np.float64).ravel()]
+    G1 = _conv_matrix(H, W, _gauss_taps(1.0), _gauss_taps(1.0))
+    Sx = _conv_matrix(H, W, np.array([3, 10, 3]) / 16, np.array([-1, 0, 1]) / 2)
+    Sy = _conv_matrix(H, W, np.array([-1, 0, 1]) / 2, np.array([3, 10, 3]) / 16)
+    for i in range(1, O_ * S_):
+        Ls = G1 @ L[-1]
+        gx, gy = Sx @ Ls, Sy @ Ls
+        c = 1.0 / (1.0 + (gx * gx + gy * gy) / (k * k))
+        tau = t[i] - t[i - 1]
+        Ax, Ay = _edge_laplacian(H, W, c, "x"), _edge_laplacian(H, W, c, "y")
+        if scheme == 0:
+            L.append(0.5 * (np.linalg.solve(np.eye(n) - 2 * tau * Ay, L[-1]) + np.linalg.solve(np.eye(n) - 2 * tau * Ax, L[-1])))
+        else:
+            v = L[-1].copy()
+            for tj in O.fed_cycle(tau, 0.25):
+                v = v + tj * ((Ax + Ay) @ v)
+            L.append(v)
+    ref = np.array([l.reshape(H, W) for l in L])
+    np.testing.assert_allclose(lv, ref, rtol=0, atol=1e-12)
+    assert np.max(np.abs(ref[-1] - ref[0])) > 1e-2  # the pyramid really evolves
 
 
 def test_fed_order_is_permutation_and_stable(O):
