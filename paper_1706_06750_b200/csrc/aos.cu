@@ -486,7 +486,7 @@ void run_rows_cta(const float* L, const float* c, const float* U, float* Lout, S
     int T = (g.W + M - 1) / M;
     if (T > 1 && g.W - (T - 1) * M == 1) --T;
     const size_t smem = sizeof(float) * 3 * ((g.W + 3) & ~3);
-    if (smem > 48 * 1024) ensure_smem_optin(reinterpret_cast<const void*>(k_aos_rows_cta<M, NW>), (int)smem);
+    ensure_smem_optin(reinterpret_cast<const void*>(k_aos_rows_cta<M, NW>), (int)smem);  // + static smem may pass 48 KB
     kz_launch(k_aos_rows_cta<M, NW>, dim3(g.H * nimg), dim3(32 * NW), smem, s, L, c, U, Lout, st, g, tau, T);
 }
 
@@ -497,7 +497,7 @@ void run_cols(const float* L, const float* c, float* U, Strides st, Geom g, int 
     const int T = (g.H + M - 1) / M;  // the last chunk is padded (decoupled rows)
     const int TP = round_up(T, 32 / CW);
     const size_t smem = sizeof(float) * 7 * CW * TP;
-    if (smem > 48 * 1024) ensure_smem_optin(reinterpret_cast<const void*>(k_aos_cols_u<CW, M, NT, MINB>), (int)smem);
+    ensure_smem_optin(reinterpret_cast<const void*>(k_aos_cols_u<CW, M, NT, MINB>), (int)smem);
     dim3 grid((g.W + CW - 1) / CW, 1, nimg);
     kz_launch(k_aos_cols_u<CW, M, NT, MINB>, dim3(grid), dim3(CW * TP), smem, s, L, c, U, st, g, tau, T, TP);
 }

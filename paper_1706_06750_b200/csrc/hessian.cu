@@ -17,14 +17,40 @@ namespace kz {
 
 namespace {
 
-constexpr float kW0 = 0.1875f, kW1 = 0.625f;  // (3, 10, 3) / 16
+// The Scharr step-s operators in separable form (A8, A9): with the row terms
+//   D(r) = L(r, x+s) − L(r, x−s)      (x-difference)      Mh(r) = hw0·(L(r, x−s) + L(r, x+s)) + hw1·L(r, x)   (x-smoothing)
+// and hw = (3, 10, 3)/32 (the (3, 10, 3)/16 cross smoothing with the ½ of the central difference folded in — a
+// power-of-two scaling, so exact), N_x L = hw0·(D(y−s) + D(y+s)) + hw1·D(y) and N_y L = Mh(y+s) − Mh(y−s).  Every
+// row term is computed once and shared by the up-to-three outputs that use it (the chain rows of phase A, the
+// ring rows of phase B): 4 instead of 7 operations per derivative.  All paths (fused fast / clamped, two-pass)
+// use exactly these operations, so a value computed by two CTAs (column halos) is bit-identical.
+constexpr float hw0 = 0.09375f, hw1 = 0.3125f;  // (3, 10, 3) / 32
 
-__device__ __forceinline__ float det_from_ring(float2 a, float2 b, float2 c, float2 d, float2 f, float2 h, float2 i,
-                                               float2 j) {
-    const float lxx = 0.5f * (kW0 * (c.x - a.x) + kW1 * (f.x - d.x) + kW0 * (j.x - h.x));  // N_x(Lx)
-    const float lxy = 0.5f * (kW0 * (h.x - a.x) + kW1 * (i.x - b.x) + kW0 * (j.x - c.x));  // N_y(Lx)
-    const float lyy = 0.5f * (kW0 * (h.y - a.y) + kW1 * (i.y - b.y) + kW0 * (j.y - c.y));  // N_y(Ly)
+struct RowTerms {  // D, Mh of one row of taps (x−s, x, x+s)
+    float d, mh;
+};
+__device__ __forceinline__ RowTerms row_terms(float a, float m, float c) { return {c - a, fmaf(hw0, a + c, hw1 * m)}; }
+// (N_x L, N_y L) at the middle row from the row terms of rows y−s, y, y+s
+__device__ __forceinline__ float2 first_from_rows(RowTerms r0, RowTerms r1, RowTerms r2) {
+    return make_float2(fmaf(hw0, r0.d + r2.d, hw1 * r1.d), r2.mh - r0.mh);
+}
+// Second-stage row terms of one ring row (columns x−s, x, x+s of (Lx, Ly)): E = x-difference of Lx, P / Q =
+// x-smoothing of Lx / Ly; then N_x(Lx) = hw0·(E0 + E2) + hw1·E1, N_y(Lx) = P2 − P0, N_y(Ly) = Q2 − Q0.
+struct RingTerms {
+    float e, p, q;
+};
+__device__ __forceinline__ RingTerms ring_terms(float2 a, float2 b, float2 c) {
+    return {c.x - a.x, fmaf(hw0, a.x + c.x, hw1 * b.x), fmaf(hw0, a.y + c.y, hw1 * b.y)};
+}
+__device__ __forceinline__ float det_from_terms(RingTerms r0, RingTerms r1, RingTerms r2) {
+    const float lxx = fmaf(hw0, r0.e + r2.e, hw1 * r1.e);  // N_x(Lx)
+    const float lxy = r2.p - r0.p;                          // N_y(Lx)
+    const float lyy = r2.q - r0.q;                          // N_y(Ly)
     return lxx * lyy - lxy * lxy;
+}
+__device__ __forceinline__ float det_from_ring(float2 a, float2 b, float2 c, float2 d, float2 e, float2 f, float2 h,
+                                               float2 i, float2 j) {
+    return det_from_terms(ring_terms(a, b, c), ring_terms(d, e, f), ring_terms(h, i, j));
 }
 
 // Chain form: a thread computes R outputs of one column at rows y_j = y_0 + j·s (j < R) — a "chain" in the row
@@ -91,8 +117,8 @@ __device__ __forceinline__ void hess_first_body(const float* __restrict__ L, flo
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int y = y0 + j * s;
-        const float2 v = make_float2(0.5f * (kW0 * (c[j] - a[j]) + kW1 * (c[j + 1] - a[j + 1]) + kW0 * (c[j + 2] - a[j + 2])),
-                                     0.5f * (kW0 * (a[j + 2] - a[j]) + kW1 * (m[j + 2] - m[j]) + kW0 * (c[j + 2] - c[j])));
+        const float2 v = first_from_rows(row_terms(a[j], m[j], c[j]), row_terms(a[j + 1], m[j + 1], c[j + 1]),
+                                         row_terms(a[j + 2], m[j + 2], c[j + 2]));
         if (fast || y < g.H) __stwb(D + (unsigned)(y * g.P + x), v);
     }
 }
@@ -108,7 +134,7 @@ __device__ __forceinline__ void hess_det_body(const float2* __restrict__ D, floa
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int y = y0 + j * s;
-        const float v = det_from_ring(a[j], m[j], c[j], a[j + 1], c[j + 1], a[j + 2], m[j + 2], c[j + 2]);
+        const float v = det_from_ring(a[j], m[j], c[j], a[j + 1], m[j + 1], c[j + 1], a[j + 2], m[j + 2], c[j + 2]);
         if (fast || y < g.H) __stwb(O + (unsigned)(y * g.P + x), v);
     }
 }
@@ -192,20 +218,16 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
         const int cc = clampi(vc, 0, g.W - 1);
         const bool store_col = keep_d && vc >= x0 && vc < x0 + cw && vc < g.W;
         if (fast) {
-            // chain rows k = -2..R+1 of columns cc - s, cc, cc + s (no clamps anywhere)
-            float a[R + 4], m[R + 4], c[R + 4];
+            // chain rows k = -2..R+1 of columns cc - s, cc, cc + s (no clamps anywhere); each row's terms once
+            RowTerms rt[R + 4];
 #pragma unroll
             for (int k = 0; k < R + 4; ++k) {
                 const float* p = L + (unsigned)((y0 + (k - 2) * SC) * g.P + cc);
-                a[k] = __ldg(p - SC);
-                m[k] = __ldg(p);
-                c[k] = __ldg(p + SC);
+                rt[k] = row_terms(__ldg(p - SC), __ldg(p), __ldg(p + SC));
             }
 #pragma unroll
             for (int k = 0; k < R + 2; ++k) {  // chain row k - 1 uses rows k, k+1, k+2 of the arrays
-                const float2 v = make_float2(
-                    0.5f * (kW0 * (c[k] - a[k]) + kW1 * (c[k + 1] - a[k + 1]) + kW0 * (c[k + 2] - a[k + 2])),
-                    0.5f * (kW0 * (a[k + 2] - a[k]) + kW1 * (m[k + 2] - m[k]) + kW0 * (c[k + 2] - c[k])));
+                const float2 v = first_from_rows(rt[k], rt[k + 1], rt[k + 2]);
                 sm[k][t] = v;
                 if (k >= 1 && k <= R && store_col) __stwb(D + (unsigned)((y0 + (k - 1) * SC) * g.P + vc), v);
             }
@@ -216,16 +238,12 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
                 const int yv = y0 + (k - 1) * s;  // chain row k - 1 (virtual)
                 const int yc = clampi(yv, 0, g.H - 1);
                 const int ro[3] = {max(yc - s, 0) * g.P, yc * g.P, min(yc + s, g.H - 1) * g.P};
-                float a3[3], m3[3], c3[3];
+                RowTerms r3[3];
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    a3[q] = __ldg(L + (unsigned)(ro[q] + xm));
-                    m3[q] = __ldg(L + (unsigned)(ro[q] + cc));
-                    c3[q] = __ldg(L + (unsigned)(ro[q] + xp));
-                }
-                const float2 v = make_float2(
-                    0.5f * (kW0 * (c3[0] - a3[0]) + kW1 * (c3[1] - a3[1]) + kW0 * (c3[2] - a3[2])),
-                    0.5f * (kW0 * (a3[2] - a3[0]) + kW1 * (m3[2] - m3[0]) + kW0 * (c3[2] - c3[0])));
+                for (int q = 0; q < 3; ++q)
+                    r3[q] = row_terms(__ldg(L + (unsigned)(ro[q] + xm)), __ldg(L + (unsigned)(ro[q] + cc)),
+                                      __ldg(L + (unsigned)(ro[q] + xp)));
+                const float2 v = first_from_rows(r3[0], r3[1], r3[2]);
                 sm[k][t] = v;
                 if (k >= 1 && k <= R && store_col && yv < g.H) __stwb(D + (unsigned)(yv * g.P + vc), v);
             }
@@ -233,14 +251,18 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
     }
     __syncthreads();
     if (t < cw && x0 + t < g.W) {
-        // ring: columns x − s, x, x + s ↔ shared columns t, t + s, t + 2s; chain rows −1..R ↔ shared rows 0..R+1
+        // ring: columns x − s, x, x + s ↔ shared columns t, t + s, t + 2s; chain rows −1..R ↔ shared rows 0..R+1;
+        // each ring row's terms (E, P, Q) once, shared by the three outputs that read the row
+        RingTerms r0 = ring_terms(sm[0][t], sm[0][t + s], sm[0][t + 2 * s]);
+        RingTerms r1 = ring_terms(sm[1][t], sm[1][t + s], sm[1][t + 2 * s]);
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const int y = y0 + j * s;
             if (!fast && y >= g.H) break;
-            const float v = det_from_ring(sm[j][t], sm[j][t + s], sm[j][t + 2 * s], sm[j + 1][t], sm[j + 1][t + 2 * s],
-                                          sm[j + 2][t], sm[j + 2][t + s], sm[j + 2][t + 2 * s]);
-            __stwb(O + (unsigned)(y * g.P + x0 + t), v);
+            const RingTerms r2 = ring_terms(sm[j + 2][t], sm[j + 2][t + s], sm[j + 2][t + 2 * s]);
+            __stwb(O + (unsigned)(y * g.P + x0 + t), det_from_terms(r0, r1, r2));
+            r0 = r1;
+            r1 = r2;
         }
     }
 }

@@ -350,49 +350,61 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
         launch_kfinal(c->hist, c->p.k_bins, c->hmax, n, c->p.k_percentile, c->p.k_override, c->kval, c->fallback, s);
     }
     KZ_CHECK_LAUNCH(c, "k_final");
-    for (int i = 1; i < N; ++i) {
-        const float* prev = c->Lt + (size_t)(i - 1) * g.plane;
-        float* cur = c->Lt + (size_t)i * g.plane;
-        {   // level 1 too: recomputing |∇(G1∗L0)|² in the conductivity pass beats converting the stored |∇|²
-            // (measured 1.45 vs 2.6 ms per 256-image step)
-            Launch L(c, KC_COND, 8.0 * px, s);
-            launch_cond(prev, SL, c->cbuf, SP, g, n, c->g1, 1, c->p.diffusivity, c->kval, nullptr, s);
-        }
-        KZ_CHECK_LAUNCH(c, "cond");
-        if (c->p.scheme == KAZE_SCHEME_FED) {  // one FED cycle, K <= kFedMaxK steps per launch (A20, A21)
-            const std::vector<float>& taus = c->fed[i];
-            const int ns = (int)taus.size(), nl = (ns + kFedMaxK - 1) / kFedMaxK;
-            int done = 0;
-            for (int j = 0; j < nl; ++j) {
-                const int k = (ns - done + (nl - j) - 1) / (nl - j);
-                FedTaus ft{};
-                for (int q = 0; q < k; ++q) ft.t[q] = taus[done + q];
-                // ping-pong so that the last launch writes L_i: launch j writes cur iff nl-1-j is even
-                float* dst = ((nl - 1 - j) % 2 == 0) ? cur : c->ubuf;
-                const float* src = j == 0 ? prev : (((nl - j) % 2 == 0) ? cur : c->ubuf);
-                const size_t s_src = j == 0 ? SL : (src == cur ? SL : SP), s_dst = dst == cur ? SL : SP;
-                {
-                    Launch L(c, KC_FED, 12.0 * px, s);
-                    launch_fed_steps(src, s_src, c->cbuf, SP, dst, s_dst, g, n, ft, k, s);
-                }
-                KZ_CHECK_LAUNCH(c, "fed");
-                done += k;
+    // Level loop.  KAZE_BUILD_SUB=k (diagnostic knob) runs it on sub-batches of k images, image-major, so that a
+    // sub-batch's c, U and L_i planes can stay in L2 between the passes of a level.
+    static const int sub = tune_knob("KAZE_BUILD_SUB", 0);
+    const int sb = sub > 0 ? std::min(sub, n) : n;
+    for (int b0 = 0; b0 < n; b0 += sb) {
+        const int m = std::min(sb, n - b0);
+        const double mpx = (double)w * h * m;
+        float* Lt = c->Lt + (size_t)b0 * SL;
+        float* cb = c->cbuf + (size_t)b0 * SP;
+        float* ub = c->ubuf + (size_t)b0 * SP;
+        const float* kv = c->kval + b0;
+        for (int i = 1; i < N; ++i) {
+            const float* prev = Lt + (size_t)(i - 1) * g.plane;
+            float* cur = Lt + (size_t)i * g.plane;
+            {   // level 1 too: recomputing |∇(G1∗L0)|² in the conductivity pass beats converting the stored |∇|²
+                // (measured 1.45 vs 2.6 ms per 256-image step)
+                Launch L(c, KC_COND, 8.0 * mpx, s);
+                launch_cond(prev, SL, cb, SP, g, m, c->g1, 1, c->p.diffusivity, kv, nullptr, s);
             }
-            continue;
+            KZ_CHECK_LAUNCH(c, "cond");
+            if (c->p.scheme == KAZE_SCHEME_FED) {  // one FED cycle, K <= kFedMaxK steps per launch (A20, A21)
+                const std::vector<float>& taus = c->fed[i];
+                const int ns = (int)taus.size(), nl = (ns + kFedMaxK - 1) / kFedMaxK;
+                int done = 0;
+                for (int j = 0; j < nl; ++j) {
+                    const int k = (ns - done + (nl - j) - 1) / (nl - j);
+                    FedTaus ft{};
+                    for (int q = 0; q < k; ++q) ft.t[q] = taus[done + q];
+                    // ping-pong so that the last launch writes L_i: launch j writes cur iff nl-1-j is even
+                    float* dst = ((nl - 1 - j) % 2 == 0) ? cur : ub;
+                    const float* src = j == 0 ? prev : (((nl - j) % 2 == 0) ? cur : ub);
+                    const size_t s_src = j == 0 ? SL : (src == cur ? SL : SP), s_dst = dst == cur ? SL : SP;
+                    {
+                        Launch L(c, KC_FED, 12.0 * mpx, s);
+                        launch_fed_steps(src, s_src, cb, SP, dst, s_dst, g, m, ft, k, s);
+                    }
+                    KZ_CHECK_LAUNCH(c, "fed");
+                    done += k;
+                }
+                continue;
+            }
+            const float tau = (float)(c->t[i] - c->t[i - 1]);
+            {   // U = column solves (ubuf holds U)
+                Launch L(c, KC_AOS_COLS, 12.0 * mpx, s);
+                if (!launch_aos_cols(prev, cb, ub, Strides{SL, SP, 0, SP}, g, m, tau, s))
+                    return KAZE_ERR_INVALID_ARGUMENT;
+            }
+            KZ_CHECK_LAUNCH(c, "aos_cols");
+            {   // L_i = ½(U + V), V = row solves
+                Launch L(c, KC_AOS_ROWS, 16.0 * mpx, s);
+                if (!launch_aos_rows(prev, cb, ub, cur, Strides{SL, SP, SP, SL}, g, m, tau, s))
+                    return KAZE_ERR_INVALID_ARGUMENT;
+            }
+            KZ_CHECK_LAUNCH(c, "aos_rows");
         }
-        const float tau = (float)(c->t[i] - c->t[i - 1]);
-        {   // U = column solves (ubuf holds U)
-            Launch L(c, KC_AOS_COLS, 12.0 * px, s);
-            if (!launch_aos_cols(prev, c->cbuf, c->ubuf, Strides{SL, SP, 0, SP}, g, n, tau, s))
-                return KAZE_ERR_INVALID_ARGUMENT;
-        }
-        KZ_CHECK_LAUNCH(c, "aos_cols");
-        {   // L_i = ½(U + V), V = row solves
-            Launch L(c, KC_AOS_ROWS, 16.0 * px, s);
-            if (!launch_aos_rows(prev, c->cbuf, c->ubuf, cur, Strides{SL, SP, SP, SL}, g, n, tau, s))
-                return KAZE_ERR_INVALID_ARGUMENT;
-        }
-        KZ_CHECK_LAUNCH(c, "aos_rows");
     }
     c->built = true;
     c->last_stream = s;

@@ -1,20 +1,22 @@
 // match.cu — brute-force descriptor matching (reading A25) on the 5th-generation tensor
 // cores: the one dense contraction of the method, desc_A · desc_Bᵀ.
 //
-//   1. k_match_prep: fp32 [n][64] → fp16 rows in the UMMA K-major SWIZZLE_128B layout, pre-tiled by 256 rows
-//      (each 32 KB tile is the exact shared-memory image, so one 1-D TMA bulk copy stages it), a 256-bit validity
+//   1. k_match_prep: fp32 [n][64] → fp16 rows in the UMMA K-major SWIZZLE_128B layout, pre-tiled by kTileR = 128
+//      rows (each 16 KB tile is the exact shared-memory image, so one 1-D TMA bulk copy stages it), a 128-bit validity
 //      mask per tile (degenerate = all-zero descriptors and padding rows are never candidates) and the norm
 //      range of the valid rows.
-//   2. k_match_topk: one CTA per 128 query rows.  A TMA warp streams the reference tiles (double-buffered
-//      mbarrier ring), one thread issues tcgen05.mma kind::f16 (M = 128, N = 128, K = 4 x 16) into a
-//      double-buffered TMEM accumulator (2 x 256 columns), and 8 epilogue warps drain it with tcgen05.ld
-//      (warp w reads TMEM lanes 32·(w%4).. = its 32 query rows, column half w/4), keeping each row's eight best
-//      approximate scores.  fp16 operands (descriptor components lie in [−1, 1]; fp16 has bf16's tensor rate and
+//   2. k_match_topk: one CTA per 128 query rows and reference part (the reference range is split into up to
+//      kMaxSplit parts when the query blocks alone cannot fill two CTAs per SM).  A TMA warp streams the reference
+//      tiles through a kStages = 3 mbarrier ring, one thread issues tcgen05.mma kind::f16 (M = 128, N = 128,
+//      K = 4 x 16) into a double-buffered TMEM accumulator (2 x 128 columns), and 8 epilogue warps drain it with
+//      tcgen05.ld (warp w reads TMEM lanes 32·(w%4).. = its 32 query rows, column half w/4), keeping each row's
+//      eight best approximate scores per part.  fp16 operands (descriptor components lie in [−1, 1]; fp16 has bf16's tensor rate and
 //      3 more significand bits), fp32 accumulation: |s_approx − a·b| <= 2^-10·|a||b| + accumulation slack.
 //   3. k_match_rerank: one warp per query: exact fp32 distances ||a − b|| for the eight candidates, ordered by
 //      (distance, index).  The result is CERTIFIED exact when the second candidate distance is below the
 //      smallest distance any non-candidate can have, |a|² + min|b|² − 2(s_8 + ε); otherwise the warp scans every
-//      reference exactly (rare).  So tensor cores do the bulk and the decision is the exact fp32 one.
+//      reference exactly (rare).  With a split range the parts' top-8 lists are merged here, and the certificate
+//      bound uses the largest part-wise 8th score.  So tensor cores do the bulk and the decision is the exact fp32 one.
 //   4. k_match_final: ratio test d1 < ratio·d2 and the symmetric cross-check from the reverse pass.
 #include <cmath>
 
@@ -29,7 +31,7 @@ namespace {
 
 constexpr int kTileR = 128;                 // reference rows per tile (UMMA N); 128 lets two CTAs share an SM's TMEM
 constexpr int kTileQ = 128;                 // query rows per CTA (UMMA M)
-constexpr int kTileBytes = kTileR * 128;    // 64 bf16 = 128 B per row
+constexpr int kTileBytes = kTileR * 128;    // 64 fp16 = 128 B per row
 constexpr int kStages = 3;  // reference-tile ring depth (TMA → MMA)
 constexpr int kMaxSplit = 4;  // reference-range parts per query block when the query blocks alone cannot fill the GPU
 constexpr int kCand = 8;  // approximate candidates kept per query (4: 1400 of 15.8k KAZE rows uncertified, 3.4 ms)
@@ -49,7 +51,7 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
     // 1024-byte alignment for the swizzle atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;                    // 16 KB
-    uint8_t* sB = smem + kTileQ * 128;     // kStages x 32 KB
+    uint8_t* sB = smem + kTileQ * 128;     // kStages x 16 KB
     __shared__ __align__(8) uint64_t bar_full[kStages], bar_empty[kStages], bar_acc_full[2], bar_acc_empty[2], bar_a;
     __shared__ uint32_t tmem_base_slot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -241,13 +243,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
                 const uint32_t b_addr = smem_u32(sB + s * kTileBytes);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)  // K = 64 = 4 x 16, +32 B along the swizzled row per step
-                    mma_bf16(tmem + a * kTileR, smem_desc_sw128(a_addr + 32 * k), smem_desc_sw128(b_addr + 32 * k),
+                    mma_f16(tmem + a * kTileR, smem_desc_sw128(a_addr + 32 * k), smem_desc_sw128(b_addr + 32 * k),
                              kIdesc, k > 0 ? 1u : 0u);
                 mma_commit(&bar_empty[s]);     // smem stage free once these MMAs are done
                 mma_commit(&bar_acc_full[a]);  // accumulator ready for the epilogue
             }
         }
-    } else {  // ===== epilogue warps: TMEM → registers → running top-4 per query row =====
+    } else {  // ===== epilogue warps: TMEM → registers → running top-8 (kCand) per query row =====
         const int g = warp & 3, h = warp >> 2;  // TMEM lane group (query rows 32g..), column group
         float* sv = reinterpret_cast<float*>(sB + kStages * kTileBytes) + warp * 32 * 32;  // 4 KB per epilogue warp
         TopK tk;

@@ -1,0 +1,8 @@
+set -u
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 > gpurun_out/gpu_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+echo "bench rc=$?"
+scripts/ncu_full.sh cond k_cond2 3
+scripts/ncu_full.sh pre k_prefilter 0
