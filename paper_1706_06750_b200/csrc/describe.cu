@@ -88,7 +88,16 @@ __global__ void __launch_bounds__(256, 5) k_describe(const float2* __restrict__ 
             continue;
         }
         const float2* lxy = Lxy + img * img_stride + (size_t)level * g.plane;
-        const cudaTextureObject_t tex = texs[img * N + level];
+        // The texture handle is the same for the whole warp; broadcasting it from lane 0 lets ptxas prove that, so
+        // every tex2D below takes the handle from a uniform register directly.  (Loaded per lane, the handle is
+        // "maybe divergent" to the compiler, which then wraps each fetch in a uniformisation loop — R2UR + BRA.U.ANY
+        // — and issues the 24 fetches of a grid line one at a time, each waiting out the full fetch latency.)
+        cudaTextureObject_t tex = texs[img * N + level];
+        {
+            const unsigned lo = __shfl_sync(0xffffffffu, (unsigned)tex, 0);
+            const unsigned hi = __shfl_sync(0xffffffffu, (unsigned)(tex >> 32), 0);
+            tex = ((cudaTextureObject_t)hi << 32) | lo;
+        }
         float angle;
         int flags = 0;
         if (keep_angle) {
