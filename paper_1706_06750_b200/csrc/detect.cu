@@ -256,6 +256,99 @@ __global__ void __launch_bounds__(256, EXT ? 1 : 4) k_nms_mark(const float* __re
     }
 }
 
+// Default detector, lean form: the number of centre levels NC is a compile-time constant (a launch per distinct
+// block size; N = 16 gives two blocks of 7), the column part of the border test and the threshold are hoisted out
+// of the row loop, and the plane offsets are uniform, so a row costs per plane one load, the vertical max, two
+// shuffles and three max ops, and per centre one max3, one max, one compare and a ballot.  (The generic kernel
+// above re-derived `c <= nc`, the threshold and the border predicates every row: ~30% of its instructions.)
+template <int NC, int PH>
+__device__ __forceinline__ void nms_row_fast(float (&w)[NC + 2][3], const float* __restrict__ base,
+                                             const unsigned (&off)[NC + 2], unsigned P, int y, int H, bool xin,
+                                             float thr, float er, int lane, uint32_t* __restrict__ bm,
+                                             size_t lvl_stride, int words) {
+    const unsigned ro = (unsigned)min(y + 1, H - 1) * P;
+#pragma unroll
+    for (int q = 0; q < NC + 2; ++q) w[q][(PH + 2) % 3] = __ldg(base + (off[q] + ro));
+    float M[NC + 2], N8[NC + 2];
+#pragma unroll
+    for (int q = 0; q < NC + 2; ++q) {
+        const float up = w[q][PH % 3], ce = w[q][(PH + 1) % 3], dn = w[q][(PH + 2) % 3];
+        const float vm = fmaxf(up, fmaxf(ce, dn));
+        const float vl = __shfl_up_sync(0xffffffffu, vm, 1), vr = __shfl_down_sync(0xffffffffu, vm, 1);
+        M[q] = fmaxf(vm, fmaxf(vl, vr));
+        if (q >= 1 && q <= NC) N8[q] = fmaxf(fmaxf(vl, vr), fmaxf(up, dn));
+    }
+    const bool inside = xin && y >= 1 && y <= H - 2;
+    uint32_t bits[NC], anyb = 0u;
+#pragma unroll
+    for (int c = 1; c <= NC; ++c) {
+        const float v = w[c][(PH + 1) % 3];
+        const float nb = fmaxf(fmaxf(N8[c], M[c - 1]), fmaxf(M[c + 1], thr));
+        bits[c - 1] = __ballot_sync(0xffffffffu, inside && v > nb);
+        anyb |= bits[c - 1];
+    }
+    if (anyb) {  // warp-uniform and rare: the level's 3x3 patch by shuffles, edge test and 2-D fit
+#pragma unroll
+        for (int c = 1; c <= NC; ++c) {
+            if (!bits[c - 1]) continue;  // warp-uniform
+            const float v = w[c][(PH + 1) % 3];
+            const float u0 = w[c][PH % 3], u2 = w[c][(PH + 2) % 3];
+            const float l0s = __shfl_up_sync(0xffffffffu, u0, 1), l1 = __shfl_up_sync(0xffffffffu, v, 1);
+            const float l2 = __shfl_up_sync(0xffffffffu, u2, 1);
+            const float r0 = __shfl_down_sync(0xffffffffu, u0, 1), r1 = __shfl_down_sync(0xffffffffu, v, 1);
+            const float r2 = __shfl_down_sync(0xffffffffu, u2, 1);
+            bool k = (bits[c - 1] >> lane) & 1u;
+            if (k) {
+                const float patch[3][3] = {{l0s, u0, r0}, {l1, v, r1}, {l2, u2, r2}};
+                float ox, oy;
+                k = refine(patch, er, ox, oy);
+            }
+            bits[c - 1] = __ballot_sync(0xffffffffu, k);
+        }
+    }
+    uint32_t mine = 0u;
+#pragma unroll
+    for (int c = 1; c <= NC; ++c)
+        if (lane == c - 1) mine = bits[c - 1];
+    if (lane < NC) bm[(size_t)lane * lvl_stride + (size_t)y * words] = (mine >> 1) & ((1u << STRIP) - 1u);
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256, 4) k_nms_mark_fast(const float* __restrict__ Ldet, size_t img_stride, Geom g,
+                                                          int N, int l_first, int nblk, DetectParams dp,
+                                                          uint32_t* __restrict__ bitmap, int words) {
+    KZ_PDL_PROLOGUE();
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (strip >= words) return;  // warp-uniform
+    const int blk = blockIdx.z % nblk, img = blockIdx.z / nblk;
+    const int l0 = l_first + blk * NC;  // first centre level; planes q = 0..NC+1 are levels l0−1 .. l0+NC
+    const int W = g.W, H = g.H;
+    const int x = strip * STRIP - 1 + lane;
+    const bool xin = lane >= 1 && lane <= STRIP && x >= 1 && x <= W - 2;
+    const float* base = opaque(Ldet + img * img_stride + (size_t)(l0 - 1) * g.plane + clampi(x, 0, W - 1));
+    unsigned off[NC + 2];
+#pragma unroll
+    for (int q = 0; q < NC + 2; ++q) off[q] = (unsigned)q * (unsigned)g.plane;
+    const size_t lvl_stride = (size_t)H * words;
+    uint32_t* bm = bitmap + ((size_t)img * (N - 2) + (l0 - 1)) * lvl_stride + strip;
+    const float thr = dp.threshold, er = dp.edge_ratio;
+    const unsigned P = (unsigned)g.P;
+    const int y0 = blockIdx.y * NSEG, yend = min(y0 + NSEG, H);
+    float w[NC + 2][3];
+    const unsigned rm = (unsigned)max(y0 - 1, 0) * P, r0 = (unsigned)y0 * P;
+#pragma unroll
+    for (int q = 0; q < NC + 2; ++q) {
+        w[q][0] = __ldg(base + (off[q] + rm));
+        w[q][1] = __ldg(base + (off[q] + r0));
+    }
+    for (int y = y0; y < yend; y += 3) {
+        nms_row_fast<NC, 0>(w, base, off, P, y, H, xin, thr, er, lane, bm, lvl_stride, words);
+        if (y + 1 < yend) nms_row_fast<NC, 1>(w, base, off, P, y + 1, H, xin, thr, er, lane, bm, lvl_stride, words);
+        if (y + 2 < yend) nms_row_fast<NC, 2>(w, base, off, P, y + 2, H, xin, thr, er, lane, bm, lvl_stride, words);
+    }
+}
+
 // Row candidate counts from the bitmap: one warp per (image, level, row).
 __global__ void __launch_bounds__(256) k_rowcount(const uint32_t* __restrict__ bitmap, int words, int total_rows,
                                                   int* __restrict__ rowcnt) {
@@ -365,18 +458,40 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
 
 int nms_words(int W) { return (W + STRIP - 1) / STRIP; }
 
-void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
-                     uint32_t* bitmap, int* rowcnt, cudaStream_t s) {
+int launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
+                    uint32_t* bitmap, int* rowcnt, cudaStream_t s) {
+    int nk = 1;  // kernels launched (rowcount included)
     const int N = lt.n;
     const int words = nms_words(g.W);
     const int nblk = (N - 2 + NMS_LB - 1) / NMS_LB;
     dim3 grid((words + 7) / 8, (g.H + NSEG - 1) / NSEG, nimg * nblk);
-    if (dp.exact || dp.refine3d)  // detector variants (§8 f2) in their own instantiation: the default stays lean
+    static const int lean = tune_knob("KAZE_NMS_LEAN", 1);
+    if (dp.exact || dp.refine3d) {  // detector variants (§8 f2) in their own instantiation: the default stays lean
         kz_launch(k_nms_mark<NMS_LB, true>, dim3(grid), dim3(256), 0, s, Ldet, img_stride, g, N, dp, lt, bitmap, words);
-    else
+    } else if (!lean) {
         kz_launch(k_nms_mark<NMS_LB, false>, dim3(grid), dim3(256), 0, s, Ldet, img_stride, g, N, dp, lt, bitmap, words);
+    } else {
+        // full blocks of NMS_LB centre levels in one launch, the remainder (if any) in a second
+        const int full = (N - 2) / NMS_LB, rem = (N - 2) - full * NMS_LB;
+        nk += (full > 0) + (rem > 0) - 1;
+        if (full > 0)
+            kz_launch(k_nms_mark_fast<NMS_LB>, dim3(dim3(grid.x, grid.y, nimg * full)), dim3(256), 0, s, Ldet,
+                      img_stride, g, N, 1, full, dp, bitmap, words);
+        const int lr = 1 + full * NMS_LB;
+        switch (rem) {
+#define KZ_NMS_REM(R)                                                                                              \
+    case R:                                                                                                        \
+        kz_launch(k_nms_mark_fast<R>, dim3(dim3(grid.x, grid.y, nimg)), dim3(256), 0, s, Ldet, img_stride, g, N, lr, \
+                  1, dp, bitmap, words);                                                                           \
+        break;
+            KZ_NMS_REM(1) KZ_NMS_REM(2) KZ_NMS_REM(3) KZ_NMS_REM(4) KZ_NMS_REM(5) KZ_NMS_REM(6)
+#undef KZ_NMS_REM
+            default: break;
+        }
+    }
     const int total = g.H * (N - 2) * nimg;
     kz_launch(k_rowcount, dim3((total + 7) / 8), dim3(256), 0, s, bitmap, words, total, rowcnt);
+    return nk + 1;
 }
 
 void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, int* counts, cudaStream_t s) {

@@ -444,8 +444,8 @@ kaze_status do_detect(kaze_ctx* c, kaze_keypoint* d_kps, int32_t* d_counts, cuda
         DetectParams dp{(float)c->p.threshold, (float)c->p.edge_ratio, c->p.max_keypoints,
                         (c->p.flags & KAZE_FLAG_EXACT_WINDOW) ? 1 : 0, (c->p.flags & KAZE_FLAG_REFINE_3D) ? 1 : 0};
         {
-            Launch L(c, KC_NMS_MARK, 4.0 * px * N, s, 2);  // nms_mark + rowcount
-            launch_nms_mark(c->Ldet, c->img_stride, g, n, c->lt, dp, c->bitmap, c->rowcnt, s);
+            Launch L(c, KC_NMS_MARK, 4.0 * px * N, s, 2);  // nms_mark (1 or 2 launches) + rowcount
+            L.nk = launch_nms_mark(c->Ldet, c->img_stride, g, n, c->lt, dp, c->bitmap, c->rowcnt, s);
         }
         KZ_CHECK_LAUNCH(c, "nms_mark");
         const int R = (N - 2) * g.H;

@@ -137,8 +137,9 @@ struct DetectParams {
 };
 // Candidate bitmap words per row: 30 columns per 32-bit word (bit b of word w ↔ column 30·w + b).
 int nms_words(int W);
-void launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
-                     uint32_t* bitmap, int* rowcnt, cudaStream_t s);
+// returns the number of kernels launched (the mark pass, one or two launches, + the row count)
+int launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
+                    uint32_t* bitmap, int* rowcnt, cudaStream_t s);
 void launch_kp_scan(const int* rowcnt, int rows_per_img, int nimg, int* rowoff, int* counts, cudaStream_t s);
 void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt,
                     DetectParams dp, const uint32_t* bitmap, const int* rowcnt, const int* rowoff, kaze_keypoint* kps,
