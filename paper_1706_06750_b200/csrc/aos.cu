@@ -26,6 +26,9 @@
 //   rows:    one CTA (4 or 8 warps) per row.  The TMA engine streams the row's L, c and U into shared memory (1-D
 //            bulk copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is
 //            solved by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "kaze_internal.cuh"
 #include "ptx.cuh"
 
@@ -334,6 +337,112 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_u(const float* __restrict
     else chunk_finish<M, false>(dv, tq, xf, xl, Ub, o0, P, nvalid);
 }
 
+// Column pass with TMA-staged inputs (the default for H <= 64·19): one thread issues 3-D tiled tensor copies of the
+// CTA's CW-column strip of L and c (boxes of CW x BR rows, zero fill past the image) into shared memory, [row][CW]
+// floats, and every thread reads its chunk from there.  The chunk length M is odd, so the four chunks a warp covers
+// (rows p·M + i, p = 4w..4w+3) fall in four different bank groups: one conflict-free LDS per sample and array
+// instead of an LDG that touches four 32-byte sectors in four lines (41 such loads per thread kept the LSU/MIO queue
+// full in the register-staged kernel above — mio_throttle was its top stall).  Solve and stores as above.
+template <int CW, int M, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_aos_cols_tma(const __grid_constant__ CUtensorMap tmL,
+                                                           const __grid_constant__ CUtensorMap tmC,
+                                                           float* __restrict__ U, size_t u_stride, Geom g, float tau,
+                                                           int T, int TP, int nbox, int BR) {
+    KZ_PDL_PROLOGUE();
+    extern __shared__ __align__(128) float smem_cols[];
+    __shared__ __align__(8) uint64_t bar;
+    const int HB = nbox * BR;
+    float* smL = smem_cols;      // [HB][CW]
+    float* smC = smL + HB * CW;  // [HB][CW]
+    const int NTOT = CW * TP;
+    float* sa = smC + HB * CW;
+    float* sb = sa + NTOT;
+    float* sc = sb + NTOT;
+    float* sd = sc + NTOT;
+    float* slF = sd + NTOT;
+    float* slG = slF + NTOT;
+    float* slH = slG + NTOT;
+    const int x0 = blockIdx.x * CW, img = blockIdx.z;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&bar, 2u * (uint32_t)(HB * CW) * 4u);
+        for (int b = 0; b < nbox; ++b) {
+            tma_load_3d(smL + b * BR * CW, &tmL, x0, b * BR, img, &bar);
+            tma_load_3d(smC + b * BR * CW, &tmC, x0, b * BR, img, &bar);
+        }
+    }
+    const int cx = threadIdx.x % CW, p = threadIdx.x / CW;
+    const int x = x0 + cx;
+    const bool active = (p < T) && (x < g.W);
+    const int n = g.H;
+    const int j0 = p * M;
+    const int nvalid = n - j0;
+    float dv[M], tq[M + 1];
+    ChunkEq e{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+    if (active) {
+        // padding samples of the last chunk (rows >= H; they may lie past the staged rows) read 0 and their edge
+        // weights are zero, so they decouple exactly as in the register-staged kernel
+        float cv[M];
+        const bool full = nvalid > M;
+        if (full) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                dv[i] = smL[(j0 + i) * CW + cx];
+                cv[i] = smC[(j0 + i) * CW + cx];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                dv[i] = i < nvalid ? smL[(j0 + i) * CW + cx] : 0.f;
+                cv[i] = i < nvalid ? smC[(j0 + i) * CW + cx] : 0.f;
+            }
+        }
+        const float cprev = j0 > 0 ? smC[(j0 - 1) * CW + cx] : 0.f;
+        tq[0] = j0 > 0 ? tau * (cprev + cv[0]) : 0.f;
+        if (full) {
+#pragma unroll
+            for (int i = 1; i < M; ++i) tq[i] = tau * (cv[i - 1] + cv[i]);
+            tq[M] = tau * (cv[M - 1] + smC[(j0 + M) * CW + cx]);
+        } else {
+#pragma unroll
+            for (int i = 1; i < M; ++i) tq[i] = i < nvalid ? tau * (cv[i - 1] + cv[i]) : 0.f;
+            tq[M] = 0.f;
+        }
+        chunk_reduce<M>(dv, tq, e);
+    }
+    const int idx = p * CW + cx;
+    slF[idx] = e.lF;
+    slG[idx] = e.lG;
+    slH[idx] = e.lH;
+    __syncthreads();
+    float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
+    if (active) {
+        float pF = 0.f, pG = 0.f, pH = 0.f;
+        if (p > 0) {
+            pF = slF[idx - CW];
+            pG = slG[idx - CW];
+            pH = slH[idx - CW];
+        }
+        af = -e.A * pH;
+        bf = 1.f - e.A * pG - e.C * e.lH;
+        cf = -e.C * e.lG;
+        df = e.D - e.A * pF - e.C * e.lF;
+    }
+    const float xf = pcr_solve(af, bf, cf, df, p, TP, CW, idx, sa, sb, sc, sd);
+    sa[idx] = xf;
+    __syncthreads();
+    if (!active) return;
+    const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
+    const float xl = e.lF - e.lG * xnext - e.lH * xf;
+    float* Ub = opaque(U + blockIdx.z * u_stride);
+    const unsigned P = (unsigned)g.P, o0 = (unsigned)j0 * P + (unsigned)x;
+    if (nvalid > M) chunk_finish<M, true>(dv, tq, xf, xl, Ub, o0, P, nvalid);
+    else chunk_finish<M, false>(dv, tq, xf, xl, Ub, o0, P, nvalid);
+}
+
 // -------------------------------------------------------------------------------------------------------------
 // Row systems, one CTA of NW warps per row (the row pass runs first and writes V).  The TMA engine streams the
 // row's L and c into shared memory; thread p owns the chunk [p·M, p·M + m) (M odd: conflict-free strided reads)
@@ -492,6 +601,54 @@ void run_rows_cta(const float* L, const float* c, const float* U, float* Lout, S
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// 3-D fp32 map over nimg planes of W x H (row pitch P floats, plane stride `plane_stride` floats), box CW x BR x 1.
+bool encode_plane_map(CUtensorMap* m, const float* base, Geom g, int nimg, size_t plane_stride, int CW, int BR) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)nimg};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.P * 4, (cuuint64_t)plane_stride * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)CW, (cuuint32_t)BR, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int CW, int M, int NT, int MINB>
+bool run_cols_tma(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau, cudaStream_t s) {
+    const int T = (g.H + M - 1) / M;
+    const int TP = round_up(T, 32 / CW);
+    if (CW * TP > NT) return false;
+    // boxes of BR rows, BR a multiple of 4 (CW = 8 floats x 4 rows = 128 B: every box lands 128-byte aligned)
+    const int nbox = (g.H + 255) / 256, BR = round_up((g.H + nbox - 1) / nbox, 4);
+    CUtensorMap tmL, tmC;
+    if (!encode_plane_map(&tmL, L, g, nimg, st.L, CW, BR) || !encode_plane_map(&tmC, c, g, nimg, st.c, CW, BR))
+        return false;
+    const size_t smem = sizeof(float) * (2 * (size_t)nbox * BR * CW + 7 * (size_t)CW * TP);
+    if (!ensure_smem_optin(reinterpret_cast<const void*>(k_aos_cols_tma<CW, M, NT, MINB>), (int)smem)) return false;
+    dim3 grid((g.W + CW - 1) / CW, 1, nimg);
+    kz_launch(k_aos_cols_tma<CW, M, NT, MINB>, dim3(grid), dim3(CW * TP), smem, s, tmL, tmC, U, st.out, g, tau, T, TP,
+              nbox, BR);
+    return true;
+}
+
 template <int CW, int M, int NT, int MINB>
 void run_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau, cudaStream_t s) {
     const int T = (g.H + M - 1) / M;  // the last chunk is padded (decoupled rows)
@@ -510,6 +667,16 @@ void run_cols(const float* L, const float* c, float* U, Strides st, Geom g, int 
 bool launch_aos_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau,
                      cudaStream_t s) {
     const int H = g.H;
+    static const int tma = tune_knob("KAZE_COLS_TMA", 1);
+    // TMA-staged inputs, odd chunk lengths (conflict-free shared reads), <= 64 chunks per column
+    if (tma && H <= 64 * 19) {
+        bool ok;
+        if (H <= 64 * 9) ok = run_cols_tma<8, 9, 512, 2>(L, c, U, st, g, nimg, tau, s);
+        else if (H <= 64 * 13) ok = run_cols_tma<8, 13, 512, 2>(L, c, U, st, g, nimg, tau, s);
+        else if (H <= 64 * 17) ok = run_cols_tma<8, 17, 512, 2>(L, c, U, st, g, nimg, tau, s);
+        else ok = run_cols_tma<8, 19, 512, 2>(L, c, U, st, g, nimg, tau, s);
+        if (ok) return true;
+    }
     if (H <= 8 * 64) run_cols<8, 8, 512, 2>(L, c, U, st, g, nimg, tau, s);
     else if (H <= 12 * 64) run_cols<8, 12, 512, 2>(L, c, U, st, g, nimg, tau, s);
     else if (H <= 16 * 64) run_cols<8, 16, 512, 2>(L, c, U, st, g, nimg, tau, s);

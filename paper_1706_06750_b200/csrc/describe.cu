@@ -69,9 +69,9 @@ __global__ void __launch_bounds__(256, 5) k_describe(const float2* __restrict__ 
     // of the (image, level, y, x)-ordered list, so the planes it samples stay in L2.  (A contiguous range per CTA —
     // more L1 sharing, but the grid spread over every image and level at once — measured 48.8 vs 24.7 ms; 2 or 4
     // consecutive keypoints per warp per round 24.2 / 27.8 vs 23.5.)
+    int img = 0;  // f only grows, so the image search resumes where the previous keypoint left it
     for (int f = blockIdx.x * kWarps + warp; f < total; f += gridDim.x * kWarps) {
-        int img = 0;
-        while (img + 1 < nimg && pre[img + 1] <= f) ++img;  // nimg is small
+        while (img + 1 < nimg && pre[img + 1] <= f) ++img;
         const int k = f - pre[img];
         kaze_keypoint* kp = kps + (size_t)img * cap + k;
         const float x = kp->x, y = kp->y, sigma = kp->sigma;
@@ -184,15 +184,25 @@ __global__ void __launch_bounds__(256, 5) k_describe(const float2* __restrict__ 
                     bsum[i] = make_float2(ax, ay);
                 }
                 __syncwarp();
+                // Window k = bins [2k − h, 2k + h): h whole bin pairs starting at bins of parity o = h & 1, so the
+                // window sums pair sums Q_j = bin[2j + o] + bin[2j + o + 1], j = k − (h + o)/2 .. + h − 1 (mod nwin):
+                // h adds per window instead of 2h (srt is free again and holds Q).
+                float2* qs = srt;
+                const int o = h & 1;
+                for (int j = lane; j < nwin; j += 32) {
+                    const float2 a = bsum[2 * j + o], b = bsum[(2 * j + o + 1) % nb];
+                    qs[j] = make_float2(a.x + b.x, a.y + b.y);
+                }
+                __syncwarp();
                 for (int kw = lane; kw < nwin; kw += 32) {
                     float ax = 0.f, ay = 0.f;
-                    int i = 2 * kw - h;
-                    if (i < 0) i += nb;
-                    for (int q = 0; q < 2 * h; ++q) {
-                        const float2 v = bsum[i];
+                    int i = kw - (h + o) / 2;
+                    if (i < 0) i += nwin;
+                    for (int q = 0; q < h; ++q) {
+                        const float2 v = qs[i];
                         ax += v.x;
                         ay += v.y;
-                        if (++i == nb) i = 0;
+                        if (++i == nwin) i = 0;
                     }
                     const float m = ax * ax + ay * ay;
                     if (m > best) {
