@@ -355,7 +355,9 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
 // sub-histogram with plain shared atomics (bins <= 1024; one shared histogram above), one global add per bin.
 // bin = min(floor(bins·|∇| / hmax), bins − 1) for |∇| > 0, IEEE sqrt and division (the same decision as before).
 // (Measured on B200, 256-image 1920x1200 step: a flattened interior index with an integer division per pixel and
-// __match_any_sync aggregation took 4.1 ms.)
+// __match_any_sync aggregation took 4.1 ms; one sub-histogram per lane index interleaved [bin][32] — conflict-free
+// banks, but the same (bin, lane) counter shared by the CTA's 8 warps — 2.45 ms at 296 CTAs per image and 2.62 at
+// ~37, against 1.58 for these per-warp sub-histograms.)
 __global__ void __launch_bounds__(256) k_khist(const float* __restrict__ g2buf, size_t img_stride, Geom g, int bins,
                                                const unsigned* __restrict__ hmax_bits, int* __restrict__ hist) {
     KZ_PDL_PROLOGUE();
