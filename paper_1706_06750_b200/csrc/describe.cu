@@ -27,6 +27,29 @@ __constant__ float c_w2[16];  // exp(-((a-1.5)^2 + (b-1.5)^2) / (2 * 1.5^2)), in
 constexpr float kTwoPi = 6.283185307179586f;
 constexpr float kPi = 3.141592653589793f;
 
+// atan2 for the orientation BIN of a sample (|error| <= 1.1e-7 rad, like atan2f's 2 ulp; the final angle keeps
+// atan2f): octant reduction, a = min/max in [0, 1], atan(a) = a + a·s·p(s), s = a², p of degree 6 fitted to
+// minimise the max fp32 error on [0, 1]; about half of atan2f's instructions.
+__device__ __forceinline__ float atan2_bin(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(mx));
+    const float a = mx > 0.f ? mn * r : 0.f;
+    const float q = a * a;
+    float p = -0.004355322103947401f;
+    p = fmaf(p, q, 0.023039856925606728f);
+    p = fmaf(p, q, -0.057773225009441376f);
+    p = fmaf(p, q, 0.09794210642576218f);
+    p = fmaf(p, q, -0.13976573944091797f);
+    p = fmaf(p, q, 0.19962702691555023f);
+    p = fmaf(p, q, -0.3333165943622589f);
+    float t = fmaf(a * q, p, a);
+    if (ay > ax) t = 1.5707963267948966f - t;
+    if (x < 0.f) t = 3.141592653589793f - t;
+    return y < 0.f ? -t : t;
+}
+
 // Bilinear (Lx, Ly) at (px, py) with clamped taps (A14, A16): four 8-byte loads of the interleaved plane.
 __device__ __forceinline__ float2 bilinear2(const float2* __restrict__ img, int W, int H, int P, float px, float py) {
     const float fx0 = floorf(px), fy0 = floorf(py);
@@ -134,7 +157,7 @@ __global__ void __launch_bounds__(256, 5) k_describe(const float2* __restrict__ 
                         const float2 gv = bilinear2(lxy, g.W, g.H, g.P, px, py);  // exact: the window is an argmax
                         rx = w * gv.x;
                         ry = w * gv.y;
-                        float ph = atan2f(ry, rx);
+                        float ph = atan2_bin(ry, rx);
                         if (ph < 0.f) ph += kTwoPi;
                         bb = min((int)(ph * fb), nb - 1);
                     }
