@@ -72,7 +72,8 @@ constexpr int kMaxBinWin = 48;  // binned orientation path: nwin % 6 == 0 and nw
 __global__ void __launch_bounds__(256, 5) k_describe(const float2* __restrict__ Lxy,
                                                   const cudaTextureObject_t* __restrict__ texs, size_t img_stride, Geom g, int nimg, kaze_keypoint* __restrict__ kps,
                                                   const int* __restrict__ counts, int cap, float* __restrict__ desc,
-                                                  int nwin, int keep_angle, int N, int lvl_lo, int lvl_hi) {
+                                                  int nwin, int keep_angle, int N, int lvl_lo, int lvl_hi,
+                                                  int* __restrict__ work) {
     KZ_PDL_PROLOGUE();
     __shared__ int pre[kMaxBatch + 1];
     __shared__ __align__(16) float sbuf[kWarps][kWarpBuf];
@@ -93,7 +94,17 @@ __global__ void __launch_bounds__(256, 5) k_describe(const float2* __restrict__ 
     // more L1 sharing, but the grid spread over every image and level at once — measured 48.8 vs 24.7 ms; 2 or 4
     // consecutive keypoints per warp per round 24.2 / 27.8 vs 23.5.)
     int img = 0;  // f only grows, so the image search resumes where the previous keypoint left it
-    for (int f = blockIdx.x * kWarps + warp; f < total; f += gridDim.x * kWarps) {
+    // Work distribution: with `work` (a zeroed device counter) each warp takes the next keypoint of the flat
+    // (image, level, y, x) list when it is free, so the grid still sweeps one narrow window of the list (planes
+    // stay L2-resident) and no warp idles while another finishes a static share; without it, a static stride.
+    const int stride = gridDim.x * kWarps;
+    auto next = [&](int cur) {
+        if (!work) return cur < 0 ? (int)(blockIdx.x * kWarps + warp) : cur + stride;
+        int v = 0;
+        if (lane == 0) v = atomicAdd(work, 1);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    for (int f = next(-1); f < total; f = next(f)) {
         while (img + 1 < nimg && pre[img + 1] <= f) ++img;
         const int k = f - pre[img];
         kaze_keypoint* kp = kps + (size_t)img * cap + k;
@@ -384,7 +395,7 @@ void init_describe_tables() {
 }
 
 void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t img_stride, Geom g, int nimg, int N,
-                     int lvl_lo, int lvl_hi, kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
+                     int lvl_lo, int lvl_hi, int* work, kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
                      cudaStream_t s) {
     // Persistent grid of exactly one wave: the CTAs that fit on every SM at once (registers limit it to 4 of 256
     // threads).  A grid larger than one wave leaves the surplus CTAs' share of the static keypoint stride to a
@@ -392,7 +403,7 @@ void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t 
     int per_sm = 0;  // (a per-device figure: cheap, and correct when contexts on other devices share the process)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_describe, 256, 0);
     const int grid = device_sm_count() * (per_sm > 0 ? per_sm : 1);
-    kz_launch(k_describe, dim3(grid), dim3(256), 0, s, Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N, lvl_lo, lvl_hi);
+    kz_launch(k_describe, dim3(grid), dim3(256), 0, s, Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N, lvl_lo, lvl_hi, work);
 }
 
 }  // namespace kz

@@ -70,6 +70,7 @@ struct kaze_ctx {
     int* hist = nullptr;
     int* fallback = nullptr;
     uint32_t* bitmap = nullptr;
+    int* work = nullptr;  // the descriptor pass's keypoint counter
     int* rowcnt = nullptr;
     int* rowoff = nullptr;
     // current build
@@ -288,7 +289,7 @@ kaze_status validate_params(const kaze_params* p) {
 
 void free_arena(kaze_ctx* c) {
     void* ptrs[] = {c->Lt, c->Lxy, c->Ldet, c->cbuf, c->ubuf, c->kval, c->hmax, c->hist, c->fallback,
-                    c->bitmap, c->rowcnt, c->rowoff, c->hin[0], c->hin[1], c->hkps[0], c->hkps[1],
+                    c->bitmap, c->rowcnt, c->rowoff, c->work, c->hin[0], c->hin[1], c->hkps[0], c->hkps[1],
                     c->hcnt[0], c->hcnt[1], c->hdesc[0], c->hdesc[1]};
     for (void* q : ptrs)
         if (q) cudaFree(q);
@@ -543,7 +544,9 @@ kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_coun
     {
         Launch L(c, KC_DESCRIBE, 0.0, s);
         const int lo = c->edge_derivs ? 0 : 1, hi = c->edge_derivs ? c->N - 1 : c->N - 2;  // sampleable levels
-        launch_describe(c->Lxy, texs, c->img_stride, c->geom, c->n, c->N, lo, hi, d_kps, d_counts, c->p.max_keypoints,
+        static const int dyn = tune_knob("KAZE_DESC_DYN", 1);
+        if (dyn) KZ_CUDA(c, cudaMemsetAsync(c->work, 0, sizeof(int), s));
+        launch_describe(c->Lxy, texs, c->img_stride, c->geom, c->n, c->N, lo, hi, dyn ? c->work : nullptr, d_kps, d_counts, c->p.max_keypoints,
                         d_desc, c->p.ori_windows, (c->p.flags & KAZE_FLAG_KEEP_ANGLE) ? 1 : 0, s);
     }
     KZ_CHECK_LAUNCH(c, "describe");
@@ -752,7 +755,8 @@ kaze_status kaze_create(const kaze_params* p, int device, kaze_ctx** out) {
               cudaMalloc(&c->fallback, sizeof(int) * B) == cudaSuccess &&
               cudaMalloc(&c->bitmap, sizeof(uint32_t) * rows * words) == cudaSuccess &&
               cudaMalloc(&c->rowcnt, sizeof(int) * rows) == cudaSuccess &&
-              cudaMalloc(&c->rowoff, sizeof(int) * rows) == cudaSuccess;
+              cudaMalloc(&c->rowoff, sizeof(int) * rows) == cudaSuccess &&
+              cudaMalloc(&c->work, sizeof(int)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_arena(c);
@@ -1099,7 +1103,7 @@ kaze_status kaze_memory_footprint(const kaze_ctx* c, kaze_memory* out) {
     out->response = plane * N * B;
     out->scratch = 2 * plane * B;
     out->detector = sizeof(float) * B + sizeof(unsigned) * B + sizeof(int) * B * c->p.k_bins + sizeof(int) * B +
-                    sizeof(uint32_t) * rows * nms_words(c->p.max_width) + 2 * sizeof(int) * rows;
+                    sizeof(uint32_t) * rows * nms_words(c->p.max_width) + 2 * sizeof(int) * rows + sizeof(int);
     out->textures = sizeof(cudaTextureObject_t) * B * N * (uint64_t)c->tex_tables.size();
     if (c->s_h2d) {
         out->host_path = 2 * (plane * B + sizeof(kaze_keypoint) * cap * B + sizeof(int) * B + sizeof(float) * 64 * cap * B);
