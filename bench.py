@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kaze", choices=["kaze", "reference"])
     ap.add_argument("--images", type=int, default=N_IMAGES)
-    ap.add_argument("--batch", type=int, default=16, help="images per launch (max_batch of the context); measured 1421/1536/1608/1651/1661/1627 img/s at 2/4/8/16/32/64")
+    ap.add_argument("--batch", type=int, default=32, help="images per launch (max_batch of the context); measured (r01) 1421/1536/1608/1651/1661/1627 img/s at 2/4/8/16/32/64, (r02, overlapped describe) 1703 at 16, 1719 at 32")
     ap.add_argument("--max-keypoints", type=int, default=32768)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
@@ -343,7 +343,7 @@ def main():
             "gpu_launches": launches * ws,
             "kernel_ms_per_step": step_kernel_ms,
             "ms_per_step_profiled": ms_profiled,
-            "timing": "value: CUDA-graph replays, no per-kernel events; kernels/roofline: a second pass of the same steps with CUDA events around every launch",
+            "timing": "value: CUDA-graph replays of each step (the chunks' descriptor passes overlap the next chunk's scale space on a second stream), no per-kernel events; kernels/roofline: a second pass of the same steps, chunks one after the other, with CUDA events around every launch",
             "kernels": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                             "gbs": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] > 0 else None}
                         for k, v in prof.items()},

@@ -395,13 +395,17 @@ void init_describe_tables() {
 }
 
 void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t img_stride, Geom g, int nimg, int N,
-                     int lvl_lo, int lvl_hi, int* work, kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
+                     int lvl_lo, int lvl_hi, int* work, int overlapped, kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
                      cudaStream_t s) {
     // Persistent grid of exactly one wave: the CTAs that fit on every SM at once (registers limit it to 4 of 256
     // threads).  A grid larger than one wave leaves the surplus CTAs' share of the static keypoint stride to a
     // second, mostly idle wave (measured: 148·5 CTAs = 1.25 waves).
     int per_sm = 0;  // (a per-device figure: cheap, and correct when contexts on other devices share the process)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_describe, 256, 0);
+    // Overlapped with the next chunk's scale space, a smaller persistent grid (3 CTAs per SM) leaves the SMs room for
+    // those passes' CTAs (256-image step, 32 per launch: 149.0 vs 149.6 ms at the full 5); KAZE_DESC_OCC overrides.
+    static const int occ = tune_knob("KAZE_DESC_OCC", 3);
+    if (overlapped && occ > 0 && per_sm > occ) per_sm = occ;
     const int grid = device_sm_count() * (per_sm > 0 ? per_sm : 1);
     kz_launch(k_describe, dim3(grid), dim3(256), 0, s, Lxy, texs, img_stride, g, nimg, kps, counts, cap, desc, nwin, keep_angle, N, lvl_lo, lvl_hi, work);
 }

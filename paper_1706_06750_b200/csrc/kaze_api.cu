@@ -121,6 +121,10 @@ struct kaze_ctx {
     std::vector<GraphKey> seen;
     uint64_t tick = 0;
     cudaStream_t s_cap = nullptr;
+    // overlapped multi-chunk extraction: the descriptor pass of chunk j on a side stream, concurrent with the
+    // scale space of chunk j+1 (s_side for direct runs, s_cap2 inside captures); per-chunk events
+    cudaStream_t s_side = nullptr, s_cap2 = nullptr;
+    std::vector<cudaEvent_t> ovl_ev;
     std::vector<ProfRec> recs;
     std::vector<cudaEvent_t> pool;
     int64_t launches = 0;
@@ -537,7 +541,8 @@ kaze_status ensure_textures(kaze_ctx* c, const cudaTextureObject_t** out) {
 }
 
 // Step 3.
-kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_counts, float* d_desc, cudaStream_t s) {
+kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_counts, float* d_desc, cudaStream_t s,
+                        bool overlapped = false) {
     const cudaTextureObject_t* texs = nullptr;
     kaze_status st = ensure_textures(c, &texs);
     if (st != KAZE_OK) return st;
@@ -546,7 +551,8 @@ kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_coun
         const int lo = c->edge_derivs ? 0 : 1, hi = c->edge_derivs ? c->N - 1 : c->N - 2;  // sampleable levels
         static const int dyn = tune_knob("KAZE_DESC_DYN", 1);
         if (dyn) KZ_CUDA(c, cudaMemsetAsync(c->work, 0, sizeof(int), s));
-        launch_describe(c->Lxy, texs, c->img_stride, c->geom, c->n, c->N, lo, hi, dyn ? c->work : nullptr, d_kps, d_counts, c->p.max_keypoints,
+        launch_describe(c->Lxy, texs, c->img_stride, c->geom, c->n, c->N, lo, hi, dyn ? c->work : nullptr,
+                        overlapped ? 1 : 0, d_kps, d_counts, c->p.max_keypoints,
                         d_desc, c->p.ori_windows, (c->p.flags & KAZE_FLAG_KEEP_ANGLE) ? 1 : 0, s);
     }
     KZ_CHECK_LAUNCH(c, "describe");
@@ -648,6 +654,108 @@ void drop_graphs_of_size(kaze_ctx* c, int w, int h) {
         if (c->seen[i].w == w && c->seen[i].h == h) c->seen.erase(c->seen.begin() + (long)i);
         else ++i;
     }
+}
+
+// Several chunks with the descriptor pass overlapped: describe(j) runs on `side` while build(j+1) runs on `main`;
+// detect(j+1) rewrites the Lxy pyramid that describe(j) samples, so it waits for describe(j).  Every other buffer a
+// describe reads (keypoints, counts of its own chunk, the texture table) is untouched by the next chunk.  The
+// describe pass is gather/TEX-bound while the scale-space passes are L1/latency-bound, so they share the SMs.
+kaze_status run_chunks_overlapped(kaze_ctx* c, const float* img, int n, int w, int h, int64_t pitch,
+                                  kaze_keypoint* kps, int32_t* cnt, float* desc, cudaStream_t main_s,
+                                  cudaStream_t side_s) {
+    const int B = c->p.max_batch;
+    const size_t cap = (size_t)c->p.max_keypoints;
+    const int nch = (n + B - 1) / B;
+    while ((int)c->ovl_ev.size() < 2 * nch) {
+        cudaEvent_t e;
+        KZ_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ovl_ev.push_back(e);
+    }
+    for (int j = 0; j < nch; ++j) {
+        const int i0 = j * B, m = std::min(B, n - i0);
+        kaze_status st = do_build(c, img + (size_t)i0 * pitch * h, m, w, h, pitch, main_s);
+        if (st != KAZE_OK) return st;
+        if (j > 0) KZ_CUDA(c, cudaStreamWaitEvent(main_s, c->ovl_ev[2 * (j - 1) + 1], 0));
+        st = do_detect(c, kps + (size_t)i0 * cap, cnt + i0, main_s);
+        if (st != KAZE_OK) return st;
+        KZ_CUDA(c, cudaEventRecord(c->ovl_ev[2 * j], main_s));
+        KZ_CUDA(c, cudaStreamWaitEvent(side_s, c->ovl_ev[2 * j], 0));
+        st = do_describe(c, kps + (size_t)i0 * cap, cnt + i0, desc + (size_t)i0 * cap * 64, side_s, true);
+        if (st != KAZE_OK) return st;
+        KZ_CUDA(c, cudaEventRecord(c->ovl_ev[2 * j + 1], side_s));
+    }
+    KZ_CUDA(c, cudaStreamWaitEvent(main_s, c->ovl_ev[2 * (nch - 1) + 1], 0));
+    c->last_stream = main_s;
+    return KAZE_OK;
+}
+
+// The whole call (n > max_batch) as one overlapped CUDA graph, by the same first-direct / second-capture /
+// then-replay rule as run_chunk (the key's n > max_batch keeps it apart from the chunk graphs).
+kaze_status run_overlapped(kaze_ctx* c, const float* img, int n, int w, int h, int64_t pitch, kaze_keypoint* kps,
+                           int32_t* cnt, float* desc, cudaStream_t s) {
+    if (!c->s_side) KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_side, cudaStreamNonBlocking));
+    const kaze_ctx::GraphKey key{img, kps, cnt, desc, n, w, h, pitch, s};
+    for (auto& ge : c->graphs)
+        if (ge.key == key) {
+            set_geometry(c, std::min(c->p.max_batch, n - (n - 1) / c->p.max_batch * c->p.max_batch), w, h);
+            KZ_CUDA(c, cudaGraphLaunch(ge.exec, s));
+            c->launches += ge.nk;
+            ge.used = ++c->tick;
+            c->built = c->detected = true;
+            c->last_stream = s;
+            return KAZE_OK;
+        }
+    bool again = false;
+    for (auto& k : c->seen) again |= (k == key);
+    if (!again || (c->p.flags & KAZE_FLAG_NO_GRAPHS)) {
+        if (!again) {
+            if (c->seen.size() >= 4 * kMaxGraphs) c->seen.erase(c->seen.begin());
+            c->seen.push_back(key);
+        }
+        return run_chunks_overlapped(c, img, n, w, h, pitch, kps, cnt, desc, s, c->s_side);
+    }
+    if (!c->s_cap) KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking));
+    if (!c->s_cap2) KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_cap2, cudaStreamNonBlocking));
+    set_geometry(c, c->p.max_batch, w, h);
+    const cudaTextureObject_t* texs = nullptr;
+    kaze_status st = ensure_textures(c, &texs);  // host-side setup before the capture
+    if (st != KAZE_OK) return st;
+    const int64_t l0 = c->launches;
+    KZ_CUDA(c, cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal));
+    pdl_set_capturing(true);
+    st = run_chunks_overlapped(c, img, n, w, h, pitch, kps, cnt, desc, c->s_cap, c->s_cap2);
+    pdl_set_capturing(false);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->s_cap, &graph);
+    if (st != KAZE_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (ec != cudaSuccess) {
+        c->err = std::string("graph capture: ") + cudaGetErrorString(ec);
+        return KAZE_ERR_CUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        c->err = std::string("graph instantiate: ") + cudaGetErrorString(ei);
+        return KAZE_ERR_CUDA;
+    }
+    const int64_t nk = c->launches - l0;
+    c->launches = l0;
+    if (c->graphs.size() >= kMaxGraphs) {
+        auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                    [](const auto& a, const auto& b) { return a.used < b.used; });
+        cudaGraphExecDestroy(lru->exec);
+        c->graphs.erase(lru);
+    }
+    c->graphs.push_back({key, exec, nk, ++c->tick});
+    KZ_CUDA(c, cudaGraphLaunch(exec, s));
+    c->launches += nk;
+    c->built = c->detected = true;
+    c->last_stream = s;
+    return KAZE_OK;
 }
 
 kaze_status check_dims(const kaze_ctx* c, int n, int w, int h, int64_t pitch) {
@@ -792,6 +900,9 @@ kaze_status kaze_destroy(kaze_ctx* c) {
         if (c->ev_d2h[b]) cudaEventDestroy(c->ev_d2h[b]);
     }
     for (auto& ge : c->graphs) cudaGraphExecDestroy(ge.exec);
+    for (auto e : c->ovl_ev) cudaEventDestroy(e);
+    if (c->s_side) cudaStreamDestroy(c->s_side);
+    if (c->s_cap2) cudaStreamDestroy(c->s_cap2);
     if (c->s_cap) cudaStreamDestroy(c->s_cap);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
@@ -832,6 +943,11 @@ kaze_status kaze_extract(kaze_ctx* c, const float* d_imgs, int32_t n, int32_t w,
     DeviceGuard guard(c->device);
     cudaStream_t s = (cudaStream_t)stream;
     const size_t cap = (size_t)c->p.max_keypoints;
+    // several chunks: the descriptor pass of each chunk overlaps the next chunk's scale space (KAZE_OVERLAP=0: one
+    // chunk after the other); profiling keeps the sequential direct launches so per-kernel times stay separable
+    static const int overlap = tune_knob("KAZE_OVERLAP", 1);
+    if (overlap && n > c->p.max_batch && !c->prof)
+        return run_overlapped(c, d_imgs, n, w, h, pitch, d_kps, d_counts, d_desc, s);
     for (int i0 = 0; i0 < n; i0 += c->p.max_batch) {
         const int m = n - i0 < c->p.max_batch ? n - i0 : c->p.max_batch;
         st = run_chunk(c, d_imgs + (size_t)i0 * pitch * h, m, w, h, pitch, d_kps + i0 * cap, d_counts + i0,

@@ -149,9 +149,10 @@ void launch_kp_emit(const float* Ldet, size_t img_stride, Geom g, int nimg, cons
 void init_describe_tables();
 // texs: [nimg][N] texture objects over the Lxy planes (linear filtering, clamp) for the M-SURF samples.
 // Keypoints whose level lies outside [lvl_lo, lvl_hi] get a zero descriptor, angle 0 and flags = 1.
-// work: a device counter zeroed before the launch (dynamic keypoint distribution), or nullptr (static stride).
+// work: a device counter zeroed before the launch (dynamic keypoint distribution), or nullptr (static stride);
+// overlapped: the pass shares the GPU with the next chunk's scale space (smaller persistent grid).
 void launch_describe(const float2* Lxy, const cudaTextureObject_t* texs, size_t img_stride, Geom g, int nimg, int N,
-                     int lvl_lo, int lvl_hi, int* work, kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
+                     int lvl_lo, int lvl_hi, int* work, int overlapped, kaze_keypoint* kps, const int* counts, int cap, float* desc, int nwin, int keep_angle,
                      cudaStream_t s);
 
 __host__ __device__ inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

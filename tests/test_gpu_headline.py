@@ -1,11 +1,11 @@
 """GPU-vs-oracle parity at the instantiations the headline bench runs, and the paths round 1 left untested (needs a
 B200).  Every call goes through the C ABI (ctypes -> libkaze_b200.so).
 
-* 1920x1200 scale space in the bench launch configuration (16 images per launch, kaze_extract replaying the chunk
+* 1920x1200 scale space in the bench launch configuration (32 images per launch, kaze_extract replaying the chunk
   as a CUDA graph, k estimated on the device), AOS and FED: every level of the first and last image within 1e-4
   relative of the oracle's fp64 levels, run with the GPU's k (itself in the oracle's histogram bin);
-  this is the only configuration that instantiates k_aos_cols_u<8,20,512,2> (1024 < H <= 1280) and
-  k_aos_rows_cta<15,4> (1792 < W <= 1920).
+  this is the only configuration that instantiates the TMA-staged column pass k_aos_cols_tma<8,19,512,2>
+  (832 < H <= 1216 with the 1088 < H rung) and k_aos_rows_cta<15,4> (1792 < W <= 1920).
 * Hessian stage-isolated at 1920x1200, O = S = 4 (steps 2, 3, 4, 5, 6, 8, 9, 11, 13, 15, 18, 22: both column-block
   widths of the fused kernel), and at O = 5 (steps up to 43: the two-pass form for s > 32).
 * The generic prefilter (σ0 = 1.2 and 2.5; σ0 = 1.6 takes the radius-5 kernel) and the g1 diffusivity (Eq. 3).
@@ -40,15 +40,15 @@ def O(oracle_lib):
 @pytest.mark.slow
 @pytest.mark.parametrize("scheme", [0, 1])
 def test_levels_1920x1200_in_bench_launch_configuration(O, scheme):
-    imgs = kaze_inputs.synth_batch(16, 1920, 1200, distinct=2)
-    kz = make(1920, 1200, batch=16, max_keypoints=32768, scheme=scheme)
+    imgs = kaze_inputs.synth_batch(32, 1920, 1200, distinct=2)
+    kz = make(1920, 1200, batch=32, max_keypoints=32768, scheme=scheme)
     dimg = torch.from_numpy(imgs).cuda()
-    out = kz.alloc_outputs(16)
+    out = kz.alloc_outputs(32)
     for _ in range(3):  # direct, captured, replayed: the levels read below come from the graph replay
         K.kaze_extract(kz.ctx, dimg, *out)
     torch.cuda.synchronize()
-    kg, fb = K.kaze_get_k(kz.ctx, 16)
-    for i in (0, 15):
+    kg, fb = K.kaze_get_k(kz.ctx, 32)
+    for i in (0, 31):
         # k: the device histogram picks the oracle's bin (k = hmax (b+1)/300, hmax differs by fp32 rounding)
         L0 = O.gaussian_blur(imgs[i].astype(np.float64), 1.6)
         kref, _, _ = O.contrast_k(L0)
@@ -88,20 +88,20 @@ def _hessian_stage_isolated(O, kz, imgs_idx, levels, st, n_levels):
 
 @pytest.mark.slow
 def test_hessian_stage_isolated_1920x1200_all_steps(O):
-    """The fused Hessian in the bench configuration (batch of 16, every level of two images injected from the
+    """The fused Hessian in the bench configuration (batch of 32, every level of two images injected from the
     oracle): steps 2..22 cover both column-block widths (224 for s <= 16, 192 above) and every template case the
     headline instantiates; Lx, Ly < 1e-5 and Ldet < 1e-4 relative per level; the keypoints of image 0 equal the
     oracle's extrema of the GPU's own Ldet."""
-    imgs = kaze_inputs.synth_batch(16, 1920, 1200, distinct=2)
+    imgs = kaze_inputs.synth_batch(32, 1920, 1200, distinct=2)
     sg, _, st = O.schedule(4, 4, 1.6)
     assert sorted(set(st.tolist())) == [2, 3, 4, 5, 6, 8, 9, 11, 13, 15, 18, 22]
-    kz = make(1920, 1200, batch=16, max_keypoints=32768, flags=K.FLAG_ALL_DERIVATIVES)
-    kz.batch = 16
+    kz = make(1920, 1200, batch=32, max_keypoints=32768, flags=K.FLAG_ALL_DERIVATIVES)
+    kz.batch = 32
     dimg = torch.from_numpy(imgs).cuda()
-    out = kz.alloc_outputs(16)
-    K.kaze_extract(kz.ctx, dimg, *out)  # builds all 16 images (the chunk geometry the bench uses)
-    levels = [O.scale_space(imgs[i], k_override=0.033)[0] for i in (0, 15)]
-    kps, counts, _ = _hessian_stage_isolated(O, kz, (0, 15), levels, st, 16)
+    out = kz.alloc_outputs(32)
+    K.kaze_extract(kz.ctx, dimg, *out)  # builds all 32 images (the chunk geometry the bench uses)
+    levels = [O.scale_space(imgs[i], k_override=0.033)[0] for i in (0, 31)]
+    kps, counts, _ = _hessian_stage_isolated(O, kz, (0, 31), levels, st, 16)
     Ld = gpu_levels(kz, 16, K.PLANE_LDET, img=0)
     kref, nref = O.extrema(Ld, 4, sg)
     got = K.Kaze.keypoints_numpy(kps, counts)[0]

@@ -449,20 +449,22 @@ def test_memory_footprint_accounts_for_the_arena():
 # ------------------------------------------------------------------------------------------- full sizes
 @pytest.mark.slow
 def test_full_size_1920x1200_in_bench_launch_configuration(O):
-    """BASELINE configs[2]/[4] size, in the launch configuration bench.py times (16 images per launch, 32768-keypoint
-    capacity, kaze_extract replaying the chunk as a CUDA graph on its third call): the first and the last image of
-    the batch against the full oracle."""
-    imgs = kaze_inputs.synth_batch(16, 1920, 1200, distinct=2)
-    kz = make(1920, 1200, batch=16, max_keypoints=32768)
+    """BASELINE configs[2]/[4] size, in the launch configuration bench.py times (32 images per launch, 32768-keypoint
+    capacity, several chunks per call: the whole call replays as one CUDA graph from its third call, each chunk's
+    descriptor pass overlapping the next chunk's scale space on a second stream): 48 images (a full chunk and a
+    16-image one), the first and the last image against the full oracle."""
+    imgs = kaze_inputs.synth_batch(48, 1920, 1200, distinct=2)
+    kz = make(1920, 1200, batch=32, max_keypoints=32768)
     dimg = torch.from_numpy(imgs).cuda()
-    out = kz.alloc_outputs(16)
+    out = kz.alloc_outputs(48)
     for _ in range(3):  # direct, captured, replayed
         K.kaze_extract(kz.ctx, dimg, *out)
     kps, counts, desc = out
-    k, _ = K.kaze_get_k(kz.ctx, 16)  # the last chunk is the whole batch here
-    for i in (0, 15):
+    k, _ = K.kaze_get_k(kz.ctx, 16)  # the last chunk: images 32..47
+    for i in (0, 47):
         ref = O.run(imgs[i], cap=1 << 17)
-        assert abs(k[i] / ref["k"] - 1) < 1e-5
+        if i >= 32:
+            assert abs(k[i - 32] / ref["k"] - 1) < 1e-5
         got = K.Kaze.keypoints_numpy(kps, counts)[i]
         f1, idx = match_keypoints(ref["kps"], got)
         f2, _ = match_keypoints(got, ref["kps"])
@@ -474,6 +476,7 @@ def test_full_size_1920x1200_in_bench_launch_configuration(O):
         assert np.mean(cos >= 0.999) >= 0.99, (i, np.mean(cos >= 0.999))
     # images 2.. are shifted/flipped copies of 0 and 1: same keypoint counts up to border effects
     assert abs(int(counts[2]) - int(counts[0])) < 0.05 * int(counts[0])
+    assert abs(int(counts[34]) - int(counts[0])) < 0.05 * int(counts[0])
     kz.close()
 
 
@@ -567,17 +570,17 @@ def test_fed_keypoints_and_descriptors_end_to_end(O):
 @pytest.mark.slow
 @pytest.mark.parametrize("mode", ["fed", "exact", "refine3d"])
 def test_f_rows_at_full_size_in_bench_launch_configuration(O, mode):
-    """SURVEY §8 f1/f2 at BASELINE configs[2] size in the bench's launch configuration (16 images per launch, graph
+    """SURVEY §8 f1/f2 at BASELINE configs[2] size in the bench's launch configuration (32 images per launch, graph
     replay): the FED backend and the two detector variants, image 0 of the batch against the full fp64 oracle
     (>= 99% of keypoints both ways, >= 99% of matched descriptors with cos >= 0.999)."""
     kw, gk = {"fed": ({"scheme": 1}, {"scheme": K.SCHEME_FED}),
               "exact": ({"exact_window": 1}, {"flags": K.FLAG_EXACT_WINDOW}),
               "refine3d": ({"refine3d": 1}, {"flags": K.FLAG_REFINE_3D})}[mode]
-    imgs = kaze_inputs.synth_batch(16, 1920, 1200, distinct=2)
+    imgs = kaze_inputs.synth_batch(32, 1920, 1200, distinct=2)
     ref = O.run(imgs[0], cap=1 << 17, **kw)
-    kz = make(1920, 1200, batch=16, max_keypoints=32768, **gk)
+    kz = make(1920, 1200, batch=32, max_keypoints=32768, **gk)
     dimg = torch.from_numpy(imgs).cuda()
-    out = kz.alloc_outputs(16)
+    out = kz.alloc_outputs(32)
     for _ in range(3):
         K.kaze_extract(kz.ctx, dimg, *out)
     kps, counts, desc = out
