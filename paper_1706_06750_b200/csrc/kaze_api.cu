@@ -106,9 +106,10 @@ struct kaze_ctx {
         int n, w, h;
         int64_t pitch;
         cudaStream_t s;
+        int part = 7;  // steps captured: 1 build, 2 detect, 4 describe
         bool operator==(const GraphKey& o) const {
             return img == o.img && kps == o.kps && cnt == o.cnt && desc == o.desc && n == o.n && w == o.w &&
-                   h == o.h && pitch == o.pitch && s == o.s;
+                   h == o.h && pitch == o.pitch && s == o.s && part == o.part;
         }
     };
     struct GraphEntry {
@@ -566,19 +567,24 @@ kaze_status do_describe(kaze_ctx* c, kaze_keypoint* d_kps, const int32_t* d_coun
 // replayed on the caller's stream.  Graphs are per key (pointers, sizes, stream); at most kMaxGraphs are kept.
 constexpr size_t kMaxGraphs = 96;
 
+// `part` selects the steps (1 build, 2 detect, 4 describe; the describe of an overlapped schedule passes 8 too, for
+// the smaller persistent grid).
 kaze_status run_chunk_direct(kaze_ctx* c, const float* img, int m, int w, int h, int64_t pitch, kaze_keypoint* kps,
-                             int32_t* cnt, float* desc, cudaStream_t s) {
-    kaze_status st = do_build(c, img, m, w, h, pitch, s);
+                             int32_t* cnt, float* desc, cudaStream_t s, int part = 7) {
+    kaze_status st = KAZE_OK;
+    if (part & 1) st = do_build(c, img, m, w, h, pitch, s);
     if (st != KAZE_OK) return st;
-    st = do_detect(c, kps, cnt, s);
+    if (part & 2) st = do_detect(c, kps, cnt, s);
     if (st != KAZE_OK) return st;
-    return do_describe(c, kps, cnt, desc, s);
+    if (part & 4) st = do_describe(c, kps, cnt, desc, s, (part & 8) != 0);
+    return st;
 }
 
 kaze_status run_chunk(kaze_ctx* c, const float* img, int m, int w, int h, int64_t pitch, kaze_keypoint* kps,
-                      int32_t* cnt, float* desc, cudaStream_t s) {
-    if (c->prof || (c->p.flags & KAZE_FLAG_NO_GRAPHS)) return run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, s);
-    const kaze_ctx::GraphKey key{img, kps, cnt, desc, m, w, h, pitch, s};
+                      int32_t* cnt, float* desc, cudaStream_t s, int part = 7) {
+    if (c->prof || (c->p.flags & KAZE_FLAG_NO_GRAPHS))
+        return run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, s, part);
+    const kaze_ctx::GraphKey key{img, kps, cnt, desc, m, w, h, pitch, s, part};
     for (auto& ge : c->graphs)
         if (ge.key == key) {
             set_geometry(c, m, w, h);
@@ -594,7 +600,7 @@ kaze_status run_chunk(kaze_ctx* c, const float* img, int m, int w, int h, int64_
     if (!again) {
         if (c->seen.size() >= 4 * kMaxGraphs) c->seen.erase(c->seen.begin());
         c->seen.push_back(key);
-        return run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, s);
+        return run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, s, part);
     }
     if (!c->s_cap) KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking));
     set_geometry(c, m, w, h);
@@ -606,7 +612,7 @@ kaze_status run_chunk(kaze_ctx* c, const float* img, int m, int w, int h, int64_
     const int64_t l0 = c->launches;
     KZ_CUDA(c, cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal));
     pdl_set_capturing(true);
-    st = run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, c->s_cap);
+    st = run_chunk_direct(c, img, m, w, h, pitch, kps, cnt, desc, c->s_cap, part);
     pdl_set_capturing(false);
     cudaGraph_t graph = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(c->s_cap, &graph);
@@ -987,10 +993,22 @@ kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32
     };
     std::vector<int> tmarks;
     const int t0mark = mark(s);
+    // Overlap (as kaze_extract, KAZE_OVERLAP): chunk j's describe runs on the side stream while chunk j+1's scale
+    // space runs on s; detect(j+1) waits for describe(j) (Lxy), and chunk j's keypoint/descriptor copies for its
+    // describe (ev_desc[b]).  The parts run as separate graphs (keyed by part).
+    static const int overlap = tune_knob("KAZE_OVERLAP", 1);
+    const bool ovl = overlap && nchunks > 1 && !c->prof;
+    if (ovl && !c->s_side) KZ_CUDA(c, cudaStreamCreateWithFlags(&c->s_side, cudaStreamNonBlocking));
+    while (ovl && (int)c->ovl_ev.size() < 4) {
+        cudaEvent_t e;
+        KZ_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ovl_ev.push_back(e);
+    }
+    // ovl_ev[b]: describe of the chunk in buffer b done; ovl_ev[2 + b]: its detect done
     auto finalize = [&](int j) -> kaze_status {
         const int b = j & 1, i0 = j * B, m = (n - i0 < B) ? n - i0 : B;
         KZ_CUDA(c, cudaEventSynchronize(c->ev_cnt[b]));
-        KZ_CUDA(c, cudaStreamWaitEvent(c->s_d2h, c->ev_cnt[b], 0));
+        KZ_CUDA(c, cudaStreamWaitEvent(c->s_d2h, ovl ? c->ovl_ev[b] : c->ev_cnt[b], 0));
         tmarks.push_back(mark(c->s_d2h));
         const int* cnt = c->pinned_counts + b * B;
         for (int i = 0; i < m; ++i) {
@@ -1024,10 +1042,24 @@ kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32
         if (j >= 2) KZ_CUDA(c, cudaStreamWaitEvent(s, c->ev_d2h[b], 0));
         tmarks.push_back(mark(c->s_h2d));
         tmarks.push_back(mark(s));
-        st = run_chunk(c, c->hin[b], m, w, h, P, c->hkps[b], c->hcnt[b], c->hdesc[b], s);
+        if (ovl) {
+            st = run_chunk(c, c->hin[b], m, w, h, P, c->hkps[b], c->hcnt[b], c->hdesc[b], s, 1);
+            if (st != KAZE_OK) return st;
+            KZ_CUDA(c, cudaEventRecord(c->ev_comp[b], s));  // input buffer b is free once the build is done
+            if (j >= 1) KZ_CUDA(c, cudaStreamWaitEvent(s, c->ovl_ev[b ^ 1], 0));  // describe(j-1) done with Lxy
+            st = run_chunk(c, c->hin[b], m, w, h, P, c->hkps[b], c->hcnt[b], c->hdesc[b], s, 2);
+            if (st != KAZE_OK) return st;
+            KZ_CUDA(c, cudaEventRecord(c->ovl_ev[2 + b], s));
+            KZ_CUDA(c, cudaStreamWaitEvent(c->s_side, c->ovl_ev[2 + b], 0));
+            st = run_chunk(c, c->hin[b], m, w, h, P, c->hkps[b], c->hcnt[b], c->hdesc[b], c->s_side, 4 | 8);
+            if (st != KAZE_OK) return st;
+            KZ_CUDA(c, cudaEventRecord(c->ovl_ev[b], c->s_side));
+        } else {
+            st = run_chunk(c, c->hin[b], m, w, h, P, c->hkps[b], c->hcnt[b], c->hdesc[b], s);
+            if (st != KAZE_OK) return st;
+            KZ_CUDA(c, cudaEventRecord(c->ev_comp[b], s));  // input buffer b is free once the chunk is done
+        }
         tmarks.push_back(mark(s));
-        if (st != KAZE_OK) return st;
-        KZ_CUDA(c, cudaEventRecord(c->ev_comp[b], s));  // input buffer b is free once the chunk is done
         KZ_CUDA(c, cudaMemcpyAsync(c->pinned_counts + b * B, c->hcnt[b], sizeof(int) * m, cudaMemcpyDeviceToHost, s));
         KZ_CUDA(c, cudaEventRecord(c->ev_cnt[b], s));
         // (the D2H stream waits for this chunk inside finalize(j), right before its copies: a wait enqueued here
@@ -1039,6 +1071,7 @@ kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32
     }
     st = finalize(nchunks - 1);
     if (st != KAZE_OK) return st;
+    if (ovl) KZ_CUDA(c, cudaStreamWaitEvent(s, c->ovl_ev[(nchunks - 1) & 1], 0));  // s ends after the last describe
     KZ_CUDA(c, cudaStreamSynchronize(c->s_d2h));
     if (trace) {
         cudaDeviceSynchronize();

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """profiles/ncu_summary.json from one round's `ncu --set full` captures (scripts/profile_round.sh): per kaze
 profile class (kaze_get_profile names), DRAM bytes per launch = dram__bytes_read.sum + dram__bytes_write.sum of
-the captured launch (16 images of 1920x1200 per launch, bench launch configuration; ncu flushes caches between
+the captured launch (32 images of 1920x1200 per launch, bench launch configuration; ncu flushes caches between
 replays, so this is cold-cache traffic).  'hessian' is one kaze launch unit = the mean of hess_first and hess_det
 (kaze_get_profile counts the pair as two launches).  bench.py reads it for roofline.traffic.
 
@@ -37,7 +37,7 @@ def main():
         res["hessian"] = {"dram_bytes_per_launch": 0.5 * (a["dram_read"] + a["dram_write"] + b["dram_read"] + b["dram_write"]),
                           "time_us": 0.5 * (a["time"] + b["time"]),
                           "note": "mean of hess_first and hess_det (16 levels x 8 images each)"}
-    out = {"about": "ncu --set full --clock-control none, one launch per kernel (16 images of 1920x1200 per launch, "
+    out = {"about": "ncu --set full --clock-control none, one launch per kernel (32 images of 1920x1200 per launch, "
                     "cold cache between replays); dram_bytes_per_launch = dram__bytes_read.sum + "
                     f"dram__bytes_write.sum. Source: profiles/{tag}/ncu_full_summary.txt", "kernels": res}
     json.dump(out, open("profiles/ncu_summary.json", "w"), indent=1)
