@@ -151,22 +151,25 @@ kaze_status kaze_describe(kaze_ctx* ctx, kaze_keypoint* d_kps, const int32_t* d_
                           void* stream);
 
 /* Convenience: build + detect + describe for n images (any n >= 0; processed in chunks of
- * max_batch).  Outputs are indexed by image as in kaze_detect / kaze_describe.  Unless
- * KAZE_FLAG_NO_GRAPHS is set (or profiling is on), a chunk whose (d_imgs, d_kps, d_counts, d_desc
- * offsets, n, w, h, pitch, stream) key has been seen twice is replayed as one CUDA graph captured on
- * a context-private stream (the graph bakes in those pointers; up to 96 keys are cached, least
- * recently used evicted); results are bit-identical to direct launches.  The call is asynchronous on
- * `stream` like the stage entry points.  Errors: as the stage entry points, plus CUDA for a failed
- * capture or instantiation. */
+ * max_batch).  Outputs are indexed by image as in kaze_detect / kaze_describe.  With more than one
+ * chunk, each chunk's describe runs on a context-private side stream concurrently with the next
+ * chunk's build (the next detect waits for it); the call still completes in `stream` order.  Unless
+ * KAZE_FLAG_NO_GRAPHS is set (or profiling is on, which also runs the chunks one after the other), a
+ * call whose (d_imgs, d_kps, d_counts, d_desc, n, w, h, pitch, stream) key has been seen twice is
+ * replayed as one CUDA graph captured on context-private streams (the graph bakes in those pointers;
+ * up to 96 keys are cached, least recently used evicted); results are bit-identical to direct
+ * launches.  The call is asynchronous on `stream` like the stage entry points.  Errors: as the stage
+ * entry points, plus CUDA for a failed capture or instantiation. */
 kaze_status kaze_extract(kaze_ctx* ctx, const float* d_imgs, int32_t n, int32_t w, int32_t h,
                          int64_t pitch_elems, kaze_keypoint* d_kps, int32_t* d_counts, float* d_desc,
                          void* stream);
 
 /* End-to-end from HOST buffers: h_imgs[n][h][pitch] → h_kps[n][max_keypoints], h_counts[n],
  * h_desc[n][max_keypoints][64] (h_desc may be NULL to skip descriptor download).  Copies run on
- * context-owned streams overlapped with compute (double-buffered chunks of max_batch images); the
- * call returns after everything has landed in host memory.  `stream` orders the work after prior
- * work on it.  Errors: as kaze_extract. */
+ * context-owned streams overlapped with compute (double-buffered chunks of at most max_batch images;
+ * with more than one chunk the first holds max_batch/4 images, so the upload nothing can overlap is
+ * short; describes overlap the next chunk as in kaze_extract); the call returns after everything has
+ * landed in host memory.  `stream` orders the work after prior work on it.  Errors: as kaze_extract. */
 kaze_status kaze_extract_host(kaze_ctx* ctx, const float* h_imgs, int32_t n, int32_t w, int32_t h,
                               int64_t pitch_elems, kaze_keypoint* h_kps, int32_t* h_counts, float* h_desc,
                               void* stream);

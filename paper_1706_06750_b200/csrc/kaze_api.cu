@@ -976,7 +976,15 @@ kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32
     const int B = c->p.max_batch;
     const size_t cap = (size_t)c->p.max_keypoints;
     const int P = round_up(w, 32);
-    const int nchunks = (n + B - 1) / B;
+    // Chunk boundaries: when there is more than one chunk, the first holds a quarter of max_batch, so the upload the
+    // first build must wait for (nothing overlaps it) is short; the others are full, the remainder last.
+    std::vector<int> cb{0};
+    if (n > B) {
+        const int first = std::max(1, B / 4);
+        cb.push_back(first);
+    }
+    while (cb.back() < n) cb.push_back(std::min(n, cb.back() + B));
+    const int nchunks = (int)cb.size() - 1;
     // Make the context's copy streams start after prior work on the caller's stream.
     KZ_CUDA(c, cudaEventRecord(c->ev_comp[0], s));
     KZ_CUDA(c, cudaStreamWaitEvent(c->s_h2d, c->ev_comp[0], 0));
@@ -1006,7 +1014,7 @@ kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32
     }
     // ovl_ev[b]: describe of the chunk in buffer b done; ovl_ev[2 + b]: its detect done
     auto finalize = [&](int j) -> kaze_status {
-        const int b = j & 1, i0 = j * B, m = (n - i0 < B) ? n - i0 : B;
+        const int b = j & 1, i0 = cb[j], m = cb[j + 1] - cb[j];
         KZ_CUDA(c, cudaEventSynchronize(c->ev_cnt[b]));
         KZ_CUDA(c, cudaStreamWaitEvent(c->s_d2h, ovl ? c->ovl_ev[b] : c->ev_cnt[b], 0));
         tmarks.push_back(mark(c->s_d2h));
@@ -1026,7 +1034,7 @@ kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32
         return KAZE_OK;
     };
     for (int j = 0; j < nchunks; ++j) {
-        const int b = j & 1, i0 = j * B, m = (n - i0 < B) ? n - i0 : B;
+        const int b = j & 1, i0 = cb[j], m = cb[j + 1] - cb[j];
         // H2D of chunk j into buffer b, once the compute of chunk j-2 stopped reading it
         if (j >= 2) KZ_CUDA(c, cudaStreamWaitEvent(c->s_h2d, c->ev_comp[b], 0));
         tmarks.push_back(mark(c->s_h2d));

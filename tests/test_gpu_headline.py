@@ -257,3 +257,48 @@ def test_rot90_equivariance_on_the_gpu():
     assert np.mean(cos >= 0.999) >= 0.99, np.mean(cos >= 0.999)
     ka_.close()
     kb_.close()
+
+
+def test_overlapped_chunks_equal_sequential_chunks(tmp_path):
+    """kaze_extract / kaze_extract_host with several chunks overlap each chunk's describe with the next chunk's
+    build on a second stream (KAZE_OVERLAP, read once per process): the outputs equal those of a process that runs
+    the chunks one after the other, bit for bit, direct and graph-replayed."""
+    import os
+    import subprocess
+    import sys
+
+    imgs = kaze_inputs.synth_batch(5, 200, 150, first=11)
+    np.save(tmp_path / "imgs.npy", imgs)
+    script = (
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "import paper_1706_06750_b200 as K\n"
+        f"imgs = torch.from_numpy(np.load({str(tmp_path / 'imgs.npy')!r})).cuda()\n"
+        "kz = K.Kaze(200, 150, batch=2, octaves=3, sublevels=3, max_keypoints=2048)\n"
+        "out = kz.alloc_outputs(5)\n"
+        "for _ in range(3): K.kaze_extract(kz.ctx, imgs, *out)\n"
+        "torch.cuda.synchronize()\n"
+        f"np.savez({str(tmp_path / 'seq.npz')!r}, *[t.cpu().numpy() for t in out])\n"
+    )
+    env = dict(os.environ, KAZE_OVERLAP="0")
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    seq = np.load(tmp_path / "seq.npz")
+    kz = make(200, 150, batch=2, octaves=3, sublevels=3, max_keypoints=2048)
+    out = kz.alloc_outputs(5)
+    dimg = torch.from_numpy(imgs).cuda()
+    for it in range(3):  # direct, captured, replayed
+        K.kaze_extract(kz.ctx, dimg, *out)
+        torch.cuda.synchronize()
+        for a, key in zip(out, ("arr_0", "arr_1", "arr_2")):
+            assert np.array_equal(a.cpu().numpy(), seq[key]), (it, key)
+    hk = np.zeros((5, 2048, 8), np.int32)
+    hc = np.zeros(5, np.int32)
+    hd = np.zeros((5, 2048, 64), np.float32)
+    for it in range(3):
+        K.kaze_extract_host(kz.ctx, np.ascontiguousarray(imgs), hk, hc, hd)
+        assert np.array_equal(hc, seq["arr_1"])
+        for i in range(5):
+            n = int(hc[i])
+            assert np.array_equal(hk[i, :n], seq["arr_0"][i, :n]) and np.array_equal(hd[i, :n], seq["arr_2"][i, :n])
+    kz.close()
