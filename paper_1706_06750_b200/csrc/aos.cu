@@ -343,9 +343,33 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_u(const float* __restrict
 // (rows p·M + i, p = 4w..4w+3) fall in four different bank groups: one conflict-free LDS per sample and array
 // instead of an LDG that touches four 32-byte sectors in four lines (41 such loads per thread kept the LSU/MIO queue
 // full in the register-staged kernel above — mio_throttle was its top stall).  Solve and stores as above.
+// chunk_finish into the CTA's shared staging rows (row stride CW) instead of global memory.
+template <int M, bool FULL, int CW>
+__device__ __forceinline__ void chunk_finish_smem(float (&dv)[M], float (&tq)[M + 1], float x0, float xl,
+                                                  float* __restrict__ s, int nvalid) {
+    float Fp = x0, G = 0.f;
+#pragma unroll
+    for (int i = 1; i < M - 1; ++i) {
+        const float r = frcp(fmaf(tq[i], G, 1.f + tq[i] + tq[i + 1]));
+        Fp = fmaf(tq[i], Fp, dv[i]) * r;
+        G = -tq[i + 1] * r;
+        dv[i] = Fp;
+        tq[i] = G;
+    }
+    s[0] = x0;
+    if (FULL || M - 1 < nvalid) s[(M - 1) * CW] = xl;
+    float xn = xl;
+#pragma unroll
+    for (int i = M - 2; i >= 1; --i) {
+        xn = fmaf(-tq[i], xn, dv[i]);
+        if (FULL || i < nvalid) s[i * CW] = xn;
+    }
+}
+
 template <int CW, int M, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_aos_cols_tma(const __grid_constant__ CUtensorMap tmL,
                                                            const __grid_constant__ CUtensorMap tmC,
+                                                           const __grid_constant__ CUtensorMap tmU,
                                                            float* __restrict__ U, size_t u_stride, Geom g, float tau,
                                                            int T, int TP, int nbox, int BR) {
     KZ_PDL_PROLOGUE();
@@ -434,13 +458,22 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_tma(const __grid_constant
     const float xf = pcr_solve(af, bf, cf, df, p, TP, CW, idx, sa, sb, sc, sd);
     sa[idx] = xf;
     __syncthreads();
-    if (!active) return;
-    const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
-    const float xl = e.lF - e.lG * xnext - e.lH * xf;
-    float* Ub = opaque(U + blockIdx.z * u_stride);
-    const unsigned P = (unsigned)g.P, o0 = (unsigned)j0 * P + (unsigned)x;
-    if (nvalid > M) chunk_finish<M, true>(dv, tq, xf, xl, Ub, o0, P, nvalid);
-    else chunk_finish<M, false>(dv, tq, xf, xl, Ub, o0, P, nvalid);
+    // U goes to the L staging rows (every thread read its L samples before the first barrier) and leaves with one
+    // tensor store per box: no per-sample global stores (19 STG touching four lines each per thread before)
+    if (active) {
+        const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
+        const float xl = e.lF - e.lG * xnext - e.lH * xf;
+        if (nvalid > M) chunk_finish_smem<M, true, CW>(dv, tq, xf, xl, smL + j0 * CW + cx, nvalid);
+        else chunk_finish_smem<M, false, CW>(dv, tq, xf, xl, smL + j0 * CW + cx, nvalid);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < nbox; ++b) tma_store_3d(&tmU, x0, b * BR, img, smL + b * BR * CW);
+        bulk_commit_and_wait_read();
+    }
+    (void)U;
+    (void)u_stride;
 }
 
 // -------------------------------------------------------------------------------------------------------------
@@ -638,14 +671,15 @@ bool run_cols_tma(const float* L, const float* c, float* U, Strides st, Geom g, 
     if (CW * TP > NT) return false;
     // boxes of BR rows, BR a multiple of 4 (CW = 8 floats x 4 rows = 128 B: every box lands 128-byte aligned)
     const int nbox = (g.H + 255) / 256, BR = round_up((g.H + nbox - 1) / nbox, 4);
-    CUtensorMap tmL, tmC;
-    if (!encode_plane_map(&tmL, L, g, nimg, st.L, CW, BR) || !encode_plane_map(&tmC, c, g, nimg, st.c, CW, BR))
+    CUtensorMap tmL, tmC, tmU;
+    if (!encode_plane_map(&tmL, L, g, nimg, st.L, CW, BR) || !encode_plane_map(&tmC, c, g, nimg, st.c, CW, BR) ||
+        !encode_plane_map(&tmU, U, g, nimg, st.out, CW, BR))
         return false;
     const size_t smem = sizeof(float) * (2 * (size_t)nbox * BR * CW + 7 * (size_t)CW * TP);
     if (!ensure_smem_optin(reinterpret_cast<const void*>(k_aos_cols_tma<CW, M, NT, MINB>), (int)smem)) return false;
     dim3 grid((g.W + CW - 1) / CW, 1, nimg);
-    kz_launch(k_aos_cols_tma<CW, M, NT, MINB>, dim3(grid), dim3(CW * TP), smem, s, tmL, tmC, U, st.out, g, tau, T, TP,
-              nbox, BR);
+    kz_launch(k_aos_cols_tma<CW, M, NT, MINB>, dim3(grid), dim3(CW * TP), smem, s, tmL, tmC, tmU, U, st.out, g, tau,
+              T, TP, nbox, BR);
     return true;
 }
 
