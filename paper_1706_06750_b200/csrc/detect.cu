@@ -273,6 +273,8 @@ __device__ __forceinline__ void nms_row_fast(float (&w)[NC + 2][3], const float*
     const unsigned ro = (unsigned)min(y + 1, H - 1) * P;
 #pragma unroll
     for (int q = 0; q < NC + 2; ++q) w[q][(PH + 2) % 3] = __ldg(base + (off[q] + ro));
+    // (Prefetching the row after next into L1 — prefetch.global.L1, no registers — measured 12.0 vs 10.8 ms per
+    // 256-image step: the prefetches cost more issue slots and L1 tag lookups than the latency they hid.)
     nms_row_compute<NC, PH>(w, y, H, xin, thr, er, lane, bm, lvl_stride, words);
 }
 
