@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict
 // the s-column halo of (Lx, Ly) is recomputed (CW + 2s ≤ 256 columns per 256 threads), and the L taps of the
 // column halo and of the two extra chain rows come from L1/L2.  Same arithmetic, same order as the two passes:
 // bit-identical results.
-constexpr int kFusedR = 16;  // measured (256-image step): R = 16 38.3 ms, 8 39.8, 4 43.4, 20 44.1, 32 77.5; 512-thread CTAs
+constexpr int kFusedR = 16;  // measured (256-image step): R = 16 38.3 ms, 8 39.8, 4 43.4, 20 44.1, 32 77.5 (round 2, with
+                             // the row-term form: 16 36.9, 12 38.5 (32 registers, 7 CTAs/SM), 20 41.5); 512-thread CTAs
                              // (CW = 480/448, less column halo) 46.4 vs 38.7
 
 // CW + 2s <= 256.  (Phase-A threads on 32-float aligned columns x0 − 32 + t with CW = 192 for every s — aligned centre
