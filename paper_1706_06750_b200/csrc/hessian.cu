@@ -233,20 +233,37 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
                 if (k >= 1 && k <= R && store_col) __stwb(D + (unsigned)((y0 + (k - 1) * SC) * g.P + vc), v);
             }
         } else {
+            // Border chains (and steps without a template case): the same sliding row terms, over CLAMPED rows and
+            // columns.  For a chain row yv inside the image its taps are rows clamp(yv − s), yv, clamp(yv + s) —
+            // exactly rows k, k+1, k+2 of the clamped array.  A chain row outside the image holds (Lx, Ly) of the
+            // clamped image row (A10: the second derivatives read the first ones at clamped coordinates), i.e. of
+            // row 0 (taps 0, 0, s) or row H−1 (taps H−1−s, H−1, H−1), computed once when the chain needs it.  Same
+            // operations on the same values as the per-row form this replaces (bit-identical), ~1/3 of its loads
+            // (R + 4 tap rows instead of 3(R + 2)).
             const int xm = max(cc - s, 0), xp = min(cc + s, g.W - 1);
+            auto terms_at = [&](int y) {
+                const unsigned ro = (unsigned)(clampi(y, 0, g.H - 1) * g.P);
+                return row_terms(__ldg(L + (ro + xm)), __ldg(L + (ro + cc)), __ldg(L + (ro + xp)));
+            };
+            float2 top = make_float2(0.f, 0.f), bot = top;
+            if (y0 - s < 0) {  // chain row −1 (and only it, y0 < s) lies above the image
+                const RowTerms r0 = terms_at(0);
+                top = first_from_rows(r0, r0, terms_at(s));
+            }
+            if (y0 + R * s > g.H - 1) {  // some chain rows lie below the image
+                const RowTerms rl = terms_at(g.H - 1);
+                bot = first_from_rows(terms_at(g.H - 1 - s), rl, rl);
+            }
+            RowTerms ra = terms_at(y0 - 2 * s), rb = terms_at(y0 - s);  // a rolling window of three tap rows
 #pragma unroll
             for (int k = 0; k < R + 2; ++k) {
+                const RowTerms rc = terms_at(y0 + k * s);
                 const int yv = y0 + (k - 1) * s;  // chain row k - 1 (virtual)
-                const int yc = clampi(yv, 0, g.H - 1);
-                const int ro[3] = {max(yc - s, 0) * g.P, yc * g.P, min(yc + s, g.H - 1) * g.P};
-                RowTerms r3[3];
-#pragma unroll
-                for (int q = 0; q < 3; ++q)
-                    r3[q] = row_terms(__ldg(L + (unsigned)(ro[q] + xm)), __ldg(L + (unsigned)(ro[q] + cc)),
-                                      __ldg(L + (unsigned)(ro[q] + xp)));
-                const float2 v = first_from_rows(r3[0], r3[1], r3[2]);
+                const float2 v = yv < 0 ? top : (yv > g.H - 1 ? bot : first_from_rows(ra, rb, rc));
                 sm[k][t] = v;
                 if (k >= 1 && k <= R && store_col && yv < g.H) __stwb(D + (unsigned)(yv * g.P + vc), v);
+                ra = rb;
+                rb = rc;
             }
         }
     }
@@ -269,7 +286,7 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) k_hess_fused(const float* __restrict__ Lt, float2* __restrict__ Lxy,
+__global__ void __launch_bounds__(256, 6) k_hess_fused(const float* __restrict__ Lt, float2* __restrict__ Lxy,
                                                     float* __restrict__ Ldet, size_t img_stride, Geom g, LevelTable lt,
                                                     int keep_edges) {
     KZ_PDL_PROLOGUE();
