@@ -195,6 +195,14 @@ __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict
 constexpr int kFusedR = 16;  // measured (256-image step): R = 16 38.3 ms, 8 39.8, 4 43.4, 20 44.1, 32 77.5 (round 2, with
                              // the row-term form: 16 36.9, 12 38.5 (32 registers, 7 CTAs/SM), 20 41.5); 512-thread CTAs
                              // (CW = 480/448, less column halo) 46.4 vs 38.7
+// (Round 2, measured and dropped: the chain's L tap rows staged by ONE TMA tensor copy per CTA through a per-level
+// 4-D "chain view" map (x: W, r: s, q: ⌈H/s⌉, image; byte strides 4, 4P, 4sP, image stride), box (256, 1, R + 4, 1)
+// at (x0 − 2s, r, b·R − 2, img), phase A reading its taps from shared memory — bit-identical results, but the
+// (R + 4) KB tile on top of the (Lx, Ly) rows costs occupancy and the copy latency is exposed per CTA: R = 16/14/12
+// at 3/4/5 CTAs per SM 43.9/38.0/36.1 vs 34.1 ms per 256-image step; persistent CTAs double-buffering the next
+// items' copies R = 12/8/16 at 3/4/2 CTAs per SM 41.8/64.5/47.9 vs 34.4.  The kernel needs its 48 warps per SM.  Also
+// measured: a 4-D tiled copy whose first coordinate is not a multiple of 4 floats faults with an illegal
+// instruction on B200, a 3-D one does not.)
 
 // CW + 2s <= 256.  (Phase-A threads on 32-float aligned columns x0 − 32 + t with CW = 192 for every s — aligned centre
 // taps, more halo blocks — measured 44.8 vs 38.6 ms.)

@@ -1,6 +1,7 @@
 // kaze_internal.cuh — shared declarations of the sm_100a KAZE kernels and their launchers.
 // Product code: nothing here is shared with oracle/ (DESIGN.md §2).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -71,6 +72,11 @@ int tune_knob(const char* name, int def);
 // into `bytes` of dynamic shared memory on the CURRENT device (once per (function, device), thread safe; a larger
 // request raises it).  Returns false if the driver refuses.
 bool ensure_smem_optin(const void* func, int bytes);
+// Tiled fp32 tensor map of `rank` dimensions (strides in bytes for dimensions 1..rank-1, element strides 1, no
+// swizzle, out-of-bounds elements zero-filled) through cuTensorMapEncodeTiled (runtime driver entry point, no libcuda
+// link).  Returns false if the encoder is unavailable or rejects the map.
+bool encode_f32_map(CUtensorMap* m, int rank, const void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+                    const cuuint32_t* box);
 // Multiprocessor count of the current device (cached per device).
 int device_sm_count();
 

@@ -1,0 +1,8 @@
+set -u
+# session-2 check at HEAD: full GPU suite, smoke, headline bench
+O=gpurun_out/s2a; mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > $O/smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 > $O/gpu_tests.log 2>&1
+echo "gpu tests rc=$?" >> $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err
