@@ -297,8 +297,9 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_u(const float* __restrict
     float dv[M], tq[M + 1];
     ChunkEq e{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     // 32-bit element offsets from opaque per-image bases (the plane is < 2^32 elements)
-    const float* Lb = opaque(L + blockIdx.z * st.L);
-    const float* cb = opaque(c + blockIdx.z * st.c);
+    const int img = batch_image(blockIdx.z, gridDim.z, g);
+    const float* Lb = opaque(L + img * st.L);
+    const float* cb = opaque(c + img * st.c);
     const unsigned P = (unsigned)g.P, o0 = (unsigned)j0 * P + (unsigned)x;
     const bool full = nvalid > M;  // all M samples and the next chunk's first sample exist
     if (active) {
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_u(const float* __restrict
     if (!active) return;
     const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
     const float xl = e.lF - e.lG * xnext - e.lH * xf;
-    float* Ub = opaque(U + blockIdx.z * st.out);
+    float* Ub = opaque(U + img * st.out);
     if (full) chunk_finish<M, true>(dv, tq, xf, xl, Ub, o0, P, nvalid);
     else chunk_finish<M, false>(dv, tq, xf, xl, Ub, o0, P, nvalid);
 }
@@ -412,7 +413,7 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_tma(const __grid_constant
     float* slF = sd + NTOT;
     float* slG = slF + NTOT;
     float* slH = slG + NTOT;
-    const int x0 = blockIdx.x * CW, img = blockIdx.z;
+    const int x0 = blockIdx.x * CW, img = batch_image(blockIdx.z, gridDim.z, g);
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         fence_mbar_init();
@@ -523,7 +524,8 @@ __global__ void __launch_bounds__(32 * NW) k_aos_rows_cta(const float* __restric
     float* sC = rs + Wp;
     float* sU = rs + 2 * Wp;
     const int p = threadIdx.x, lane = p & 31, w = p >> 5;
-    const int img = blockIdx.x / g.H, y = blockIdx.x - img * g.H;
+    const int q = g.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x;  // descending: last image's last row first
+    const int img = q / g.H, y = q - img * g.H;
     const size_t ry = (size_t)y * g.P;
     if (p == 0) {
         mbar_init(&bar, 1);

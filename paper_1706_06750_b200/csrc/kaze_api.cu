@@ -328,7 +328,7 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
     set_geometry(c, n, w, h);
     c->built = false;
     c->detected = false;
-    const Geom g = c->geom;
+    Geom g = c->geom;  // g.rev: the conductivity and AOS passes alternate their image order (see below)
     const size_t SL = c->img_stride, SP = g.plane;  // pyramid stride, scratch stride
     const double px = (double)w * h * n;
     {
@@ -360,6 +360,15 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
     // sub-batch's c, U and L_i planes can stay in L2 between the passes of a level.
     static const int sub = tune_knob("KAZE_BUILD_SUB", 0);
     const int sb = sub > 0 ? std::min(sub, n) : n;
+    // Pass order: each conductivity / column / row pass walks the batch in the opposite image order to the pass
+    // before it, so it starts on the images whose planes the previous pass touched last (still L2-resident);
+    // KAZE_ALTERNATE=0 keeps every pass ascending.
+    static const int alternate = tune_knob("KAZE_ALTERNATE", 1);
+    int pass = 1;
+    auto next_order = [&]() {
+        g.rev = alternate ? (pass & 1) : 0;
+        ++pass;
+    };
     for (int b0 = 0; b0 < n; b0 += sb) {
         const int m = std::min(sb, n - b0);
         const double mpx = (double)w * h * m;
@@ -373,6 +382,7 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
             {   // level 1 too: recomputing |∇(G1∗L0)|² in the conductivity pass beats converting the stored |∇|²
                 // (measured 1.45 vs 2.6 ms per 256-image step)
                 Launch L(c, KC_COND, 8.0 * mpx, s);
+                next_order();
                 launch_cond(prev, SL, cb, SP, g, m, c->g1, 1, c->p.diffusivity, kv, nullptr, s);
             }
             KZ_CHECK_LAUNCH(c, "cond");
@@ -390,6 +400,7 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
                     const size_t s_src = j == 0 ? SL : (src == cur ? SL : SP), s_dst = dst == cur ? SL : SP;
                     {
                         Launch L(c, KC_FED, 12.0 * mpx, s);
+                        g.rev = 0;
                         launch_fed_steps(src, s_src, cb, SP, dst, s_dst, g, m, ft, k, s);
                     }
                     KZ_CHECK_LAUNCH(c, "fed");
@@ -400,12 +411,14 @@ kaze_status do_build(kaze_ctx* c, const float* d_imgs, int n, int w, int h, int6
             const float tau = (float)(c->t[i] - c->t[i - 1]);
             {   // U = column solves (ubuf holds U)
                 Launch L(c, KC_AOS_COLS, 12.0 * mpx, s);
+                next_order();
                 if (!launch_aos_cols(prev, cb, ub, Strides{SL, SP, 0, SP}, g, m, tau, s))
                     return KAZE_ERR_INVALID_ARGUMENT;
             }
             KZ_CHECK_LAUNCH(c, "aos_cols");
             {   // L_i = ½(U + V), V = row solves
                 Launch L(c, KC_AOS_ROWS, 16.0 * mpx, s);
+                next_order();
                 if (!launch_aos_rows(prev, cb, ub, cur, Strides{SL, SP, SP, SL}, g, m, tau, s))
                     return KAZE_ERR_INVALID_ARGUMENT;
             }

@@ -17,8 +17,12 @@ constexpr int kMaxBatch = 1024;
 // Plane geometry of one build: W x H pixels, pitch P floats (multiple of 32), plane = P * H.
 struct Geom {
     int W, H, P;
+    int rev;  // image order of a batched launch (cond / AOS passes): 0 ascending, 1 descending — consecutive passes
+              // alternate, so a pass starts on the images the previous one touched last (still in L2)
     size_t plane;
 };
+// Image of batch slot z (of n) under the launch's order.
+__device__ __forceinline__ int batch_image(int z, int n, const Geom& g) { return g.rev ? n - 1 - z : z; }
 
 struct GaussTaps {
     int r;

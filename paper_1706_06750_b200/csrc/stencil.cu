@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
     __shared__ __align__(16) float sA[CR2][CW2];
     __shared__ __align__(16) float sB[CR2][CW2];
     __shared__ float red[8];
-    const int x0 = blockIdx.x * CW2, y0 = blockIdx.y * CH2, img = blockIdx.z;
+    const int x0 = blockIdx.x * CW2, y0 = blockIdx.y * CH2, img = batch_image(blockIdx.z, gridDim.z, g);
     const float* src = L + img * in_img_stride;
     const int tid = threadIdx.x;
     float w[7];

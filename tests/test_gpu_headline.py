@@ -302,3 +302,52 @@ def test_overlapped_chunks_equal_sequential_chunks(tmp_path):
             n = int(hc[i])
             assert np.array_equal(hk[i, :n], seq["arr_0"][i, :n]) and np.array_equal(hd[i, :n], seq["arr_2"][i, :n])
     kz.close()
+
+
+@pytest.mark.parametrize("knob", ["KAZE_ALTERNATE=0", "KAZE_HESS_FUSED=0"])
+def test_launch_order_and_hessian_form_do_not_change_results(tmp_path, knob):
+    """Bit-identical outputs across launch-shape knobs (read once per process, so the reference runs in a
+    subprocess): KAZE_ALTERNATE=0 runs every conductivity / AOS pass in ascending image order instead of alternating
+    the order pass by pass; KAZE_HESS_FUSED=0 computes the Hessian with the two chain passes instead of the fused
+    one (same operations, same order)."""
+    import os
+    import subprocess
+    import sys
+
+    w, h, n = 333, 257, 3
+    imgs = kaze_inputs.synth_batch(n, w, h, first=21)
+    np.save(tmp_path / "imgs.npy", imgs)
+    script = (
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "import paper_1706_06750_b200 as K\n"
+        f"imgs = torch.from_numpy(np.load({str(tmp_path / 'imgs.npy')!r})).cuda()\n"
+        f"kz = K.Kaze({w}, {h}, batch={n}, max_keypoints=8192, flags=K.FLAG_ALL_DERIVATIVES)\n"
+        f"out = kz.alloc_outputs({n})\n"
+        "K.kaze_extract(kz.ctx, imgs, *out)\n"
+        "torch.cuda.synchronize()\n"
+        "lv = {}\n"
+        f"for i in range({n}):\n"
+        "    for p in (K.PLANE_LT, K.PLANE_LX, K.PLANE_LY, K.PLANE_LDET):\n"
+        "        for l in range(16):\n"
+        f"            t = torch.empty(({h}, {w}), device='cuda'); K.kaze_get_level(kz.ctx, i, l, p, t)\n"
+        "            lv[f'{i}_{p}_{l}'] = t.cpu().numpy()\n"
+        f"np.savez({str(tmp_path / 'ref.npz')!r}, *[t.cpu().numpy() for t in out], **lv)\n"
+    )
+    k, v = knob.split("=")
+    r = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, **{k: v}), capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    ref = np.load(tmp_path / "ref.npz")
+    kz = make(w, h, batch=n, max_keypoints=8192, flags=K.FLAG_ALL_DERIVATIVES)
+    out = kz.alloc_outputs(n)
+    K.kaze_extract(kz.ctx, torch.from_numpy(imgs).cuda(), *out)
+    torch.cuda.synchronize()
+    for a, key in zip(out, ("arr_0", "arr_1", "arr_2")):
+        assert np.array_equal(a.cpu().numpy(), ref[key]), key
+    for i in range(n):
+        for p in (K.PLANE_LT, K.PLANE_LX, K.PLANE_LY, K.PLANE_LDET):
+            lv = gpu_levels(kz, 16, p, img=i).astype(np.float32)
+            for lvl in range(16):
+                assert np.array_equal(lv[lvl], ref[f"{i}_{p}_{lvl}"]), (knob, i, p, lvl)
+    kz.close()
