@@ -25,7 +25,10 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libkaze_b200.so")
+# KAZE_LIB_VARIANT=name loads libkaze_b200.name.so instead (A/B builds from `python -m paper_1706_06750_b200.build
+# --variant name -DFLAG...`; experiments only)
+_variant = os.environ.get("KAZE_LIB_VARIANT", "")
+lib_path = os.path.join(_HERE, f"libkaze_b200.{_variant}.so" if _variant else "libkaze_b200.so")
 
 PLANE_LT, PLANE_LX, PLANE_LY, PLANE_LDET, PLANE_COND = 0, 1, 2, 3, 4
 FLAG_KEEP_ANGLE = 1

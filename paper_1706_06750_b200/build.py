@@ -30,9 +30,9 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def _compile(src: str) -> tuple[str, str]:
-    obj = os.path.join(OBJ, src.replace(".cu", ".o"))
-    cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src: str, extra: tuple[str, ...] = (), objdir: str = OBJ) -> tuple[str, str]:
+    obj = os.path.join(objdir, src.replace(".cu", ".o"))
+    cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -54,6 +54,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, extra: list[str]) -> str:
+    """A/B build: every source with extra nvcc flags into libkaze_b200.<name>.so (loaded with KAZE_LIB_VARIANT)."""
+    objdir = os.path.join(OBJ, name)
+    os.makedirs(objdir, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = [o for o, _ in ex.map(lambda f: _compile(f, tuple(extra), objdir), SOURCES)]
+    out = os.path.join(HERE, f"libkaze_b200.{name}.so")
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", *objs, "-o", out],
+                   check=True)
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

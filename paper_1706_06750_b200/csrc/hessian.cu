@@ -195,6 +195,9 @@ __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict
 constexpr int kFusedR = 16;  // measured (256-image step): R = 16 38.3 ms, 8 39.8, 4 43.4, 20 44.1, 32 77.5 (round 2, with
                              // the row-term form: 16 36.9, 12 38.5 (32 registers, 7 CTAs/SM), 20 41.5); 512-thread CTAs
                              // (CW = 480/448, less column halo) 46.4 vs 38.7
+// (Round 2, measured and dropped: phase A as a rolling window of three tap rows with bounded unrolling, to cut the
+// ~1600 straight-line instructions per step case (ncu: 16% of stalls are "no instruction"): unroll 1/2/4/8/full
+// 46.1/38.4/38.6/34.6/35.7 vs 34.0 ms — hoisting all tap loads ahead of the arithmetic matters more.)
 // (Round 2, measured and dropped: the chain's L tap rows staged by ONE TMA tensor copy per CTA through a per-level
 // 4-D "chain view" map (x: W, r: s, q: ⌈H/s⌉, image; byte strides 4, 4P, 4sP, image stride), box (256, 1, R + 4, 1)
 // at (x0 − 2s, r, b·R − 2, img), phase A reading its taps from shared memory — bit-identical results, but the
