@@ -7,8 +7,10 @@
 //  * khist / kfinal: 300-bin histogram of |∇| over the interior, percentile → k on the device
 //               (A7), no host round trip.
 #include <algorithm>
+#include <cstring>
 
 #include "kaze_internal.cuh"
+#include "ptx.cuh"
 
 namespace kz {
 
@@ -18,11 +20,6 @@ constexpr float kW0c = 0.1875f, kW1c = 0.625f;  // Scharr cross smoothing (3, 10
 constexpr int TW = 32;  // tile width  (one warp per tile row → coalesced 128 B rows)
 constexpr int TH = 32;  // tile height (block 32 x 8, four output rows per thread)
 
-__device__ __forceinline__ float frcp(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
 
 // -------------------------------------------------------------------------------------------------
 // Separable Gaussian over a TW x TH output tile.  The input tile stores I(clamp(u)) for the virtual
@@ -204,7 +201,7 @@ __device__ __forceinline__ void cond_load16(const float* __restrict__ row, int x
     }
 }
 
-__device__ __forceinline__ void cond_hpass(const float (&v)[16], const float (&w)[7], int xb, int W, bool fast,
+__device__ __forceinline__ void cond_hpass(const float (&v)[16], const float (&w)[7], int xb, int W, bool fast, bool sw,
                                            float* __restrict__ dA, float* __restrict__ dB) {
     float h[10];  // Hl at columns xb-1 .. xb+8
 #pragma unroll
@@ -226,10 +223,9 @@ __device__ __forceinline__ void cond_hpass(const float (&v)[16], const float (&w
         A[i] = h[i + 2] - h[i];
         B[i] = fmaf(kW0c, h[i] + h[i + 2], kW1c * h[i + 1]);
     }
-    // The 8 lanes of a 128-bit store phase hold segments sg = 0..7 of one 64-float row: segment halves 8sg and
-    // 8(sg+4) fall in the same 4-bank group, so segments 4..7 store their upper half first (a 2-way conflict on
-    // every STS.128 otherwise: 26% of the kernel's shared wavefronts in the round-1 capture).
-    const bool sw = (xb >> 5) & 1;  // sg >= 4 ⇔ bit 5 of xb = x0 + 8sg (x0 is a multiple of 64)
+    // sw: store the upper half first.  The 8 lanes of a 128-bit store phase must hit 8 distinct 4-bank groups; the
+    // caller's lane mapping decides which lanes swap (a 2-way conflict on every STS.128 otherwise: 26% of the
+    // kernel's shared wavefronts in the round-1 capture).
     const float4 a0 = make_float4(A[0], A[1], A[2], A[3]), a1 = make_float4(A[4], A[5], A[6], A[7]);
     const float4 b0 = make_float4(B[0], B[1], B[2], B[3]), b1 = make_float4(B[4], B[5], B[6], B[7]);
     reinterpret_cast<float4*>(dA)[sw] = sw ? a1 : a0;
@@ -307,21 +303,54 @@ __device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const flo
     return lmax;
 }
 
+// Interior tiles (every tap inside the image) stage the 64 input rows x 72 columns with ONE 2-D TMA tensor copy
+// (box 76 x 64: a row pitch of 76 floats puts the two rows of a 128-bit load phase 4 banks apart) instead of four
+// 16-byte loads per item whose lanes use half of each 32-byte sector; border tiles keep the clamped global loads.
+constexpr int kCondTP = 76;  // staged row pitch (floats)
+
 template <int MODE, int DIFF>
-__global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size_t in_img_stride,
+__global__ void __launch_bounds__(256) k_cond2(const __grid_constant__ CUtensorMap tmL, int use_tma,
+                                               const float* __restrict__ L, size_t in_img_stride,
                                                float* __restrict__ out, size_t out_img_stride, Geom g, GaussTaps t,
                                                const float* __restrict__ kval, unsigned* __restrict__ hmax_bits) {
     KZ_PDL_PROLOGUE();
     __shared__ __align__(16) float sA[CR2][CW2];
     __shared__ __align__(16) float sB[CR2][CW2];
     __shared__ float red[8];
+    extern __shared__ __align__(128) float sT[];  // [CR2][kCondTP] (TMA path only)
+    __shared__ __align__(8) uint64_t bar;
     const int x0 = blockIdx.x * CW2, y0 = blockIdx.y * CH2, img = batch_image(blockIdx.z, gridDim.z, g);
     const float* src = L + img * in_img_stride;
     const int tid = threadIdx.x;
     float w[7];
 #pragma unroll
     for (int d = 0; d < 7; ++d) w[d] = t.w[d];
-    {
+    const bool staged = use_tma && x0 >= 4 && x0 + CW2 + 4 <= g.W && y0 >= 4 && y0 + CH2 + 4 <= g.H;  // CTA-uniform
+    if (staged) {
+        if (tid == 0) {
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(&bar, (uint32_t)(sizeof(float) * CR2 * kCondTP));
+            tma_load_3d(sT, &tmL, x0 - 4, y0 - 4, img, &bar);
+        }
+        // lane → (row, segment): a 128-bit phase (8 lanes) covers segments 0..3 or 4..7 of two adjacent rows, 4
+        // banks apart at the 76-float pitch: conflict-free loads; odd rows store their upper half first
+        const int l = tid & 31, sg = (l & 3) + 4 * ((l >> 3) & 1);
+        const int r0 = 4 * (tid >> 5) + ((l >> 2) & 1) + 2 * (l >> 4);
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+        mbar_wait(&bar, 0);
+        float v0[16], v1[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 a = *reinterpret_cast<const float4*>(&sT[r0 * kCondTP + 8 * sg + 4 * q]);
+            const float4 b = *reinterpret_cast<const float4*>(&sT[(r0 + 32) * kCondTP + 8 * sg + 4 * q]);
+            v0[4 * q] = a.x; v0[4 * q + 1] = a.y; v0[4 * q + 2] = a.z; v0[4 * q + 3] = a.w;
+            v1[4 * q] = b.x; v1[4 * q + 1] = b.y; v1[4 * q + 2] = b.z; v1[4 * q + 3] = b.w;
+        }
+        const int xb = x0 + 8 * sg;
+        cond_hpass(v0, w, xb, g.W, true, r0 & 1, &sA[r0][8 * sg], &sB[r0][8 * sg]);
+        cond_hpass(v1, w, xb, g.W, true, r0 & 1, &sA[r0 + 32][8 * sg], &sB[r0 + 32][8 * sg]);
+    } else {
         const int sg = tid & 7, r0 = tid >> 3, xb = x0 + 8 * sg;
         const bool fast = (xb >= 4) && (xb + 12 <= g.W);
         const float* row0 = src + (size_t)clampi(y0 - 4 + r0, 0, g.H - 1) * g.P;
@@ -329,8 +358,11 @@ __global__ void __launch_bounds__(256) k_cond2(const float* __restrict__ L, size
         float v0[16], v1[16];
         cond_load16(row0, xb, g.W, fast, v0);
         cond_load16(row1, xb, g.W, fast, v1);
-        cond_hpass(v0, w, xb, g.W, fast, &sA[r0][8 * sg], &sB[r0][8 * sg]);
-        cond_hpass(v1, w, xb, g.W, fast, &sA[r0 + 32][8 * sg], &sB[r0 + 32][8 * sg]);
+        // the 8 lanes of a 128-bit phase are segments 0..7 of one row: halves 8sg and 8(sg + 4) share a bank group,
+        // so segments 4..7 (bit 5 of xb; x0 is a multiple of 64) store their upper half first
+        const bool sw = (xb >> 5) & 1;
+        cond_hpass(v0, w, xb, g.W, fast, sw, &sA[r0][8 * sg], &sB[r0][8 * sg]);
+        cond_hpass(v1, w, xb, g.W, fast, sw, &sA[r0 + 32][8 * sg], &sB[r0 + 32][8 * sg]);
     }
     __syncthreads();
     if constexpr (MODE == 1) {
@@ -446,14 +478,30 @@ void launch_cond(const float* L, size_t in_img_stride, float* out, size_t out_im
                  cudaStream_t s) {
     // G(σ=1) always has radius 3 (A6), which k_cond2's 7-tap loops and 4-row halo assume
     dim3 grid((g.W + CW2 - 1) / CW2, (g.H + CH2 - 1) / CH2, nimg);
+    static const int tma_knob = tune_knob("KAZE_COND_TMA", 1);
+    CUtensorMap tm;
+    int use_tma = 0;
+    if (tma_knob) {
+        const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)nimg};
+        const cuuint64_t strides[2] = {(cuuint64_t)g.P * 4, (cuuint64_t)in_img_stride * 4};
+        const cuuint32_t box[3] = {(cuuint32_t)kCondTP, (cuuint32_t)CR2, 1};
+        use_tma = encode_f32_map(&tm, 3, L, dims, strides, box) ? 1 : 0;
+    }
+    if (!use_tma) memset(&tm, 0, sizeof(tm));
+    const size_t smem = use_tma ? sizeof(float) * CR2 * kCondTP : 0;
+    auto go = [&](auto kern) {
+        if (smem) ensure_smem_optin(reinterpret_cast<const void*>(kern), (int)smem);
+        kz_launch(kern, dim3(grid), dim3(256), smem, s, tm, use_tma, L, in_img_stride, out, out_img_stride, g, t1, kval,
+                  hmax_bits);
+    };
     if (mode == 0) {
-        kz_launch(k_cond2<0, 2>, dim3(grid), dim3(256), 0, s, L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits);
+        go(k_cond2<0, 2>);
         return;
     }
     switch (diffusivity) {
-        case 1: kz_launch(k_cond2<1, 1>, dim3(grid), dim3(256), 0, s, L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
-        case 3: kz_launch(k_cond2<1, 3>, dim3(grid), dim3(256), 0, s, L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
-        default: kz_launch(k_cond2<1, 2>, dim3(grid), dim3(256), 0, s, L, in_img_stride, out, out_img_stride, g, t1, kval, hmax_bits); break;
+        case 1: go(k_cond2<1, 1>); break;
+        case 3: go(k_cond2<1, 3>); break;
+        default: go(k_cond2<1, 2>); break;
     }
 }
 

@@ -1,11 +1,12 @@
 #!/bin/bash
 # A/B of library variants / knobs on the headline bench (one GPU, under gpurun):
 #   scripts/gpu_ab.sh OUTDIR "cfg1" "cfg2" ...   where cfg = space-separated VAR=value list ("-" = defaults)
-# Prints per config: img/s, selected per-kernel ms per step, SM clock.  KAZE_AB_TESTS="-k expr" runs those GPU tests first.
+# Prints per config: img/s, selected per-kernel ms per step, SM clock.  KAZE_AB_TESTS="expr" first runs the GPU tests
+# selected by -k "expr".
 set -u
 O=$1; shift; mkdir -p $O
 if [ -n "${KAZE_AB_TESTS:-}" ]; then
-  timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider $KAZE_AB_TESTS > $O/tests.log 2>&1; tail -2 $O/tests.log
+  timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -k "$KAZE_AB_TESTS" > $O/tests.log 2>&1; tail -2 $O/tests.log
 fi
 i=0
 for cfg in "$@"; do
