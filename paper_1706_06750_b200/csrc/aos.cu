@@ -26,6 +26,7 @@
 //   rows:    one CTA (4 or 8 warps) per row.  The TMA engine streams the row's L, c and U into shared memory (1-D
 //            bulk copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is
 //            solved by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve).
+#include <algorithm>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -503,6 +504,133 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_tma(const __grid_constant
     (void)u_stride;
 }
 
+// Persistent form of k_aos_cols_tma: one CTA per SM walks the launch's strips round-robin with TWO shared-memory
+// (L, c) strip buffers and a separate U staging strip.  A strip's L and c are in registers once its chunk
+// reductions are done, so right after that barrier the buffer is refilled with strip i + 2 — its tensor copies
+// stream in during the rest of strip i and all of strip i + 1 (the per-strip CTA above waited for its copies with
+// only one other CTA per SM to fill the gap: 34% of its stalls were that barrier wait).  U leaves from the staging
+// strip with tensor stores; the next strip's finish writes it only after they have read it.
+template <int CW, int M, int NT>
+__global__ void __launch_bounds__(NT, 1) k_aos_cols_tmap(const __grid_constant__ CUtensorMap tmL,
+                                                         const __grid_constant__ CUtensorMap tmC,
+                                                         const __grid_constant__ CUtensorMap tmU, Geom g, float tau,
+                                                         int T, int TP, int nbox, int BR, int nsx, int nimg,
+                                                         int total) {
+    KZ_PDL_PROLOGUE();
+    extern __shared__ __align__(128) float smem_cols[];
+    __shared__ __align__(8) uint64_t bar[2];
+    const int HB = nbox * BR;
+    const int NTOT = CW * TP;
+    float* smU = smem_cols + 4 * HB * CW;  // after [2][L, c][HB][CW]
+    float* sa = smU + HB * CW;
+    float* sb = sa + NTOT;
+    float* sc = sb + NTOT;
+    float* sd = sc + NTOT;
+    float* slF = sd + NTOT;
+    float* slG = slF + NTOT;
+    float* slH = slG + NTOT;
+    const int G = gridDim.x;
+    auto issue = [&](int w, int b) {
+        const int z = w / nsx, x0 = (w - z * nsx) * CW, img = batch_image(z, nimg, g);
+        float* dL = smem_cols + 2 * b * HB * CW;
+        float* dC = dL + HB * CW;
+        mbar_arrive_expect_tx(&bar[b], 2u * (uint32_t)(HB * CW) * 4u);
+        for (int q = 0; q < nbox; ++q) {
+            tma_load_3d(dL + q * BR * CW, &tmL, x0, q * BR, img, &bar[b]);
+            tma_load_3d(dC + q * BR * CW, &tmC, x0, q * BR, img, &bar[b]);
+        }
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        if ((int)blockIdx.x < total) issue(blockIdx.x, 0);
+        if ((int)blockIdx.x + G < total) issue(blockIdx.x + G, 1);
+    }
+    __syncthreads();  // the barriers are initialised before anyone waits on them
+    const int cx = threadIdx.x % CW, p = threadIdx.x / CW;
+    const int n = g.H;
+    const int j0 = p * M;
+    const int nvalid = n - j0;
+    const int idx = p * CW + cx;
+    int it = 0;
+    for (int w = blockIdx.x; w < total; w += G, ++it) {
+        const int b = it & 1;
+        const int z = w / nsx, x0 = (w - z * nsx) * CW, img = batch_image(z, nimg, g);
+        const float* smL = smem_cols + 2 * b * HB * CW;
+        const float* smC = smL + HB * CW;
+        const bool active = (p < T) && (x0 + cx < g.W);
+        float dv[M], tq[M + 1];
+        ChunkEq e{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        mbar_wait(&bar[b], (uint32_t)((it >> 1) & 1));
+        if (active) {
+            float cv[M];
+            const bool full = nvalid > M;
+            if (full) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    dv[i] = smL[(j0 + i) * CW + cx];
+                    cv[i] = smC[(j0 + i) * CW + cx];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    dv[i] = i < nvalid ? smL[(j0 + i) * CW + cx] : 0.f;
+                    cv[i] = i < nvalid ? smC[(j0 + i) * CW + cx] : 0.f;
+                }
+            }
+            const float cprev = j0 > 0 ? smC[(j0 - 1) * CW + cx] : 0.f;
+            tq[0] = j0 > 0 ? tau * (cprev + cv[0]) : 0.f;
+            if (full) {
+#pragma unroll
+                for (int i = 1; i < M; ++i) tq[i] = tau * (cv[i - 1] + cv[i]);
+                tq[M] = tau * (cv[M - 1] + smC[(j0 + M) * CW + cx]);
+            } else {
+#pragma unroll
+                for (int i = 1; i < M; ++i) tq[i] = i < nvalid ? tau * (cv[i - 1] + cv[i]) : 0.f;
+                tq[M] = 0.f;
+            }
+            chunk_reduce<M>(dv, tq, e);
+        }
+        slF[idx] = e.lF;
+        slG[idx] = e.lG;
+        slH[idx] = e.lH;
+        __syncthreads();  // every thread holds its strip samples in registers: refill the buffer with strip i + 2
+        if (threadIdx.x == 0 && w + 2 * G < total) issue(w + 2 * G, b);
+        float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
+        if (active) {
+            float pF = 0.f, pG = 0.f, pH = 0.f;
+            if (p > 0) {
+                pF = slF[idx - CW];
+                pG = slG[idx - CW];
+                pH = slH[idx - CW];
+            }
+            af = -e.A * pH;
+            bf = 1.f - e.A * pG - e.C * e.lH;
+            cf = -e.C * e.lG;
+            df = e.D - e.A * pF - e.C * e.lF;
+        }
+        const float xf = pcr_solve(af, bf, cf, df, p, TP, CW, idx, sa, sb, sc, sd);
+        sa[idx] = xf;
+        // the previous strip's U stores must have read the staging strip before this strip's finish rewrites it
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+        if (active) {
+            const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
+            const float xl = e.lF - e.lG * xnext - e.lH * xf;
+            if (nvalid > M) chunk_finish_smem<M, true, CW>(dv, tq, xf, xl, smU + j0 * CW + cx, nvalid);
+            else chunk_finish_smem<M, false, CW>(dv, tq, xf, xl, smU + j0 * CW + cx, nvalid);
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < nbox; ++q) tma_store_3d(&tmU, x0, q * BR, img, smU + q * BR * CW);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // -------------------------------------------------------------------------------------------------------------
 // Row systems, one CTA of NW warps per row (the row pass runs first and writes V).  The TMA engine streams the
 // row's L and c into shared memory; thread p owns the chunk [p·M, p·M + m) (M odd: conflict-free strided reads)
@@ -689,6 +817,25 @@ bool run_cols_tma(const float* L, const float* c, float* U, Strides st, Geom g, 
     return true;
 }
 
+template <int CW, int M, int NT>
+bool run_cols_tmap(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau, cudaStream_t s) {
+    const int T = (g.H + M - 1) / M;
+    const int TP = round_up(T, 32 / CW);
+    if (CW * TP > NT) return false;
+    const int nbox = (g.H + 255) / 256, BR = round_up((g.H + nbox - 1) / nbox, 4);
+    CUtensorMap tmL, tmC, tmU;
+    if (!encode_plane_map(&tmL, L, g, nimg, st.L, CW, BR) || !encode_plane_map(&tmC, c, g, nimg, st.c, CW, BR) ||
+        !encode_plane_map(&tmU, U, g, nimg, st.out, CW, BR))
+        return false;
+    const size_t smem = sizeof(float) * (5 * (size_t)nbox * BR * CW + 7 * (size_t)CW * TP);
+    if (!ensure_smem_optin(reinterpret_cast<const void*>(k_aos_cols_tmap<CW, M, NT>), (int)smem)) return false;
+    const int nsx = (g.W + CW - 1) / CW, total = nsx * nimg;
+    const int grid = std::min(total, device_sm_count());
+    kz_launch(k_aos_cols_tmap<CW, M, NT>, dim3(grid), dim3(CW * TP), smem, s, tmL, tmC, tmU, g, tau, T, TP, nbox, BR,
+              nsx, nimg, total);
+    return true;
+}
+
 template <int CW, int M, int NT, int MINB>
 void run_cols(const float* L, const float* c, float* U, Strides st, Geom g, int nimg, float tau, cudaStream_t s) {
     const int T = (g.H + M - 1) / M;  // the last chunk is padded (decoupled rows)
@@ -709,6 +856,17 @@ bool launch_aos_cols(const float* L, const float* c, float* U, Strides st, Geom 
     const int H = g.H;
     static const int tma = tune_knob("KAZE_COLS_TMA", 1);
     // TMA-staged inputs, odd chunk lengths (conflict-free shared reads), <= 64 chunks per column
+    static const int persistent = tune_knob("KAZE_COLS_PERSIST", 1);
+    if (tma && persistent && H <= 64 * 19) {
+        bool ok;
+        // (smaller chunks with more threads measured slower: M = 11 x 128 chunks 32.3 ms, M = 13 x 96 30.8, vs 27.1
+        // at M = 19 x 64 — one more PCR level and its barriers)
+        if (H <= 64 * 9) ok = run_cols_tmap<8, 9, 512>(L, c, U, st, g, nimg, tau, s);
+        else if (H <= 64 * 13) ok = run_cols_tmap<8, 13, 512>(L, c, U, st, g, nimg, tau, s);
+        else if (H <= 64 * 17) ok = run_cols_tmap<8, 17, 512>(L, c, U, st, g, nimg, tau, s);
+        else ok = run_cols_tmap<8, 19, 512>(L, c, U, st, g, nimg, tau, s);
+        if (ok) return true;
+    }
     if (tma && H <= 64 * 19) {
         bool ok;
         if (H <= 64 * 9) ok = run_cols_tma<8, 9, 512, 2>(L, c, U, st, g, nimg, tau, s);

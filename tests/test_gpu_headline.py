@@ -304,13 +304,14 @@ def test_overlapped_chunks_equal_sequential_chunks(tmp_path):
     kz.close()
 
 
-@pytest.mark.parametrize("knob", ["KAZE_ALTERNATE=0", "KAZE_HESS_FUSED=0", "KAZE_COND_TMA=0"])
+@pytest.mark.parametrize("knob", ["KAZE_ALTERNATE=0", "KAZE_HESS_FUSED=0", "KAZE_COND_TMA=0", "KAZE_COLS_PERSIST=0"])
 def test_launch_order_and_hessian_form_do_not_change_results(tmp_path, knob):
     """Bit-identical outputs across launch-shape knobs (read once per process, so the reference runs in a
     subprocess): KAZE_ALTERNATE=0 runs every conductivity / AOS pass in ascending image order instead of alternating
     the order pass by pass; KAZE_HESS_FUSED=0 computes the Hessian with the two chain passes instead of the fused
     one (same operations, same order); KAZE_COND_TMA=0 loads every conductivity tile with global loads instead of
-    staging the interior tiles with TMA tensor copies."""
+    staging the interior tiles with TMA tensor copies; KAZE_COLS_PERSIST=0 runs the AOS column pass one CTA per strip
+    instead of persistent double-buffered CTAs."""
     import os
     import subprocess
     import sys
