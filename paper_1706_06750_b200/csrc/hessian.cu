@@ -195,6 +195,9 @@ __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict
 constexpr int kFusedR = 16;  // measured (256-image step): R = 16 38.3 ms, 8 39.8, 4 43.4, 20 44.1, 32 77.5 (round 2, with
                              // the row-term form: 16 36.9, 12 38.5 (32 registers, 7 CTAs/SM), 20 41.5); 512-thread CTAs
                              // (CW = 480/448, less column halo) 46.4 vs 38.7
+// (Round 2, measured and dropped: the (Lx, Ly) rows leaving through 1-D TMA bulk stores straight from the shared rows
+// (columns shifted by s & 1 for 16-byte alignment) instead of per-thread 8-byte stores: 33.9/34.1 vs 34.2/34.1 ms —
+// no change beyond noise, and the extra state spills at 40 registers.)
 // (Round 2, measured and dropped: phase A as a rolling window of three tap rows with bounded unrolling, to cut the
 // ~1600 straight-line instructions per step case (ncu: 16% of stalls are "no instruction"): unroll 1/2/4/8/full
 // 46.1/38.4/38.6/34.6/35.7 vs 34.0 ms — hoisting all tap loads ahead of the arithmetic matters more.)
