@@ -88,6 +88,54 @@ __device__ __forceinline__ float pcr_solve(float af, float bf, float cf, float d
     return df * frcp(bf);
 }
 
+// Warp PCR for the column pass: the reduced system of one column (TP <= 64 chunk unknowns, identity rows past TP)
+// solved by ONE warp, two unknowns per lane (slots r = 2·lane, 2·lane + 1), all levels by shuffles — no CTA barriers
+// (the shared-memory PCR above takes two per level, twelve at 64 chunks).  E holds the column's (a, b, c, d) rows as
+// four arrays of `pitch` floats; returns x of the lane's two slots.
+__device__ __forceinline__ float2 warp_pcr64(const float* __restrict__ E, int pitch, int lane) {
+    float a[2], b[2], c[2], d[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        a[s] = E[2 * lane + s];
+        b[s] = E[pitch + 2 * lane + s];
+        c[s] = E[2 * pitch + 2 * lane + s];
+        d[s] = E[3 * pitch + 2 * lane + s];
+    }
+#pragma unroll
+    for (int st = 1; st < 64; st <<= 1) {
+        float na[2], nb[2], nc[2], nd[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int r = 2 * lane + s, jm = r - st, jp = r + st;
+            const bool hm = jm >= 0, hp = jp < 64;
+            const int sm_ = (s - st) & 1, sp_ = (s + st) & 1;  // slots of the partners (uniform)
+            const int lm = hm ? jm >> 1 : 0, lp = hp ? jp >> 1 : 0;
+            const float am = __shfl_sync(0xffffffffu, sm_ ? a[1] : a[0], lm);
+            const float bm = __shfl_sync(0xffffffffu, sm_ ? b[1] : b[0], lm);
+            const float cm = __shfl_sync(0xffffffffu, sm_ ? c[1] : c[0], lm);
+            const float dm = __shfl_sync(0xffffffffu, sm_ ? d[1] : d[0], lm);
+            const float ap = __shfl_sync(0xffffffffu, sp_ ? a[1] : a[0], lp);
+            const float bp = __shfl_sync(0xffffffffu, sp_ ? b[1] : b[0], lp);
+            const float cp = __shfl_sync(0xffffffffu, sp_ ? c[1] : c[0], lp);
+            const float dp = __shfl_sync(0xffffffffu, sp_ ? d[1] : d[0], lp);
+            const float k1 = hm ? a[s] * frcp(bm) : 0.f;
+            const float k2 = hp ? c[s] * frcp(bp) : 0.f;
+            na[s] = -am * k1;
+            nc[s] = -cp * k2;
+            nb[s] = b[s] - cm * k1 - ap * k2;
+            nd[s] = d[s] - dm * k1 - dp * k2;
+        }
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            a[s] = na[s];
+            b[s] = nb[s];
+            c[s] = nc[s];
+            d[s] = nd[s];
+        }
+    }
+    return make_float2(d[0] * frcp(b[0]), d[1] * frcp(b[1]));
+}
+
 template <int MC>
 struct Chunk {
     float al[MC], ga[MC], de[MC];  // α', γ', δ' of rows 1..m-2
@@ -510,6 +558,8 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_tma(const __grid_constant
 // stream in during the rest of strip i and all of strip i + 1 (the per-strip CTA above waited for its copies with
 // only one other CTA per SM to fill the gap: 34% of its stalls were that barrier wait).  U leaves from the staging
 // strip with tensor stores; the next strip's finish writes it only after they have read it.
+constexpr int kEP = 68;  // warp-PCR row pitch (floats)
+
 template <int CW, int M, int NT>
 __global__ void __launch_bounds__(NT, 1) k_aos_cols_tmap(const __grid_constant__ CUtensorMap tmL,
                                                          const __grid_constant__ CUtensorMap tmC,
@@ -522,11 +572,9 @@ __global__ void __launch_bounds__(NT, 1) k_aos_cols_tmap(const __grid_constant__
     const int HB = nbox * BR;
     const int NTOT = CW * TP;
     float* smU = smem_cols + 4 * HB * CW;  // after [2][L, c][HB][CW]
-    float* sa = smU + HB * CW;
-    float* sb = sa + NTOT;
-    float* sc = sb + NTOT;
-    float* sd = sc + NTOT;
-    float* slF = sd + NTOT;
+    float* E = smU + HB * CW;              // reduced systems [CW][a, b, c, d][kEP]
+    float* X = E + CW * 4 * kEP;           // their solutions [CW][kEP]
+    float* slF = X + CW * kEP;             // last-equation exchange
     float* slG = slF + NTOT;
     float* slH = slG + NTOT;
     const int G = gridDim.x;
@@ -610,13 +658,33 @@ __global__ void __launch_bounds__(NT, 1) k_aos_cols_tmap(const __grid_constant__
             cf = -e.C * e.lG;
             df = e.D - e.A * pF - e.C * e.lF;
         }
-        const float xf = pcr_solve(af, bf, cf, df, p, TP, CW, idx, sa, sb, sc, sd);
-        sa[idx] = xf;
+        // reduced systems: column cx's rows go to E[cx] (pitch kEP ≡ 4 mod 32: the 8 columns x 4 chunks of a warp hit
+        // 32 distinct banks), a warp solves each column (identity rows past TP) and x comes back through X[cx]
+        {
+            float* Ec = E + cx * 4 * kEP;
+            Ec[p] = af;
+            Ec[kEP + p] = bf;
+            Ec[2 * kEP + p] = cf;
+            Ec[3 * kEP + p] = df;
+            for (int r = TP + p; r < 64; r += TP) {  // identity rows TP..63
+                Ec[r] = 0.f;
+                Ec[kEP + r] = 1.f;
+                Ec[2 * kEP + r] = 0.f;
+                Ec[3 * kEP + r] = 0.f;
+            }
+        }
+        __syncthreads();
+        // warp wq solves columns wq, wq + nw, ... (CW·TP/32 warps; 16 at 64 chunks, so one column each) into X
+        const int wq = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = (CW * TP) >> 5;
+        for (int q = wq; q < CW; q += nw)
+            *reinterpret_cast<float2*>(X + q * kEP + 2 * ln) = warp_pcr64(E + q * 4 * kEP, kEP, ln);
+        __syncthreads();
+        const float xf = X[cx * kEP + p];
         // the previous strip's U stores must have read the staging strip before this strip's finish rewrites it
         if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
         if (active) {
-            const float xnext = (p + 1 < T) ? sa[idx + CW] : 0.f;
+            const float xnext = (p + 1 < T) ? X[cx * kEP + p + 1] : 0.f;
             const float xl = e.lF - e.lG * xnext - e.lH * xf;
             if (nvalid > M) chunk_finish_smem<M, true, CW>(dv, tq, xf, xl, smU + j0 * CW + cx, nvalid);
             else chunk_finish_smem<M, false, CW>(dv, tq, xf, xl, smU + j0 * CW + cx, nvalid);
@@ -827,7 +895,9 @@ bool run_cols_tmap(const float* L, const float* c, float* U, Strides st, Geom g,
     if (!encode_plane_map(&tmL, L, g, nimg, st.L, CW, BR) || !encode_plane_map(&tmC, c, g, nimg, st.c, CW, BR) ||
         !encode_plane_map(&tmU, U, g, nimg, st.out, CW, BR))
         return false;
-    const size_t smem = sizeof(float) * (5 * (size_t)nbox * BR * CW + 7 * (size_t)CW * TP);
+    if (TP > 64) return false;  // the warp PCR holds 64 chunk unknowns per column
+    // workspace: the last-equation exchange (3 x CW·TP) after the reduced-system arrays (CW x 4 x kEP >= 4·CW·TP)
+    const size_t smem = sizeof(float) * (5 * (size_t)nbox * BR * CW + (size_t)CW * 5 * kEP + 3 * (size_t)CW * TP);
     if (!ensure_smem_optin(reinterpret_cast<const void*>(k_aos_cols_tmap<CW, M, NT>), (int)smem)) return false;
     const int nsx = (g.W + CW - 1) / CW, total = nsx * nimg;
     const int grid = std::min(total, device_sm_count());
