@@ -88,19 +88,11 @@ __device__ __forceinline__ float pcr_solve(float af, float bf, float cf, float d
     return df * frcp(bf);
 }
 
-// Warp PCR for the column pass: the reduced system of one column (TP <= 64 chunk unknowns, identity rows past TP)
-// solved by ONE warp, two unknowns per lane (slots r = 2·lane, 2·lane + 1), all levels by shuffles — no CTA barriers
-// (the shared-memory PCR above takes two per level, twelve at 64 chunks).  E holds the column's (a, b, c, d) rows as
-// four arrays of `pitch` floats; returns x of the lane's two slots.
-__device__ __forceinline__ float2 warp_pcr64(const float* __restrict__ E, int pitch, int lane) {
-    float a[2], b[2], c[2], d[2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        a[s] = E[2 * lane + s];
-        b[s] = E[pitch + 2 * lane + s];
-        c[s] = E[2 * pitch + 2 * lane + s];
-        d[s] = E[3 * pitch + 2 * lane + s];
-    }
+// Warp PCR for the column pass: the reduced system of one column (64 chunk unknowns, identity rows past the real
+// ones) solved by ONE warp, two unknowns per lane (slots r = 2·lane, 2·lane + 1), all levels by shuffles — no CTA
+// barriers (the shared-memory PCR above takes two per level, twelve at 64 chunks).  In: the lane's two rows
+// (a, b, c, d); returns x of its two slots.
+__device__ __forceinline__ float2 warp_pcr64(float (&a)[2], float (&b)[2], float (&c)[2], float (&d)[2], int lane) {
 #pragma unroll
     for (int st = 1; st < 64; st <<= 1) {
         float na[2], nb[2], nc[2], nd[2];
@@ -570,13 +562,9 @@ __global__ void __launch_bounds__(NT, 1) k_aos_cols_tmap(const __grid_constant__
     extern __shared__ __align__(128) float smem_cols[];
     __shared__ __align__(8) uint64_t bar[2];
     const int HB = nbox * BR;
-    const int NTOT = CW * TP;
     float* smU = smem_cols + 4 * HB * CW;  // after [2][L, c][HB][CW]
-    float* E = smU + HB * CW;              // reduced systems [CW][a, b, c, d][kEP]
-    float* X = E + CW * 4 * kEP;           // their solutions [CW][kEP]
-    float* slF = X + CW * kEP;             // last-equation exchange
-    float* slG = slF + NTOT;
-    float* slH = slG + NTOT;
+    float* Q = smU + HB * CW;              // chunk equations [CW][A, C, D, lF, lG, lH][kEP]
+    float* X = Q + CW * 6 * kEP;           // reduced-system solutions [CW][kEP]
     const int G = gridDim.x;
     auto issue = [&](int w, int b) {
         const int z = w / nsx, x0 = (w - z * nsx) * CW, img = batch_image(z, nimg, g);
@@ -600,7 +588,6 @@ __global__ void __launch_bounds__(NT, 1) k_aos_cols_tmap(const __grid_constant__
     const int n = g.H;
     const int j0 = p * M;
     const int nvalid = n - j0;
-    const int idx = p * CW + cx;
     int it = 0;
     for (int w = blockIdx.x; w < total; w += G, ++it) {
         const int b = it & 1;
@@ -640,49 +627,57 @@ __global__ void __launch_bounds__(NT, 1) k_aos_cols_tmap(const __grid_constant__
             }
             chunk_reduce<M>(dv, tq, e);
         }
-        slF[idx] = e.lF;
-        slG[idx] = e.lG;
-        slH[idx] = e.lH;
+        // chunk equations → Q[cx][A, C, D, lF, lG, lH][p] (pitch kEP ≡ 4 mod 32: the 8 columns x 4 chunks of a warp
+        // hit 32 distinct banks); a warp per column forms the reduced rows from them and solves them (warp PCR)
+        {
+            float* Qc = Q + cx * 6 * kEP;
+            Qc[p] = e.A;
+            Qc[kEP + p] = e.C;
+            Qc[2 * kEP + p] = e.D;
+            Qc[3 * kEP + p] = e.lF;
+            Qc[4 * kEP + p] = e.lG;
+            Qc[5 * kEP + p] = e.lH;
+        }
         __syncthreads();  // every thread holds its strip samples in registers: refill the buffer with strip i + 2
         if (threadIdx.x == 0 && w + 2 * G < total) issue(w + 2 * G, b);
-        float af = 0.f, bf = 1.f, cf = 0.f, df = 0.f;
-        if (active) {
-            float pF = 0.f, pG = 0.f, pH = 0.f;
-            if (p > 0) {
-                pF = slF[idx - CW];
-                pG = slG[idx - CW];
-                pH = slH[idx - CW];
-            }
-            af = -e.A * pH;
-            bf = 1.f - e.A * pG - e.C * e.lH;
-            cf = -e.C * e.lG;
-            df = e.D - e.A * pF - e.C * e.lF;
-        }
-        // reduced systems: column cx's rows go to E[cx] (pitch kEP ≡ 4 mod 32: the 8 columns x 4 chunks of a warp hit
-        // 32 distinct banks), a warp solves each column (identity rows past TP) and x comes back through X[cx]
         {
-            float* Ec = E + cx * 4 * kEP;
-            Ec[p] = af;
-            Ec[kEP + p] = bf;
-            Ec[2 * kEP + p] = cf;
-            Ec[3 * kEP + p] = df;
-            for (int r = TP + p; r < 64; r += TP) {  // identity rows TP..63
-                Ec[r] = 0.f;
-                Ec[kEP + r] = 1.f;
-                Ec[2 * kEP + r] = 0.f;
-                Ec[3 * kEP + r] = 0.f;
+            // warp wq solves columns wq, wq + nw, ... (CW·TP/32 warps; 16 at 64 chunks, so one column each); row r of
+            // column q couples chunk r with chunk r − 1's last equation; rows of padding chunks / columns past the
+            // image are identity rows (exactly as the per-strip kernel builds them)
+            const int wq = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = (CW * TP) >> 5;
+            for (int q = wq; q < CW; q += nw) {
+                const float* Qq = Q + q * 6 * kEP;
+                const bool col = x0 + q < g.W;
+                float ra[2], rb[2], rc[2], rd[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int r = 2 * ln + u;
+                    ra[u] = 0.f;
+                    rb[u] = 1.f;
+                    rc[u] = 0.f;
+                    rd[u] = 0.f;
+                    if (col && r < T) {
+                        const float A = Qq[r], C = Qq[kEP + r], D = Qq[2 * kEP + r];
+                        const float lF = Qq[3 * kEP + r], lG = Qq[4 * kEP + r], lH = Qq[5 * kEP + r];
+                        float pF = 0.f, pG = 0.f, pH = 0.f;
+                        if (r > 0) {
+                            pF = Qq[3 * kEP + r - 1];
+                            pG = Qq[4 * kEP + r - 1];
+                            pH = Qq[5 * kEP + r - 1];
+                        }
+                        ra[u] = -A * pH;
+                        rb[u] = 1.f - A * pG - C * lH;
+                        rc[u] = -C * lG;
+                        rd[u] = D - A * pF - C * lF;
+                    }
+                }
+                *reinterpret_cast<float2*>(X + q * kEP + 2 * ln) = warp_pcr64(ra, rb, rc, rd, ln);
             }
         }
-        __syncthreads();
-        // warp wq solves columns wq, wq + nw, ... (CW·TP/32 warps; 16 at 64 chunks, so one column each) into X
-        const int wq = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = (CW * TP) >> 5;
-        for (int q = wq; q < CW; q += nw)
-            *reinterpret_cast<float2*>(X + q * kEP + 2 * ln) = warp_pcr64(E + q * 4 * kEP, kEP, ln);
-        __syncthreads();
-        const float xf = X[cx * kEP + p];
         // the previous strip's U stores must have read the staging strip before this strip's finish rewrites it
         if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
+        const float xf = X[cx * kEP + p];
         if (active) {
             const float xnext = (p + 1 < T) ? X[cx * kEP + p + 1] : 0.f;
             const float xl = e.lF - e.lG * xnext - e.lH * xf;
@@ -896,8 +891,7 @@ bool run_cols_tmap(const float* L, const float* c, float* U, Strides st, Geom g,
         !encode_plane_map(&tmU, U, g, nimg, st.out, CW, BR))
         return false;
     if (TP > 64) return false;  // the warp PCR holds 64 chunk unknowns per column
-    // workspace: the last-equation exchange (3 x CW·TP) after the reduced-system arrays (CW x 4 x kEP >= 4·CW·TP)
-    const size_t smem = sizeof(float) * (5 * (size_t)nbox * BR * CW + (size_t)CW * 5 * kEP + 3 * (size_t)CW * TP);
+    const size_t smem = sizeof(float) * (5 * (size_t)nbox * BR * CW + (size_t)CW * 7 * kEP);
     if (!ensure_smem_optin(reinterpret_cast<const void*>(k_aos_cols_tmap<CW, M, NT>), (int)smem)) return false;
     const int nsx = (g.W + CW - 1) / CW, total = nsx * nimg;
     const int grid = std::min(total, device_sm_count());
