@@ -307,6 +307,8 @@ __device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const flo
 // (box 76 x 64: a row pitch of 76 floats puts the two rows of a 128-bit load phase 4 banks apart) instead of four
 // 16-byte loads per item whose lanes use half of each 32-byte sector; border tiles keep the clamped global loads.
 constexpr int kCondTP = 76;  // staged row pitch (floats)
+// (Round 2, measured and dropped: persistent CTAs, 3 per SM, double-buffering the next tiles' tensor copies behind
+// the current tile's work: 22.6 vs 21.1 ms per 256-image step — the 4 CTAs per SM of the per-tile form win.)
 
 template <int MODE, int DIFF>
 __global__ void __launch_bounds__(256) k_cond2(const __grid_constant__ CUtensorMap tmL, int use_tma,
