@@ -198,6 +198,9 @@ __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict
 constexpr int kFusedR = 16;  // measured (256-image step): R = 16 38.3 ms, 8 39.8, 4 43.4, 20 44.1, 32 77.5 (round 2, with
                              // the row-term form: 16 36.9, 12 38.5 (32 registers, 7 CTAs/SM), 20 41.5); 512-thread CTAs
                              // (CW = 480/448, less column halo) 46.4 vs 38.7
+// (Round 2, measured and dropped: a compact grid (blockIdx.x = work item of the image in (level, chain, column block)
+// order, decoded from a per-level table) instead of the (columns, chains, image x level) grid sized by the largest
+// level, whose 21% empty CTAs exit at once: 35.3 vs 33.4 ms — the decode costs more than the empty CTAs.)
 // (Round 2, measured and dropped: the (Lx, Ly) rows leaving through 1-D TMA bulk stores straight from the shared rows
 // (columns shifted by s & 1 for 16-byte alignment) instead of per-thread 8-byte stores: 33.9/34.1 vs 34.2/34.1 ms —
 // no change beyond noise, and the extra state spills at 40 registers.)
