@@ -1,4 +1,4 @@
-"""Debug: one small detect through the TMA Hessian (run under compute-sanitizer)."""
+"""One small kaze_extract of two synthetic W x H images (for compute-sanitizer runs): python scripts/dbg_extract.py W H"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
