@@ -924,7 +924,8 @@ bool launch_aos_cols(const float* L, const float* c, float* U, Strides st, Geom 
     if (tma && persistent && H <= 64 * 19) {
         bool ok;
         // (smaller chunks with more threads measured slower: M = 11 x 128 chunks 32.3 ms, M = 13 x 96 30.8, vs 27.1
-        // at M = 19 x 64 — one more PCR level and its barriers)
+        // at M = 19 x 64 — one more PCR level and its barriers; with the warp PCR, 4-column strips at two CTAs per SM
+        // 28.2 vs 24.7 ms)
         if (H <= 64 * 9) ok = run_cols_tmap<8, 9, 512>(L, c, U, st, g, nimg, tau, s);
         else if (H <= 64 * 13) ok = run_cols_tmap<8, 13, 512>(L, c, U, st, g, nimg, tau, s);
         else if (H <= 64 * 17) ok = run_cols_tmap<8, 17, 512>(L, c, U, st, g, nimg, tau, s);
