@@ -197,9 +197,17 @@ __global__ void __launch_bounds__(256) k_hess_det_chain(const float2* __restrict
 // the s-column halo of (Lx, Ly) is recomputed (CW + 2s ≤ 256 columns per 256 threads), and the L taps of the
 // column halo and of the two extra chain rows come from L1/L2.  Same arithmetic, same order as the two passes:
 // bit-identical results.
-constexpr int kFusedR = 16;  // measured (256-image step): R = 16 38.3 ms, 8 39.8, 4 43.4, 20 44.1, 32 77.5 (round 2, with
-                             // the row-term form: 16 36.9, 12 38.5 (32 registers, 7 CTAs/SM), 20 41.5); 512-thread CTAs
-                             // (CW = 480/448, less column halo) 46.4 vs 38.7
+#ifndef KZ_HESS_R
+#define KZ_HESS_R 12
+#endif
+#ifndef KZ_HESS_MINB
+#define KZ_HESS_MINB 6
+#endif
+constexpr int kFusedR = KZ_HESS_R;  // measured (256-image step): R = 16 38.3 ms, 8 39.8, 4 43.4, 20 44.1, 32 77.5 (round 2,
+                                    // with the row-term form: 16 36.9, 12 38.5 (32 registers, 7 CTAs/SM), 20 41.5;
+                                    // 512-thread CTAs (CW = 480/448) 46.4 vs 38.7).  With the one-path kernel (step in
+                                    // a register): R = 12 at 6 CTAs/SM 33.0 vs 33.6 at 16, 33.3 at 12 with 7 CTAs/SM,
+                                    // 33.5 at 16 with 5, 33.3 at 20 with 5.
 // (Round 2, measured and dropped: a compact grid (blockIdx.x = work item of the image in (level, chain, column block)
 // order, decoded from a per-level table) instead of the (columns, chains, image x level) grid sized by the largest
 // level, whose 21% empty CTAs exit at once: 35.3 vs 33.4 ms — the decode costs more than the empty CTAs.)
@@ -307,11 +315,11 @@ __device__ __forceinline__ void hess_fused_body(const float* __restrict__ L, flo
 }
 
 template <int R>
-__global__ void __launch_bounds__(256, 6) k_hess_fused(const float* __restrict__ Lt, float2* __restrict__ Lxy,
+__global__ void __launch_bounds__(256, KZ_HESS_MINB) k_hess_fused(const float* __restrict__ Lt, float2* __restrict__ Lxy,
                                                     float* __restrict__ Ldet, size_t img_stride, Geom g, LevelTable lt,
                                                     int keep_edges) {
     KZ_PDL_PROLOGUE();
-    __shared__ float2 sm[R + 2][256];  // 36 KB at R = 16.  (Staging the L taps in shared memory as well — each
+    __shared__ float2 sm[R + 2][256];  // 28 KB at R = 12.  (Staging the L taps in shared memory as well — each
                                        // loaded once instead of three times through L1 — measured slower: 76.7 ms.)
     const int img = chain_band(blockIdx.z, lt.n), level = blockIdx.z - img * lt.n;
     const int s = lt.step[level];
