@@ -256,12 +256,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             tk.s[q] = -INFINITY;
             tk.j[q] = -1;
         }
+        constexpr int kChunks = kTileR / kColGroups / 32;
         for (int t = 0; t < ntiles; ++t) {
             const int a = t & 1;
+            // the tile's validity words (32 columns each) are loaded before the accumulator wait, so their latency
+            // hides behind it instead of stalling the chunk scan
+            uint32_t vmk[kChunks];
+#pragma unroll
+            for (int ch = 0; ch < kChunks; ++ch)
+                vmk[ch] = __ldg(rvalid + ((t * kTileR + h * (kTileR / kColGroups) + ch * 32) >> 5));
             mbar_wait(&bar_acc_full[a], (t >> 1) & 1);
             tc_fence_after();
             // all of this warp's chunks of the tile leave TMEM behind one wait (several loads in flight, not one)
-            constexpr int kChunks = kTileR / kColGroups / 32;
             uint32_t vr[kChunks][32];
 #pragma unroll
             for (int ch = 0; ch < kChunks; ++ch)
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(vr[ch][i]);
                 const int j0 = (tb + t) * kTileR + col;
-                const uint32_t vm = __ldg(rvalid + ((t * kTileR + col) >> 5));  // 32 columns = one validity word
+                const uint32_t vm = vmk[ch];  // 32 columns = one validity word
                 if (vm != 0xffffffffu) {  // warp-uniform and rare: padding / degenerate references never compete
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = ((vm >> i) & 1u) ? v[i] : -INFINITY;
