@@ -23,6 +23,10 @@
 //            fp32x2 (FFMA2/FMUL2, M = 10 to fit 64 registers) issued 35 instead of 55 instructions per pixel but
 //            ran 42.0 vs 32.2 ms: twice the chunks make the shared-memory PCR (7 steps, float2) the bottleneck.
 //            CTA shape at M = 20: 4 columns x 4 CTAs/SM 39.3 ms, 16 columns x 1 CTA/SM 34.1, 8 x 2 (kept) 29.5.)
+//            Default for H <= 64·19 (round 2): k_aos_cols_tmap — persistent CTAs, one per SM, double-buffered TMA
+//            strips, and the reduced systems solved by one warp per column with a shuffle PCR (3 CTA barriers per
+//            strip): 24.3 vs 27.4 ms for the per-strip TMA kernel k_aos_cols_tma (kept for KAZE_COLS_PERSIST=0),
+//            k_aos_cols_u for taller images.
 //   rows:    one CTA (4 or 8 warps) per row.  The TMA engine streams the row's L, c and U into shared memory (1-D
 //            bulk copies, mbarrier), M is odd so the strided chunk reads are conflict free; the reduced system is
 //            solved by a warp-level SPIKE (shuffle PCR on three right-hand sides + a 2·NW-unknown boundary solve).
@@ -549,7 +553,10 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_tma(const __grid_constant
 // reductions are done, so right after that barrier the buffer is refilled with strip i + 2 — its tensor copies
 // stream in during the rest of strip i and all of strip i + 1 (the per-strip CTA above waited for its copies with
 // only one other CTA per SM to fill the gap: 34% of its stalls were that barrier wait).  U leaves from the staging
-// strip with tensor stores; the next strip's finish writes it only after they have read it.
+// strip with tensor stores; the next strip's finish writes it only after they have read it.  After the reductions
+// the chunk equations go to shared memory once and a warp per column forms its reduced rows and solves them with
+// warp_pcr64 (no CTA barriers inside the solve): three barriers per strip in all.  One CTA of 16 warps per SM (the
+// two strip buffers take 154 KB); 4-column strips at two CTAs per SM measured slower (28.2 vs 24.7 ms).
 constexpr int kEP = 68;  // warp-PCR row pitch (floats)
 
 template <int CW, int M, int NT>
