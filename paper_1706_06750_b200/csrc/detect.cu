@@ -110,6 +110,8 @@ constexpr int NSEG = 63;   // rows per warp (multiple of 3).  (Streaming rows th
 constexpr int NMS_LB = 7;  // centre levels per warp (16 levels → two blocks of 7).  Round 2, lean kernel, 256-image
                            // step: 7 centres at 4 CTAs/SM (64 registers) 11.1 ms; 6 / 5 / 4 / 3 centres at 5 / 5 / 5 / 6
                            // CTAs/SM 12.8 / 12.8 / 13.7 / 14.5; 14 centres at 2 CTAs/SM 17.5; 7 at 3 CTAs/SM 12.7.
+                           // Two columns per lane (64-column warps, aligned 8-byte loads, even/odd ballots interleaved
+                           // into the same bitmap; bit-identical): 19.6 / 23.7 / 26.8 ms at 4 / 5 / 7 centres..
                            // Register-ring prefetch of 1 or 2 rows ahead (window of 4/5 slots per plane): 11.1 at 4
                            // CTAs/SM (4 bytes spilled), 12.1 / 12.5 at 3, 14.2 at 2 — no gain over 11.2.
 constexpr int STRIP = 30;  // output columns per strip
