@@ -556,7 +556,8 @@ __global__ void __launch_bounds__(NT, MINB) k_aos_cols_tma(const __grid_constant
 // strip with tensor stores; the next strip's finish writes it only after they have read it.  After the reductions
 // the chunk equations go to shared memory once and a warp per column forms its reduced rows and solves them with
 // warp_pcr64 (no CTA barriers inside the solve): three barriers per strip in all.  One CTA of 16 warps per SM (the
-// two strip buffers take 154 KB); 4-column strips at two CTAs per SM measured slower (28.2 vs 24.7 ms).
+// two strip buffers take 154 KB); 4-column strips at two CTAs per SM measured slower (28.2 vs 24.7 ms), and so did
+// the per-strip CTA (two per SM, single-buffered) with this warp PCR (27.7 vs 24.9: 64 registers spill).
 constexpr int kEP = 68;  // warp-PCR row pitch (floats)
 
 template <int CW, int M, int NT>
