@@ -454,8 +454,21 @@ __global__ void __launch_bounds__(256) k_kp_emit(const float* __restrict__ Ldet,
             if (rank < dp.cap) {
                 const int x = (w0 + lane) * STRIP + bit;
                 float ox = 0.f, oy = 0.f, os = 0.f, v = 0.f;
-                is_keypoint(D0 - g.plane, D0, D0 + g.plane, g.P, x, y, dp.threshold, dp.edge_ratio, dp.refine3d, ox,
-                            oy, os, v);
+                if (dp.refine3d) {
+                    is_keypoint(D0 - g.plane, D0, D0 + g.plane, g.P, x, y, dp.threshold, dp.edge_ratio, 1, ox, oy,
+                                os, v);
+                } else {
+                    // the mark pass has decided; the 2-D fit needs only the level's 3x3 patch — the very values and
+                    // code of the mark pass, so the very offsets (9 loads instead of the 26-neighbour re-check's 35)
+                    const size_t o = (size_t)y * g.P + x;
+                    float patch[3][3];
+#pragma unroll
+                    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                        for (int dx = -1; dx <= 1; ++dx) patch[dy + 1][dx + 1] = __ldg(D0 + o + (ptrdiff_t)dy * g.P + dx);
+                    v = patch[1][1];
+                    refine(patch, dp.edge_ratio, ox, oy);
+                }
                 kaze_keypoint kp;
                 kp.x = (float)x + ox;
                 kp.y = (float)y + oy;
