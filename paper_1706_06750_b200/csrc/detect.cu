@@ -6,8 +6,8 @@
 // the quadratic fit offset δ = −H⁻¹∇D has |δx|, |δy| <= 1.
 //
 // Compaction is deterministic and ordered by (level, y, x) without a sort:
-//   nms_mark : warps streaming 32-column strips down the rows — ballots produce a 1-bit-per-pixel candidate bitmap;
-//              k_rowcount turns it into per-row candidate counts;
+//   nms_mark : warps streaming 32-column strips down the rows — ballots produce a 1-bit-per-pixel candidate bitmap
+//              and (lean kernel) per-row candidate counts by atomics; the generic kernel leaves those to k_rowcount;
 //   kp_scan  : one CTA per image — exclusive scan of the row counts → row offsets, total → d_counts;
 //   kp_emit  : one warp per (image, level, row) — rank of each set bit = row offset + popcounts before it; the
 //              sub-pixel fit is re-evaluated (same fp32 code as the mark pass, so the same decision) and the
@@ -269,25 +269,27 @@ __global__ void __launch_bounds__(256, EXT ? 1 : 4) k_nms_mark(const float* __re
 // above re-derived `c <= nc`, the threshold and the border predicates every row: ~30% of its instructions.)
 template <int NC, int PH>
 __device__ __forceinline__ void nms_row_compute(float (&w)[NC + 2][3], int y, int H, bool xin, float thr, float er,
-                                                int lane, uint32_t* __restrict__ bm, size_t lvl_stride, int words);
+                                                int lane, uint32_t* __restrict__ bm, size_t lvl_stride, int words,
+                                                int* __restrict__ rc);
 
 template <int NC, int PH>
 __device__ __forceinline__ void nms_row_fast(float (&w)[NC + 2][3], const float* __restrict__ base,
                                              const unsigned (&off)[NC + 2], unsigned P, int y, int H, bool xin,
                                              float thr, float er, int lane, uint32_t* __restrict__ bm,
-                                             size_t lvl_stride, int words) {
+                                             size_t lvl_stride, int words, int* __restrict__ rc) {
     const unsigned ro = (unsigned)min(y + 1, H - 1) * P;
 #pragma unroll
     for (int q = 0; q < NC + 2; ++q) w[q][(PH + 2) % 3] = __ldg(base + (off[q] + ro));
     // (Prefetching the row after next into L1 — prefetch.global.L1, no registers — measured 12.0 vs 10.8 ms per
     // 256-image step: the prefetches cost more issue slots and L1 tag lookups than the latency they hid.)
-    nms_row_compute<NC, PH>(w, y, H, xin, thr, er, lane, bm, lvl_stride, words);
+    nms_row_compute<NC, PH>(w, y, H, xin, thr, er, lane, bm, lvl_stride, words, rc);
 }
 
 // One row of the lean detector once row y+1 sits in window slot (PH + 2) % 3.
 template <int NC, int PH>
 __device__ __forceinline__ void nms_row_compute(float (&w)[NC + 2][3], int y, int H, bool xin, float thr, float er,
-                                                int lane, uint32_t* __restrict__ bm, size_t lvl_stride, int words) {
+                                                int lane, uint32_t* __restrict__ bm, size_t lvl_stride, int words,
+                                                int* __restrict__ rc) {
     float M[NC + 2], N8[NC + 2];
 #pragma unroll
     for (int q = 0; q < NC + 2; ++q) {
@@ -329,13 +331,20 @@ __device__ __forceinline__ void nms_row_compute(float (&w)[NC + 2][3], int y, in
 #pragma unroll
     for (int c = 1; c <= NC; ++c)
         if (lane == c - 1) mine = bits[c - 1];
-    if (lane < NC) bm[(size_t)lane * lvl_stride + (size_t)y * words] = (mine >> 1) & ((1u << STRIP) - 1u);
+    if (lane < NC) {
+        const uint32_t word = (mine >> 1) & ((1u << STRIP) - 1u);
+        bm[(size_t)lane * lvl_stride + (size_t)y * words] = word;
+        // the row's candidate count directly (rc: zeroed counts of this block's levels, H per level) — no separate
+        // pass over the bitmap
+        if (word) atomicAdd(rc + (size_t)lane * H + y, __popc(word));
+    }
 }
 
 template <int NC>
 __global__ void __launch_bounds__(256, 4) k_nms_mark_fast(const float* __restrict__ Ldet, size_t img_stride, Geom g,
                                                           int N, int l_first, int nblk, DetectParams dp,
-                                                          uint32_t* __restrict__ bitmap, int words) {
+                                                          uint32_t* __restrict__ bitmap, int words,
+                                                          int* __restrict__ rowcnt) {
     KZ_PDL_PROLOGUE();
     const int lane = threadIdx.x & 31;
     const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -351,6 +360,7 @@ __global__ void __launch_bounds__(256, 4) k_nms_mark_fast(const float* __restric
     for (int q = 0; q < NC + 2; ++q) off[q] = (unsigned)q * (unsigned)g.plane;
     const size_t lvl_stride = (size_t)H * words;
     uint32_t* bm = bitmap + ((size_t)img * (N - 2) + (l0 - 1)) * lvl_stride + strip;
+    int* rc = rowcnt + ((size_t)img * (N - 2) + (l0 - 1)) * H;
     const float thr = dp.threshold, er = dp.edge_ratio;
     const unsigned P = (unsigned)g.P;
     const int y0 = blockIdx.y * NSEG, yend = min(y0 + NSEG, H);
@@ -362,9 +372,9 @@ __global__ void __launch_bounds__(256, 4) k_nms_mark_fast(const float* __restric
         w[q][1] = __ldg(base + (off[q] + r0));
     }
     for (int y = y0; y < yend; y += 3) {
-        nms_row_fast<NC, 0>(w, base, off, P, y, H, xin, thr, er, lane, bm, lvl_stride, words);
-        if (y + 1 < yend) nms_row_fast<NC, 1>(w, base, off, P, y + 1, H, xin, thr, er, lane, bm, lvl_stride, words);
-        if (y + 2 < yend) nms_row_fast<NC, 2>(w, base, off, P, y + 2, H, xin, thr, er, lane, bm, lvl_stride, words);
+        nms_row_fast<NC, 0>(w, base, off, P, y, H, xin, thr, er, lane, bm, lvl_stride, words, rc);
+        if (y + 1 < yend) nms_row_fast<NC, 1>(w, base, off, P, y + 1, H, xin, thr, er, lane, bm, lvl_stride, words, rc);
+        if (y + 2 < yend) nms_row_fast<NC, 2>(w, base, off, P, y + 2, H, xin, thr, er, lane, bm, lvl_stride, words, rc);
     }
 }
 
@@ -492,7 +502,7 @@ int nms_words(int W) { return (W + STRIP - 1) / STRIP; }
 
 int launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, const LevelTable& lt, DetectParams dp,
                     uint32_t* bitmap, int* rowcnt, cudaStream_t s) {
-    int nk = 1;  // kernels launched (rowcount included)
+    int nk = 1;  // kernels launched (the generic paths add k_rowcount)
     const int N = lt.n;
     const int words = nms_words(g.W);
     const int nblk = (N - 2 + NMS_LB - 1) / NMS_LB;
@@ -509,20 +519,22 @@ int launch_nms_mark(const float* Ldet, size_t img_stride, Geom g, int nimg, cons
         // (A variant streaming the rows through a 6-slot shared-memory ring filled by 1-D bulk copies, 5 rows
         // ahead of the warps, measured 14.9 vs 11.5 ms per 256-image step: the mbarrier waits and the extra
         // bookkeeping cost more issue slots than the hidden load latency saved.)
+        cudaMemsetAsync(rowcnt, 0, sizeof(int) * (size_t)g.H * (N - 2) * nimg, s);  // counted by the mark pass
         if (full > 0)
             kz_launch(k_nms_mark_fast<NMS_LB>, dim3(dim3(grid.x, grid.y, nimg * full)), dim3(256), 0, s, Ldet,
-                      img_stride, g, N, 1, full, dp, bitmap, words);
+                      img_stride, g, N, 1, full, dp, bitmap, words, rowcnt);
         const int lr = 1 + full * NMS_LB;
         switch (rem) {
 #define KZ_NMS_REM(R)                                                                                              \
     case R:                                                                                                        \
         kz_launch(k_nms_mark_fast<R>, dim3(dim3(grid.x, grid.y, nimg)), dim3(256), 0, s, Ldet, img_stride, g, N, lr, \
-                  1, dp, bitmap, words);                                                                           \
+                  1, dp, bitmap, words, rowcnt);                                                                   \
         break;
             KZ_NMS_REM(1) KZ_NMS_REM(2) KZ_NMS_REM(3) KZ_NMS_REM(4) KZ_NMS_REM(5) KZ_NMS_REM(6)
 #undef KZ_NMS_REM
             default: break;
         }
+        return nk;  // the lean mark pass counted the rows itself (0.7 ms per 256-image step of k_rowcount saved)
     }
     const int total = g.H * (N - 2) * nimg;
     kz_launch(k_rowcount, dim3((total + 7) / 8), dim3(256), 0, s, bitmap, words, total, rowcnt);
