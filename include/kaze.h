@@ -168,8 +168,10 @@ kaze_status kaze_extract(kaze_ctx* ctx, const float* d_imgs, int32_t n, int32_t 
  * h_desc[n][max_keypoints][64] (h_desc may be NULL to skip descriptor download).  Copies run on
  * context-owned streams overlapped with compute (double-buffered chunks of at most max_batch images;
  * with more than one chunk the first holds max_batch/4 images, so the upload nothing can overlap is
- * short; describes overlap the next chunk as in kaze_extract); the call returns after everything has
- * landed in host memory.  `stream` orders the work after prior work on it.  Errors: as kaze_extract. */
+ * short, and beyond max_batch + max_batch/4 images so does the last, whose descriptor pass and result
+ * copies nothing can overlap; describes overlap the next chunk as in kaze_extract); the call returns
+ * after everything has landed in host memory.  `stream` orders the work after prior work on it.
+ * Errors: as kaze_extract. */
 kaze_status kaze_extract_host(kaze_ctx* ctx, const float* h_imgs, int32_t n, int32_t w, int32_t h,
                               int64_t pitch_elems, kaze_keypoint* h_kps, int32_t* h_counts, float* h_desc,
                               void* stream);

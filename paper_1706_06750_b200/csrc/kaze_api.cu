@@ -684,6 +684,8 @@ kaze_status run_chunks_overlapped(kaze_ctx* c, const float* img, int n, int w, i
                                   cudaStream_t side_s) {
     const int B = c->p.max_batch;
     const size_t cap = (size_t)c->p.max_keypoints;
+    // (A quarter-size last chunk, whose descriptor pass nothing overlaps, measured no change here: 1836.7 / 1832.0 vs
+    // 1835.8 / 1832.9 img/s; the host path keeps it for its result copies.)
     const int nch = (n + B - 1) / B;
     while ((int)c->ovl_ev.size() < 2 * nch) {
         cudaEvent_t e;
@@ -990,13 +992,15 @@ kaze_status kaze_extract_host(kaze_ctx* c, const float* h_imgs, int32_t n, int32
     const size_t cap = (size_t)c->p.max_keypoints;
     const int P = round_up(w, 32);
     // Chunk boundaries: when there is more than one chunk, the first holds a quarter of max_batch, so the upload the
-    // first build must wait for (nothing overlaps it) is short; the others are full, the remainder last.
+    // first build must wait for (nothing overlaps it) is short; so does the last (KAZE_HOST_TAIL), whose descriptor
+    // pass and result copies nothing overlaps either; the others are full, a remainder before the last.
+    static const int small_tail = tune_knob("KAZE_HOST_TAIL", 1);
     std::vector<int> cb{0};
-    if (n > B) {
-        const int first = std::max(1, B / 4);
-        cb.push_back(first);
-    }
-    while (cb.back() < n) cb.push_back(std::min(n, cb.back() + B));
+    const int quarter = std::max(1, B / 4);
+    const int tail = (small_tail && n > B + quarter) ? quarter : 0;
+    if (n > B) cb.push_back(quarter);
+    while (cb.back() < n - tail) cb.push_back(std::min(n - tail, cb.back() + B));
+    if (tail) cb.push_back(n);
     const int nchunks = (int)cb.size() - 1;
     // Make the context's copy streams start after prior work on the caller's stream.
     KZ_CUDA(c, cudaEventRecord(c->ev_comp[0], s));
