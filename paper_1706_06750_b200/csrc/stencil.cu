@@ -348,7 +348,9 @@ __device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const flo
 // 16-byte loads per item whose lanes use half of each 32-byte sector; border tiles keep the clamped global loads.
 constexpr int kCondTP = 76;  // staged row pitch (floats)
 // (Round 2, measured and dropped: persistent CTAs, 3 per SM, double-buffering the next tiles' tensor copies behind
-// the current tile's work: 22.6 vs 21.1 ms per 256-image step — the 4 CTAs per SM of the per-tile form win.)
+// the current tile's work: 22.6 vs 21.1 ms per 256-image step — the 4 CTAs per SM of the per-tile form win.  Border
+// tiles staged as well, their out-of-image elements replaced by the clamped values in a shared-memory fix-up pass:
+// 24.8 vs 21.3 ms — the fix-up costs more than the clamped global loads it replaces.)
 
 template <int MODE, int DIFF>
 __global__ void __launch_bounds__(256) k_cond2(const __grid_constant__ CUtensorMap tmL, int use_tma,
