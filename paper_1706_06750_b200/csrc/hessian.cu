@@ -208,6 +208,10 @@ constexpr int kFusedR = KZ_HESS_R;  // measured (256-image step): R = 16 38.3 ms
                                     // 512-thread CTAs (CW = 480/448) 46.4 vs 38.7).  With the one-path kernel (step in
                                     // a register): R = 12 at 6 CTAs/SM 33.0 vs 33.6 at 16, 33.3 at 12 with 7 CTAs/SM,
                                     // 33.5 at 16 with 5, 33.3 at 20 with 5.
+// (Round 2, measured and dropped: border chains are 35% of the CTAs at 1920x1200 and cost ~1.7x an interior chain
+// (all chains forced onto the border path: 43.8 vs 31.8 ms at equal clocks), but hoisting their 3(R + 4) loads like
+// the interior path — one clamped path for every chain 39.4, clamped hoisting for the border chains only 35.2, for
+// the row-border chains only 34.5, vs 33.1 ms — spills at the 40-register budget of 6 CTAs per SM.)
 // (Round 2, measured and dropped: a compact grid (blockIdx.x = work item of the image in (level, chain, column block)
 // order, decoded from a per-level table) instead of the (columns, chains, image x level) grid sized by the largest
 // level, whose 21% empty CTAs exit at once: 35.3 vs 33.4 ms — the decode costs more than the empty CTAs.)
