@@ -281,7 +281,13 @@ __device__ __forceinline__ void cond_hpass_fast(const float (&v)[16], const floa
 __device__ __forceinline__ float2 c2(float a) { return make_float2(a, a); }
 
 // MODE 1 stores the conductivity; MODE 0 stores |∇|² and returns this thread's max |∇| over the image interior.
-template <int MODE, int DIFF>
+// INTERIOR (CTA-uniform, a compile-time instantiation): no clamp selects and no store predicates in the row loop.
+// In MODE 1 the ½ of both central differences is folded into 1/k² as ¼ (a power-of-two scaling of every product
+// and sum: bit-identical to the scaled form, two FMUL2 per row fewer).
+#ifndef KZ_COND_SPLIT
+#define KZ_COND_SPLIT 1
+#endif
+template <int MODE, int DIFF, bool INTERIOR>
 __device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const float (*sB)[CW2], const float (&w)[7],
                                                float* __restrict__ dst, Geom g, int x0, int y0, int tid, float ik2) {
     float lmax = 0.f;
@@ -295,8 +301,9 @@ __device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const flo
         wa[d] = *reinterpret_cast<const float2*>(&sA[q0 + d][2 * cp]);
         wb[d] = *reinterpret_cast<const float2*>(&sB[q0 + d][2 * cp]);
     }
-    const bool interior = (y0 > 0) && (y0 + CH2 < g.H) && (x0 + CW2 <= g.W);  // CTA-uniform
-    const float2 ik = c2(ik2);
+    const bool interior = INTERIOR || (KZ_COND_SPLIT == 0 && (y0 > 0) && (y0 + CH2 < g.H) && (x0 + CW2 <= g.W));
+    constexpr bool kFold = MODE == 1 && KZ_COND_SPLIT;
+    const float2 ik = c2(kFold ? 0.25f * ik2 : ik2);
     float2 va0 = c2(0.f), va1 = c2(0.f), vb0 = c2(0.f), vb1 = c2(0.f);  // va/vb at window rows j-2, j-1
 #pragma unroll
     for (int j = 0; j < RG + 2; ++j) {  // va_j, vb_j at tile row q0 - 1 + j
@@ -315,8 +322,10 @@ __device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const flo
                 if (y == 0) { aup = va1; bup = vb1; }
                 if (y >= g.H - 1) { adn = va1; bdn = vb1; }
             }
-            const float2 gx = __fmul2_rn(c2(0.5f), __ffma2_rn(c2(kW0c), __fadd2_rn(aup, adn), __fmul2_rn(c2(kW1c), va1)));
-            const float2 gy = __fmul2_rn(c2(0.5f), __fadd2_rn(bdn, make_float2(-bup.x, -bup.y)));
+            const float2 gx2 = __ffma2_rn(c2(kW0c), __fadd2_rn(aup, adn), __fmul2_rn(c2(kW1c), va1));
+            const float2 gy2 = __fadd2_rn(bdn, make_float2(-bup.x, -bup.y));
+            const float2 gx = kFold ? gx2 : __fmul2_rn(c2(0.5f), gx2);
+            const float2 gy = kFold ? gy2 : __fmul2_rn(c2(0.5f), gy2);
             const float2 g2 = __ffma2_rn(gx, gx, __fmul2_rn(gy, gy));
             float2 cv;
             if constexpr (MODE == 1) {
@@ -409,10 +418,15 @@ __global__ void __launch_bounds__(256) k_cond2(const __grid_constant__ CUtensorM
     }
     __syncthreads();
     if constexpr (MODE == 1) {
-        cond_vpass_x2<1, DIFF>(sA, sB, w, opaque(out + img * out_img_stride), g, x0, y0, tid, frcp(kval[img] * kval[img]));
+        float* o = opaque(out + img * out_img_stride);
+        const float ik2 = frcp(kval[img] * kval[img]);
+        if (KZ_COND_SPLIT && (y0 > 0) && (y0 + CH2 < g.H) && (x0 + CW2 <= g.W))  // CTA-uniform
+            cond_vpass_x2<1, DIFF, true>(sA, sB, w, o, g, x0, y0, tid, ik2);
+        else
+            cond_vpass_x2<1, DIFF, false>(sA, sB, w, o, g, x0, y0, tid, ik2);
         return;
     } else {
-        float lmax = cond_vpass_x2<0, DIFF>(sA, sB, w, opaque(out + img * out_img_stride), g, x0, y0, tid, 1.f);
+        float lmax = cond_vpass_x2<0, DIFF, false>(sA, sB, w, opaque(out + img * out_img_stride), g, x0, y0, tid, 1.f);
         for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
         if ((tid & 31) == 0) red[tid >> 5] = lmax;
         __syncthreads();
