@@ -38,6 +38,9 @@ constexpr int kMaxSplit = 4;  // reference-range parts per query block when the 
 constexpr int kCand = 8;  // approximate candidates kept per query (4: 1400 of 15.8k KAZE rows uncertified, 3.4 ms)
 constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 3.64 vs 3.59 ms at 65536^2)
 constexpr int kColGroups = kEpiWarps / 4;
+#ifndef KZ_MATCH_SIGNMASK
+#define KZ_MATCH_SIGNMASK 1
+#endif
 constexpr int kThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
 constexpr float kEps = 1.0f / 1024.0f + 2e-5f;  // fp16 rounding of both operands (2·2^-11) + fp32 sum slack
 
@@ -299,8 +302,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
                 if (!__any_sync(0xffffffffu, mx > thr)) continue;
                 // candidate mask of this lane's row: columns scoring above its current 8th best
                 uint32_t cand = 0u;
+#if KZ_MATCH_SIGNMASK
+                // bit i = sign of thr − v[i] (v > thr ⇔ thr − v < 0; equal scores give +0, and −inf − (−inf) the
+                // positive canonical NaN): one FADD2 per column pair and one funnel shift per column, instead of a
+                // compare, a select and half an add per column
+#pragma unroll
+                for (int i = 30; i >= 0; i -= 2) {
+                    const float2 d = __fadd2_rn(make_float2(thr, thr), make_float2(-v[i], -v[i + 1]));
+                    cand = __funnelshift_l(__float_as_uint(d.y), cand, 1);
+                    cand = __funnelshift_l(__float_as_uint(d.x), cand, 1);
+                }
+                // one candidate in the row's chunk (the common case once the lists have settled) is the chunk
+                // maximum itself: insert it straight from the register, without the shared-memory round trip
+                if (!__any_sync(0xffffffffu, (cand & (cand - 1u)) != 0u)) {
+                    if (cand) topk_push_scan(tk, mx, j0 + __ffs(cand) - 1);
+                    continue;
+                }
+#else
 #pragma unroll
                 for (int i = 0; i < 32; ++i) cand |= (v[i] > thr ? 1u : 0u) << i;
+#endif
                 if (__any_sync(0xffffffffu, cand != 0u)) {
                     // Insert each lane's candidates in column order; the warp iterates max-over-lanes times, not
                     // once per column any lane needs (the values go through shared memory for indexed access).
