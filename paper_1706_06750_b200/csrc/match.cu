@@ -38,6 +38,9 @@ constexpr int kMaxSplit = 4;  // reference-range parts per query block when the 
 constexpr int kCand = 8;  // approximate candidates kept per query (4: 1400 of 15.8k KAZE rows uncertified, 3.4 ms)
 constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 3.64 vs 3.59 ms at 65536^2)
 constexpr int kColGroups = kEpiWarps / 4;
+#ifndef KZ_MATCH_SHARE_THR
+#define KZ_MATCH_SHARE_THR 1
+#endif
 #ifndef KZ_MATCH_SIGNMASK
 #define KZ_MATCH_SIGNMASK 1
 #endif
@@ -193,6 +196,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
     uint8_t* sB = smem + kTileQ * 128;     // kStages x 16 KB
     __shared__ __align__(8) uint64_t bar_full[kStages], bar_empty[kStages], bar_acc_full[2], bar_acc_empty[2], bar_a;
     __shared__ uint32_t tmem_base_slot;
+#if KZ_MATCH_SHARE_THR
+    // each column group's current 8th-best score per query row, published once per tile: a column group filters with
+    // the larger of its own and the other groups' (a score at or below another group's 8th best has 8 scores at
+    // least as high elsewhere, so dropping it keeps every non-candidate at or below the merged list's 8th score —
+    // what the re-rank certificate assumes).  Stale values are smaller, so they are safe too.
+    __shared__ float thr_sh[kColGroups][kTileQ];
+    for (int i = threadIdx.x; i < kColGroups * kTileQ; i += blockDim.x) (&thr_sh[0][0])[i] = -INFINITY;
+#endif
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // this CTA scans reference tiles [tb, tb + ntiles) — part blockIdx.y of gridDim.y — and writes its own top-8
     const int ntiles_all = (nr + kTileR - 1) / kTileR;
@@ -260,8 +271,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             tk.j[q] = -1;
         }
         constexpr int kChunks = kTileR / kColGroups / 32;
+        float thr_other = -INFINITY;  // the other column groups' published 8th best for this lane's row
         for (int t = 0; t < ntiles; ++t) {
             const int a = t & 1;
+#if KZ_MATCH_SHARE_THR
+            {
+                const int row = 32 * g + lane;
+                *(volatile float*)&thr_sh[h][row] = tk.s[kCand - 1];
+#pragma unroll
+                for (int h2 = 0; h2 < kColGroups; ++h2)
+                    if (h2 != h) thr_other = fmaxf(thr_other, *(volatile float*)&thr_sh[h2][row]);
+            }
+#endif
             // the tile's validity words (32 columns each) are loaded before the accumulator wait, so their latency
             // hides behind it instead of stalling the chunk scan
             uint32_t vmk[kChunks];
@@ -294,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
                 }
                 // Chunk maximum first: once the lists have settled, most chunks beat no row's 8th best and cost
                 // ~16 FMNMX3 instead of a per-column candidate mask.
-                const float thr = tk.s[kCand - 1];
+                const float thr = fmaxf(tk.s[kCand - 1], thr_other);
                 float mx = v[0];
 #pragma unroll
                 for (int i = 1; i < 31; i += 2) mx = fmaxf(mx, fmaxf(v[i], v[i + 1]));
