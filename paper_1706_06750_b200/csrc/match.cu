@@ -45,6 +45,17 @@ constexpr int kColGroups = kEpiWarps / 4;
 #define KZ_MATCH_SIGNMASK 1
 #endif
 constexpr int kThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
+// Accumulator stages: each reference tile is accumulated as kHalves column slices of kAccW columns (N = kAccW MMAs),
+// in a ring of kAcc = 2·kHalves TMEM stages (256 columns per CTA either way).  Finer slices let the MMA run further
+// ahead of the epilogue: with whole-tile stages (kHalves = 1) the issuer waited on a free accumulator for every tile
+// and the epilogue on a full one (ncu, 65536^2: 60-70 try-wait spins per tile in the issuer, ~10 per warp and tile in
+// the epilogue).
+#ifndef KZ_MATCH_HALVES
+#define KZ_MATCH_HALVES 1
+#endif
+constexpr int kHalves = KZ_MATCH_HALVES;
+constexpr int kAccW = kTileR / kHalves;
+constexpr int kAcc = 2 * kHalves;
 constexpr float kEps = 1.0f / 1024.0f + 2e-5f;  // fp16 rounding of both operands (2·2^-11) + fp32 sum slack
 
 // ---- tcgen05 / mbarrier wrappers (PTX ISA 8.7, sm_100a) ----
@@ -103,7 +114,7 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 }
 // Instruction descriptor kind::f16: D f32 (bits 4-5 = 1), A/B f16 (format 0 at bits 7-9 / 10-12), both K-major,
 // N = kTileR (bits 17-22 = N/8), M = 128 (bits 24-28 = M/16).
-constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kTileR >> 3) << 17) | ((uint32_t)(kTileQ >> 4) << 24);
+constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kAccW >> 3) << 17) | ((uint32_t)(kTileQ >> 4) << 24);
 
 __global__ void __launch_bounds__(256) k_match_prep(const float* __restrict__ D, int n, int ntiles,
                                                     uint8_t* __restrict__ tiles, uint32_t* __restrict__ valid,
@@ -194,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;                    // 16 KB
     uint8_t* sB = smem + kTileQ * 128;     // kStages x 16 KB
-    __shared__ __align__(8) uint64_t bar_full[kStages], bar_empty[kStages], bar_acc_full[2], bar_acc_empty[2], bar_a;
+    __shared__ __align__(8) uint64_t bar_full[kStages], bar_empty[kStages], bar_acc_full[kAcc], bar_acc_empty[kAcc], bar_a;
     __shared__ uint32_t tmem_base_slot;
 #if KZ_MATCH_SHARE_THR
     // each column group's current 8th-best score per query row, published once per tile: a column group filters with
@@ -219,14 +230,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             mbar_init(&bar_full[i], 1);
             mbar_init(&bar_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kAcc; ++i) {
             mbar_init(&bar_acc_full[i], 1);
             mbar_init(&bar_acc_empty[i], kEpiWarps * 32);
         }
         mbar_init(&bar_a, 1);
         fence_mbar_init();
     }
-    if (warp == kEpiWarps + 1) tmem_alloc(&tmem_base_slot, 2 * kTileR);  // double-buffered accumulator
+    if (warp == kEpiWarps + 1) tmem_alloc(&tmem_base_slot, kAcc * kAccW);  // the accumulator ring (256 columns)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -248,17 +259,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             mbar_wait(&bar_a, 0);
             const uint32_t a_addr = smem_u32(sA);
             for (int t = 0; t < ntiles; ++t) {
-                const int s = t % kStages, a = t & 1;
+                const int s = t % kStages;
                 mbar_wait(&bar_full[s], (t / kStages) & 1);
-                if (t >= 2) mbar_wait(&bar_acc_empty[a], ((t >> 1) - 1) & 1);
-                tc_fence_after();
-                const uint32_t b_addr = smem_u32(sB + s * kTileBytes);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)  // K = 64 = 4 x 16, +32 B along the swizzled row per step
-                    mma_f16(tmem + a * kTileR, smem_desc_sw128(a_addr + 32 * k), smem_desc_sw128(b_addr + 32 * k),
-                             kIdesc, k > 0 ? 1u : 0u);
-                mma_commit(&bar_empty[s]);     // smem stage free once these MMAs are done
-                mma_commit(&bar_acc_full[a]);  // accumulator ready for the epilogue
+                for (int hh = 0; hh < kHalves; ++hh) {
+                    const int u = t * kHalves + hh, st = u % kAcc;
+                    if (u >= kAcc) mbar_wait(&bar_acc_empty[st], ((u / kAcc) - 1) & 1);
+                    tc_fence_after();
+                    // reference rows hh·kAccW.. of the tile: whole 8-row swizzle atoms, kAccW·128 B further on
+                    const uint32_t b_addr = smem_u32(sB + s * kTileBytes) + hh * kAccW * 128;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)  // K = 64 = 4 x 16, +32 B along the swizzled row per step
+                        mma_f16(tmem + st * kAccW, smem_desc_sw128(a_addr + 32 * k), smem_desc_sw128(b_addr + 32 * k),
+                                kIdesc, k > 0 ? 1u : 0u);
+                    mma_commit(&bar_acc_full[st]);  // accumulator stage ready for the epilogue
+                }
+                mma_commit(&bar_empty[s]);  // smem stage free once these MMAs are done
             }
         }
     } else {  // ===== epilogue warps: TMEM → registers → running top-8 (kCand) per query row =====
@@ -270,17 +286,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             tk.s[q] = -INFINITY;
             tk.j[q] = -1;
         }
-        constexpr int kChunks = kTileR / kColGroups / 32;
+        constexpr int kChunks = kAccW / kColGroups / 32;  // 32-column chunks per warp and accumulator stage
         float thr_other = -INFINITY;  // the other column groups' published 8th best for this lane's row
-        for (int t = 0; t < ntiles; ++t) {
-            const int a = t & 1;
+        // loop-invariant addresses (the per-tile code re-derived them from the generic pointers: ~1/3 of its
+        // instructions)
+        const uint32_t acc_full0 = smem_u32(&bar_acc_full[0]), acc_empty0 = smem_u32(&bar_acc_empty[0]);
+        const uint32_t tmem_row = tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(h * (kAccW / kColGroups));
+        const uint32_t* rv = rvalid + ((h * (kAccW / kColGroups)) >> 5);
 #if KZ_MATCH_SHARE_THR
-            {
-                const int row = 32 * g + lane;
-                *(volatile float*)&thr_sh[h][row] = tk.s[kCand - 1];
+        volatile float* thr_mine = &thr_sh[h][32 * g + lane];
+        volatile float* thr_col = &thr_sh[0][32 * g + lane];
+#endif
+        for (int u = 0; u < ntiles * kHalves; ++u) {
+            const int t = u / kHalves, hh = u - t * kHalves, st = u % kAcc;
+#if KZ_MATCH_SHARE_THR
+            if (hh == 0) {
+                *thr_mine = tk.s[kCand - 1];
 #pragma unroll
                 for (int h2 = 0; h2 < kColGroups; ++h2)
-                    if (h2 != h) thr_other = fmaxf(thr_other, *(volatile float*)&thr_sh[h2][row]);
+                    if (h2 != h) thr_other = fmaxf(thr_other, thr_col[h2 * kTileQ]);
             }
 #endif
             // the tile's validity words (32 columns each) are loaded before the accumulator wait, so their latency
@@ -288,22 +312,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             uint32_t vmk[kChunks];
 #pragma unroll
             for (int ch = 0; ch < kChunks; ++ch)
-                vmk[ch] = __ldg(rvalid + ((t * kTileR + h * (kTileR / kColGroups) + ch * 32) >> 5));
-            mbar_wait(&bar_acc_full[a], (t >> 1) & 1);
+                vmk[ch] = __ldg(rv + ((t * kTileR + hh * kAccW + ch * 32) >> 5));
+            mbar_wait_u32(acc_full0 + 8 * st, (u / kAcc) & 1);
             tc_fence_after();
             // all of this warp's chunks of the tile leave TMEM behind one wait (several loads in flight, not one)
             uint32_t vr[kChunks][32];
 #pragma unroll
             for (int ch = 0; ch < kChunks; ++ch)
-                tmem_ld32_nowait(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(a * kTileR + h * (kTileR / kColGroups) + ch * 32),
-                                 vr[ch]);
+                tmem_ld32_nowait(tmem_row + (uint32_t)(st * kAccW + ch * 32), vr[ch]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             // the accumulator is in registers now: hand it back to the MMA issuer before scanning it
             tc_fence_before();
-            mbar_arrive(&bar_acc_empty[a]);
+            mbar_arrive_u32(acc_empty0 + 8 * st);
 #pragma unroll
             for (int ch = 0; ch < kChunks; ++ch) {
-                const int col = h * (kTileR / kColGroups) + ch * 32;
+                const int col = hh * kAccW + h * (kAccW / kColGroups) + ch * 32;
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(vr[ch][i]);
@@ -395,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
     __syncthreads();
     if (warp == kEpiWarps + 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 2 * kTileR);
+        tmem_dealloc(tmem, kAcc * kAccW);
     }
 }
 
