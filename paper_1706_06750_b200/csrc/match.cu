@@ -41,6 +41,9 @@ constexpr int kColGroups = kEpiWarps / 4;
 #ifndef KZ_MATCH_SHARE_THR
 #define KZ_MATCH_SHARE_THR 1
 #endif
+#ifndef KZ_MATCH_SLEEP
+#define KZ_MATCH_SLEEP 1
+#endif
 #ifndef KZ_MATCH_SIGNMASK
 #define KZ_MATCH_SIGNMASK 1
 #endif
@@ -159,6 +162,15 @@ __global__ void __launch_bounds__(256) k_match_prep(const float* __restrict__ D,
     }
 }
 
+// Producer / MMA-issuer waits (one thread each): suspended rather than spinning (KZ_MATCH_SLEEP).
+__device__ __forceinline__ void kwait(uint64_t* bar, uint32_t parity) {
+#if KZ_MATCH_SLEEP
+    mbar_wait_sleep(smem_u32(bar), parity);
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+
 struct TopK {
     float s[kCand];
     int j[kCand];
@@ -249,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             bulk_g2s(sA, Qt + (size_t)q0 * 128, kTileQ * 128, &bar_a);
             for (int t = 0; t < ntiles; ++t) {
                 const int s = t % kStages;
-                if (t >= kStages) mbar_wait(&bar_empty[s], ((t / kStages) - 1) & 1);
+                if (t >= kStages) kwait(&bar_empty[s], ((t / kStages) - 1) & 1);
                 mbar_arrive_expect_tx(&bar_full[s], kTileBytes);
                 bulk_g2s(sB + s * kTileBytes, Rt + (size_t)t * kTileBytes, kTileBytes, &bar_full[s]);
             }
@@ -260,11 +272,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             const uint32_t a_addr = smem_u32(sA);
             for (int t = 0; t < ntiles; ++t) {
                 const int s = t % kStages;
-                mbar_wait(&bar_full[s], (t / kStages) & 1);
+                kwait(&bar_full[s], (t / kStages) & 1);
 #pragma unroll
                 for (int hh = 0; hh < kHalves; ++hh) {
                     const int u = t * kHalves + hh, st = u % kAcc;
-                    if (u >= kAcc) mbar_wait(&bar_acc_empty[st], ((u / kAcc) - 1) & 1);
+                    if (u >= kAcc) kwait(&bar_acc_empty[st], ((u / kAcc) - 1) & 1);
                     tc_fence_after();
                     // reference rows hh·kAccW.. of the tile: whole 8-row swizzle atoms, kAccW·128 B further on
                     const uint32_t b_addr = smem_u32(sB + s * kTileBytes) + hh * kAccW * 128;
@@ -313,7 +325,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
 #pragma unroll
             for (int ch = 0; ch < kChunks; ++ch)
                 vmk[ch] = __ldg(rv + ((t * kTileR + hh * kAccW + ch * 32) >> 5));
+#if KZ_MATCH_SLEEP
+            mbar_wait_sleep(acc_full0 + 8 * st, (u / kAcc) & 1);
+#else
             mbar_wait_u32(acc_full0 + 8 * st, (u / kAcc) & 1);
+#endif
             tc_fence_after();
             // all of this warp's chunks of the tile leave TMEM behind one wait (several loads in flight, not one)
             uint32_t vr[kChunks][32];
