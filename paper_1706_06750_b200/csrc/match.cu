@@ -10,7 +10,10 @@
 //      tiles through a kStages = 3 mbarrier ring, one thread issues tcgen05.mma kind::f16 (M = 128, N = 128,
 //      K = 4 x 16) into a double-buffered TMEM accumulator (2 x 128 columns), and 8 epilogue warps drain it with
 //      tcgen05.ld (warp w reads TMEM lanes 32·(w%4).. = its 32 query rows, column half w/4), keeping each row's
-//      eight best approximate scores per part.  fp16 operands (descriptor components lie in [−1, 1]; fp16 has bf16's tensor rate and
+//      eight best approximate scores per part.  Per 32-column chunk: the chunk maximum against each row's 8th best
+//      (the larger of its own column group's and the other group's, published once per tile); rows with candidates
+//      build a mask from the sign bits of thr − v; one candidate per row is the chunk maximum, inserted from
+//      registers; more go through shared memory.  All mbarrier waits sleep (suspend-time hint) instead of spinning.  fp16 operands (descriptor components lie in [−1, 1]; fp16 has bf16's tensor rate and
 //      3 more significand bits), fp32 accumulation: |s_approx − a·b| <= 2^-10·|a||b| + accumulation slack.
 //   3. k_match_rerank: one warp per query: exact fp32 distances ||a − b|| for the eight candidates, ordered by
 //      (distance, index).  The result is CERTIFIED exact when the second candidate distance is below the
