@@ -22,10 +22,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 // KZ_WAIT_SLEEP=1: the try-wait carries a suspend-time hint, so waiting threads sleep until the phase completes
 // instead of re-issuing the loop.  Measured for the scale-space kernels (cond, AOS columns and rows, whose CTAs
 // wait once per tile or strip): no change (1862 vs 1861 img/s; cond 20.2 vs 20.1 ms), so the default spins; the
