@@ -333,9 +333,11 @@ __device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const flo
                 cv = make_float2(diffusivity_g(q.x, DIFF), diffusivity_g(q.y, DIFF));
             } else {
                 cv = g2;
-                if (y >= 1 && y <= g.H - 2) {
-                    if (x >= 1 && x <= g.W - 2) lmax = fmaxf(lmax, sqrtf(g2.x));
-                    if (x + 1 >= 1 && x + 1 <= g.W - 2) lmax = fmaxf(lmax, sqrtf(g2.y));
+                // the max of |∇|² and ONE square root at the end: IEEE sqrt is correctly rounded and monotonic, so
+                // sqrt(max) = max(sqrt) bit for bit
+                if (INTERIOR || (y >= 1 && y <= g.H - 2)) {
+                    if (x >= 1 && x <= g.W - 2) lmax = fmaxf(lmax, g2.x);
+                    if (x + 1 >= 1 && x + 1 <= g.W - 2) lmax = fmaxf(lmax, g2.y);
                 }
             }
             float* o = dst + (unsigned)(y * g.P + x);  // dst is opaque: one IMAD.WIDE per row
@@ -349,7 +351,7 @@ __device__ __forceinline__ float cond_vpass_x2(const float (*sA)[CW2], const flo
         va0 = va1; va1 = a;
         vb0 = vb1; vb1 = b;
     }
-    return lmax;
+    return MODE == 0 ? sqrtf(lmax) : lmax;
 }
 
 // Interior tiles (every tap inside the image) stage the 64 input rows x 72 columns with ONE 2-D TMA tensor copy
@@ -426,7 +428,10 @@ __global__ void __launch_bounds__(256) k_cond2(const __grid_constant__ CUtensorM
             cond_vpass_x2<1, DIFF, false>(sA, sB, w, o, g, x0, y0, tid, ik2);
         return;
     } else {
-        float lmax = cond_vpass_x2<0, DIFF, false>(sA, sB, w, opaque(out + img * out_img_stride), g, x0, y0, tid, 1.f);
+        float* op = opaque(out + img * out_img_stride);
+        float lmax = (KZ_COND_SPLIT && (y0 > 0) && (y0 + CH2 < g.H) && (x0 + CW2 <= g.W))  // CTA-uniform
+                         ? cond_vpass_x2<0, DIFF, true>(sA, sB, w, op, g, x0, y0, tid, 1.f)
+                         : cond_vpass_x2<0, DIFF, false>(sA, sB, w, op, g, x0, y0, tid, 1.f);
         for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
         if ((tid & 31) == 0) red[tid >> 5] = lmax;
         __syncthreads();
