@@ -47,6 +47,9 @@ constexpr int kColGroups = kEpiWarps / 4;
 #ifndef KZ_MATCH_SLEEP
 #define KZ_MATCH_SLEEP 1
 #endif
+#ifndef KZ_MATCH_ONELD
+#define KZ_MATCH_ONELD 1
+#endif
 #ifndef KZ_MATCH_SIGNMASK
 #define KZ_MATCH_SIGNMASK 1
 #endif
@@ -334,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             mbar_wait_u32(acc_full0 + 8 * st, (u / kAcc) & 1);
 #endif
             tc_fence_after();
+#if !KZ_MATCH_ONELD
             // all of this warp's chunks of the tile leave TMEM behind one wait (several loads in flight, not one)
             uint32_t vr[kChunks][32];
 #pragma unroll
@@ -343,12 +347,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __res
             // the accumulator is in registers now: hand it back to the MMA issuer before scanning it
             tc_fence_before();
             mbar_arrive_u32(acc_empty0 + 8 * st);
+#endif
 #pragma unroll
             for (int ch = 0; ch < kChunks; ++ch) {
+#if KZ_MATCH_ONELD
+                // one chunk in registers at a time (32 instead of 64 live values); the accumulator goes back to
+                // the MMA issuer once the last chunk is loaded
+                uint32_t vrc[32];
+                tmem_ld32_nowait(tmem_row + (uint32_t)(st * kAccW + ch * 32), vrc);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (ch == kChunks - 1) {
+                    tc_fence_before();
+                    mbar_arrive_u32(acc_empty0 + 8 * st);
+                }
+#else
+                const uint32_t (&vrc)[32] = vr[ch];
+#endif
                 const int col = hh * kAccW + h * (kAccW / kColGroups) + ch * 32;
                 float v[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(vr[ch][i]);
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(vrc[i]);
                 const int j0 = (tb + t) * kTileR + col;
                 const uint32_t vm = vmk[ch];  // 32 columns = one validity word
                 if (vm != 0xffffffffu) {  // warp-uniform and rare: padding / degenerate references never compete
