@@ -39,7 +39,13 @@ constexpr int kTileBytes = kTileR * 128;    // 64 fp16 = 128 B per row
 constexpr int kStages = 3;  // reference-tile ring depth (TMA → MMA)
 constexpr int kMaxSplit = 4;  // reference-range parts per query block when the query blocks alone cannot fill the GPU
 constexpr int kCand = 8;  // approximate candidates kept per query (4: 1400 of 15.8k KAZE rows uncertified, 3.4 ms)
-constexpr int kEpiWarps = 8;  // 4 TMEM lane groups x 2 column halves (16 warps with column quarters: 3.64 vs 3.59 ms at 65536^2)
+// KZ_MATCH_DEEP: one CTA per SM with a 4-deep ring of whole-tile accumulators (all 512 TMEM columns) and 16
+// epilogue warps on column quarters, instead of two CTAs per SM with 2-deep rings and 8 warps each.
+#ifndef KZ_MATCH_DEEP
+#define KZ_MATCH_DEEP 0
+#endif
+constexpr int kCtasPerSm = KZ_MATCH_DEEP ? 1 : 2;
+constexpr int kEpiWarps = KZ_MATCH_DEEP ? 16 : 8;  // 4 TMEM lane groups x column groups (round 1, 2 CTAs/SM: 16 warps with column quarters 3.64 vs 3.59 ms at 65536^2)
 constexpr int kColGroups = kEpiWarps / 4;
 #ifndef KZ_MATCH_SHARE_THR
 #define KZ_MATCH_SHARE_THR 1
@@ -64,7 +70,7 @@ constexpr int kThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
 #endif
 constexpr int kHalves = KZ_MATCH_HALVES;
 constexpr int kAccW = kTileR / kHalves;
-constexpr int kAcc = 2 * kHalves;
+constexpr int kAcc = (KZ_MATCH_DEEP ? 4 : 2) * kHalves;
 constexpr float kEps = 1.0f / 1024.0f + 2e-5f;  // fp16 rounding of both operands (2·2^-11) + fp32 sum slack
 
 // ---- tcgen05 / mbarrier wrappers (PTX ISA 8.7, sm_100a) ----
@@ -214,7 +220,7 @@ __device__ __forceinline__ void topk_insert(TopK& t, float v, int j) {
     if (v > t.s[kCand - 1]) topk_push_scan(t, v, j);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) k_match_topk(const uint8_t* __restrict__ Qt, int nq,
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_match_topk(const uint8_t* __restrict__ Qt, int nq,
                                                             const uint8_t* __restrict__ Rt, int nr,
                                                             const uint32_t* __restrict__ rvalid,
                                                             float* __restrict__ cand_s, int* __restrict__ cand_j) {
@@ -653,7 +659,7 @@ static cudaError_t run_direction(const float* Q, int nq, const uint8_t* Qt, cons
     // unsplit, although 4 parts fill 6.92 of 7 waves and 1 part 1.73 of 2).
     const int qblocks = (nq + kTileQ - 1) / kTileQ, rtiles = (nr + kTileR - 1) / kTileR;
     static const int split_knob = tune_knob("KAZE_MATCH_SPLIT", 0);  // > 0 forces the part count (A/B)
-    const int slots = 2 * device_sm_count();
+    const int slots = kCtasPerSm * device_sm_count();
     int nsplit = 1;
     double best_eff = -1.0;
     for (int sp = 1; qblocks < slots && sp <= kMaxSplit && sp <= (rtiles > 0 ? rtiles : 1); ++sp) {
