@@ -318,17 +318,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_match_topk(const uint8
         const uint32_t tmem_row = tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(h * (kAccW / kColGroups));
         const uint32_t* rv = rvalid + ((h * (kAccW / kColGroups)) >> 5);
 #if KZ_MATCH_SHARE_THR
-        volatile float* thr_mine = &thr_sh[h][32 * g + lane];
-        volatile float* thr_col = &thr_sh[0][32 * g + lane];
+        // relaxed CTA-scope accesses: the publication is unordered by design (any value seen is a valid bound), and
+        // relaxed atomics make that explicit instead of a data race
+        const uint32_t thr_mine = smem_u32(&thr_sh[h][32 * g + lane]);
+        const uint32_t thr_col = smem_u32(&thr_sh[0][32 * g + lane]);
 #endif
         for (int u = 0; u < ntiles * kHalves; ++u) {
             const int t = u / kHalves, hh = u - t * kHalves, st = u % kAcc;
 #if KZ_MATCH_SHARE_THR
             if (hh == 0) {
-                *thr_mine = tk.s[kCand - 1];
+                asm volatile("st.relaxed.cta.shared.f32 [%0], %1;" ::"r"(thr_mine), "f"(tk.s[kCand - 1]) : "memory");
 #pragma unroll
                 for (int h2 = 0; h2 < kColGroups; ++h2)
-                    if (h2 != h) thr_other = fmaxf(thr_other, thr_col[h2 * kTileQ]);
+                    if (h2 != h) {
+                        float o;
+                        asm volatile("ld.relaxed.cta.shared.f32 %0, [%1];" : "=f"(o) : "r"(thr_col + 4u * h2 * kTileQ) : "memory");
+                        thr_other = fmaxf(thr_other, o);
+                    }
             }
 #endif
             // the tile's validity words (32 columns each) are loaded before the accumulator wait, so their latency

@@ -16,7 +16,7 @@ for cfg in "$@"; do
 import json, sys
 try:
     d = json.load(open(sys.argv[1])); k = d["kernels"]
-    print(sys.argv[2], round(d["value"], 1), {n: round(k[n]["ms_per_step"], 2) for n in ("grad_l1", "cond", "aos_cols", "aos_rows", "hessian", "nms_mark", "describe") if n in k}, d["clocks"]["sm_mhz"])
+    print(sys.argv[2], round(d["value"], 1), {n: round(k[n]["ms_per_step"], 2) for n in ("prefilter", "grad_l1", "cond", "aos_cols", "aos_rows", "hessian", "nms_mark", "describe") if n in k}, d["clocks"]["sm_mhz"])
 except Exception as ex:
     print(sys.argv[2], "FAILED", ex)
 PY
