@@ -207,7 +207,8 @@ constexpr int kFusedR = KZ_HESS_R;  // measured (256-image step): R = 16 38.3 ms
                                     // with the row-term form: 16 36.9, 12 38.5 (32 registers, 7 CTAs/SM), 20 41.5;
                                     // 512-thread CTAs (CW = 480/448) 46.4 vs 38.7).  With the one-path kernel (step in
                                     // a register): R = 12 at 6 CTAs/SM 33.0 vs 33.6 at 16, 33.3 at 12 with 7 CTAs/SM,
-                                    // 33.5 at 16 with 5, 33.3 at 20 with 5.
+                                    // 33.5 at 16 with 5, 33.3 at 20 with 5.  Session 3 (one box): R = 12 33.65 vs
+                                    // R = 14 at 6 (spills) 34.67, R = 10 at 7 CTAs/SM (32 registers) 34.0.
 // (Round 2, measured and dropped: border chains are 35% of the CTAs at 1920x1200 and cost ~1.7x an interior chain
 // (all chains forced onto the border path: 43.8 vs 31.8 ms at equal clocks), but hoisting their 3(R + 4) loads like
 // the interior path — one clamped path for every chain 39.4, clamped hoisting for the border chains only 35.2, for
